@@ -1,0 +1,183 @@
+/* baechi_b200.h — the drop-in C ABI of the B200 placement engine.
+ *
+ * Plain C, plain pointers and sizes; no CUDA or torch types cross this line.
+ * Every entry point replaces one function of the reference C++ placer API
+ * (namespace dagsched, /root/reference/proj/include/dagsched/*.hpp); the
+ * citation sits above each declaration. INTEGRATION.md shows the bindings
+ * (C++ shim, ctypes) a maintainer of the reference would add.
+ *
+ * Conventions:
+ *  - status codes mirror dagsched::ErrorKind -> CLI exit code
+ *    (errors.hpp:12-51, tools/dagsched.cpp:350-368): 0 ok, 2 validation,
+ *    3 infeasible, 4 solver; 5 = CUDA/runtime failure (no reference analogue).
+ *    Nothing throws across the ABI; `msg` receives the reference's message.
+ *  - graphs are META graphs (GroupedGraph, transforms.hpp:34-53): V meta
+ *    nodes numbered as the transforms number them, E meta edges sorted by
+ *    (src, dst) and unique, plus the adjacency GroupedGraph carries
+ *    (in_edges / out_edges as CSR of edge ids, ascending).
+ *  - all costs are int64 microseconds / bytes; placements are bit-exact with
+ *    the reference (device_of, exec_order, start_us, PlacerStats).
+ *  - inputs are caller-owned and read-only; outputs are caller-allocated.
+ *  - there is no CPU fallback: without a CUDA device every compute entry
+ *    point returns 5 with a message saying so.
+ */
+#ifndef BAECHI_B200_H
+#define BAECHI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BX_OK 0
+#define BX_VALIDATION 2
+#define BX_INFEASIBLE 3
+#define BX_SOLVER 4
+#define BX_RUNTIME 5
+
+#define BX_ALGO_MTOPO 0
+#define BX_ALGO_METF 1
+#define BX_ALGO_MSCT 2
+
+#define BX_COMM_SEQUENTIAL 0 /* CommMode::Sequential (cost_model.hpp:11) */
+#define BX_COMM_PARALLEL 1   /* CommMode::Parallel */
+
+#define BX_MEM_GRAPH_STATIC 0        /* MemoryMode::GraphStatic (cost_model.hpp:13) */
+#define BX_MEM_TRAINING_PERSISTENT 1 /* MemoryMode::TrainingPersistent */
+
+/* GroupedGraph (transforms.hpp:34-53) flattened. in_edge lists, per meta
+ * node, the ids of its incoming meta edges in ascending order
+ * (GroupedGraph::in_edges); out-edges are contiguous because edges are
+ * sorted by src, so out_off alone describes GroupedGraph::out_edges.
+ * first_id (nullable) is the external id of each meta node's smallest
+ * member, used only in error messages (simulator.cpp:54-56). */
+typedef struct {
+  int32_t V, E;
+  const int64_t *compute_us, *temp_bytes, *perm_bytes, *out_bytes; /* [V] */
+  const int32_t *esrc, *edst;                                      /* [E] */
+  const int64_t *tensor_bytes;                                     /* [E] */
+  const int32_t *in_off, *in_edge;                                 /* [V+1], [E] */
+  const int32_t *out_off;                                          /* [V+1] */
+  const int64_t *first_id;                                         /* [V] or NULL */
+} bx_graph;
+
+/* CommModel (cost_model.hpp:19-24). */
+typedef struct {
+  double intercept_us, us_per_byte;
+  int32_t mode; /* BX_COMM_* */
+} bx_comm;
+
+/* One placement problem: place_mtopo / place_metf / place_msct
+ * (placers.hpp:73-89) of `graph` on a roster of n devices. */
+typedef struct {
+  int32_t graph;               /* index into the plan's graph array */
+  int32_t algo;                /* BX_ALGO_* */
+  int32_t n;                   /* DeviceRoster::count() */
+  const int64_t *capacity;     /* [n] DeviceRoster capacities (bytes) */
+  bx_comm cm;
+  const int32_t *fav_child;    /* m-sct FavoriteMap::fav_child [V]; NULL = empty map */
+  int32_t fav_len;             /* length of fav_child as given (0 or V), for the size check */
+} bx_job;
+
+/* Placement (placers.hpp:25-32) + PlacerStats (:34-38), caller-allocated. */
+typedef struct {
+  int32_t *device_of;   /* [V] */
+  int64_t *start_us;    /* [V] */
+  int32_t *exec_order;  /* [V]  concatenated per-device lists */
+  int32_t *exec_off;    /* [n+1] */
+  int64_t stats[3];     /* discarded_pairs, excluded_devices, awake_reservations */
+  int32_t status;       /* BX_* of this job */
+  char msg[256];        /* reference error text when status != 0 */
+} bx_placement;
+
+/* SimReport (simulator.hpp:25-34), caller-allocated. */
+typedef struct {
+  int64_t makespan_us;
+  int64_t *start_us;        /* [V] */
+  int64_t *peak_bytes;      /* [n] DeviceReport::peak_bytes */
+  int64_t *busy_us;         /* [n] */
+  int64_t *idle_us;         /* [n] */
+  int64_t transfer_count, transfer_bytes, duplicate_transfers, cache_hits;
+  int32_t status;
+  char msg[256];
+} bx_sim_report;
+
+/* ---- library ---------------------------------------------------------- */
+const char *bx_version(void);
+/* Number of CUDA devices visible (0 on a CPU-only host). */
+int bx_device_count(void);
+
+/* comm_time (cost_model.cpp:30-36): round_half_up(intercept + per_byte*bytes)
+ * with separately rounded multiply and add (no FMA). Host-side scalar
+ * helper used by the C++ shim; the kernels compute the same thing on device. */
+int bx_comm_time(const bx_comm *cm, int64_t bytes, int64_t *out_us);
+
+/* Builds GroupedGraph adjacency for a meta edge list already sorted by
+ * (src, dst): in_off/in_edge and out_off (transforms.cpp:169-223 fills the
+ * same lists). Host-side ingest helper, O(V+E). */
+int bx_build_adjacency(int32_t V, int32_t E, const int32_t *esrc,
+                       const int32_t *edst, int32_t *in_off, int32_t *in_edge,
+                       int32_t *out_off, char *msg, int msglen);
+
+/* ---- plans: device-resident batches of placement problems --------------
+ * A plan owns device copies of `ngraphs` graphs and `njobs` jobs plus the
+ * scheduling workspace. It remembers the caller's host pointers, so
+ * bx_plan_upload / bx_plan_download re-copy inputs and outputs (the
+ * end-to-end path) while bx_plan_place runs on device-resident data only.
+ * `device` selects the CUDA device the plan lives on. */
+typedef struct bx_plan bx_plan;
+
+int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs,
+                   const bx_job *jobs, int32_t device, bx_plan **out,
+                   char *msg, int msglen);
+void bx_plan_destroy(bx_plan *plan);
+
+/* Host -> device copy of every graph/job input, enqueued on `stream`
+ * (a cudaStream_t passed as void*; NULL = legacy default stream). */
+int bx_plan_upload(bx_plan *plan, void *stream);
+
+/* Ingest (K1) + placement (K2) of every job, device-resident, on `stream`.
+ * Runs the reference's validation order per job: fav size (place_msct,
+ * placers.cpp:304-310), roster (:19-29), m-topo cap (:327-335), acyclicity
+ * (meta_topo_order, transforms.cpp:446-479), then the placer. Asynchronous;
+ * per-job status lands on the device and is read by bx_plan_download. */
+int bx_plan_place(bx_plan *plan, void *stream);
+
+/* Device -> host copy of every job's placement into `out[njobs]`
+ * (caller-allocated arrays sized by each job's V and n). Synchronises
+ * `stream`. Returns BX_OK if the copy worked; per-job status is in out[i]. */
+int bx_plan_download(bx_plan *plan, void *stream, bx_placement *out);
+
+/* Number of placer kernel launches the last bx_plan_place issued. */
+int bx_plan_launch_count(const bx_plan *plan);
+
+/* simulate (simulator.cpp:273-278) of every job's current device-resident
+ * placement (K4), in `mem_mode`. Device-resident; use bx_plan_sim_download
+ * for the reports. */
+int bx_plan_simulate(bx_plan *plan, int32_t mem_mode, void *stream);
+int bx_plan_sim_download(bx_plan *plan, void *stream, bx_sim_report *out);
+
+/* ---- one-shot entry points (host buffers in, host buffers out) ---------
+ * bx_place == place_mtopo / place_metf / place_msct (placers.hpp:73-89). */
+int bx_place(const bx_graph *graph, const bx_job *job, bx_placement *out);
+
+/* bx_simulate == simulate (simulator.hpp:53-55) of an externally given
+ * placement (device_of [V], exec_order/exec_off per device). */
+int bx_simulate(const bx_graph *graph, int32_t n, const int64_t *capacity,
+                const bx_comm *cm, int32_t mem_mode, const int32_t *device_of,
+                const int32_t *exec_order, const int32_t *exec_off,
+                bx_sim_report *out);
+
+/* bx_round_extract == round_and_extract (lp.hpp:88-90, lp.cpp:280-326) on
+ * the device (K3): x[E] per meta edge, threshold in (0, 0.5).
+ * stats2 = {favorite_edges, repaired_nodes}. */
+int bx_round_extract(int32_t V, int32_t E, const int32_t *esrc,
+                     const int32_t *edst, const double *x, double threshold,
+                     int32_t *fav_child, int32_t *fav_parent, int32_t *stats2,
+                     char *msg, int msglen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BAECHI_B200_H */

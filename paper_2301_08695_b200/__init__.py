@@ -1,0 +1,454 @@
+"""baechi-b200 — B200-native Baechi placement engine (arXiv 2301.08695).
+
+Python face of the C ABI in ``include/baechi_b200.h`` (``libbaechi_b200.so``,
+built in-tree for sm_100a). Names and error behaviour mirror the reference
+C++ placer API (``/root/reference/proj/include/dagsched``):
+
+=====================  ==============================================
+reference              here
+=====================  ==============================================
+``place_mtopo``        :func:`place_mtopo`  (placers.hpp:73-74)
+``place_metf``         :func:`place_metf`   (placers.hpp:78-79)
+``place_msct``         :func:`place_msct`   (placers.hpp:87-89)
+``simulate``           :func:`simulate`     (simulator.hpp:53-55)
+``verify_placement``   :func:`verify_placement` (simulator.hpp:64-67)
+``round_and_extract``  :func:`round_and_extract` (lp.hpp:88-90)
+``comm_time``          :func:`comm_time`    (cost_model.hpp:29)
+``max_comm_time``      :func:`max_comm_time` (cost_model.hpp:71)
+``ValidationError``..  same names (errors.hpp:10-51)
+=====================  ==============================================
+
+Every compute call runs on the GPU through the .so; there is no CPU path.
+If the library is missing or no CUDA device is visible the call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbaechi_b200.so")
+
+BX_OK, BX_VALIDATION, BX_INFEASIBLE, BX_SOLVER, BX_RUNTIME = 0, 2, 3, 4, 5
+ALGOS = {"m-topo": 0, "m-etf": 1, "m-sct": 2}
+SEQUENTIAL, PARALLEL = 0, 1
+GRAPH_STATIC, TRAINING_PERSISTENT = 0, 1
+
+
+# ---- errors (errors.hpp:10-51) ------------------------------------------
+class Error(RuntimeError):
+    kind = None
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        self.msg = msg
+
+
+class ValidationError(Error):
+    kind = BX_VALIDATION
+
+
+class CycleError(ValidationError):
+    pass
+
+
+class InfeasibleError(Error):
+    kind = BX_INFEASIBLE
+
+
+class SolverError(Error):
+    kind = BX_SOLVER
+
+
+class DeviceError(Error):
+    """CUDA/runtime failure (no reference analogue)."""
+    kind = BX_RUNTIME
+
+
+def _raise(status: int, msg: str):
+    if status == BX_OK:
+        return
+    if status == BX_VALIDATION:
+        if msg.startswith("meta graph is cyclic"):
+            raise CycleError(msg)
+        raise ValidationError(msg)
+    if status == BX_INFEASIBLE:
+        raise InfeasibleError(msg)
+    if status == BX_SOLVER:
+        raise SolverError(msg)
+    raise DeviceError(msg)
+
+
+# ---- ctypes mirror of baechi_b200.h ---------------------------------------
+_vp = C.c_void_p
+
+
+class _Graph(C.Structure):
+    _fields_ = [("V", C.c_int32), ("E", C.c_int32),
+                ("compute_us", _vp), ("temp_bytes", _vp), ("perm_bytes", _vp), ("out_bytes", _vp),
+                ("esrc", _vp), ("edst", _vp), ("tensor_bytes", _vp),
+                ("in_off", _vp), ("in_edge", _vp), ("out_off", _vp), ("first_id", _vp)]
+
+
+class _Comm(C.Structure):
+    _fields_ = [("intercept_us", C.c_double), ("us_per_byte", C.c_double), ("mode", C.c_int32)]
+
+
+class _Job(C.Structure):
+    _fields_ = [("graph", C.c_int32), ("algo", C.c_int32), ("n", C.c_int32), ("capacity", _vp),
+                ("cm", _Comm), ("fav_child", _vp), ("fav_len", C.c_int32)]
+
+
+class _Placement(C.Structure):
+    _fields_ = [("device_of", _vp), ("start_us", _vp), ("exec_order", _vp), ("exec_off", _vp),
+                ("stats", C.c_int64 * 3), ("status", C.c_int32), ("msg", C.c_char * 256)]
+
+
+class _SimReport(C.Structure):
+    _fields_ = [("makespan_us", C.c_int64), ("start_us", _vp), ("peak_bytes", _vp), ("busy_us", _vp),
+                ("idle_us", _vp), ("transfer_count", C.c_int64), ("transfer_bytes", C.c_int64),
+                ("duplicate_transfers", C.c_int64), ("cache_hits", C.c_int64),
+                ("status", C.c_int32), ("msg", C.c_char * 256)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads libbaechi_b200.so; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(the placement engine has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        i32, i64, cp = C.c_int32, C.c_int64, C.c_char_p
+        L.bx_version.restype = C.c_char_p
+        L.bx_device_count.restype = C.c_int
+        L.bx_comm_time.argtypes = [C.POINTER(_Comm), i64, C.POINTER(i64)]
+        L.bx_build_adjacency.argtypes = [i32, i32, _vp, _vp, _vp, _vp, _vp, cp, C.c_int]
+        L.bx_plan_create.argtypes = [i32, C.POINTER(_Graph), i32, C.POINTER(_Job), i32,
+                                     C.POINTER(_vp), cp, C.c_int]
+        L.bx_plan_destroy.argtypes = [_vp]
+        L.bx_plan_destroy.restype = None
+        L.bx_plan_upload.argtypes = [_vp, _vp]
+        L.bx_plan_place.argtypes = [_vp, _vp]
+        L.bx_plan_download.argtypes = [_vp, _vp, C.POINTER(_Placement)]
+        L.bx_plan_launch_count.argtypes = [_vp]
+        L.bx_plan_simulate.argtypes = [_vp, i32, _vp]
+        L.bx_plan_sim_download.argtypes = [_vp, _vp, C.POINTER(_SimReport)]
+        L.bx_place.argtypes = [C.POINTER(_Graph), C.POINTER(_Job), C.POINTER(_Placement)]
+        L.bx_simulate.argtypes = [C.POINTER(_Graph), i32, _vp, C.POINTER(_Comm), i32, _vp, _vp, _vp,
+                                  C.POINTER(_SimReport)]
+        L.bx_round_extract.argtypes = [i32, i32, _vp, _vp, _vp, C.c_double, _vp, _vp, _vp, cp, C.c_int]
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["bx_version", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
+            "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download",
+            "bx_plan_launch_count", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
+            "bx_simulate", "bx_round_extract"]
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(np.asarray(a, dtype=dt))
+
+
+# ---- data model -----------------------------------------------------------
+@dataclass
+class CommModel:
+    """CommModel (cost_model.hpp:19-24); mode 0 sequential, 1 parallel."""
+    intercept_us: float = 0.0
+    us_per_byte: float = 0.0
+    mode: int = SEQUENTIAL
+
+    def _c(self):
+        return _Comm(float(self.intercept_us), float(self.us_per_byte), int(self.mode))
+
+
+class MetaGraph:
+    """A GroupedGraph (transforms.hpp:34-53) as flat arrays: meta-node
+    aggregates, meta edges sorted by (src, dst), and the adjacency."""
+
+    def __init__(self, k, temp, perm, out, esrc, edst, ebytes, first_id=None):
+        self.k = _c(k, np.int64)
+        self.temp = _c(temp, np.int64)
+        self.perm = _c(perm, np.int64)
+        self.out = _c(out, np.int64)
+        self.esrc = _c(esrc, np.int32)
+        self.edst = _c(edst, np.int32)
+        self.ebytes = _c(ebytes, np.int64)
+        self.first_id = None if first_id is None else _c(first_id, np.int64)
+        self.V = len(self.k)
+        self.E = len(self.esrc)
+        self.in_off = np.zeros(self.V + 1, np.int32)
+        self.out_off = np.zeros(self.V + 1, np.int32)
+        self.in_edge = np.zeros(max(self.E, 1), np.int32)
+        msg = C.create_string_buffer(256)
+        rc = lib().bx_build_adjacency(self.V, self.E, _ptr(self.esrc), _ptr(self.edst),
+                                      _ptr(self.in_off), _ptr(self.in_edge), _ptr(self.out_off), msg, 256)
+        _raise(rc, msg.value.decode())
+
+    @classmethod
+    def from_dict(cls, m: dict) -> "MetaGraph":
+        return cls(m["k"], m["temp"], m["perm"], m["out"], m["esrc"], m["edst"], m["ebytes"],
+                   m.get("first_id"))
+
+    def need(self):
+        return self.perm + self.out + self.temp
+
+    def _c(self):
+        return _Graph(self.V, self.E, _ptr(self.k), _ptr(self.temp), _ptr(self.perm), _ptr(self.out),
+                      _ptr(self.esrc), _ptr(self.edst), _ptr(self.ebytes), _ptr(self.in_off),
+                      _ptr(self.in_edge), _ptr(self.out_off), _ptr(self.first_id))
+
+
+@dataclass
+class Placement:
+    """Placement (placers.hpp:25-32) + PlacerStats (:34-38)."""
+    algorithm: str
+    device_of: np.ndarray
+    start_us: np.ndarray
+    exec_order_flat: np.ndarray
+    exec_off: np.ndarray
+    stats: tuple = (0, 0, 0)
+
+    @property
+    def exec_order(self):
+        return [self.exec_order_flat[self.exec_off[d]:self.exec_off[d + 1]].tolist()
+                for d in range(len(self.exec_off) - 1)]
+
+    def __eq__(self, o):
+        return (self.algorithm == o.algorithm and np.array_equal(self.device_of, o.device_of)
+                and np.array_equal(self.start_us, o.start_us)
+                and np.array_equal(self.exec_order_flat, o.exec_order_flat)
+                and np.array_equal(self.exec_off, o.exec_off))
+
+
+@dataclass
+class SimReport:
+    """SimReport (simulator.hpp:25-34)."""
+    makespan_us: int
+    start_us: np.ndarray
+    peak_bytes: np.ndarray
+    busy_us: np.ndarray
+    idle_us: np.ndarray
+    transfer_count: int
+    transfer_bytes: int
+    duplicate_transfers: int
+    cache_hits: int
+
+
+@dataclass
+class Job:
+    graph: int
+    algo: str
+    capacity: np.ndarray
+    cm: CommModel
+    fav_child: np.ndarray | None = None
+
+
+class Plan:
+    """A device-resident batch of placement problems (bx_plan_*).
+
+    ``upload`` copies host inputs to HBM, ``place`` runs K1+K2 on the given
+    CUDA stream with inputs already resident, ``download`` copies the
+    placements back (synchronising the stream)."""
+
+    def __init__(self, graphs: list[MetaGraph], jobs: list[Job], device: int = 0):
+        self.graphs = graphs
+        self.jobs = jobs
+        self._keep = []
+        self._gc = (_Graph * len(graphs))(*[g._c() for g in graphs])
+        jc = []
+        for j in jobs:
+            cap = _c(j.capacity, np.int64)
+            fav = None if j.fav_child is None else _c(j.fav_child, np.int32)
+            self._keep += [cap, fav]
+            jc.append(_Job(j.graph, ALGOS[j.algo], len(cap), _ptr(cap), j.cm._c(), _ptr(fav),
+                           0 if fav is None else len(fav)))
+        self._jc = (_Job * len(jobs))(*jc)
+        h = _vp()
+        msg = C.create_string_buffer(512)
+        rc = lib().bx_plan_create(len(graphs), self._gc, len(jobs), self._jc, device, C.byref(h), msg, 512)
+        _raise(rc, msg.value.decode())
+        self.h = h
+        # host output buffers (pinned by numpy allocation; plain pageable)
+        self.out = (_Placement * len(jobs))()
+        self._bufs = []
+        for i, j in enumerate(jobs):
+            V = graphs[j.graph].V
+            n = len(j.capacity)
+            b = (np.zeros(max(V, 1), np.int32), np.zeros(max(V, 1), np.int64),
+                 np.zeros(max(V, 1), np.int32), np.zeros(n + 1, np.int32))
+            self._bufs.append(b)
+            self.out[i].device_of, self.out[i].start_us = _ptr(b[0]), _ptr(b[1])
+            self.out[i].exec_order, self.out[i].exec_off = _ptr(b[2]), _ptr(b[3])
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().bx_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, stream=None):
+        rc = lib().bx_plan_upload(self.h, stream)
+        _raise(rc, "bx_plan_upload failed")
+
+    def place(self, stream=None):
+        rc = lib().bx_plan_place(self.h, stream)
+        _raise(rc, "bx_plan_place failed")
+
+    def launch_count(self) -> int:
+        return lib().bx_plan_launch_count(self.h)
+
+    def download(self, stream=None):
+        rc = lib().bx_plan_download(self.h, stream, self.out)
+        _raise(rc, "bx_plan_download failed")
+
+    def result(self, i: int, copy=True) -> Placement:
+        """Placement of job i; raises the job's reference error."""
+        o = self.out[i]
+        _raise(o.status, o.msg.decode())
+        j = self.jobs[i]
+        V = self.graphs[j.graph].V
+        b = self._bufs[i]
+        f = (lambda a: a.copy()) if copy else (lambda a: a)
+        return Placement(j.algo, f(b[0][:V]), f(b[1][:V]), f(b[2][:V]), f(b[3]), tuple(o.stats))
+
+    def status(self, i: int) -> tuple[int, str]:
+        return self.out[i].status, self.out[i].msg.decode()
+
+    def simulate(self, mem_mode=TRAINING_PERSISTENT, stream=None):
+        rc = lib().bx_plan_simulate(self.h, mem_mode, stream)
+        _raise(rc, "bx_plan_simulate failed")
+
+    def sim_download(self, stream=None) -> list:
+        reps = (_SimReport * len(self.jobs))()
+        keep = []
+        for i, j in enumerate(self.jobs):
+            V = self.graphs[j.graph].V
+            n = len(j.capacity)
+            b = [np.zeros(max(V, 1), np.int64)] + [np.zeros(n, np.int64) for _ in range(3)]
+            keep.append(b)
+            reps[i].start_us, reps[i].peak_bytes = _ptr(b[0]), _ptr(b[1])
+            reps[i].busy_us, reps[i].idle_us = _ptr(b[2]), _ptr(b[3])
+        rc = lib().bx_plan_sim_download(self.h, stream, reps)
+        _raise(rc, "bx_plan_sim_download failed")
+        out = []
+        for i, j in enumerate(self.jobs):
+            r = reps[i]
+            if r.status:
+                out.append((r.status, r.msg.decode()))
+                continue
+            V = self.graphs[j.graph].V
+            b = keep[i]
+            out.append(SimReport(r.makespan_us, b[0][:V], b[1], b[2], b[3], r.transfer_count,
+                                 r.transfer_bytes, r.duplicate_transfers, r.cache_hits))
+        return out
+
+
+# ---- reference-shaped entry points ---------------------------------------
+def _one(gg: MetaGraph, algo: str, capacity, cm: CommModel, fav=None, stats_out=None) -> Placement:
+    cap = _c(capacity, np.int64)
+    favc = None if fav is None else _c(fav, np.int32)
+    job = _Job(0, ALGOS[algo], len(cap), _ptr(cap), cm._c(), _ptr(favc), 0 if favc is None else len(favc))
+    V, n = gg.V, len(cap)
+    bufs = (np.zeros(max(V, 1), np.int32), np.zeros(max(V, 1), np.int64), np.zeros(max(V, 1), np.int32),
+            np.zeros(n + 1, np.int32))
+    out = _Placement(_ptr(bufs[0]), _ptr(bufs[1]), _ptr(bufs[2]), _ptr(bufs[3]))
+    g = gg._c()
+    lib().bx_place(C.byref(g), C.byref(job), C.byref(out))
+    _raise(out.status, out.msg.decode())
+    if stats_out is not None:
+        stats_out[:] = list(out.stats)
+    return Placement(algo, bufs[0][:V].copy(), bufs[1][:V].copy(), bufs[2][:V].copy(), bufs[3].copy(),
+                     tuple(out.stats))
+
+
+def place_mtopo(gg: MetaGraph, capacity, cm: CommModel) -> Placement:
+    return _one(gg, "m-topo", capacity, cm)
+
+
+def place_metf(gg: MetaGraph, capacity, cm: CommModel, stats_out=None) -> Placement:
+    return _one(gg, "m-etf", capacity, cm, stats_out=stats_out)
+
+
+def place_msct(gg: MetaGraph, capacity, cm: CommModel, fav_child=None, stats_out=None) -> Placement:
+    return _one(gg, "m-sct", capacity, cm, fav=fav_child, stats_out=stats_out)
+
+
+def simulate(gg: MetaGraph, placement: Placement, capacity, cm: CommModel,
+             mem_mode: int = TRAINING_PERSISTENT) -> SimReport:
+    cap = _c(capacity, np.int64)
+    n = len(cap)
+    V = gg.V
+    b = [np.zeros(max(V, 1), np.int64)] + [np.zeros(max(n, 1), np.int64) for _ in range(3)]
+    rep = _SimReport(0, _ptr(b[0]), _ptr(b[1]), _ptr(b[2]), _ptr(b[3]))
+    dev = _c(placement.device_of, np.int32)
+    eo = _c(placement.exec_order_flat, np.int32)
+    off = _c(placement.exec_off, np.int32)
+    if len(off) != n + 1 or len(dev) != V:
+        raise ValidationError("placement does not match graph or roster")
+    g = gg._c()
+    cmc = cm._c()
+    lib().bx_simulate(C.byref(g), n, _ptr(cap), C.byref(cmc), mem_mode, _ptr(dev), _ptr(eo), _ptr(off),
+                      C.byref(rep))
+    _raise(rep.status, rep.msg.decode())
+    return SimReport(rep.makespan_us, b[0][:V].copy(), b[1][:n].copy(), b[2][:n].copy(), b[3][:n].copy(),
+                     rep.transfer_count, rep.transfer_bytes, rep.duplicate_transfers, rep.cache_hits)
+
+
+def verify_placement(gg, placement, capacity, cm, mem_mode=TRAINING_PERSISTENT):
+    """verify_placement (simulator.cpp:280-294): (pass, diagnostic, report)."""
+    try:
+        r = simulate(gg, placement, capacity, cm, mem_mode)
+        return True, "ok", r
+    except Error as e:
+        if isinstance(e, DeviceError):
+            raise
+        return False, e.msg, None
+
+
+def round_and_extract(V: int, esrc, edst, x, threshold: float = 0.1):
+    """round_and_extract (lp.cpp:280-326) on the GPU (K3). Returns
+    (fav_child, fav_parent, (favorite_edges, repaired_nodes))."""
+    esrc, edst, x = _c(esrc, np.int32), _c(edst, np.int32), _c(x, np.float64)
+    fc = np.zeros(max(V, 1), np.int32)
+    fp = np.zeros(max(V, 1), np.int32)
+    s2 = np.zeros(2, np.int32)
+    msg = C.create_string_buffer(256)
+    rc = lib().bx_round_extract(V, len(esrc), _ptr(esrc), _ptr(edst), _ptr(x), float(threshold), _ptr(fc),
+                                _ptr(fp), _ptr(s2), msg, 256)
+    _raise(rc, msg.value.decode())
+    return fc[:V], fp[:V], (int(s2[0]), int(s2[1]))
+
+
+def comm_time(cm: CommModel, nbytes: int) -> int:
+    out = C.c_int64()
+    cmc = cm._c()
+    rc = lib().bx_comm_time(C.byref(cmc), int(nbytes), C.byref(out))
+    if rc:
+        raise ValidationError("comm_time: negative byte count")
+    return out.value
+
+
+def max_comm_time(gg: MetaGraph, cm: CommModel) -> int:
+    return max((comm_time(cm, b) for b in gg.ebytes.tolist()), default=0)
+
+
+def device_count() -> int:
+    return lib().bx_device_count()

@@ -1,0 +1,153 @@
+// Device-side data layout shared by the ingest (K1), placer (K2), extract
+// (K3) and simulator (K4) kernels. Everything is int64 microseconds / bytes,
+// so every kernel result is bit-exact with the reference.
+//
+// HBM layout per plan (one cudaMalloc pool, 256-byte aligned sub-arrays):
+//   graph arrays  (read-only, shared by every job on that graph)
+//     k, temp, perm, out, need        int64 [V]
+//     esrc, edst(=out-CSR dst list)   int32 [E]   ascending (src, dst)
+//     ebytes                          int64 [E]
+//     in_off / out_off                int32 [V+1]
+//     in_edge, in_src                 int32 [E]   in-CSR, ascending src
+//     need_order                      int32 [V]   ascending need (min remaining)
+//   prep arrays (per distinct (graph, comm model))
+//     in_c                            int64 [E]   comm_time per in-CSR slot
+//   job workspace (per job)
+//     K, cache                        int64 [V*n] key lower bound / arrival
+//     dead                            uint8 [V*n]
+//     pending, alive, ready, rpos,
+//     cseq, nc                        int32 [V]
+//     finish, urgent                  int64 [V]
+//     scratch tails                   int64/int32 [32*n] per warp lane
+//   job outputs
+//     device_of int32 [V], start int64 [V], exec_order int32 [V],
+//     exec_off int32 [n+1], stats int64 [3], err (status, code, a, b)
+#pragma once
+#include <cstdint>
+
+namespace bx {
+
+constexpr int kOk = 0;
+constexpr int kValidation = 2;
+constexpr int kInfeasible = 3;
+constexpr int kRuntime = 5;
+
+// Device-side error codes; the host formats the reference's message text.
+enum ErrCode : int32_t {
+  E_NONE = 0,
+  E_FITS_NONE = 1,   // "node j fits on no device"              placers.cpp:173-179
+  E_NO_PAIR = 2,     // "no schedulable (node, device) pair..."  placers.cpp:190-192
+  E_CYCLE = 3,       // CycleError from meta_topo_order          transforms.cpp:446-479
+  E_NEG_BYTES = 4,   // "comm_time: negative byte count"         cost_model.cpp:31-33
+  E_TOPO_CAP = 5,    // m-topo cap > smallest capacity           placers.cpp:327-335
+  E_SIM_MEMORY = 6,  // simulator memory violation               simulator.cpp:66-76
+  E_SIM_DEADLOCK = 7,// simulator deadlock                       simulator.cpp:234-246
+  E_SIM_STALL = 8,   // "deadlock: simulation stalled"
+  E_SIM_EXEC = 9,    // "exec_order disagrees with assignments"   simulator.cpp:87-89
+  E_SIM_ONCE = 10,   // "placement must assign every node exactly once" :92-95
+};
+
+struct DErr {
+  int32_t status;
+  int32_t code;
+  int64_t a, b, c, d;
+};
+
+struct DGraph {
+  int32_t V, E;
+  const int64_t *k, *temp, *perm, *outb;
+  const int32_t *esrc, *edst;
+  const int64_t *ebytes;
+  const int32_t *in_off, *in_edge, *out_off;
+  // derived by K1 (graph level)
+  int64_t *need;
+  int32_t *need_order;  // node indices by ascending (need, index)
+  int32_t *iota;        // sort scratch
+  int64_t *need_keys;   // sort scratch
+  int32_t *in_src;
+  int32_t *indeg_left;  // Kahn residue (cycle message)
+  int32_t *flags;       // [0] peeled count, [1] negative-bytes flag
+};
+
+struct DPrep {
+  int32_t graph;
+  double ic, pb;
+  int64_t *in_c;   // [E] comm_time of the in-CSR slot's edge
+  int64_t *cmax;   // max_comm_time (cost_model.cpp:234-240)
+};
+
+struct DJob {
+  int32_t graph, prep, algo, n, mode, skip;
+  const int64_t *cap;
+  const int32_t *fav;
+  // workspace
+  int64_t *K, *cache;
+  uint8_t *dead;
+  int32_t *pending, *alive, *ready, *rpos, *cseq, *nc;
+  int64_t *finish, *urgent;
+  int64_t *sc_val;
+  int32_t *sc_gen;
+  // outputs
+  int32_t *device_of;
+  int64_t *start;
+  int32_t *exec_order, *exec_off;
+  int64_t *stats;
+  DErr *err;
+};
+
+// Simulator job (K4) — reads a placement (device_of / exec lists).
+struct DSim {
+  int32_t graph, n, mode, mem_mode;
+  double ic, pb;
+  const int64_t *cap;
+  const int32_t *device_of, *exec_order, *exec_off;
+  // workspace
+  int64_t *mem, *peak, *xfree;      // [n]
+  int32_t *qpos;                    // [n]
+  uint8_t *busy;                    // [n]
+  int32_t *consumers_left;          // [V]
+  uint8_t *finished, *start_q;      // [V]
+  uint8_t *resident, *sent;         // [V*n]
+  int64_t *heap_t;                  // event heap: time
+  int64_t *heap_k;                  // packed (kind, a, b)
+  int64_t heap_cap;
+  int32_t *seen;                    // [V] validation
+  int64_t *dest_bytes;              // [n]
+  int32_t *dest_cnt;                // [n]
+  // outputs
+  int64_t *start;                   // [V]
+  int64_t *dev3n;                   // [3n] peak, busy, idle
+  int64_t *xfer4;                   // count, bytes, duplicates, cache hits
+  int64_t *makespan;
+  DErr *err;
+};
+
+// K3 arguments (round_and_extract).
+struct XCtx {
+  int V, E;
+  const int32_t *esrc, *edst;
+  const double *x;
+  double thr;
+  unsigned long long *src_min, *dst_min;  // [V] init ~0
+  int32_t *src_peer, *dst_peer;           // [V] init INT_MAX
+  int32_t *cnt_src, *cnt_dst;             // [V] init 0
+  int32_t *best_edge;                     // [V] init -1
+  int32_t *fav_child, *fav_parent;        // [V] init -1
+  int32_t *stats2;                        // [2] init 0
+};
+
+// comm_time with the reference's exact double arithmetic: multiply, then
+// add, each rounded once (no FMA contraction), then floor(v + 0.5).
+__host__ __device__ inline int64_t comm_time_exact(double ic, double pb, int64_t bytes) {
+#ifdef __CUDA_ARCH__
+  double v = __dadd_rn(ic, __dmul_rn(pb, static_cast<double>(bytes)));
+  return static_cast<int64_t>(floor(__dadd_rn(v, 0.5)));
+#else
+  volatile double prod = pb * static_cast<double>(bytes);
+  volatile double sum = ic + prod;
+  volatile double half = sum + 0.5;
+  return static_cast<int64_t>(__builtin_floor(half));
+#endif
+}
+
+}  // namespace bx

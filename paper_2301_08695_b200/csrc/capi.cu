@@ -1,0 +1,915 @@
+// The C ABI (include/baechi_b200.h): plans of device-resident placement
+// problems, their uploads/downloads, kernel launches and the reference's
+// error texts. Host-side C++; the compute is K1-K4 on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/baechi_b200.h"
+#include "bx_device.cuh"
+
+namespace bx {
+void launch_prep(const DGraph &g, const DPrep &pr, bool first, cudaStream_t s);
+void launch_kahn(DGraph *graphs_dev, int32_t *const *queues_dev, int ngraphs, cudaStream_t s);
+cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bit, cudaStream_t s);
+void launch_extract(const XCtx &c, cudaStream_t s);
+void launch_placers(const DJob *jobs, int njobs, const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo,
+                    bool any_list, cudaStream_t s);
+void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, cudaStream_t s);
+}  // namespace bx
+
+using namespace bx;
+
+namespace {
+
+void put_msg(char *msg, int msglen, const std::string &s) {
+  if (msg && msglen > 0) std::snprintf(msg, static_cast<size_t>(msglen), "%s", s.c_str());
+}
+
+std::string fmt(const char *f, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, f);
+  std::vsnprintf(buf, sizeof buf, f, ap);
+  va_end(ap);
+  return buf;
+}
+
+#define BX_CUDA(call, msg, msglen)                                                    \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      put_msg(msg, msglen, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call); \
+      return BX_RUNTIME;                                                              \
+    }                                                                                 \
+  } while (0)
+
+// Bump allocator over one device pool.
+struct Layout {
+  size_t off = 0;
+  template <typename T>
+  size_t take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    size_t at = off;
+    off += std::max<size_t>(count, 1) * sizeof(T);
+    return at;
+  }
+};
+
+template <typename T>
+T *at(void *pool, size_t off) {
+  return reinterpret_cast<T *>(static_cast<char *>(pool) + off);
+}
+
+struct HostCopy {  // one H2D or D2H copy
+  void *dst;
+  const void *src;
+  size_t bytes;
+};
+
+struct Fill {  // one memset
+  void *ptr;
+  int value;
+  size_t bytes;
+};
+
+}  // namespace
+
+struct bx_plan {
+  int device = 0;
+  int ngraphs = 0, njobs = 0, nprep = 0;
+  std::vector<bx_graph> hg;
+  std::vector<bx_job> hj;
+  std::vector<DGraph> dg;
+  std::vector<DPrep> dp;
+  std::vector<DJob> dj;
+  std::vector<int> prep_first;      // prep index -> 1 if first prep of its graph
+  std::vector<int> sort_bits;       // radix bits covering the graph's largest need
+  std::vector<int> sort_launches;   // kernels the need sort issues
+  std::vector<int> host_status;     // per job host-side validation result
+  std::vector<std::string> host_msg;
+  void *pool = nullptr;
+  size_t pool_bytes = 0;
+  DGraph *dg_dev = nullptr;
+  DPrep *dp_dev = nullptr;
+  DJob *dj_dev = nullptr;
+  int32_t **queues_dev = nullptr;
+  void *sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  std::vector<HostCopy> uploads;
+  std::vector<Fill> fills;
+  int maxn = 1;
+  bool any_topo = false, any_list = false;
+  int launches = 0;
+  // simulator
+  void *sim_pool = nullptr;
+  DSim *ds_dev = nullptr;
+  std::vector<DSim> ds;
+  std::vector<Fill> sim_fills;
+  int sim_mem_mode = -1;
+  // external placements (bx_simulate)
+  bool external = false;
+};
+
+extern "C" {
+
+const char *bx_version(void) { return "baechi-b200 0.1 (sm_100a)"; }
+
+int bx_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int bx_comm_time(const bx_comm *cm, int64_t bytes, int64_t *out_us) {
+  if (bytes < 0) return BX_VALIDATION;
+  *out_us = comm_time_exact(cm->intercept_us, cm->us_per_byte, bytes);
+  return BX_OK;
+}
+
+int bx_build_adjacency(int32_t V, int32_t E, const int32_t *esrc, const int32_t *edst, int32_t *in_off,
+                       int32_t *in_edge, int32_t *out_off, char *msg, int msglen) {
+  for (int v = 0; v <= V; ++v) in_off[v] = out_off[v] = 0;
+  for (int e = 0; e < E; ++e) {
+    if (esrc[e] < 0 || esrc[e] >= V || edst[e] < 0 || edst[e] >= V) {
+      put_msg(msg, msglen, fmt("meta edge %d references an unknown node", e));
+      return BX_VALIDATION;
+    }
+    if (e > 0 && (esrc[e] < esrc[e - 1] || (esrc[e] == esrc[e - 1] && edst[e] <= edst[e - 1]))) {
+      put_msg(msg, msglen, "meta edges must be sorted by (src, dst) and unique");
+      return BX_VALIDATION;
+    }
+    in_off[edst[e] + 1]++;
+    out_off[esrc[e] + 1]++;
+  }
+  for (int v = 0; v < V; ++v) {
+    in_off[v + 1] += in_off[v];
+    out_off[v + 1] += out_off[v];
+  }
+  std::vector<int32_t> pos(in_off, in_off + V);
+  for (int e = 0; e < E; ++e) in_edge[pos[edst[e]]++] = e;
+  put_msg(msg, msglen, "");
+  return BX_OK;
+}
+
+void bx_plan_destroy(bx_plan *plan) {
+  if (!plan) return;
+  cudaSetDevice(plan->device);
+  if (plan->pool) cudaFree(plan->pool);
+  if (plan->sim_pool) cudaFree(plan->sim_pool);
+  if (plan->sort_tmp) cudaFree(plan->sort_tmp);
+  delete plan;
+}
+
+int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const bx_job *jobs, int32_t device,
+                   bx_plan **out, char *msg, int msglen) {
+  *out = nullptr;
+  int ndev = bx_device_count();
+  if (ndev <= 0) {
+    put_msg(msg, msglen, "no CUDA device: the B200 placement engine has no CPU fallback");
+    return BX_RUNTIME;
+  }
+  if (device < 0 || device >= ndev) {
+    put_msg(msg, msglen, fmt("CUDA device %d out of range (%d visible)", device, ndev));
+    return BX_RUNTIME;
+  }
+  BX_CUDA(cudaSetDevice(device), msg, msglen);
+  auto *P = new (std::nothrow) bx_plan();
+  if (!P) return BX_RUNTIME;
+  P->device = device;
+  P->ngraphs = ngraphs;
+  P->njobs = njobs;
+  P->hg.assign(graphs, graphs + ngraphs);
+  P->hj.assign(jobs, jobs + njobs);
+  P->host_status.assign(njobs, 0);
+  P->host_msg.assign(njobs, "");
+
+  // prepared graphs: one per distinct (graph, intercept, per_byte)
+  std::map<std::tuple<int, double, double>, int> prep_of;
+  std::vector<int> job_prep(njobs);
+  for (int i = 0; i < njobs; ++i) {
+    const bx_job &J = jobs[i];
+    if (J.graph < 0 || J.graph >= ngraphs) {
+      put_msg(msg, msglen, fmt("job %d names graph %d of %d", i, J.graph, ngraphs));
+      delete P;
+      return BX_VALIDATION;
+    }
+    auto key = std::make_tuple(J.graph, J.cm.intercept_us, J.cm.us_per_byte);
+    auto it = prep_of.find(key);
+    if (it == prep_of.end()) it = prep_of.emplace(key, static_cast<int>(prep_of.size())).first;
+    job_prep[i] = it->second;
+    P->maxn = std::max(P->maxn, J.n);
+  }
+  P->nprep = static_cast<int>(prep_of.size());
+
+  Layout L;
+  struct GOff {
+    size_t k, temp, perm, outb, esrc, edst, ebytes, in_off, in_edge, out_off, need, need_order, iota, need_keys,
+        in_src, indeg_left, flags, queue;
+  };
+  std::vector<GOff> go(ngraphs);
+  size_t max_sort_V = 0;
+  for (int g = 0; g < ngraphs; ++g) {
+    const bx_graph &G = graphs[g];
+    GOff &o = go[g];
+    o.k = L.take<int64_t>(G.V);
+    o.temp = L.take<int64_t>(G.V);
+    o.perm = L.take<int64_t>(G.V);
+    o.outb = L.take<int64_t>(G.V);
+    o.esrc = L.take<int32_t>(G.E);
+    o.edst = L.take<int32_t>(G.E);
+    o.ebytes = L.take<int64_t>(G.E);
+    o.in_off = L.take<int32_t>(G.V + 1);
+    o.in_edge = L.take<int32_t>(G.E);
+    o.out_off = L.take<int32_t>(G.V + 1);
+    o.need = L.take<int64_t>(G.V);
+    o.need_order = L.take<int32_t>(G.V);
+    o.iota = L.take<int32_t>(G.V);
+    o.need_keys = L.take<int64_t>(G.V);
+    o.in_src = L.take<int32_t>(G.E);
+    o.indeg_left = L.take<int32_t>(G.V);
+    o.flags = L.take<int32_t>(4);
+    o.queue = L.take<int32_t>(2 * static_cast<size_t>(G.V));
+    max_sort_V = std::max(max_sort_V, static_cast<size_t>(G.V));
+  }
+  std::vector<std::pair<size_t, size_t>> po(P->nprep);  // in_c, cmax
+  std::vector<int> prep_graph(P->nprep);
+  std::vector<std::pair<double, double>> prep_cm(P->nprep);
+  for (auto &kv : prep_of) {
+    int pi = kv.second;
+    int g = std::get<0>(kv.first);
+    prep_graph[pi] = g;
+    prep_cm[pi] = {std::get<1>(kv.first), std::get<2>(kv.first)};
+    po[pi].first = L.take<int64_t>(graphs[g].E);
+    po[pi].second = L.take<int64_t>(1);
+  }
+  struct JOff {
+    size_t cap, fav, K, cache, dead, pending, alive, ready, rpos, cseq, nc, finish, urgent, scv, scg, device_of,
+        start, exec_order, exec_off, stats, err;
+  };
+  std::vector<JOff> jo(njobs);
+  for (int i = 0; i < njobs; ++i) {
+    const bx_job &J = jobs[i];
+    const int64_t V = graphs[J.graph].V;
+    const int64_t n = std::max(J.n, 1);
+    JOff &o = jo[i];
+    o.cap = L.take<int64_t>(n);
+    o.fav = L.take<int32_t>(V);
+    o.K = L.take<int64_t>(V * n);
+    o.cache = L.take<int64_t>(V * n);
+    o.dead = L.take<uint8_t>(V * n);
+    o.pending = L.take<int32_t>(V);
+    o.alive = L.take<int32_t>(V);
+    o.ready = L.take<int32_t>(V);
+    o.rpos = L.take<int32_t>(V);
+    o.cseq = L.take<int32_t>(V);
+    o.nc = L.take<int32_t>(V);
+    o.finish = L.take<int64_t>(V);
+    o.urgent = L.take<int64_t>(V);
+    o.scv = L.take<int64_t>(32 * n);
+    o.scg = L.take<int32_t>(32 * n);
+    o.device_of = L.take<int32_t>(V);
+    o.start = L.take<int64_t>(V);
+    o.exec_order = L.take<int32_t>(V);
+    o.exec_off = L.take<int32_t>(n + 1);
+    o.stats = L.take<int64_t>(3);
+    o.err = L.take<DErr>(1);
+  }
+  size_t tables = L.take<DGraph>(ngraphs);
+  size_t ptables = L.take<DPrep>(P->nprep);
+  size_t jtables = L.take<DJob>(njobs);
+  size_t qtables = L.take<int32_t *>(ngraphs);
+  P->pool_bytes = L.off;
+  cudaError_t ce = cudaMalloc(&P->pool, P->pool_bytes);
+  if (ce != cudaSuccess) {
+    put_msg(msg, msglen, fmt("cudaMalloc of %zu bytes failed: %s", P->pool_bytes, cudaGetErrorString(ce)));
+    delete P;
+    return BX_RUNTIME;
+  }
+  void *pool = P->pool;
+
+  P->dg.resize(ngraphs);
+  std::vector<int32_t *> queues(ngraphs);
+  for (int g = 0; g < ngraphs; ++g) {
+    const bx_graph &G = graphs[g];
+    const GOff &o = go[g];
+    DGraph &d = P->dg[g];
+    d.V = G.V;
+    d.E = G.E;
+    d.k = at<int64_t>(pool, o.k);
+    d.temp = at<int64_t>(pool, o.temp);
+    d.perm = at<int64_t>(pool, o.perm);
+    d.outb = at<int64_t>(pool, o.outb);
+    d.esrc = at<int32_t>(pool, o.esrc);
+    d.edst = at<int32_t>(pool, o.edst);
+    d.ebytes = at<int64_t>(pool, o.ebytes);
+    d.in_off = at<int32_t>(pool, o.in_off);
+    d.in_edge = at<int32_t>(pool, o.in_edge);
+    d.out_off = at<int32_t>(pool, o.out_off);
+    d.need = at<int64_t>(pool, o.need);
+    d.need_order = at<int32_t>(pool, o.need_order);
+    d.iota = at<int32_t>(pool, o.iota);
+    d.need_keys = at<int64_t>(pool, o.need_keys);
+    d.in_src = at<int32_t>(pool, o.in_src);
+    d.indeg_left = at<int32_t>(pool, o.indeg_left);
+    d.flags = at<int32_t>(pool, o.flags);
+    queues[g] = at<int32_t>(pool, o.queue);
+    auto up = [&](const void *dev, const void *host, size_t bytes) {
+      if (bytes) P->uploads.push_back({const_cast<void *>(dev), host, bytes});
+    };
+    up(d.k, G.compute_us, 8 * size_t(G.V));
+    up(d.temp, G.temp_bytes, 8 * size_t(G.V));
+    up(d.perm, G.perm_bytes, 8 * size_t(G.V));
+    up(d.outb, G.out_bytes, 8 * size_t(G.V));
+    up(d.esrc, G.esrc, 4 * size_t(G.E));
+    up(d.edst, G.edst, 4 * size_t(G.E));
+    up(d.ebytes, G.tensor_bytes, 8 * size_t(G.E));
+    up(d.in_off, G.in_off, 4 * size_t(G.V + 1));
+    up(d.in_edge, G.in_edge, 4 * size_t(G.E));
+    up(d.out_off, G.out_off, 4 * size_t(G.V + 1));
+    P->fills.push_back({d.flags, 0, 16});
+    // largest need bounds the radix bits (needs are non-negative after
+    // make_graph validation; a negative field keeps all 64 bits)
+    int64_t mx = 0;
+    bool neg = false;
+    for (int j = 0; j < G.V; ++j) {
+      int64_t v = G.perm_bytes[j] + G.out_bytes[j] + G.temp_bytes[j];
+      if (v < 0) neg = true;
+      mx = std::max(mx, v);
+    }
+    int bits = 1;
+    while (bits < 63 && (int64_t(1) << bits) <= mx) ++bits;
+    if (neg) bits = 64;
+    P->sort_bits.push_back(bits);
+    // onesweep: histogram + exclusive sum + one pass per 8-bit digit;
+    // small inputs take the single-tile path
+    P->sort_launches.push_back(G.V <= 3072 ? 1 : 2 + (bits + 7) / 8);
+  }
+  P->dp.resize(P->nprep);
+  P->prep_first.assign(P->nprep, 0);
+  std::vector<char> graph_seen(ngraphs, 0);
+  for (int pi = 0; pi < P->nprep; ++pi) {
+    DPrep &d = P->dp[pi];
+    d.graph = prep_graph[pi];
+    d.ic = prep_cm[pi].first;
+    d.pb = prep_cm[pi].second;
+    d.in_c = at<int64_t>(pool, po[pi].first);
+    d.cmax = at<int64_t>(pool, po[pi].second);
+    P->fills.push_back({d.cmax, 0, 8});
+    if (!graph_seen[d.graph]) {
+      graph_seen[d.graph] = 1;
+      P->prep_first[pi] = 1;
+    }
+  }
+  P->dj.resize(njobs);
+  for (int i = 0; i < njobs; ++i) {
+    const bx_job &J = jobs[i];
+    const bx_graph &G = graphs[J.graph];
+    const JOff &o = jo[i];
+    DJob &d = P->dj[i];
+    const int64_t V = G.V, n = std::max(J.n, 1);
+    d.graph = J.graph;
+    d.prep = job_prep[i];
+    d.algo = J.algo;
+    d.n = J.n;
+    d.mode = J.cm.mode == BX_COMM_PARALLEL ? 1 : 0;
+    d.skip = 0;
+    d.cap = at<int64_t>(pool, o.cap);
+    d.fav = nullptr;
+    d.K = at<int64_t>(pool, o.K);
+    d.cache = at<int64_t>(pool, o.cache);
+    d.dead = at<uint8_t>(pool, o.dead);
+    d.pending = at<int32_t>(pool, o.pending);
+    d.alive = at<int32_t>(pool, o.alive);
+    d.ready = at<int32_t>(pool, o.ready);
+    d.rpos = at<int32_t>(pool, o.rpos);
+    d.cseq = at<int32_t>(pool, o.cseq);
+    d.nc = at<int32_t>(pool, o.nc);
+    d.finish = at<int64_t>(pool, o.finish);
+    d.urgent = at<int64_t>(pool, o.urgent);
+    d.sc_val = at<int64_t>(pool, o.scv);
+    d.sc_gen = at<int32_t>(pool, o.scg);
+    d.device_of = at<int32_t>(pool, o.device_of);
+    d.start = at<int64_t>(pool, o.start);
+    d.exec_order = at<int32_t>(pool, o.exec_order);
+    d.exec_off = at<int32_t>(pool, o.exec_off);
+    d.stats = at<int64_t>(pool, o.stats);
+    d.err = at<DErr>(pool, o.err);
+    // host-side validation in the reference's order
+    std::string why;
+    int st = 0;
+    if (J.algo == BX_ALGO_MSCT && J.fav_child && J.fav_len != 0 && J.fav_len != G.V) {
+      st = BX_VALIDATION;
+      why = "favorite map does not match graph size";  // placers.cpp:306-309
+    } else if (J.n <= 0) {
+      st = BX_VALIDATION;
+      why = "device roster is empty";  // placers.cpp:20-22
+    } else {
+      for (int x = 0; x < J.n; ++x)
+        if (J.capacity[x] <= 0) {
+          st = BX_VALIDATION;
+          why = "device capacities must be positive";  // placers.cpp:25-27
+        }
+    }
+    if (J.algo < 0 || J.algo > 2) {
+      st = BX_VALIDATION;
+      why = "unknown placement algorithm";
+    }
+    P->host_status[i] = st;
+    P->host_msg[i] = why;
+    d.skip = st != 0;
+    if (J.n > 0) P->uploads.push_back({const_cast<int64_t *>(d.cap), J.capacity, 8 * size_t(J.n)});
+    if (!d.skip) {
+      if (J.algo == BX_ALGO_MSCT && J.fav_child && J.fav_len == G.V && G.V > 0) {
+        d.fav = at<int32_t>(pool, o.fav);
+        P->uploads.push_back({const_cast<int32_t *>(d.fav), J.fav_child, 4 * size_t(V)});
+      }
+      if (J.algo == BX_ALGO_MTOPO) P->any_topo = true;
+      else P->any_list = true;
+    }
+    P->fills.push_back({d.cache, 0xff, 8 * size_t(V * n)});
+    P->fills.push_back({d.dead, 0, size_t(V * n)});
+    P->fills.push_back({d.sc_gen, 0, 4 * size_t(32 * n)});
+    P->fills.push_back({d.err, 0, sizeof(DErr)});
+  }
+  P->dg_dev = at<DGraph>(pool, tables);
+  P->dp_dev = at<DPrep>(pool, ptables);
+  P->dj_dev = at<DJob>(pool, jtables);
+  P->queues_dev = at<int32_t *>(pool, qtables);
+  // descriptor tables are static: copy once
+  BX_CUDA(cudaMemcpy(P->dg_dev, P->dg.data(), sizeof(DGraph) * ngraphs, cudaMemcpyHostToDevice), msg, msglen);
+  BX_CUDA(cudaMemcpy(P->dp_dev, P->dp.data(), sizeof(DPrep) * P->nprep, cudaMemcpyHostToDevice), msg, msglen);
+  BX_CUDA(cudaMemcpy(P->dj_dev, P->dj.data(), sizeof(DJob) * njobs, cudaMemcpyHostToDevice), msg, msglen);
+  BX_CUDA(cudaMemcpy(P->queues_dev, queues.data(), sizeof(int32_t *) * ngraphs, cudaMemcpyHostToDevice), msg,
+          msglen);
+  // radix-sort scratch sized for the largest graph
+  {
+    DGraph probe = {};
+    probe.V = static_cast<int32_t>(max_sort_V);
+    size_t bytes = 0;
+    sort_needs(nullptr, bytes, probe, 64, nullptr);
+    P->sort_tmp_bytes = std::max<size_t>(bytes, 256);
+    BX_CUDA(cudaMalloc(&P->sort_tmp, P->sort_tmp_bytes), msg, msglen);
+  }
+  *out = P;
+  put_msg(msg, msglen, "");
+  return BX_OK;
+}
+
+int bx_plan_upload(bx_plan *P, void *stream) {
+  cudaSetDevice(P->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (const HostCopy &c : P->uploads) {
+    if (cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return BX_RUNTIME;
+  }
+  return BX_OK;
+}
+
+int bx_plan_place(bx_plan *P, void *stream) {
+  cudaSetDevice(P->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  P->launches = 0;
+  for (const Fill &f : P->fills)
+    if (cudaMemsetAsync(f.ptr, f.value, f.bytes, s) != cudaSuccess) return BX_RUNTIME;
+  for (int pi = 0; pi < P->nprep; ++pi) {
+    const DGraph &g = P->dg[P->dp[pi].graph];
+    launch_prep(g, P->dp[pi], P->prep_first[pi] != 0, s);
+    P->launches += (P->prep_first[pi] && g.V > 0 ? 1 : 0) + (g.E > 0 ? 1 : 0);
+  }
+  for (int g = 0; g < P->ngraphs; ++g) {
+    if (P->dg[g].V == 0) continue;
+    size_t bytes = P->sort_tmp_bytes;
+    if (sort_needs(P->sort_tmp, bytes, P->dg[g], P->sort_bits[g], s) != cudaSuccess) return BX_RUNTIME;
+    P->launches += P->sort_launches[g];
+  }
+  launch_kahn(P->dg_dev, P->queues_dev, P->ngraphs, s);
+  P->launches += 1;
+  launch_placers(P->dj_dev, P->njobs, P->dg_dev, P->dp_dev, P->maxn, P->any_topo, P->any_list, s);
+  P->launches += (P->any_topo ? 1 : 0) + (P->any_list ? 1 : 0);
+  return cudaGetLastError() == cudaSuccess ? BX_OK : BX_RUNTIME;
+}
+
+int bx_plan_launch_count(const bx_plan *P) { return P->launches; }
+
+static std::string cycle_message(const bx_plan *P, int g, cudaStream_t s) {
+  const bx_graph &G = P->hg[g];
+  std::vector<int32_t> left(G.V);
+  cudaMemcpyAsync(left.data(), P->dg[g].indeg_left, 4 * size_t(G.V), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  std::string m = "meta graph is cyclic; groups of base node ids {";
+  bool first = true;
+  for (int i = 0; i < G.V; ++i) {
+    if (left[i] > 0) {
+      long long id = G.first_id ? static_cast<long long>(G.first_id[i]) : i;
+      m += (first ? "" : ", ") + std::to_string(id);
+      first = false;
+    }
+  }
+  return m + "} remain";
+}
+
+int bx_plan_download(bx_plan *P, void *stream, bx_placement *out) {
+  cudaSetDevice(P->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<DErr> errs(P->njobs);
+  std::vector<int64_t> stats(3 * static_cast<size_t>(P->njobs));
+  for (int i = 0; i < P->njobs; ++i) {
+    const DJob &d = P->dj[i];
+    const int V = P->hg[d.graph].V;
+    if (cudaMemcpyAsync(&errs[i], d.err, sizeof(DErr), cudaMemcpyDeviceToHost, s) != cudaSuccess) return BX_RUNTIME;
+    if (d.skip) continue;
+    cudaMemcpyAsync(&stats[3 * i], d.stats, 24, cudaMemcpyDeviceToHost, s);
+    if (V > 0) {
+      cudaMemcpyAsync(out[i].device_of, d.device_of, 4 * size_t(V), cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(out[i].start_us, d.start, 8 * size_t(V), cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(out[i].exec_order, d.exec_order, 4 * size_t(V), cudaMemcpyDeviceToHost, s);
+    }
+    cudaMemcpyAsync(out[i].exec_off, d.exec_off, 4 * size_t(d.n + 1), cudaMemcpyDeviceToHost, s);
+  }
+  cudaError_t ce = cudaStreamSynchronize(s);
+  if (ce != cudaSuccess) {
+    for (int i = 0; i < P->njobs; ++i) {
+      out[i].status = BX_RUNTIME;
+      put_msg(out[i].msg, sizeof out[i].msg, std::string("CUDA error: ") + cudaGetErrorString(ce));
+    }
+    return BX_RUNTIME;
+  }
+  for (int i = 0; i < P->njobs; ++i) {
+    const DJob &d = P->dj[i];
+    bx_placement &o = out[i];
+    o.stats[0] = o.stats[1] = o.stats[2] = 0;
+    if (d.skip) {
+      o.status = P->host_status[i];
+      put_msg(o.msg, sizeof o.msg, P->host_msg[i]);
+      continue;
+    }
+    const DErr &e = errs[i];
+    o.status = e.status;
+    std::string m;
+    switch (e.code) {
+      case E_NONE:
+        break;
+      case E_FITS_NONE:
+        m = "node " + std::to_string(e.a) + " fits on no device";
+        break;
+      case E_NO_PAIR:
+        m = "no schedulable (node, device) pair remains";
+        break;
+      case E_CYCLE:
+        m = cycle_message(P, d.graph, s);
+        break;
+      case E_NEG_BYTES:
+        m = "comm_time: negative byte count";
+        break;
+      case E_TOPO_CAP:
+        m = "m-topo per-device cap " + std::to_string(e.a) + " bytes exceeds the smallest device capacity " +
+            std::to_string(e.b) + "; use m-etf or m-sct for tight memory limits";
+        break;
+      default:
+        m = "internal error code " + std::to_string(e.code);
+        o.status = BX_RUNTIME;
+    }
+    put_msg(o.msg, sizeof o.msg, m);
+    if (o.status == 0) {
+      o.stats[0] = stats[3 * i];
+      o.stats[1] = stats[3 * i + 1];
+      o.stats[2] = stats[3 * i + 2];
+    }
+  }
+  return BX_OK;
+}
+
+// ---- simulator -----------------------------------------------------------
+static int sim_setup(bx_plan *P, char *msg, int msglen) {
+  if (P->sim_pool) return BX_OK;
+  Layout L;
+  struct SOff {
+    size_t mem, peak, xfree, qpos, busy, cl, fin, sq, res, sent, ht, hk, seen, db, dc, start, dev3n, xfer4, mk, err;
+  };
+  std::vector<SOff> so(P->njobs);
+  for (int i = 0; i < P->njobs; ++i) {
+    const bx_graph &G = P->hg[P->dj[i].graph];
+    const int64_t V = G.V, E = G.E, n = std::max(P->dj[i].n, 1);
+    SOff &o = so[i];
+    o.mem = L.take<int64_t>(n);
+    o.peak = L.take<int64_t>(n);
+    o.xfree = L.take<int64_t>(n);
+    o.qpos = L.take<int32_t>(n);
+    o.busy = L.take<uint8_t>(n);
+    o.cl = L.take<int32_t>(V);
+    o.fin = L.take<uint8_t>(V);
+    o.sq = L.take<uint8_t>(V);
+    o.res = L.take<uint8_t>(V * n);
+    o.sent = L.take<uint8_t>(V * n);
+    o.ht = L.take<int64_t>(2 * n + E + 16);
+    o.hk = L.take<int64_t>(2 * n + E + 16);
+    o.seen = L.take<int32_t>(V);
+    o.db = L.take<int64_t>(n);
+    o.dc = L.take<int32_t>(n);
+    o.start = L.take<int64_t>(V);
+    o.dev3n = L.take<int64_t>(3 * n);
+    o.xfer4 = L.take<int64_t>(4);
+    o.mk = L.take<int64_t>(1);
+    o.err = L.take<DErr>(1);
+  }
+  size_t tab = L.take<DSim>(P->njobs);
+  BX_CUDA(cudaMalloc(&P->sim_pool, L.off), msg, msglen);
+  void *pool = P->sim_pool;
+  P->ds.resize(P->njobs);
+  for (int i = 0; i < P->njobs; ++i) {
+    const DJob &j = P->dj[i];
+    const bx_job &J = P->hj[i];
+    const bx_graph &G = P->hg[j.graph];
+    const SOff &o = so[i];
+    DSim &d = P->ds[i];
+    const int64_t V = G.V, E = G.E, n = std::max(j.n, 1);
+    d.graph = j.graph;
+    d.n = j.n;
+    d.mode = j.mode;
+    d.ic = J.cm.intercept_us;
+    d.pb = J.cm.us_per_byte;
+    d.cap = j.cap;
+    d.device_of = j.device_of;
+    d.exec_order = j.exec_order;
+    d.exec_off = j.exec_off;
+    d.mem = at<int64_t>(pool, o.mem);
+    d.peak = at<int64_t>(pool, o.peak);
+    d.xfree = at<int64_t>(pool, o.xfree);
+    d.qpos = at<int32_t>(pool, o.qpos);
+    d.busy = at<uint8_t>(pool, o.busy);
+    d.consumers_left = at<int32_t>(pool, o.cl);
+    d.finished = at<uint8_t>(pool, o.fin);
+    d.start_q = at<uint8_t>(pool, o.sq);
+    d.resident = at<uint8_t>(pool, o.res);
+    d.sent = at<uint8_t>(pool, o.sent);
+    d.heap_t = at<int64_t>(pool, o.ht);
+    d.heap_k = at<int64_t>(pool, o.hk);
+    d.heap_cap = 2 * n + E + 16;
+    d.seen = at<int32_t>(pool, o.seen);
+    d.dest_bytes = at<int64_t>(pool, o.db);
+    d.dest_cnt = at<int32_t>(pool, o.dc);
+    d.start = at<int64_t>(pool, o.start);
+    d.dev3n = at<int64_t>(pool, o.dev3n);
+    d.xfer4 = at<int64_t>(pool, o.xfer4);
+    d.makespan = at<int64_t>(pool, o.mk);
+    d.err = at<DErr>(pool, o.err);
+    P->sim_fills.push_back({d.resident, 0, size_t(V * n)});
+    P->sim_fills.push_back({d.sent, 0, size_t(V * n)});
+    P->sim_fills.push_back({d.err, 0, sizeof(DErr)});
+  }
+  P->ds_dev = at<DSim>(pool, tab);
+  BX_CUDA(cudaMemcpy(P->ds_dev, P->ds.data(), sizeof(DSim) * P->njobs, cudaMemcpyHostToDevice), msg, msglen);
+  return BX_OK;
+}
+
+int bx_plan_simulate(bx_plan *P, int32_t mem_mode, void *stream) {
+  cudaSetDevice(P->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char msg[256];
+  int rc = sim_setup(P, msg, sizeof msg);
+  if (rc) return rc;
+  if (P->sim_mem_mode != mem_mode) {
+    for (auto &d : P->ds) d.mem_mode = mem_mode;
+    if (cudaMemcpy(P->ds_dev, P->ds.data(), sizeof(DSim) * P->njobs, cudaMemcpyHostToDevice) != cudaSuccess)
+      return BX_RUNTIME;
+    P->sim_mem_mode = mem_mode;
+  }
+  for (const Fill &f : P->sim_fills)
+    if (cudaMemsetAsync(f.ptr, f.value, f.bytes, s) != cudaSuccess) return BX_RUNTIME;
+  launch_simulate(P->ds_dev, P->njobs, P->dg_dev, s);
+  return cudaGetLastError() == cudaSuccess ? BX_OK : BX_RUNTIME;
+}
+
+int bx_plan_sim_download(bx_plan *P, void *stream, bx_sim_report *out) {
+  cudaSetDevice(P->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!P->sim_pool) return BX_RUNTIME;
+  std::vector<DErr> errs(P->njobs);
+  std::vector<int64_t> dev3n, x4(4 * static_cast<size_t>(P->njobs)), mk(P->njobs);
+  std::vector<std::vector<int64_t>> d3(P->njobs);
+  for (int i = 0; i < P->njobs; ++i) {
+    const DSim &d = P->ds[i];
+    const int V = P->hg[d.graph].V;
+    d3[i].resize(3 * static_cast<size_t>(std::max(d.n, 1)));
+    cudaMemcpyAsync(&errs[i], d.err, sizeof(DErr), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&x4[4 * i], d.xfer4, 32, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&mk[i], d.makespan, 8, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(d3[i].data(), d.dev3n, 8 * d3[i].size(), cudaMemcpyDeviceToHost, s);
+    if (V > 0) cudaMemcpyAsync(out[i].start_us, d.start, 8 * size_t(V), cudaMemcpyDeviceToHost, s);
+  }
+  if (cudaStreamSynchronize(s) != cudaSuccess) return BX_RUNTIME;
+  for (int i = 0; i < P->njobs; ++i) {
+    const DSim &d = P->ds[i];
+    const bx_graph &G = P->hg[d.graph];
+    bx_sim_report &o = out[i];
+    const DErr &e = errs[i];
+    o.status = e.status;
+    auto id_of = [&](int64_t meta) -> long long {
+      return G.first_id ? static_cast<long long>(G.first_id[meta]) : static_cast<long long>(meta);
+    };
+    std::string m;
+    switch (e.code) {
+      case E_NONE:
+        break;
+      case E_SIM_MEMORY:
+        m = "memory violation on device " + std::to_string(e.a) + " at t=" + std::to_string(e.b) +
+            "us while holding node " + std::to_string(id_of(e.c)) + ": " + std::to_string(e.d) + " > " +
+            std::to_string(P->hj[i].capacity[e.a]);
+        break;
+      case E_SIM_DEADLOCK:
+        m = "deadlock: device " + std::to_string(e.a) + " waits forever for inputs of node " +
+            std::to_string(id_of(e.c)) + "; exec_order contradicts the DAG";
+        break;
+      case E_SIM_STALL:
+        m = "deadlock: simulation stalled";
+        break;
+      case E_SIM_EXEC:
+        m = "exec_order disagrees with assignments";
+        break;
+      case E_SIM_ONCE:
+        m = "placement must assign every node exactly once";
+        break;
+      default:
+        m = "internal error code " + std::to_string(e.code);
+        o.status = BX_RUNTIME;
+    }
+    put_msg(o.msg, sizeof o.msg, m);
+    o.makespan_us = mk[i];
+    o.transfer_count = x4[4 * i];
+    o.transfer_bytes = x4[4 * i + 1];
+    o.duplicate_transfers = x4[4 * i + 2];
+    o.cache_hits = x4[4 * i + 3];
+    for (int dv = 0; dv < d.n; ++dv) {
+      o.peak_bytes[dv] = d3[i][3 * dv];
+      o.busy_us[dv] = d3[i][3 * dv + 1];
+      o.idle_us[dv] = d3[i][3 * dv + 2];
+    }
+  }
+  return BX_OK;
+}
+
+// ---- one-shot entry points ----------------------------------------------
+int bx_place(const bx_graph *graph, const bx_job *job, bx_placement *out) {
+  bx_job j = *job;
+  j.graph = 0;
+  bx_plan *P = nullptr;
+  int rc = bx_plan_create(1, graph, 1, &j, 0, &P, out->msg, sizeof out->msg);
+  if (rc) {
+    out->status = rc;
+    return rc;
+  }
+  rc = bx_plan_upload(P, nullptr);
+  if (!rc) rc = bx_plan_place(P, nullptr);
+  if (!rc) rc = bx_plan_download(P, nullptr, out);
+  if (rc) {
+    out->status = rc;
+    put_msg(out->msg, sizeof out->msg, std::string("CUDA error: ") + cudaGetErrorString(cudaGetLastError()));
+  }
+  bx_plan_destroy(P);
+  return rc ? rc : out->status;
+}
+
+int bx_simulate(const bx_graph *graph, int32_t n, const int64_t *capacity, const bx_comm *cm, int32_t mem_mode,
+                const int32_t *device_of, const int32_t *exec_order, const int32_t *exec_off, bx_sim_report *out) {
+  if (n <= 0) {
+    out->status = BX_VALIDATION;
+    put_msg(out->msg, sizeof out->msg, "placement does not match graph or roster");
+    return BX_VALIDATION;
+  }
+  // a job that is never placed: its placement arrays are filled from the host
+  bx_job j = {};
+  j.graph = 0;
+  j.algo = BX_ALGO_METF;
+  j.n = n;
+  j.capacity = capacity;
+  j.cm = *cm;
+  bx_plan *P = nullptr;
+  int rc = bx_plan_create(1, graph, 1, &j, 0, &P, out->msg, sizeof out->msg);
+  if (rc) {
+    out->status = rc;
+    return rc;
+  }
+  const DJob &d = P->dj[0];
+  const int V = graph->V;
+  int total = exec_off[n] - exec_off[0];
+  if (exec_off[0] != 0 || total != V) {
+    // lists that cannot hold every node exactly once never reach the device
+    // buffers (sized V); the verdict is validate_placement's own
+    // (simulator.cpp:78-97), decided by its first failing check
+    bx_plan_destroy(P);
+    out->status = BX_VALIDATION;
+    const char *why = "placement must assign every node exactly once";
+    for (int dv = 0; dv < n; ++dv)
+      for (int x = exec_off[dv]; x < exec_off[dv + 1]; ++x) {
+        int m = exec_order[x];
+        if (m < 0 || m >= V || device_of[m] != dv) why = "exec_order disagrees with assignments";
+      }
+    put_msg(out->msg, sizeof out->msg, why);
+    return out->status;
+  }
+  rc = bx_plan_upload(P, nullptr);
+  if (!rc && V > 0) {
+    cudaMemcpy(d.device_of, device_of, 4 * size_t(V), cudaMemcpyHostToDevice);
+    cudaMemcpy(d.exec_order, exec_order, 4 * size_t(V), cudaMemcpyHostToDevice);
+  }
+  if (!rc) cudaMemcpy(d.exec_off, exec_off, 4 * size_t(n + 1), cudaMemcpyHostToDevice);
+  if (!rc) rc = bx_plan_simulate(P, mem_mode, nullptr);
+  if (!rc) rc = bx_plan_sim_download(P, nullptr, out);
+  if (rc) {
+    out->status = rc;
+    put_msg(out->msg, sizeof out->msg, "CUDA failure in bx_simulate");
+  }
+  bx_plan_destroy(P);
+  return rc ? rc : out->status;
+}
+
+int bx_round_extract(int32_t V, int32_t E, const int32_t *esrc, const int32_t *edst, const double *x,
+                     double threshold, int32_t *fav_child, int32_t *fav_parent, int32_t *stats2, char *msg,
+                     int msglen) {
+  if (threshold <= 0 || threshold >= 0.5) {  // lp.cpp:282-284
+    put_msg(msg, msglen, "rounding threshold must lie in (0, 0.5)");
+    return BX_VALIDATION;
+  }
+  if (bx_device_count() <= 0) {
+    put_msg(msg, msglen, "no CUDA device: the B200 placement engine has no CPU fallback");
+    return BX_RUNTIME;
+  }
+  for (int e = 0; e < E; ++e)
+    if (esrc[e] < 0 || esrc[e] >= V || edst[e] < 0 || edst[e] >= V) {
+      put_msg(msg, msglen, "edge endpoint outside the graph");
+      return BX_VALIDATION;
+    }
+  Layout L;
+  size_t o_src = L.take<int32_t>(E), o_dst = L.take<int32_t>(E), o_x = L.take<double>(E);
+  size_t o_smin = L.take<unsigned long long>(V), o_dmin = L.take<unsigned long long>(V);
+  size_t o_speer = L.take<int32_t>(V), o_dpeer = L.take<int32_t>(V);
+  size_t o_cs = L.take<int32_t>(V), o_cd = L.take<int32_t>(V), o_best = L.take<int32_t>(V);
+  size_t o_fc = L.take<int32_t>(V), o_fp = L.take<int32_t>(V), o_st = L.take<int32_t>(2);
+  void *pool = nullptr;
+  BX_CUDA(cudaMalloc(&pool, L.off), msg, msglen);
+  XCtx c;
+  c.V = V;
+  c.E = E;
+  c.esrc = at<int32_t>(pool, o_src);
+  c.edst = at<int32_t>(pool, o_dst);
+  c.x = at<double>(pool, o_x);
+  c.thr = threshold;
+  c.src_min = at<unsigned long long>(pool, o_smin);
+  c.dst_min = at<unsigned long long>(pool, o_dmin);
+  c.src_peer = at<int32_t>(pool, o_speer);
+  c.dst_peer = at<int32_t>(pool, o_dpeer);
+  c.cnt_src = at<int32_t>(pool, o_cs);
+  c.cnt_dst = at<int32_t>(pool, o_cd);
+  c.best_edge = at<int32_t>(pool, o_best);
+  c.fav_child = at<int32_t>(pool, o_fc);
+  c.fav_parent = at<int32_t>(pool, o_fp);
+  c.stats2 = at<int32_t>(pool, o_st);
+  cudaError_t ce = cudaSuccess;
+  auto chk = [&](cudaError_t e) {
+    if (ce == cudaSuccess) ce = e;
+  };
+  if (E > 0) {
+    chk(cudaMemcpy(const_cast<int32_t *>(c.esrc), esrc, 4 * size_t(E), cudaMemcpyHostToDevice));
+    chk(cudaMemcpy(const_cast<int32_t *>(c.edst), edst, 4 * size_t(E), cudaMemcpyHostToDevice));
+    chk(cudaMemcpy(const_cast<double *>(c.x), x, 8 * size_t(E), cudaMemcpyHostToDevice));
+  }
+  chk(cudaMemset(c.src_min, 0xff, 8 * size_t(V)));
+  chk(cudaMemset(c.dst_min, 0xff, 8 * size_t(V)));
+  chk(cudaMemset(c.src_peer, 0x7f, 4 * size_t(V)));
+  chk(cudaMemset(c.dst_peer, 0x7f, 4 * size_t(V)));
+  chk(cudaMemset(c.cnt_src, 0, 4 * size_t(V)));
+  chk(cudaMemset(c.cnt_dst, 0, 4 * size_t(V)));
+  chk(cudaMemset(c.best_edge, 0xff, 4 * size_t(V)));
+  chk(cudaMemset(c.fav_child, 0xff, 4 * size_t(V)));
+  chk(cudaMemset(c.fav_parent, 0xff, 4 * size_t(V)));
+  chk(cudaMemset(c.stats2, 0, 8));
+  if (ce == cudaSuccess && V > 0) {
+    launch_extract(c, nullptr);
+    chk(cudaGetLastError());
+  }
+  if (V > 0) {
+    chk(cudaMemcpy(fav_child, c.fav_child, 4 * size_t(V), cudaMemcpyDeviceToHost));
+    chk(cudaMemcpy(fav_parent, c.fav_parent, 4 * size_t(V), cudaMemcpyDeviceToHost));
+  }
+  chk(cudaMemcpy(stats2, c.stats2, 8, cudaMemcpyDeviceToHost));
+  cudaFree(pool);
+  if (ce != cudaSuccess) {
+    put_msg(msg, msglen, std::string("CUDA error: ") + cudaGetErrorString(ce));
+    return BX_RUNTIME;
+  }
+  put_msg(msg, msglen, "");
+  return BX_OK;
+}
+
+}  // extern "C"
