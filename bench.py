@@ -1,0 +1,333 @@
+"""Benchmark: batched m-ETF placements/sec on the C5 sweep (BASELINE.json
+configs[4]), plus the reference CPU placer timed on this box's host cores.
+
+python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+
+One process per GPU (torchrun for N > 1). Every rank places its own
+4096-problem sweep shard (64 graphs x {2,4,8,16} devices x 16 memory caps,
+graph seeds offset by rank), so per-GPU work is fixed as N grows ("weak").
+A "step" is one pass of the placement engine over the whole shard.
+`value` is device-resident (inputs already in HBM); `e2e` re-uploads every
+input from pinned host memory and downloads every placement each step
+through the C ABI (bx_plan_upload / bx_plan_place / bx_plan_download).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "batched placements/sec"
+UNIT = "placements/s"
+PEAKS = os.path.join(HERE, "MEASURED_PEAKS.json")
+NCU_SUMMARY = os.path.join(HERE, "profiles", "ncu_placer_summary.json")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_bytes(graphs, jobs):
+    """B = 40 V + 16 E per placement (m-ETF)."""
+    return sum(40 * graphs[g]["V"] + 16 * len(graphs[g]["esrc"]) for g, _, _ in jobs)
+
+
+def cpu_reference(graphs, jobs, sample_idx, threads, steps=1):
+    """The reference placer (oracle/_ref, the unmodified reference sources)
+    over `sample_idx` with the reference's own OpenMP sweep pattern
+    (proj/src/bench.cpp:121). Returns (placements/s per step list, statuses,
+    checksums, kind)."""
+    from oracle import Ref
+    from paper_2301_08695_b200 import workloads as W
+    if not Ref.available():
+        raise RuntimeError("oracle/_ref/libdagsched_ref.so missing (build with make -C oracle)")
+    used = sorted({jobs[i][0] for i in sample_idx})
+    rg = {g: Ref.graph(W.as_ref_base(graphs[g]), -1) for g in used}
+    maxn = max(jobs[i][1] for i in sample_idx)
+    caps = np.zeros((len(sample_idx), maxn), np.int64)
+    for r, i in enumerate(sample_idx):
+        caps[r, :jobs[i][1]] = jobs[i][2]
+    gl = [rg[jobs[i][0]] for i in sample_idx]
+    algos = np.ones(len(sample_idx), np.int32)
+    ns = np.array([jobs[i][1] for i in sample_idx], np.int32)
+    rates, st, chk = [], None, None
+    for _ in range(steps):
+        st, chk, wall_ns = Ref.place_batch(gl, algos, ns, caps, W.COMM_TEST, threads)
+        rates.append(len(sample_idx) / (wall_ns / 1e9))
+    return rates, st, chk
+
+
+def sample_indices(jobs, count):
+    stride = max(1, len(jobs) // count)
+    return list(range(0, len(jobs), stride))[:count]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--graphs", type=int, default=64)
+    ap.add_argument("--cpu-sample", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2301_08695_b200 import workloads as W
+
+    config = {"workload": "C5 batched sweep: 64 graphs (layered/grid/branchy/wide, V 1k-20k) x "
+                          "{2,4,8,16} devices x 16 caps (1.05+k*0.0633), m-ETF, comm_model_test.json "
+                          "(12.5us + 0.002us/B, parallel)",
+              "problems_per_gpu": None, "algo": "m-etf",
+              "l2": "inputs+workspace larger than L2 (GBs, rewritten every step)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        graphs = W.sweep_graphs(0, args.graphs)
+        jobs = W.sweep_jobs(graphs)
+        idx = sample_indices(jobs, args.cpu_sample)
+        threads = os.cpu_count() or 1
+        for _ in range(args.warmup):
+            cpu_reference(graphs, jobs, idx[: max(8, len(idx) // 8)], threads)
+        rates, _, _ = cpu_reference(graphs, jobs, idx, threads, steps=args.steps)
+        v = statistics.median(rates)
+        config["problems_per_gpu"] = len(jobs)
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": len(idx) / v * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+                "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                                 "sample": f"{len(idx)} of the {len(jobs)} sweep problems (every "
+                                           f"{len(jobs) // len(idx)}th), OpenMP over problems"},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_2301_08695_b200 as bx
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    graphs = W.sweep_graphs(rank, args.graphs)
+    jobs = W.sweep_jobs(graphs)
+    config["problems_per_gpu"] = len(jobs)
+    P = len(jobs)
+    # pinned host copies of every input (the e2e path copies from these)
+    keep = []
+
+    def pinned(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        keep.append(t)
+        return t.numpy()
+
+    mgs = []
+    for g in graphs:
+        mgs.append(bx.MetaGraph(pinned(g["k"]), pinned(g["temp"]), pinned(g["perm"]), pinned(g["out"]),
+                                pinned(g["esrc"]), pinned(g["edst"]), pinned(g["ebytes"])))
+    for m in mgs:  # adjacency arrays pinned too
+        m.in_off, m.in_edge, m.out_off = pinned(m.in_off), pinned(m.in_edge), pinned(m.out_off)
+    cm = bx.CommModel(*W.COMM_TEST)
+    bjobs = [bx.Job(gi, "m-etf", pinned(np.full(n, cap, np.int64)), cm) for gi, n, cap in jobs]
+    t0 = time.time()
+    plan = bx.Plan(mgs, bjobs, device=local)
+    log(f"[rank {rank}] plan: {P} problems, {sum(g['V'] for g in graphs)} graph nodes, "
+        f"created in {time.time() - t0:.2f}s")
+    h2d = sum(m.k.nbytes + m.temp.nbytes + m.perm.nbytes + m.out.nbytes + m.esrc.nbytes + m.edst.nbytes
+              + m.ebytes.nbytes + m.in_off.nbytes + m.in_edge.nbytes + m.out_off.nbytes for m in mgs)
+    h2d += sum(8 * n for _, n, _ in jobs)
+    d2h = sum(graphs[g]["V"] * (4 + 8 + 4) + 4 * (n + 1) + 24 + 8 for g, n, _ in jobs)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    plan.upload(sp)
+    for _ in range(args.warmup):
+        plan.upload(sp)
+        plan.place(sp)
+        plan.download(sp)
+    fails = [i for i in range(P) if plan.status(i)[0] not in (0, 3)]
+    if fails:
+        raise RuntimeError(f"problems failed: {[plan.status(i) for i in fails[:3]]}")
+
+    # ---- device-resident timed region -----------------------------------
+    kernel_ms = []
+    barrier()
+    with Clocks(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            plan.place(sp)
+            kernel_ms.append(plan.kernel_ms())
+        ev1.record(stream)
+        ev1.synchronize()
+        dev_ms = ev0.elapsed_time(ev1)
+    barrier()
+    dev_ms = max_over_ranks(dev_ms)
+    launches = plan.launch_count() * args.steps
+    ms_step = dev_ms / args.steps
+    value = world * P / (ms_step / 1e3)
+
+    # ---- end to end through the C ABI with host buffers --------------------
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        plan.upload(sp)
+        plan.place(sp)
+        plan.download(sp)
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    barrier()
+    e2e_ms = max_over_ranks(e2e_ms)
+    e2e_value = world * P / (e2e_ms / args.steps / 1e3)
+
+    # ---- final gather of per-problem summaries over NCCL --------------------
+    summ = np.zeros((P, 3), np.int64)
+    for i in range(P):
+        st, _ = plan.status(i)
+        summ[i, 0] = st
+        if st == 0:
+            r = plan.result(i, copy=False)
+            summ[i, 1] = int((r.start_us * 131 + r.device_of).sum())
+            summ[i, 2] = int(r.start_us.max() + graphs[jobs[i][0]]["k"][int(np.argmax(r.start_us))]) if len(
+                r.start_us) else 0
+    gather_ms = None
+    if dist is not None:
+        t = torch.from_numpy(summ).cuda()
+        outs = torch.empty((world * P, 3), dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        dist.all_gather_into_tensor(outs, t)
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - g0) * 1e3
+    infeasible = int((summ[:, 0] == 3).sum())
+
+    # ---- roofline of the dominant kernel (the placer) ------------------------
+    kmean = statistics.mean(kernel_ms)
+    abytes = algorithmic_bytes(graphs, jobs)
+    achieved = abytes / (kmean / 1e3) / 1e9
+    peak = None
+    peak_src = "fallback 6650 GB/s (B200_PROFILING.md)"
+    try:
+        peak = json.load(open(PEAKS))["hbm_gbs"]
+        peak_src = "measured MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        peak = 6650.0
+    traffic = None
+    try:
+        traffic = json.load(open(NCU_SUMMARY)).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # ---- CPU reference baseline (rank 0, N=1) + parity spot check ------------
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            idx = sample_indices(jobs, args.cpu_sample)
+            threads = os.cpu_count() or 1
+            rates, st, chk = cpu_reference(graphs, jobs, idx, threads)
+            cpu = {"value": rates[0], "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{len(idx)} of the {P} sweep problems (every {P // len(idx)}th), reference "
+                             f"place_metf, OpenMP over problems"}
+            mism = sum(1 for r, i in enumerate(idx)
+                       if int(st[r]) != int(summ[i, 0]) or (st[r] == 0 and int(chk[r]) != int(summ[i, 1])))
+            parity = {"checked": len(idx), "mismatches": mism}
+        except Exception as e:  # the baseline is reported, never the target
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": config,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches,
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": traffic,
+                             "kernel": "k_place_list", "kernel_ms": kmean,
+                             "algorithmic_bytes_per_launch": abytes, "peak_source": peak_src,
+                             "note": "latency-bound dependent scheduling chain; bytes = 40V+16E per problem"},
+                "cpu_baseline": cpu, "parity_vs_reference": parity, "infeasible_problems": infeasible,
+                "gather_ms": gather_ms, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    plan.close()
+
+
+if __name__ == "__main__":
+    main()

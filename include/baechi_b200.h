@@ -149,8 +149,12 @@ int bx_plan_place(bx_plan *plan, void *stream);
  * `stream`. Returns BX_OK if the copy worked; per-job status is in out[i]. */
 int bx_plan_download(bx_plan *plan, void *stream, bx_placement *out);
 
-/* Number of placer kernel launches the last bx_plan_place issued. */
+/* Number of kernel launches the last bx_plan_place issued. */
 int bx_plan_launch_count(const bx_plan *plan);
+
+/* Device time (ms) of the placer kernel(s) of the last bx_plan_place,
+ * measured with CUDA events on the plan's stream; waits for it. */
+float bx_plan_kernel_ms(bx_plan *plan);
 
 /* simulate (simulator.cpp:273-278) of every job's current device-resident
  * placement (K4), in `mem_mode`. Device-resident; use bx_plan_sim_download

@@ -138,6 +138,8 @@ def lib():
         L.bx_plan_place.argtypes = [_vp, _vp]
         L.bx_plan_download.argtypes = [_vp, _vp, C.POINTER(_Placement)]
         L.bx_plan_launch_count.argtypes = [_vp]
+        L.bx_plan_kernel_ms.argtypes = [_vp]
+        L.bx_plan_kernel_ms.restype = C.c_float
         L.bx_plan_simulate.argtypes = [_vp, i32, _vp]
         L.bx_plan_sim_download.argtypes = [_vp, _vp, C.POINTER(_SimReport)]
         L.bx_place.argtypes = [C.POINTER(_Graph), C.POINTER(_Job), C.POINTER(_Placement)]
@@ -150,7 +152,7 @@ def lib():
 
 EXPORTED = ["bx_version", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
             "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download",
-            "bx_plan_launch_count", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
+            "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
             "bx_simulate", "bx_round_extract"]
 
 
@@ -314,6 +316,10 @@ class Plan:
 
     def launch_count(self) -> int:
         return lib().bx_plan_launch_count(self.h)
+
+    def kernel_ms(self) -> float:
+        """CUDA-event time of the placer kernel(s) of the last place()."""
+        return float(lib().bx_plan_kernel_ms(self.h))
 
     def download(self, stream=None):
         rc = lib().bx_plan_download(self.h, stream, self.out)

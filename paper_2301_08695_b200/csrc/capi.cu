@@ -109,6 +109,7 @@ struct bx_plan {
   int maxn = 1;
   bool any_topo = false, any_list = false;
   int launches = 0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};  // brackets the placer kernel(s)
   // simulator
   void *sim_pool = nullptr;
   DSim *ds_dev = nullptr;
@@ -169,6 +170,8 @@ void bx_plan_destroy(bx_plan *plan) {
   if (plan->pool) cudaFree(plan->pool);
   if (plan->sim_pool) cudaFree(plan->sim_pool);
   if (plan->sort_tmp) cudaFree(plan->sort_tmp);
+  if (plan->ev[0]) cudaEventDestroy(plan->ev[0]);
+  if (plan->ev[1]) cudaEventDestroy(plan->ev[1]);
   delete plan;
 }
 
@@ -462,6 +465,8 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     P->sort_tmp_bytes = std::max<size_t>(bytes, 256);
     BX_CUDA(cudaMalloc(&P->sort_tmp, P->sort_tmp_bytes), msg, msglen);
   }
+  BX_CUDA(cudaEventCreate(&P->ev[0]), msg, msglen);
+  BX_CUDA(cudaEventCreate(&P->ev[1]), msg, msglen);
   *out = P;
   put_msg(msg, msglen, "");
   return BX_OK;
@@ -495,12 +500,22 @@ int bx_plan_place(bx_plan *P, void *stream) {
   }
   launch_kahn(P->dg_dev, P->queues_dev, P->ngraphs, s);
   P->launches += 1;
+  cudaEventRecord(P->ev[0], s);
   launch_placers(P->dj_dev, P->njobs, P->dg_dev, P->dp_dev, P->maxn, P->any_topo, P->any_list, s);
+  cudaEventRecord(P->ev[1], s);
   P->launches += (P->any_topo ? 1 : 0) + (P->any_list ? 1 : 0);
   return cudaGetLastError() == cudaSuccess ? BX_OK : BX_RUNTIME;
 }
 
 int bx_plan_launch_count(const bx_plan *P) { return P->launches; }
+
+float bx_plan_kernel_ms(bx_plan *P) {
+  cudaSetDevice(P->device);
+  if (cudaEventSynchronize(P->ev[1]) != cudaSuccess) return -1.0f;
+  float ms = -1.0f;
+  if (cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]) != cudaSuccess) return -1.0f;
+  return ms;
+}
 
 static std::string cycle_message(const bx_plan *P, int g, cudaStream_t s) {
   const bx_graph &G = P->hg[g];
