@@ -171,8 +171,8 @@ def main():
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
 
-    graphs = W.sweep_graphs(rank, args.graphs)
-    jobs = W.sweep_jobs(graphs)
+    from paper_2301_08695_b200 import sweep
+    graphs, jobs = sweep.rank_sweep(rank, args.graphs)
     config["problems_per_gpu"] = len(jobs)
     P = len(jobs)
     # pinned host copies of every input (the e2e path copies from these)
@@ -255,22 +255,14 @@ def main():
     e2e_value = world * P / (e2e_ms / args.steps / 1e3)
 
     # ---- final gather of per-problem summaries over NCCL --------------------
-    summ = np.zeros((P, 3), np.int64)
-    for i in range(P):
-        st, _ = plan.status(i)
-        summ[i, 0] = st
-        if st == 0:
-            r = plan.result(i, copy=False)
-            summ[i, 1] = int((r.start_us * 131 + r.device_of).sum())
-            summ[i, 2] = int(r.start_us.max() + graphs[jobs[i][0]]["k"][int(np.argmax(r.start_us))]) if len(
-                r.start_us) else 0
+    sts = [plan.status(i)[0] for i in range(P)]
+    summ = sweep.summarize(sts, [plan.result(i, copy=False) if sts[i] == 0 else None for i in range(P)],
+                           lambda i: graphs[jobs[i][0]]["k"], base_id=rank * P)
     gather_ms = None
     if dist is not None:
-        t = torch.from_numpy(summ).cuda()
-        outs = torch.empty((world * P, 3), dtype=torch.int64, device="cuda")
         torch.cuda.synchronize()
         g0 = time.perf_counter()
-        dist.all_gather_into_tensor(outs, t)
+        sweep.gather_summaries(summ, dist, device=torch.device("cuda", local))
         torch.cuda.synchronize()
         gather_ms = (time.perf_counter() - g0) * 1e3
     infeasible = int((summ[:, 0] == 3).sum())

@@ -156,6 +156,13 @@ int bx_plan_launch_count(const bx_plan *plan);
  * measured with CUDA events on the plan's stream; waits for it. */
 float bx_plan_kernel_ms(bx_plan *plan);
 
+/* Per-step latency breakdown of job `job` (plans created with the
+ * environment variable BX_PROFILE=1 run a clock64-instrumented placer):
+ * 16 int64 = SM cycles in rescan, argmin, rekey, discard, commit, remove,
+ * ready, rows, cache, insert, emit, then counts steps, commits, rescans,
+ * and the total cycles of the job. */
+int bx_plan_profile(bx_plan *plan, int32_t job, int64_t *out16);
+
 /* simulate (simulator.cpp:273-278) of every job's current device-resident
  * placement (K4), in `mem_mode`. Device-resident; use bx_plan_sim_download
  * for the reports. */

@@ -140,6 +140,7 @@ def lib():
         L.bx_plan_launch_count.argtypes = [_vp]
         L.bx_plan_kernel_ms.argtypes = [_vp]
         L.bx_plan_kernel_ms.restype = C.c_float
+        L.bx_plan_profile.argtypes = [_vp, i32, _vp]
         L.bx_plan_simulate.argtypes = [_vp, i32, _vp]
         L.bx_plan_sim_download.argtypes = [_vp, _vp, C.POINTER(_SimReport)]
         L.bx_place.argtypes = [C.POINTER(_Graph), C.POINTER(_Job), C.POINTER(_Placement)]
@@ -152,7 +153,7 @@ def lib():
 
 EXPORTED = ["bx_version", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
             "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download",
-            "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
+            "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_profile", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
             "bx_simulate", "bx_round_extract"]
 
 
@@ -316,6 +317,16 @@ class Plan:
 
     def launch_count(self) -> int:
         return lib().bx_plan_launch_count(self.h)
+
+    PROFILE_FIELDS = ("rescan", "argmin", "rekey", "discard", "commit", "remove", "ready", "rows", "cache",
+                      "insert", "emit", "steps", "commits", "rescans", "total")
+
+    def profile(self, i: int) -> dict:
+        """Latency breakdown of job i (plan built with BX_PROFILE=1)."""
+        out = np.zeros(16, np.int64)
+        rc = lib().bx_plan_profile(self.h, i, _ptr(out))
+        _raise(rc, "no profile: create the plan with BX_PROFILE=1")
+        return dict(zip(self.PROFILE_FIELDS, out.tolist()))
 
     def kernel_ms(self) -> float:
         """CUDA-event time of the placer kernel(s) of the last place()."""

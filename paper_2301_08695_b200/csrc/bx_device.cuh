@@ -93,6 +93,13 @@ struct DJob {
   int32_t *exec_order, *exec_off;
   int64_t *stats;
   DErr *err;
+  int64_t *prof;  // [kProfSlots] per-phase SM cycles when built with profiling, else null
+};
+
+// Per-step latency breakdown slots (clock64 cycles summed over the run, lane 0).
+enum ProfSlot : int {
+  P_RESCAN = 0, P_ARGMIN, P_REKEY, P_DISCARD, P_COMMIT, P_REMOVE, P_READY, P_ROWS, P_CACHE, P_INSERT, P_EMIT,
+  P_STEPS, P_COMMITS, P_RESCANS, P_TOTAL, kProfSlots = 16
 };
 
 // Simulator job (K4) — reads a placement (device_of / exec lists).

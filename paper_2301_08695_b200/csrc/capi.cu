@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -21,8 +22,8 @@ void launch_prep(const DGraph &g, const DPrep &pr, bool first, cudaStream_t s);
 void launch_kahn(DGraph *graphs_dev, int32_t *const *queues_dev, int ngraphs, cudaStream_t s);
 cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bit, cudaStream_t s);
 void launch_extract(const XCtx &c, cudaStream_t s);
-void launch_placers(const DJob *jobs, int njobs, const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo,
-                    bool any_list, cudaStream_t s);
+void launch_placers(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
+                    int maxn, bool any_topo, bool any_list, bool prof, cudaStream_t s);
 void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, cudaStream_t s);
 }  // namespace bx
 
@@ -101,6 +102,7 @@ struct bx_plan {
   DGraph *dg_dev = nullptr;
   DPrep *dp_dev = nullptr;
   DJob *dj_dev = nullptr;
+  int32_t *order_dev = nullptr;     // jobs by descending V*n (longest first)
   int32_t **queues_dev = nullptr;
   void *sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
@@ -110,6 +112,7 @@ struct bx_plan {
   bool any_topo = false, any_list = false;
   int launches = 0;
   cudaEvent_t ev[2] = {nullptr, nullptr};  // brackets the placer kernel(s)
+  int64_t *prof = nullptr;                 // per-job latency breakdown (BX_PROFILE=1)
   // simulator
   void *sim_pool = nullptr;
   DSim *ds_dev = nullptr;
@@ -170,6 +173,7 @@ void bx_plan_destroy(bx_plan *plan) {
   if (plan->pool) cudaFree(plan->pool);
   if (plan->sim_pool) cudaFree(plan->sim_pool);
   if (plan->sort_tmp) cudaFree(plan->sort_tmp);
+  if (plan->prof) cudaFree(plan->prof);
   if (plan->ev[0]) cudaEventDestroy(plan->ev[0]);
   if (plan->ev[1]) cudaEventDestroy(plan->ev[1]);
   delete plan;
@@ -293,6 +297,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   size_t ptables = L.take<DPrep>(P->nprep);
   size_t jtables = L.take<DJob>(njobs);
   size_t qtables = L.take<int32_t *>(ngraphs);
+  size_t otable = L.take<int32_t>(njobs);
   P->pool_bytes = L.off;
   cudaError_t ce = cudaMalloc(&P->pool, P->pool_bytes);
   if (ce != cudaSuccess) {
@@ -376,6 +381,10 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     }
   }
   P->dj.resize(njobs);
+  if (std::getenv("BX_PROFILE") && std::getenv("BX_PROFILE")[0] == '1') {
+    BX_CUDA(cudaMalloc(&P->prof, sizeof(int64_t) * kProfSlots * size_t(njobs)), msg, msglen);
+    BX_CUDA(cudaMemset(P->prof, 0, sizeof(int64_t) * kProfSlots * size_t(njobs)), msg, msglen);
+  }
   for (int i = 0; i < njobs; ++i) {
     const bx_job &J = jobs[i];
     const bx_graph &G = graphs[J.graph];
@@ -409,6 +418,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     d.exec_off = at<int32_t>(pool, o.exec_off);
     d.stats = at<int64_t>(pool, o.stats);
     d.err = at<DErr>(pool, o.err);
+    d.prof = P->prof ? P->prof + static_cast<size_t>(kProfSlots) * i : nullptr;
     // host-side validation in the reference's order
     std::string why;
     int st = 0;
@@ -450,6 +460,15 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   P->dp_dev = at<DPrep>(pool, ptables);
   P->dj_dev = at<DJob>(pool, jtables);
   P->queues_dev = at<int32_t *>(pool, qtables);
+  P->order_dev = at<int32_t>(pool, otable);
+  {
+    std::vector<int32_t> ord(njobs);
+    for (int i = 0; i < njobs; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+      return int64_t(graphs[jobs[a].graph].V) * jobs[a].n > int64_t(graphs[jobs[b].graph].V) * jobs[b].n;
+    });
+    BX_CUDA(cudaMemcpy(P->order_dev, ord.data(), 4 * size_t(njobs), cudaMemcpyHostToDevice), msg, msglen);
+  }
   // descriptor tables are static: copy once
   BX_CUDA(cudaMemcpy(P->dg_dev, P->dg.data(), sizeof(DGraph) * ngraphs, cudaMemcpyHostToDevice), msg, msglen);
   BX_CUDA(cudaMemcpy(P->dp_dev, P->dp.data(), sizeof(DPrep) * P->nprep, cudaMemcpyHostToDevice), msg, msglen);
@@ -501,13 +520,22 @@ int bx_plan_place(bx_plan *P, void *stream) {
   launch_kahn(P->dg_dev, P->queues_dev, P->ngraphs, s);
   P->launches += 1;
   cudaEventRecord(P->ev[0], s);
-  launch_placers(P->dj_dev, P->njobs, P->dg_dev, P->dp_dev, P->maxn, P->any_topo, P->any_list, s);
+  launch_placers(P->dj_dev, P->order_dev, P->njobs, P->dg_dev, P->dp_dev, P->maxn, P->any_topo, P->any_list, P->prof != nullptr, s);
   cudaEventRecord(P->ev[1], s);
   P->launches += (P->any_topo ? 1 : 0) + (P->any_list ? 1 : 0);
   return cudaGetLastError() == cudaSuccess ? BX_OK : BX_RUNTIME;
 }
 
 int bx_plan_launch_count(const bx_plan *P) { return P->launches; }
+
+int bx_plan_profile(bx_plan *P, int32_t job, int64_t *out16) {
+  cudaSetDevice(P->device);
+  if (!P->prof || job < 0 || job >= P->njobs) return BX_VALIDATION;
+  if (cudaMemcpy(out16, P->prof + static_cast<size_t>(kProfSlots) * job, sizeof(int64_t) * kProfSlots,
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return BX_RUNTIME;
+  return BX_OK;
+}
 
 float bx_plan_kernel_ms(bx_plan *P) {
   cudaSetDevice(P->device);

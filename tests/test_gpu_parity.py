@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C ABI) against the golden vectors
+made by the reference itself, the reference KATs, the C restatement on
+seeded graphs, and size-independent properties at full size. Bit-exact:
+every quantity here is integer."""
+import numpy as np
+import pytest
+
+import golden_cases
+import kats
+from oracle import OracleError, Ref, Restate
+from paper_2301_08695_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+ALGO = ["m-topo", "m-etf", "m-sct"]
+
+
+def _meta(bx, m):
+    return bx.MetaGraph.from_dict(m)
+
+
+def _assert_same(p, o, stats=True):
+    assert np.array_equal(p.device_of, o.device_of)
+    assert np.array_equal(p.start_us, o.start_us)
+    assert np.array_equal(p.exec_order_flat, o.exec_order)
+    assert np.array_equal(p.exec_off, o.exec_off)
+    if stats:
+        assert list(p.stats) == list(o.stats)
+
+
+def test_golden_vectors_batched(bx):
+    """All 600 golden cases (500 placements + 100 reference errors) in one
+    device-resident batch: one placer launch, bit-exact."""
+    z, index, graphs = golden_cases.load()
+    gis = sorted(graphs)
+    mgs = [_meta(bx, graphs[g]) for g in gis]
+    jobs = []
+    for rec in index:
+        m = graphs[rec["graph"]]
+        fav = golden_cases.fav_first(m) if rec["fav"] else None
+        jobs.append(bx.Job(gis.index(rec["graph"]), ALGO[rec["algo"]], np.array(rec["caps"], np.int64),
+                           bx.CommModel(*rec["cm"]), fav))
+    plan = bx.Plan(mgs, jobs)
+    plan.upload()
+    plan.place()
+    plan.download()
+    for i, rec in enumerate(index):
+        st, msg = plan.status(i)
+        assert st == rec["status"], (i, msg)
+        c = rec["case"]
+        if st:
+            assert msg == rec["msg"], i
+            continue
+        p = plan.result(i)
+        assert np.array_equal(p.device_of, z[f"c{c}_device_of"]), c
+        assert np.array_equal(p.start_us, z[f"c{c}_start"]), c
+        assert np.array_equal(p.exec_order_flat, z[f"c{c}_exec_order"]), c
+        assert np.array_equal(p.exec_off, z[f"c{c}_exec_off"]), c
+        if rec["algo"]:
+            assert list(p.stats) == rec["stats"], c
+    for mm in (0, 1):
+        plan.simulate(mm)
+        reps = plan.sim_download()
+        for i, rec in enumerate(index):
+            if rec["status"]:
+                continue
+            s, r, c = rec["sims"][mm], reps[i], rec["case"]
+            assert r.makespan_us == s["makespan"], c
+            assert r.peak_bytes.tolist() == s["peak"] and r.busy_us.tolist() == s["busy"], c
+            assert r.idle_us.tolist() == s["idle"], c
+            assert [r.transfer_count, r.transfer_bytes, r.duplicate_transfers, r.cache_hits] == s["xfer"], c
+            assert np.array_equal(r.start_us, z[f"c{c}_sim{mm}_start"]), c
+    plan.close()
+
+
+@pytest.mark.parametrize("kat", kats.placer_kats(), ids=lambda k: k[0])
+def test_placer_kats_cuda(bx, kat):
+    name, g, algo, caps, cm, fav, check = kat
+    gg = _meta(bx, g)
+    call = lambda: bx._one(gg, ALGO[algo], caps, bx.CommModel(*cm), fav)  # noqa: E731
+    if isinstance(check, tuple):
+        _, kind, sub = check
+        with pytest.raises(bx.Error) as ei:
+            call()
+        assert ei.value.kind == kind and sub in ei.value.msg, ei.value.msg
+    else:
+        p = call()
+
+        class P:  # the check lambdas read exec_lists() / device_of / start_us
+            device_of, start_us = p.device_of, p.start_us
+            exec_lists = staticmethod(lambda: p.exec_order)
+
+        assert check(P, p.stats), name
+
+
+@pytest.mark.parametrize("kat", kats.simulator_kats(), ids=lambda k: k[0])
+def test_simulator_kats_cuda(bx, kat):
+    name, g, dev, n, caps, cm, mm, check = kat
+    d, order, off = kats.manual(dev, n)
+    gg = _meta(bx, g)
+    pl = bx.Placement("manual", d, np.zeros(len(d), np.int64), order, off)
+    if isinstance(check, tuple):
+        _, kind, sub = check
+        with pytest.raises(bx.Error) as ei:
+            bx.simulate(gg, pl, caps, bx.CommModel(*cm), mm)
+        assert ei.value.kind == kind and sub in ei.value.msg
+        ok, diag, _ = bx.verify_placement(gg, pl, caps, bx.CommModel(*cm), mm)
+        assert not ok and sub in diag
+    else:
+        r = bx.simulate(gg, pl, caps, bx.CommModel(*cm), mm)
+
+        class R:
+            makespan, start_us = r.makespan_us, r.start_us
+            peak, busy, idle = r.peak_bytes, r.busy_us, r.idle_us
+            transfer_count, transfer_bytes = r.transfer_count, r.transfer_bytes
+            duplicate_transfers, cache_hits = r.duplicate_transfers, r.cache_hits
+
+        assert check(R), name
+
+
+def test_simulator_deadlock_and_bad_lists(bx):
+    gg = _meta(bx, kats.DEADLOCK)
+    d, order, off = kats.manual([0, 0], 1)
+    bad = bx.Placement("manual", d, np.zeros(2, np.int64), order[::-1].copy(), off)
+    with pytest.raises(bx.ValidationError) as ei:
+        bx.simulate(gg, bad, [100], bx.CommModel(), 1)
+    assert ei.value.msg == "deadlock: device 0 waits forever for inputs of node 1; exec_order contradicts the DAG"
+    wrong = bx.Placement("manual", np.array([0, 1], np.int32), np.zeros(2, np.int64), order, off)
+    with pytest.raises(bx.ValidationError) as ei:
+        bx.simulate(gg, wrong, [100], bx.CommModel(), 1)
+    assert "exec_order disagrees" in ei.value.msg
+    dup = bx.Placement("manual", d, np.zeros(2, np.int64), np.array([0, 0], np.int32), off)
+    with pytest.raises(bx.ValidationError) as ei:
+        bx.simulate(gg, dup, [100], bx.CommModel(), 1)
+    assert "exactly once" in ei.value.msg
+
+
+def _random_cases():
+    out = []
+    for seed in range(6):
+        for g in (W.layered_dag(8, 12, seed), W.grid_chain(20, 6, seed), W.branchy(6, seed),
+                  W.wide_random(150, seed)):
+            out.append((seed, g))
+    return out
+
+
+@pytest.mark.parametrize("seed,g", _random_cases(), ids=lambda x: x if isinstance(x, int) else x["name"])
+def test_cuda_vs_oracle_seeded(bx, seed, g):
+    """Seeded graphs x rosters (uniform/heterogeneous, ample/tight) x comm
+    modes x algorithms, against the C restatement."""
+    m = W.as_meta_dict(g)
+    gg = _meta(bx, m)
+    fav = golden_cases.fav_first(m)
+    rng = np.random.default_rng(seed)
+    for n in (1, 3, 4, 7):
+        for f in (1.0, 1.04, 1.6):
+            cap = W.bench_capacity(g, n, f)
+            caps = [int(cap * rng.uniform(0.8, 1.1)) for _ in range(n)]
+            for cm in ((5.0, 0.001, 0), (12.5, 0.002, 1), (0.0, 0.0, 1)):
+                for algo in (0, 1, 2):
+                    fv = fav if algo == 2 else None
+                    try:
+                        o = Restate.place(m, algo, caps, cm, fv)
+                        oe = None
+                    except OracleError as e:
+                        oe = (e.kind, e.msg)
+                    try:
+                        p = bx._one(gg, ALGO[algo], caps, bx.CommModel(*cm), fv)
+                        pe = None
+                    except bx.Error as e:
+                        pe = (e.kind, e.msg)
+                    assert oe == pe, (n, f, cm, algo)
+                    if oe is None:
+                        _assert_same(p, o, stats=algo != 0)
+
+
+def test_round_extract_vs_oracle(bx):
+    rng = np.random.default_rng(7)
+    for trial in range(30):
+        g = W.wide_random(200, trial)
+        V, E = g["V"], len(g["esrc"])
+        x = rng.choice([0.0, -0.0, 0.01, 0.05, 0.09, 0.1, 0.3, 1.0, np.nan], E)
+        if trial % 3 == 0:
+            x = rng.random(E) * 0.2
+        for thr in (0.1, 0.05, 0.49):
+            a = bx.round_and_extract(V, g["esrc"], g["edst"], x, thr)
+            b = Restate.round_extract(V, g["esrc"], g["edst"], x, thr)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+            assert list(a[2]) == b[2].tolist()
+    with pytest.raises(bx.ValidationError):
+        bx.round_and_extract(2, [0], [1], [0.0], 0.5)
+
+
+def test_acceptance_c7_degeneracies(bx):
+    """acceptance.cpp:286-337: n=1 => makespan = sum k for all three placers;
+    empty favourites => m-SCT == m-ETF; zero comm + ample memory => no discards."""
+    for seed in range(4):
+        g = W.layered_dag(10, 10, seed)
+        m = W.as_meta_dict(g)
+        gg = _meta(bx, m)
+        total = int(g["k"].sum())
+        big = [int(W.need(g).sum()) * 2]
+        for algo in ALGO:
+            p = bx._one(gg, algo, big, bx.CommModel(*W.COMM_TEST))
+            r = bx.simulate(gg, p, big, bx.CommModel(*W.COMM_TEST))
+            assert r.makespan_us == total
+        caps = [W.bench_capacity(g, 4, 1.05)] * 4
+        for cm in ((5.0, 0.001, 0), W.COMM_TEST):
+            e = bx.place_metf(gg, caps, bx.CommModel(*cm))
+            s = bx.place_msct(gg, caps, bx.CommModel(*cm), np.full(gg.V, -1, np.int32))
+            s2 = bx.place_msct(gg, caps, bx.CommModel(*cm), None)
+            for x in (s, s2):
+                assert np.array_equal(e.device_of, x.device_of) and np.array_equal(e.start_us, x.start_us)
+        st = [0, 0, 0]
+        bx.place_metf(gg, [10 ** 15] * 4, bx.CommModel(0.0, 0.0, 1), stats_out=st)
+        assert st[0] == 0 and st[1] == 0
+
+
+def test_empty_and_single_node_graphs(bx):
+    empty = bx.MetaGraph([], [], [], [], [], [], [])
+    for algo in ALGO:
+        p = bx._one(empty, algo, [10, 10], bx.CommModel())
+        assert len(p.device_of) == 0 and p.exec_off.tolist() == [0, 0, 0]
+    one = _meta(bx, kats.graph([kats.node(5, 7, 1, 1, 1)], []))
+    p = bx.place_metf(one, [10, 10], bx.CommModel())
+    assert p.device_of.tolist() == [0] and p.start_us.tolist() == [0]
+
+
+def test_batch_equals_single(bx):
+    gs = [W.branchy(20, 1), W.layered_dag(15, 20, 2)]
+    mgs = [bx.MetaGraph.from_dict(W.as_meta_dict(g)) for g in gs]
+    cm = bx.CommModel(*W.COMM_TEST)
+    jobs = [bx.Job(gi, a, np.full(n, W.bench_capacity(gs[gi], n, 1.1), np.int64), cm)
+            for gi in (0, 1) for n in (2, 5) for a in ("m-etf", "m-topo")]
+    plan = bx.Plan(mgs, jobs)
+    plan.upload()
+    plan.place()
+    plan.download()
+    for i, j in enumerate(jobs):
+        solo = bx._one(mgs[j.graph], j.algo, j.capacity, cm)
+        b = plan.result(i)
+        assert np.array_equal(b.device_of, solo.device_of) and np.array_equal(b.start_us, solo.start_us)
+    # re-running the same plan is deterministic
+    plan.place()
+    plan.download()
+    assert np.array_equal(plan.result(0).start_us, bx._one(mgs[0], "m-etf", jobs[0].capacity, cm).start_us)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_full_size_100k_properties_and_reference(bx, mode):
+    """100k ops x 4 devices (the 20x-target size): bit-exact vs the compiled
+    reference when present, plus size-independent properties: every node
+    placed once, starts respect dependencies and device order, reservations
+    fit, and the simulator replays the placement."""
+    g = W.layered_dag_fast(100, 1000, 3)
+    m = W.as_meta_dict(g)
+    gg = _meta(bx, m)
+    cm = (12.5, 0.002, mode) if mode else (5.0, 0.001, 0)
+    caps = [W.bench_capacity(g, 4, 1.2)] * 4
+    st = [0, 0, 0]
+    p = bx.place_metf(gg, caps, bx.CommModel(*cm), stats_out=st)
+    V = gg.V
+    assert sorted(p.exec_order_flat.tolist()) == list(range(V))
+    fin = p.start_us + gg.k
+    for d in range(4):
+        lst = p.exec_order_flat[p.exec_off[d]:p.exec_off[d + 1]]
+        assert np.all(p.device_of[lst] == d)
+        assert np.all(p.start_us[lst][1:] >= fin[lst][:-1])
+        assert int(W.need(g)[lst].sum()) <= caps[d]
+    assert np.all(p.start_us[gg.edst] >= fin[gg.esrc])
+    r = bx.simulate(gg, p, caps, bx.CommModel(*cm))
+    assert r.makespan_us >= int(gg.k.sum()) // 4  # no schedule beats perfect balance
+    if Ref.available():
+        rg = Ref.graph(W.as_ref_base(g), -1)
+        o = Ref.place(rg, 1, caps, cm)
+        _assert_same(p, o)
+        ro = Ref.simulate(rg, caps, cm, 1, o.device_of, o.exec_order, o.exec_off)
+        assert ro.makespan == r.makespan_us and np.array_equal(ro.start_us, r.start_us)
