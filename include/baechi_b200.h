@@ -105,6 +105,8 @@ typedef struct {
 
 /* ---- library ---------------------------------------------------------- */
 const char *bx_version(void);
+/* Text of the last CUDA launch failure seen by this thread ("" if none). */
+const char *bx_last_error(void);
 /* Number of CUDA devices visible (0 on a CPU-only host). */
 int bx_device_count(void);
 

@@ -127,6 +127,7 @@ def lib():
         L = C.CDLL(LIB_PATH)
         i32, i64, cp = C.c_int32, C.c_int64, C.c_char_p
         L.bx_version.restype = C.c_char_p
+        L.bx_last_error.restype = C.c_char_p
         L.bx_device_count.restype = C.c_int
         L.bx_comm_time.argtypes = [C.POINTER(_Comm), i64, C.POINTER(i64)]
         L.bx_build_adjacency.argtypes = [i32, i32, _vp, _vp, _vp, _vp, _vp, cp, C.c_int]
@@ -151,7 +152,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["bx_version", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
+EXPORTED = ["bx_version", "bx_last_error", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
             "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download",
             "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_profile", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
             "bx_simulate", "bx_round_extract"]
@@ -313,7 +314,7 @@ class Plan:
 
     def place(self, stream=None):
         rc = lib().bx_plan_place(self.h, stream)
-        _raise(rc, "bx_plan_place failed")
+        _raise(rc, "bx_plan_place failed: " + lib().bx_last_error().decode())
 
     def launch_count(self) -> int:
         return lib().bx_plan_launch_count(self.h)

@@ -65,6 +65,7 @@ struct DGraph {
   int32_t *iota;        // sort scratch
   int64_t *need_keys;   // sort scratch
   int32_t *in_src;
+  int32_t *inpos;       // [E] in-CSR slot of each edge (out-CSR order = edge order)
   int32_t *indeg_left;  // Kahn residue (cycle message)
   int32_t *flags;       // [0] peeled count, [1] negative-bytes flag
 };
@@ -87,6 +88,12 @@ struct DJob {
   int64_t *finish, *urgent;
   int64_t *sc_val;
   int32_t *sc_gen;
+  int32_t *pdev;  // [E] per in-CSR slot: device of the (placed) parent
+  // round kernel only (parallel comm mode, one CTA per problem): double
+  // buffers for slot compaction and the per-round work lists
+  int64_t *K2, *urgent2;
+  int32_t *ready2, *alive2, *ncw, *newl;
+  int64_t *pfin;  // [E] per in-CSR slot: finish time of the parent
   // outputs
   int32_t *device_of;
   int64_t *start;

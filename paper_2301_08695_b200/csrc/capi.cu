@@ -23,7 +23,7 @@ void launch_kahn(DGraph *graphs_dev, int32_t *const *queues_dev, int ngraphs, cu
 cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bit, cudaStream_t s);
 void launch_extract(const XCtx &c, cudaStream_t s);
 void launch_placers(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                    int maxn, bool any_topo, bool any_list, bool prof, cudaStream_t s);
+                    int maxn, bool any_topo, bool any_list, bool prof, bool wide, cudaStream_t s);
 void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, cudaStream_t s);
 }  // namespace bx
 
@@ -109,6 +109,8 @@ struct bx_plan {
   std::vector<HostCopy> uploads;
   std::vector<Fill> fills;
   int maxn = 1;
+  int64_t max_vn = 0;               // largest V*n over list-placer jobs
+  bool wide = false;                // CTA-per-problem kernels (few large problems)
   bool any_topo = false, any_list = false;
   int launches = 0;
   cudaEvent_t ev[2] = {nullptr, nullptr};  // brackets the placer kernel(s)
@@ -123,9 +125,21 @@ struct bx_plan {
   bool external = false;
 };
 
+static thread_local std::string g_last_error;
+
+// Records the first pending CUDA launch error (kernel config, smem, ...).
+static int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return BX_OK;
+  g_last_error = std::string("CUDA launch error: ") + cudaGetErrorString(e);
+  return BX_RUNTIME;
+}
+
 extern "C" {
 
 const char *bx_version(void) { return "baechi-b200 0.1 (sm_100a)"; }
+
+const char *bx_last_error(void) { return g_last_error.c_str(); }
 
 int bx_device_count(void) {
   int n = 0;
@@ -223,7 +237,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   Layout L;
   struct GOff {
     size_t k, temp, perm, outb, esrc, edst, ebytes, in_off, in_edge, out_off, need, need_order, iota, need_keys,
-        in_src, indeg_left, flags, queue;
+        in_src, inpos, indeg_left, flags, queue;
   };
   std::vector<GOff> go(ngraphs);
   size_t max_sort_V = 0;
@@ -245,6 +259,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     o.iota = L.take<int32_t>(G.V);
     o.need_keys = L.take<int64_t>(G.V);
     o.in_src = L.take<int32_t>(G.E);
+    o.inpos = L.take<int32_t>(G.E);
     o.indeg_left = L.take<int32_t>(G.V);
     o.flags = L.take<int32_t>(4);
     o.queue = L.take<int32_t>(2 * static_cast<size_t>(G.V));
@@ -262,9 +277,20 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     po[pi].second = L.take<int64_t>(1);
   }
   struct JOff {
-    size_t cap, fav, K, cache, dead, pending, alive, ready, rpos, cseq, nc, finish, urgent, scv, scg, device_of,
+    size_t cap, fav, K, cache, dead, pending, alive, ready, rpos, cseq, nc, finish, urgent, scv, scg, pdev, pfin, K2, urgent2, ready2, alive2, ncw, newl, device_of,
         start, exec_order, exec_off, stats, err;
   };
+  // Few large list-placer problems run the CTA-wide kernels (one problem per
+  // CTA); many run one warp each. Decided here because the round kernel
+  // needs double-buffered slot arrays.
+  int64_t list_jobs = 0, vn_max = 0;
+  for (int i = 0; i < njobs; ++i)
+    if (jobs[i].algo != BX_ALGO_MTOPO) {
+      ++list_jobs;
+      vn_max = std::max(vn_max, int64_t(graphs[jobs[i].graph].V) * std::max(jobs[i].n, 1));
+    }
+  const bool wide_plan = list_jobs > 0 && list_jobs <= 148 && vn_max >= (int64_t(1) << 15);
+  P->wide = wide_plan;
   std::vector<JOff> jo(njobs);
   for (int i = 0; i < njobs; ++i) {
     const bx_job &J = jobs[i];
@@ -286,6 +312,17 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     o.urgent = L.take<int64_t>(V);
     o.scv = L.take<int64_t>(32 * n);
     o.scg = L.take<int32_t>(32 * n);
+    o.pdev = L.take<int32_t>(graphs[J.graph].E);
+    {
+      const int64_t Vr = wide_plan ? V : 1;
+      o.K2 = L.take<int64_t>(Vr * (wide_plan ? n : 1));
+      o.urgent2 = L.take<int64_t>(Vr);
+      o.ready2 = L.take<int32_t>(Vr);
+      o.alive2 = L.take<int32_t>(Vr);
+      o.ncw = L.take<int32_t>(Vr);
+      o.newl = L.take<int32_t>(Vr);
+    }
+    o.pfin = L.take<int64_t>(graphs[J.graph].E);
     o.device_of = L.take<int32_t>(V);
     o.start = L.take<int64_t>(V);
     o.exec_order = L.take<int32_t>(V);
@@ -330,6 +367,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     d.iota = at<int32_t>(pool, o.iota);
     d.need_keys = at<int64_t>(pool, o.need_keys);
     d.in_src = at<int32_t>(pool, o.in_src);
+    d.inpos = at<int32_t>(pool, o.inpos);
     d.indeg_left = at<int32_t>(pool, o.indeg_left);
     d.flags = at<int32_t>(pool, o.flags);
     queues[g] = at<int32_t>(pool, o.queue);
@@ -412,6 +450,14 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     d.urgent = at<int64_t>(pool, o.urgent);
     d.sc_val = at<int64_t>(pool, o.scv);
     d.sc_gen = at<int32_t>(pool, o.scg);
+    d.pdev = at<int32_t>(pool, o.pdev);
+    d.K2 = at<int64_t>(pool, o.K2);
+    d.urgent2 = at<int64_t>(pool, o.urgent2);
+    d.ready2 = at<int32_t>(pool, o.ready2);
+    d.alive2 = at<int32_t>(pool, o.alive2);
+    d.ncw = at<int32_t>(pool, o.ncw);
+    d.newl = at<int32_t>(pool, o.newl);
+    d.pfin = at<int64_t>(pool, o.pfin);
     d.device_of = at<int32_t>(pool, o.device_of);
     d.start = at<int64_t>(pool, o.start);
     d.exec_order = at<int32_t>(pool, o.exec_order);
@@ -448,8 +494,12 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
         d.fav = at<int32_t>(pool, o.fav);
         P->uploads.push_back({const_cast<int32_t *>(d.fav), J.fav_child, 4 * size_t(V)});
       }
-      if (J.algo == BX_ALGO_MTOPO) P->any_topo = true;
-      else P->any_list = true;
+      if (J.algo == BX_ALGO_MTOPO) {
+        P->any_topo = true;
+      } else {
+        P->any_list = true;
+        P->max_vn = std::max(P->max_vn, int64_t(G.V) * J.n);
+      }
     }
     P->fills.push_back({d.cache, 0xff, 8 * size_t(V * n)});
     P->fills.push_back({d.dead, 0, size_t(V * n)});
@@ -504,8 +554,13 @@ int bx_plan_place(bx_plan *P, void *stream) {
   cudaSetDevice(P->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   P->launches = 0;
-  for (const Fill &f : P->fills)
-    if (cudaMemsetAsync(f.ptr, f.value, f.bytes, s) != cudaSuccess) return BX_RUNTIME;
+  for (const Fill &f : P->fills) {
+    cudaError_t e = cudaMemsetAsync(f.ptr, f.value, f.bytes, s);
+    if (e != cudaSuccess) {
+      g_last_error = std::string("cudaMemsetAsync: ") + cudaGetErrorString(e);
+      return BX_RUNTIME;
+    }
+  }
   for (int pi = 0; pi < P->nprep; ++pi) {
     const DGraph &g = P->dg[P->dp[pi].graph];
     launch_prep(g, P->dp[pi], P->prep_first[pi] != 0, s);
@@ -514,16 +569,20 @@ int bx_plan_place(bx_plan *P, void *stream) {
   for (int g = 0; g < P->ngraphs; ++g) {
     if (P->dg[g].V == 0) continue;
     size_t bytes = P->sort_tmp_bytes;
-    if (sort_needs(P->sort_tmp, bytes, P->dg[g], P->sort_bits[g], s) != cudaSuccess) return BX_RUNTIME;
+    cudaError_t e = sort_needs(P->sort_tmp, bytes, P->dg[g], P->sort_bits[g], s);
+    if (e != cudaSuccess) {
+      g_last_error = std::string("need sort: ") + cudaGetErrorString(e);
+      return BX_RUNTIME;
+    }
     P->launches += P->sort_launches[g];
   }
   launch_kahn(P->dg_dev, P->queues_dev, P->ngraphs, s);
   P->launches += 1;
   cudaEventRecord(P->ev[0], s);
-  launch_placers(P->dj_dev, P->order_dev, P->njobs, P->dg_dev, P->dp_dev, P->maxn, P->any_topo, P->any_list, P->prof != nullptr, s);
+  launch_placers(P->dj_dev, P->order_dev, P->njobs, P->dg_dev, P->dp_dev, P->maxn, P->any_topo, P->any_list, P->prof != nullptr, P->wide, s);
   cudaEventRecord(P->ev[1], s);
   P->launches += (P->any_topo ? 1 : 0) + (P->any_list ? 1 : 0);
-  return cudaGetLastError() == cudaSuccess ? BX_OK : BX_RUNTIME;
+  return launch_status();
 }
 
 int bx_plan_launch_count(const bx_plan *P) { return P->launches; }
@@ -731,7 +790,7 @@ int bx_plan_simulate(bx_plan *P, int32_t mem_mode, void *stream) {
   for (const Fill &f : P->sim_fills)
     if (cudaMemsetAsync(f.ptr, f.value, f.bytes, s) != cudaSuccess) return BX_RUNTIME;
   launch_simulate(P->ds_dev, P->njobs, P->dg_dev, s);
-  return cudaGetLastError() == cudaSuccess ? BX_OK : BX_RUNTIME;
+  return launch_status();
 }
 
 int bx_plan_sim_download(bx_plan *P, void *stream, bx_sim_report *out) {

@@ -6,15 +6,22 @@
 // pairs is either committed or discarded for memory. The reference reaches
 // the same sequence through a lazy min-heap with re-pushes (:188-202).
 //
-// One warp owns one placement problem for its whole life: a persistent
-// scheduling loop, no per-step launches. Layout:
-//   * shared memory (per warp): per-device state — dev_free F, queue tails,
-//     reservations, capacities, awake reservations, exclusion flags — and,
-//     per device column q, the exact top-KT pairs of that column as a sorted
-//     list of (key, node) plus dirty/complete flags;
+// A warp group owns one placement problem for its whole life: a persistent
+// scheduling loop, no per-step launches. kW = 1 packs four problems into a
+// 128-thread CTA (batched sweeps); kW > 1 gives one large problem a CTA whose
+// kW warps split the column rescans (single-graph latency).
+//
+// Layout:
+//   * shared memory (per problem): per-device state — dev_free F, queue
+//     tails, reservations, capacities, awake reservations, exclusion flags —
+//     and, per device column q, the exact top-KT pairs of that column as a
+//     sorted list of (key, node, slot) plus dirty/complete flags;
 //   * HBM/L2: ready slots. Kc[q*V + s] holds the key component of the node in
-//     slot s on device q, column-major so a column rescan is one coalesced
-//     256-byte load per warp instruction; deadc[q*V + s] marks discarded pairs.
+//     slot s on device q (INT64_MAX = discarded pair), column-major so a
+//     column rescan is one coalesced 256-byte load per warp instruction.
+//     Per in-CSR slot x, pdev[x]/pfin[x] hold the parent's device and finish,
+//     written when the parent commits, so keying a node reads its parents in
+//     one coalesced level plus the cache probe.
 // Key maintenance:
 //   * parallel comm mode: Kc = data-ready time (max over parents of the
 //     arrival term, placers.cpp:55-61); key = max(F[q], Kc, m-SCT floor) is
@@ -25,9 +32,7 @@
 // A commit on device p changes column p (F[p], cached parents) and nothing
 // else except removing the committed node from every column; so per step
 // only column p is rescanned, every other column just drops the node from
-// its top list, and new ready rows are merged into the lists. A column is
-// rescanned only when its list runs dry or its keys change (m-SCT awake
-// reservations, sequential re-keys).
+// its top list, and new ready rows are merged into the lists.
 #include "sched_common.cuh"
 
 namespace bx {
@@ -35,12 +40,75 @@ namespace bx {
 constexpr int KT = 4;  // exact top-KT pairs kept per device column
 
 struct Tops {
-  int64_t *t;    // [n*KT] keys, ascending
+  int64_t *t;    // [n*KT] keys, ascending (key, node)
   int32_t *j;    // [n*KT] nodes
+  int32_t *s;    // [n*KT] their ready slots
   int32_t *cnt;  // [n]
   int32_t *flg;  // [n] bit0 dirty, bit1 complete (list holds every live pair)
 };
 constexpr int kDirty = 1, kComplete = 2;
+
+// ---- keys ------------------------------------------------------------------
+// schedulable_time_impl (placers.cpp:43-79) for ready node j on device q,
+// from the per-slot parent arrays. Parallel mode: data-ready time (t0 = 0).
+// Sequential: the full fold through this lane's generation-tagged scratch.
+__device__ __forceinline__ int64_t key_of(const Ctx &c, int j, int q, int32_t &gen) {
+  const int b = c.in_off[j], e = c.in_off[j + 1];
+  const int n = c.n;
+  if (c.mode == 1) {
+    int64_t t = 0;
+    int x = b;
+    for (; x + 1 < e; x += 2) {  // two parents per round: loads issue together
+      int d0 = c.pdev[x], d1 = c.pdev[x + 1];
+      int64_t f0 = c.pfin[x], f1 = c.pfin[x + 1];
+      int i0 = c.in_src[x], i1 = c.in_src[x + 1];
+      int64_t c0 = c.in_c[x], c1 = c.in_c[x + 1];
+      int64_t a0 = d0 == q ? -1 : c.cache[static_cast<int64_t>(i0) * n + q];
+      int64_t a1 = d1 == q ? -1 : c.cache[static_cast<int64_t>(i1) * n + q];
+      int64_t t0 = d0 == q ? f0 : (a0 >= 0 ? max64(f0, a0) : f0 + c0);
+      int64_t t1 = d1 == q ? f1 : (a1 >= 0 ? max64(f1, a1) : f1 + c1);
+      t = max64(t, max64(t0, t1));
+    }
+    if (x < e) {
+      int d0 = c.pdev[x];
+      int64_t f0 = c.pfin[x];
+      int64_t a0 = d0 == q ? -1 : c.cache[static_cast<int64_t>(c.in_src[x]) * n + q];
+      t = max64(t, d0 == q ? f0 : (a0 >= 0 ? max64(f0, a0) : f0 + c.in_c[x]));
+    }
+    return t;
+  }
+  int64_t t = c.F[q];
+  ++gen;
+  for (int x = b; x < e; ++x) {
+    int d = c.pdev[x];
+    int64_t f = c.pfin[x];
+    int64_t term;
+    if (d == q) {
+      term = f;
+    } else {
+      int64_t cached = c.cache[static_cast<int64_t>(c.in_src[x]) * n + q];
+      if (cached >= 0) {
+        term = max64(f, cached);
+      } else {
+        int64_t td = c.scg[d] == gen ? c.scv[d] : c.tail[d];
+        int64_t tq = c.scg[q] == gen ? c.scv[q] : c.tail[q];
+        term = max64(f, max64(td, tq)) + c.in_c[x];
+        c.scv[d] = term;
+        c.scg[d] = gen;
+        c.scv[q] = term;
+        c.scg[q] = gen;
+      }
+    }
+    t = max64(t, term);
+  }
+  return t;
+}
+
+__device__ __forceinline__ int64_t urgency_e(const Ctx &c, int j) {
+  int64_t u = 0;
+  for (int x = c.in_off[j]; x < c.in_off[j + 1]; ++x) u = max64(u, c.pfin[x] + c.in_c[x]);
+  return u;
+}
 
 __device__ __forceinline__ int64_t col_key(const Ctx &c, int q, int s, int j) {
   int64_t t = max64(c.Kc[static_cast<int64_t>(q) * c.V + s], c.F[q]);
@@ -51,69 +119,97 @@ __device__ __forceinline__ int64_t col_key(const Ctx &c, int q, int s, int j) {
   return t;
 }
 
-// Warp rescan of column q over ready slots [0, R): exact top-KT list.
-__device__ void rescan(const Ctx &c, const Tops &T, int q, int R, int lane) {
+// ---- column scans ------------------------------------------------------------
+__device__ __forceinline__ void topk_insert(int64_t (&lt)[KT], int (&lj)[KT], int (&ls)[KT], int64_t t, int j,
+                                            int s) {
+  if (!lex_less(t, j, lt[KT - 1], lj[KT - 1])) return;
+  lt[KT - 1] = t;
+  lj[KT - 1] = j;
+  ls[KT - 1] = s;
+#pragma unroll
+  for (int k = KT - 1; k > 0; --k) {
+    if (lex_less(lt[k], lj[k], lt[k - 1], lj[k - 1])) {
+      int64_t a = lt[k];
+      lt[k] = lt[k - 1];
+      lt[k - 1] = a;
+      int b = lj[k];
+      lj[k] = lj[k - 1];
+      lj[k - 1] = b;
+      b = ls[k];
+      ls[k] = ls[k - 1];
+      ls[k - 1] = b;
+    }
+  }
+}
+
+// This warp's exact top-KT of column q over slots s0 + lane + k*step < R;
+// KT rounds of warp argmin leave the result in lane 0 (dt/dj/ds, cnt) and the
+// live-pair count in every lane.
+__device__ void warp_topk(const Ctx &c, int q, int s0, int step, int R, int lane, int64_t (&dt)[KT],
+                          int (&dj)[KT], int (&ds)[KT], int &cnt, int &live) {
   int64_t lt[KT];
-  int lj[KT];
+  int lj[KT], ls[KT];
 #pragma unroll
   for (int k = 0; k < KT; ++k) {
     lt[k] = kInf;
     lj[k] = INT32_MAX;
+    ls[k] = -1;
   }
-  int live = 0;
-  const uint8_t *dcol = c.deadc + static_cast<int64_t>(q) * c.V;
-  for (int s = lane; s < R; s += 32) {
-    if (dcol[s]) continue;
-    ++live;
-    int j = c.node_s[s];
-    int64_t t = col_key(c, q, s, j);
-    if (lex_less(t, j, lt[KT - 1], lj[KT - 1])) {
-      lt[KT - 1] = t;
-      lj[KT - 1] = j;
+  live = 0;
+  const int64_t *kcol = c.Kc + static_cast<int64_t>(q) * c.V;
+  const int64_t Fq = c.F[q];
+  const int aw = c.sct ? c.awf[q] : -1;
+  const int64_t awu = aw >= 0 ? c.awu[q] : 0;
+  constexpr int U = 4;
+  for (int base = s0 + lane; base < R; base += U * step) {
+    int64_t kv[U];
+    int nd[U];
+    int64_t ug[U];
 #pragma unroll
-      for (int k = KT - 1; k > 0; --k) {
-        if (lex_less(lt[k], lj[k], lt[k - 1], lj[k - 1])) {
-          int64_t a = lt[k];
-          lt[k] = lt[k - 1];
-          lt[k - 1] = a;
-          int b = lj[k];
-          lj[k] = lj[k - 1];
-          lj[k - 1] = b;
-        }
-      }
+    for (int u = 0; u < U; ++u) {
+      int s = base + u * step;
+      kv[u] = s < R ? kcol[s] : kInf;
+      nd[u] = s < R ? c.node_s[s] : 0;
+      ug[u] = (aw >= 0 && s < R) ? c.urg_s[s] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (kv[u] == kInf) continue;
+      ++live;
+      int64_t t = max64(kv[u], Fq);
+      if (aw >= 0 && aw != nd[u]) t = max64(t, min64(awu, ug[u]));
+      topk_insert(lt, lj, ls, t, nd[u], base + u * step);
     }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(kFull, live, o);
-  int cnt = 0;
+  cnt = 0;
 #pragma unroll
   for (int r = 0; r < KT; ++r) {
     int64_t bt = lt[0];
     int64_t bj = lj[0];
     warp_argmin(bt, bj);
+    int bs = __shfl_sync(kFull, ls[0], __ffs(__ballot_sync(kFull, lj[0] == bj && lt[0] == bt)) - 1);
+    dt[r] = bt;
+    dj[r] = static_cast<int>(bj);
+    ds[r] = bs;
     if (bt == kInf) break;
-    if (lane == 0) {
-      T.t[q * KT + r] = bt;
-      T.j[q * KT + r] = static_cast<int>(bj);
-    }
     ++cnt;
-    if (lj[0] == bj) {  // the owning lane pops its head
+    if (lj[0] == bj && lt[0] == bt) {  // the owning lane pops its head
 #pragma unroll
       for (int k = 0; k < KT - 1; ++k) {
         lt[k] = lt[k + 1];
         lj[k] = lj[k + 1];
+        ls[k] = ls[k + 1];
       }
       lt[KT - 1] = kInf;
       lj[KT - 1] = INT32_MAX;
+      ls[KT - 1] = -1;
     }
-  }
-  if (lane == 0) {
-    T.cnt[q] = cnt;
-    T.flg[q] = live <= KT ? kComplete : 0;
   }
 }
 
-// Lane-owned list edits (the lane with q % 32 == lane owns column q).
+// ---- lane-owned list edits (lane q % 32 owns column q) -------------------------
 __device__ __forceinline__ void list_remove(const Tops &T, int q, int j) {
   int c = T.cnt[q];
   int at = -1;
@@ -123,21 +219,19 @@ __device__ __forceinline__ void list_remove(const Tops &T, int q, int j) {
   for (int k = at; k + 1 < c; ++k) {
     T.t[q * KT + k] = T.t[q * KT + k + 1];
     T.j[q * KT + k] = T.j[q * KT + k + 1];
+    T.s[q * KT + k] = T.s[q * KT + k + 1];
   }
   T.cnt[q] = --c;
   if (c == 0 && !(T.flg[q] & kComplete)) T.flg[q] |= kDirty;
 }
 
-__device__ __forceinline__ void list_insert(const Tops &T, int q, int64_t t, int j) {
+__device__ __forceinline__ void list_insert(const Tops &T, int q, int64_t t, int j, int s) {
   int c = T.cnt[q];
   int f = T.flg[q];
   if (f & kDirty) return;
   if (c == KT) {
-    if (!lex_less(t, j, T.t[q * KT + KT - 1], T.j[q * KT + KT - 1])) {
-      T.flg[q] = f & ~kComplete;  // a live pair now sits outside the list
-      return;
-    }
-    T.flg[q] = f & ~kComplete;  // the dropped tail is no longer listed
+    T.flg[q] = f & ~kComplete;  // a live pair now sits outside the list
+    if (!lex_less(t, j, T.t[q * KT + KT - 1], T.j[q * KT + KT - 1])) return;
     --c;
   } else if (!(f & kComplete)) {
     // incomplete list: only pairs that beat the last listed one are known
@@ -147,53 +241,61 @@ __device__ __forceinline__ void list_insert(const Tops &T, int q, int64_t t, int
   while (k > 0 && lex_less(t, j, T.t[q * KT + k - 1], T.j[q * KT + k - 1])) {
     T.t[q * KT + k] = T.t[q * KT + k - 1];
     T.j[q * KT + k] = T.j[q * KT + k - 1];
+    T.s[q * KT + k] = T.s[q * KT + k - 1];
     --k;
   }
   T.t[q * KT + k] = t;
   T.j[q * KT + k] = j;
+  T.s[q * KT + k] = s;
   T.cnt[q] = c + 1;
 }
 
-constexpr int kListSmemPerDevice = 5 * 8 + 2 * 4 + KT * 12 + 2 * 4;  // bytes per device column
+// bytes of shared memory per device column per problem
+constexpr int kSmemPerDevice = 5 * 8 + KT * 8 + 2 * 4 + 2 * KT * 4 + 2 * 4;
+__host__ __device__ constexpr int stage_bytes_per_device(int w) { return w > 1 ? w * (KT * 16 + 4) : 0; }
 
-// Latency breakdown (kProf builds only): cycles since the last mark are
-// charged to a phase slot; lane 0's totals are written at the end.
-#define BX_MARK(slot)                       \
-  do {                                      \
-    if (kProf) {                            \
-      int64_t now_ = clock64();             \
-      prof[slot] += now_ - prof_last;       \
-      prof_last = now_;                     \
-    }                                       \
+#define BX_MARK(slot)                 \
+  do {                                \
+    if (kProf) {                      \
+      int64_t now_ = clock64();       \
+      prof[slot] += now_ - prof_last; \
+      prof_last = now_;               \
+    }                                 \
   } while (0)
 
-template <int kWarps, bool kProf>
-__global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs, const int32_t *order,
-                                                                        int njobs, const DGraph *graphs,
-                                                                        const DPrep *preps, int maxn) {
+template <int kW>
+__device__ __forceinline__ void group_sync() {
+  if (kW > 1) __syncthreads();
+  else __syncwarp();
+}
+
+template <int kW, bool kProf>
+__global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
+    k_place_list(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
+                 int maxn, int seq_only) {
   extern __shared__ __align__(16) unsigned char smem[];
   int64_t prof[kProfSlots];
   int64_t prof_last = 0;
   if (kProf) {
 #pragma unroll
     for (int k = 0; k < kProfSlots; ++k) prof[k] = 0;
-    prof_last = clock64();
   }
   const int64_t prof_t0 = kProf ? clock64() : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot_id = blockIdx.x * kWarps + warp;
-  if (slot_id >= njobs) return;
+  const int gw = kW > 1 ? warp : 0;             // warp index inside the problem's group
+  const int pslot = kW > 1 ? 0 : warp;          // problem index inside the CTA
+  const int slot_id = kW > 1 ? blockIdx.x : blockIdx.x * 4 + warp;
+  if (slot_id >= njobs) return;                 // uniform per problem group
   const DJob jb = jobs[order[slot_id]];
-  if (jb.skip || jb.algo == 0) return;
+  if (jb.skip || jb.algo == 0 || (seq_only && jb.mode == 1)) return;
   const DGraph g = graphs[jb.graph];
   const DPrep pr = preps[jb.prep];
   // acyclicity then byte-count validation, in the reference's order
-  if (g.flags[0] != g.V) {
-    if (lane == 0) set_err(jb.err, kValidation, E_CYCLE, 0, 0);
-    return;
-  }
-  if (g.flags[1]) {
-    if (lane == 0) set_err(jb.err, kValidation, E_NEG_BYTES, 0, 0);
+  if (g.flags[0] != g.V || g.flags[1]) {
+    if (gw == 0 && lane == 0) {
+      if (g.flags[0] != g.V) set_err(jb.err, kValidation, E_CYCLE, 0, 0);
+      else set_err(jb.err, kValidation, E_NEG_BYTES, 0, 0);
+    }
     return;
   }
 
@@ -217,7 +319,7 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
   c.finish = jb.finish;
   c.urg_s = jb.urgent;
   c.start = jb.start;
-  c.deadc = jb.dead;
+  c.deadc = nullptr;
   c.pending = jb.pending;
   c.alive_s = jb.alive;
   c.node_s = jb.ready;
@@ -227,87 +329,188 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
   c.nc = jb.nc;
   c.scv = jb.sc_val + static_cast<int64_t>(lane) * jb.n;
   c.scg = jb.sc_gen + static_cast<int64_t>(lane) * jb.n;
+  c.pdev = jb.pdev;
+  c.pfin = jb.pfin;
+  c.inpos = g.inpos;
   Tops T;
+  int64_t *stg_t = nullptr;
+  int32_t *stg_j = nullptr, *stg_s = nullptr, *stg_live = nullptr;
+  int32_t *s_R, *s_done;
   {
-    unsigned char *base = smem + static_cast<size_t>(warp) * (maxn * kListSmemPerDevice);
+    const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 16;
+    unsigned char *base = smem + static_cast<size_t>(pslot) * per;
     c.F = reinterpret_cast<int64_t *>(base);
     c.tail = c.F + maxn;
     c.res = c.tail + maxn;
     c.capS = c.res + maxn;
     c.awu = c.capS + maxn;
     T.t = c.awu + maxn;
-    c.awf = reinterpret_cast<int32_t *>(T.t + maxn * KT);
+    int64_t *p64 = T.t + maxn * KT;
+    if (kW > 1) {
+      stg_t = p64;
+      p64 += static_cast<size_t>(maxn) * kW * KT;
+    }
+    int32_t *p32 = reinterpret_cast<int32_t *>(p64);
+    c.awf = p32;
     c.excl = c.awf + maxn;
     T.j = c.excl + maxn;
-    T.cnt = T.j + maxn * KT;
+    T.s = T.j + maxn * KT;
+    T.cnt = T.s + maxn * KT;
     T.flg = T.cnt + maxn;
+    p32 = T.flg + maxn;
+    if (kW > 1) {
+      stg_j = p32;
+      stg_s = stg_j + maxn * kW * KT;
+      stg_live = stg_s + maxn * kW * KT;
+      p32 = stg_live + maxn * kW;
+    }
+    s_R = p32;
+    s_done = p32 + 1;
   }
   const int V = c.V, n = c.n;
   const int64_t Vs = V;
-  for (int d = lane; d < n; d += 32) {
-    c.F[d] = 0;
-    c.tail[d] = 0;
-    c.res[d] = 0;
-    c.capS[d] = c.cap[d];
-    c.awu[d] = 0;
-    c.awf[d] = -1;
-    c.excl[d] = 0;
-    T.cnt[d] = 0;
-    T.flg[d] = kDirty;
-  }
-  // per-node init + initial ready slots (sources), keys 0 (dev_free = 0)
-  int R = 0;
-  for (int base = 0; base < V; base += 32) {
-    int j = base + lane;
-    bool src = false;
-    if (j < V) {
-      int indeg = g.in_off[j + 1] - g.in_off[j];
-      c.pending[j] = indeg;
-      c.device_of[j] = -1;
-      c.finish[j] = 0;
-      src = indeg == 0;
+  const bool leader = gw == 0;
+
+  if (leader) {
+    for (int d = lane; d < n; d += 32) {
+      c.F[d] = 0;
+      c.tail[d] = 0;
+      c.res[d] = 0;
+      c.capS[d] = c.cap[d];
+      c.awu[d] = 0;
+      c.awf[d] = -1;
+      c.excl[d] = 0;
+      T.cnt[d] = 0;
+      T.flg[d] = kDirty;
     }
-    R = ready_append(c, R, src, j, lane);
-  }
-  __syncwarp();
-  for (int s = lane; s < R; s += 32) {
-    c.urg_s[s] = 0;
-    c.alive_s[s] = n;
-  }
-  for (int q = 0; q < n; ++q)
+    // per-node init + initial ready slots (sources), keys 0 (dev_free = 0)
+    int R = 0;
+    for (int base = 0; base < V; base += 32) {
+      int j = base + lane;
+      bool src = false;
+      if (j < V) {
+        int indeg = g.in_off[j + 1] - g.in_off[j];
+        c.pending[j] = indeg;
+        c.device_of[j] = -1;
+        c.finish[j] = 0;
+        src = indeg == 0;
+      }
+      R = ready_append(c, R, src, j, lane);
+    }
+    __syncwarp();
     for (int s = lane; s < R; s += 32) {
-      c.Kc[q * Vs + s] = 0;
-      c.deadc[q * Vs + s] = 0;
+      c.urg_s[s] = 0;
+      c.alive_s[s] = n;
     }
-  __syncwarp();
+    for (int q = 0; q < n; ++q)
+      for (int s = lane; s < R; s += 32) c.Kc[q * Vs + s] = 0;
+    if (lane == 0) {
+      *s_R = R;
+      *s_done = V == 0;
+    }
+  }
 
   int32_t gen = 0;
   int placed = 0, nexcl = 0;
   int64_t discarded = 0, excluded = 0, awake = 0;
-  int minptr = 0;  // lane 0: first possibly-unplaced slot of need_order
-
+  int minptr = 0;  // lane 0 of the leader: first possibly-unplaced slot of need_order
+  int err_status = 0, err_code = 0, err_node = 0;
   if (kProf) prof_last = clock64();
-  while (placed < V) {
+
+  while (true) {
+    group_sync<kW>();
+    if (*s_done) break;
+    int R = *s_R;
     if (kProf) ++prof[P_STEPS];
-    // ---- refresh dirty columns ------------------------------------------
+    // ---- refresh dirty columns (every warp of the group) -------------------
     for (int q0 = 0; q0 < n; q0 += 32) {
       int q = q0 + lane;
       unsigned m = __ballot_sync(kFull, q < n && (T.flg[q] & kDirty) && !c.excl[q]);
       while (m) {
         int qq = q0 + __ffs(m) - 1;
         m &= m - 1;
-        rescan(c, T, qq, R, lane);
+        int64_t dt[KT];
+        int dj[KT], ds[KT], cnt, live;
+        warp_topk(c, qq, gw * 32, 32 * kW, R, lane, dt, dj, ds, cnt, live);
         if (kProf) ++prof[P_RESCANS];
+        if (lane == 0) {
+          if (kW == 1) {
+#pragma unroll
+            for (int k = 0; k < KT; ++k) {
+              T.t[qq * KT + k] = dt[k];
+              T.j[qq * KT + k] = dj[k];
+              T.s[qq * KT + k] = ds[k];
+            }
+            T.cnt[qq] = cnt;
+            T.flg[qq] = live <= KT ? kComplete : 0;
+          } else {
+#pragma unroll
+            for (int k = 0; k < KT; ++k) {
+              stg_t[(qq * kW + gw) * KT + k] = k < cnt ? dt[k] : kInf;
+              stg_j[(qq * kW + gw) * KT + k] = k < cnt ? dj[k] : INT32_MAX;
+              stg_s[(qq * kW + gw) * KT + k] = ds[k];
+            }
+            stg_live[qq * kW + gw] = live;
+          }
+        }
+      }
+    }
+    if (kW > 1) {
+      __syncthreads();
+      if (!leader) continue;
+      // merge the group's partial lists (kW*KT <= 32 candidates per column)
+      for (int q0 = 0; q0 < n; q0 += 32) {
+        int q = q0 + lane;
+        unsigned m = __ballot_sync(kFull, q < n && (T.flg[q] & kDirty) && !c.excl[q]);
+        while (m) {
+          int qq = q0 + __ffs(m) - 1;
+          m &= m - 1;
+          int64_t ct = kInf;
+          int cj = INT32_MAX, cs = -1, lv = 0;
+          if (lane < kW * KT) {
+            ct = stg_t[qq * kW * KT + lane];
+            cj = stg_j[qq * kW * KT + lane];
+            cs = stg_s[qq * kW * KT + lane];
+          }
+          if (lane < kW) lv = stg_live[qq * kW + lane];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) lv += __shfl_xor_sync(kFull, lv, o);
+          int cnt = 0;
+#pragma unroll
+          for (int r = 0; r < KT; ++r) {
+            int64_t bt = ct;
+            int64_t bj = cj;
+            warp_argmin(bt, bj);
+            if (bt == kInf) break;
+            unsigned own = __ballot_sync(kFull, cj == bj && ct == bt);
+            int bs = __shfl_sync(kFull, cs, __ffs(own) - 1);
+            if (lane == 0) {
+              T.t[qq * KT + r] = bt;
+              T.j[qq * KT + r] = static_cast<int>(bj);
+              T.s[qq * KT + r] = bs;
+            }
+            ++cnt;
+            if (cj == bj && ct == bt) {
+              ct = kInf;
+              cj = INT32_MAX;
+            }
+          }
+          if (lane == 0) {
+            T.cnt[qq] = cnt;
+            T.flg[qq] = lv <= KT ? kComplete : 0;
+          }
+        }
       }
     }
     __syncwarp();
     BX_MARK(P_RESCAN);
-    // ---- argmin over column heads: lexicographic (key, node, device) ------
+
+    // ---- leader only from here: argmin over column heads (key, node, device)
     int64_t bt = kInf, bi = kInf;
     for (int q = lane; q < n; q += 32) {
       if (c.excl[q] || T.cnt[q] == 0) continue;
       int64_t t = T.t[q * KT];
-      int64_t cell = static_cast<int64_t>(T.j[q * KT]) * n + q;
+      int64_t cell = (static_cast<int64_t>(T.j[q * KT]) << 16) | q;
       if (lex_less(t, cell, bt, bi)) {
         bt = t;
         bi = cell;
@@ -315,19 +518,21 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
     }
     warp_argmin(bt, bi);
     if (bi == kInf) {
-      if (lane == 0) set_err(jb.err, kInfeasible, E_NO_PAIR, 0, 0);
-      return;
+      err_status = kInfeasible;
+      err_code = E_NO_PAIR;
+      if (lane == 0) *s_done = 1;
+      continue;
     }
-    const int j = static_cast<int>(bi / n);
-    const int p = static_cast<int>(bi - static_cast<int64_t>(j) * n);
+    const int j = static_cast<int>(bi >> 16);
+    const int p = static_cast<int>(bi & 0xffff);
     const int64_t t = bt;
-    const int sj = c.rpos[j];
+    const int sj = T.s[p * KT];
     BX_MARK(P_ARGMIN);
 
     if (c.mode == 0) {
       // lazy re-key of the winner (placers.cpp:198-202)
       int64_t fresh = 0;
-      if (lane == 0) fresh = est_time(c, j, p, c.F[p], gen);
+      if (lane == 0) fresh = key_of(c, j, p, gen);
       fresh = __shfl_sync(kFull, fresh, 0);
       int64_t key = fresh;
       if (c.sct) {
@@ -351,13 +556,16 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
       // discard (placers.cpp:203-219)
       int left = 0;
       if (lane == 0) {
-        c.deadc[p * Vs + sj] = 1;
+        c.Kc[p * Vs + sj] = kInf;
         left = --c.alive_s[sj];
       }
       left = __shfl_sync(kFull, left, 0);
       if (left == 0) {
-        if (lane == 0) set_err(jb.err, kInfeasible, E_FITS_NONE, j, 0);
-        return;
+        err_status = kInfeasible;
+        err_code = E_FITS_NONE;
+        err_node = j;
+        if (lane == 0) *s_done = 1;
+        continue;
       }
       ++discarded;
       if (lane == (p & 31)) list_remove(T, p, j);
@@ -377,8 +585,8 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
         ++nexcl;
         int first_dead = INT32_MAX;
         for (int s = lane; s < R; s += 32) {
-          if (!c.deadc[p * Vs + s]) {
-            c.deadc[p * Vs + s] = 1;
+          if (c.Kc[p * Vs + s] != kInf) {
+            c.Kc[p * Vs + s] = kInf;
             if (--c.alive_s[s] == 0) first_dead = min(first_dead, c.node_s[s]);
           }
         }
@@ -388,8 +596,11 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
         }
         first_dead = warp_min_i32(first_dead);
         if (first_dead != INT32_MAX) {
-          if (lane == 0) set_err(jb.err, kInfeasible, E_FITS_NONE, first_dead, 0);
-          return;
+          err_status = kInfeasible;
+          err_code = E_FITS_NONE;
+          err_node = first_dead;
+          if (lane == 0) *s_done = 1;
+          continue;
         }
         if (lane == 0) c.excl[p] = 1;
       }
@@ -401,35 +612,71 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
     // ---- commit (placers.cpp:221-233) ------------------------------------
     const int64_t fin = t + c.k[j];
     int ncount = 0;
+    if (c.mode == 1) {
+      // commit_schedulable_time, parallel mode: every remote uncached parent
+      // tensor lands on p at finish + c_e; order-free, so lanes split parents
+      for (int x0 = c.in_off[j]; x0 < c.in_off[j + 1]; x0 += 32) {
+        int x = x0 + lane;
+        bool fresh = false;
+        int i = 0;
+        if (x < c.in_off[j + 1]) {
+          i = c.in_src[x];
+          if (c.pdev[x] != p) {
+            int64_t *slot = c.cache + static_cast<int64_t>(i) * n + p;
+            if (*slot < 0) {
+              *slot = c.pfin[x] + c.in_c[x];
+              fresh = true;
+            }
+          }
+        }
+        unsigned m = __ballot_sync(kFull, fresh);
+        if (fresh) c.nc[ncount + __popc(m & ((1u << lane) - 1u))] = i;
+        ncount += __popc(m);
+      }
+    } else if (lane == 0) {
+      // sequential mode: the fold walks parents in ascending order on the
+      // live queue tails (placers.cpp:62-69)
+      for (int x = c.in_off[j]; x < c.in_off[j + 1]; ++x) {
+        int d = c.pdev[x];
+        if (d == p) continue;
+        int i = c.in_src[x];
+        int64_t *slot = c.cache + static_cast<int64_t>(i) * n + p;
+        if (*slot >= 0) continue;
+        int64_t term = max64(c.pfin[x], max64(c.tail[d], c.tail[p])) + c.in_c[x];
+        c.tail[d] = term;
+        c.tail[p] = term;
+        *slot = term;
+        c.nc[ncount++] = i;
+      }
+    }
+    if (c.mode == 0) ncount = __shfl_sync(kFull, ncount, 0);
     if (lane == 0) {
       c.device_of[j] = p;
       c.start[j] = t;
       c.finish[j] = fin;
-      commit_fold(c, j, p, &ncount);
       c.F[p] = fin;
       c.res[p] += needj;
       c.cseq[placed] = j;
     }
-    ncount = __shfl_sync(kFull, ncount, 0);
     ++placed;
     if (kProf) ++prof[P_COMMITS];
     BX_MARK(P_COMMIT);
-    // swap-remove slot sj: the last slot moves in
+    // swap-remove slot sj: the last slot moves in (lists follow its slot)
     const int last = R - 1;
     if (sj != last) {
-      for (int q = lane; q < n; q += 32) {
-        c.Kc[q * Vs + sj] = c.Kc[q * Vs + last];
-        c.deadc[q * Vs + sj] = c.deadc[q * Vs + last];
-      }
+      for (int q = lane; q < n; q += 32) c.Kc[q * Vs + sj] = c.Kc[q * Vs + last];
+      const int mv = c.node_s[last];
       if (lane == 0) {
-        int mv = c.node_s[last];
         c.node_s[sj] = mv;
         c.urg_s[sj] = c.urg_s[last];
         c.alive_s[sj] = c.alive_s[last];
         c.rpos[mv] = sj;
       }
+      for (int e = lane; e < n * KT; e += 32)
+        if (T.j[e] == mv) T.s[e] = sj;
     }
     --R;
+    __syncwarp();
     // j leaves every column; column p's keys moved with F[p]
     for (int q = lane; q < n; q += 32) {
       if (q == p) T.flg[q] |= kDirty;
@@ -459,7 +706,7 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
     __syncwarp();
     BX_MARK(P_REMOVE);
 
-    // ---- readiness (placers.cpp:256-268) ---------------------------------
+    // ---- readiness (placers.cpp:256-268); publish j to its children's slots
     const int R0 = R;
     for (int base = c.out_off[j]; base < c.out_off[j + 1]; base += 32) {
       int y = base + lane;
@@ -467,6 +714,9 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
       int child = -1;
       if (y < c.out_off[j + 1]) {
         child = c.out_dst[y];
+        int x = c.inpos[y];
+        c.pdev[x] = p;
+        c.pfin[x] = fin;
         fresh = --c.pending[child] == 0;
       }
       R = ready_append(c, R, fresh, child, lane);
@@ -477,13 +727,12 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
     if (nnew > 0) {
       for (int s = R0 + lane; s < R; s += 32) {
         c.alive_s[s] = n - nexcl;
-        c.urg_s[s] = c.sct ? urgency(c, c.node_s[s]) : 0;
+        c.urg_s[s] = c.sct ? urgency_e(c, c.node_s[s]) : 0;
       }
       for (int r = lane; r < nnew * n; r += 32) {
         int s = R0 + r / n;
         int q = r % n;
-        c.Kc[q * Vs + s] = row_value(c, c.node_s[s], q, gen);
-        c.deadc[q * Vs + s] = static_cast<uint8_t>(c.excl[q] != 0);
+        c.Kc[q * Vs + s] = c.excl[q] ? kInf : key_of(c, c.node_s[s], q, gen);
       }
     }
     __syncwarp();
@@ -493,11 +742,11 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
       int i = c.nc[a];
       for (int y = c.out_off[i] + lane; y < c.out_off[i + 1]; y += 32) {
         int cc = c.out_dst[y];
-        if (cc == j || c.device_of[cc] >= 0 || c.pending[cc] != 0) continue;
+        if (cc == j || c.pending[cc] != 0 || c.device_of[cc] >= 0) continue;
         int s = c.rpos[cc];
         if (s >= R0) continue;  // new rows were keyed after the cache update
-        if (c.deadc[p * Vs + s]) continue;
-        c.Kc[p * Vs + s] = row_value(c, cc, p, gen);
+        if (c.Kc[p * Vs + s] == kInf) continue;
+        c.Kc[p * Vs + s] = key_of(c, cc, p, gen);
       }
     }
     __syncwarp();
@@ -508,14 +757,23 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
         if (c.excl[q] || (T.flg[q] & kDirty)) continue;
         for (int s = R0; s < R; ++s) {
           int node = c.node_s[s];
-          list_insert(T, q, col_key(c, q, s, node), node);
+          list_insert(T, q, col_key(c, q, s, node), node, s);
         }
       }
+    }
+    if (lane == 0) {
+      *s_R = R;
+      if (placed == V) *s_done = 1;
     }
     __syncwarp();
     BX_MARK(P_INSERT);
   }
 
+  if (!leader) return;
+  if (err_status) {
+    if (lane == 0) set_err(jb.err, err_status, err_code, err_node, 0);
+    return;
+  }
   emit_exec_order(c, jb, c.excl, lane);
   BX_MARK(P_EMIT);
   if (lane == 0) {
@@ -530,19 +788,713 @@ __global__ void __launch_bounds__(32 * kWarps, 7) k_place_list(const DJob *jobs,
   }
 }
 
+template <int kW, bool kProf>
+static void launch_w(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
+                     int maxn, int seq_only, cudaStream_t s) {
+  const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 16;
+  const int probs_per_cta = kW > 1 ? 1 : 4;
+  const int threads = kW > 1 ? 32 * kW : 128;
+  const int blocks = (njobs + probs_per_cta - 1) / probs_per_cta;
+  const size_t sm = per * probs_per_cta;
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(k_place_list<kW, kProf>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  k_place_list<kW, kProf><<<blocks, threads, sm, s>>>(jobs, order, njobs, graphs, preps, maxn, seq_only);
+}
+
+// ============================================================================
+// K2r — the round kernel: m-ETF (and m-SCT, one commit per round) in
+// parallel comm mode, one problem per 256-thread CTA.
+//
+// Exactness argument. After committing (j, p) at time t, every key that can
+// change or appear is >= t + k_j: column p's keys are >= F[p] = t + k_j, a
+// cached parent only touches column p, and a newly ready child has j as a
+// parent, so its key is >= finish(j) = t + k_j on every device. Hence, with
+// the per-column top lists exact for every column not touched this round,
+// the next global argmin is the smallest clean head whose key is strictly
+// below min(F[q] over touched ("dirty") columns): it can be committed without
+// re-keying anything. A round commits such heads greedily (at most one per
+// column), then the whole CTA does the global-memory work of all of them at
+// once: cache arrivals, readiness, new key rows, cached-consumer re-keys, and
+// the rescans of the touched columns.
+// m-SCT commits one pair per round (a lifted reservation may lower keys in
+// another column); discards and exclusions are handled inline by the leader.
+// ============================================================================
+constexpr int RWARPS = 8;
+
+struct REnt {
+  int64_t t, need, k;
+  int32_t j, s, fav, inb, ine, outb, oute, pad;
+};
+
+struct RCommit {
+  int64_t t, fin;
+  int32_t j, q, s, inb, ine, outb, oute, pad;
+};
+
+__device__ __forceinline__ void rent_meta(REnt &e, const Ctx &c, const DGraph &g) {
+  e.need = c.need[e.j];
+  e.k = g.k[e.j];
+  e.fav = c.fav ? c.fav[e.j] : -1;
+  e.inb = g.in_off[e.j];
+  e.ine = g.in_off[e.j + 1];
+  e.outb = g.out_off[e.j];
+  e.oute = g.out_off[e.j + 1];
+}
+
+// lane-owned list edits on REnt lists (lane q % 32 owns column q)
+__device__ __forceinline__ void rlist_remove(REnt *L, int32_t *cnt, int32_t *flg, int q, int j) {
+  int c = cnt[q];
+  int at = -1;
+  for (int k = 0; k < c; ++k)
+    if (L[q * KT + k].j == j) at = k;
+  if (at < 0) return;
+  for (int k = at; k + 1 < c; ++k) L[q * KT + k] = L[q * KT + k + 1];
+  cnt[q] = --c;
+  if (c == 0 && !(flg[q] & kComplete)) flg[q] |= kDirty;
+}
+
+// insert a fully built entry; returns nothing (list stays exact top-cnt)
+__device__ __forceinline__ void rlist_insert(REnt *L, int32_t *cnt, int32_t *flg, int q, const REnt &e) {
+  int c = cnt[q];
+  int f = flg[q];
+  if (f & kDirty) return;
+  if (c == KT) {
+    flg[q] = f & ~kComplete;
+    if (!lex_less(e.t, e.j, L[q * KT + KT - 1].t, L[q * KT + KT - 1].j)) return;
+    --c;
+  } else if (!(f & kComplete)) {
+    if (c == 0 || !lex_less(e.t, e.j, L[q * KT + c - 1].t, L[q * KT + c - 1].j)) return;
+  }
+  int k = c;
+  while (k > 0 && lex_less(e.t, e.j, L[q * KT + k - 1].t, L[q * KT + k - 1].j)) {
+    L[q * KT + k] = L[q * KT + k - 1];
+    --k;
+  }
+  L[q * KT + k] = e;
+  cnt[q] = c + 1;
+}
+
+struct RShared {
+  int32_t R, live, placed, done, nnew, nnc, ncommit, ndirty, nexcl, compact;
+  int32_t err_status, err_code, err_node, pad;
+  int64_t discarded, excluded, awake;
+};
+
+__global__ void __launch_bounds__(RWARPS * 32, 1)
+    k_place_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
+                   int maxn) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
+  constexpr int NT = RWARPS * 32;
+  if (blockIdx.x >= njobs) return;
+  const DJob jb = jobs[order[blockIdx.x]];
+  if (jb.skip || jb.algo == 0 || jb.mode != 1) return;
+  const DGraph g = graphs[jb.graph];
+  const DPrep pr = preps[jb.prep];
+  if (g.flags[0] != g.V || g.flags[1]) {
+    if (tid == 0) set_err(jb.err, kValidation, g.flags[0] != g.V ? E_CYCLE : E_NEG_BYTES, 0, 0);
+    return;
+  }
+  Ctx c;
+  c.V = g.V;
+  c.n = jb.n;
+  c.mode = 1;
+  c.sct = (jb.algo == 2 && jb.fav != nullptr);
+  c.k = g.k;
+  c.need = g.need;
+  c.in_c = pr.in_c;
+  c.cap = jb.cap;
+  c.in_off = g.in_off;
+  c.in_src = g.in_src;
+  c.out_off = g.out_off;
+  c.out_dst = g.edst;
+  c.fav = c.sct ? jb.fav : nullptr;
+  c.cmax = *pr.cmax;
+  c.Kc = jb.K;
+  c.cache = jb.cache;
+  c.finish = jb.finish;
+  c.urg_s = jb.urgent;
+  c.start = jb.start;
+  c.deadc = nullptr;
+  c.pending = jb.pending;
+  c.alive_s = jb.alive;
+  c.node_s = jb.ready;
+  c.rpos = jb.rpos;
+  c.device_of = jb.device_of;
+  c.cseq = jb.cseq;
+  c.nc = jb.nc;
+  c.scv = nullptr;
+  c.scg = nullptr;
+  c.pdev = jb.pdev;
+  c.pfin = jb.pfin;
+  c.inpos = g.inpos;
+  // double buffers for compaction
+  int64_t *Kb = jb.K2, *Ub = jb.urgent2;
+  int32_t *Nb = jb.ready2, *Ab = jb.alive2;
+
+  // ---- shared memory --------------------------------------------------------
+  const int n = c.n, V = c.V;
+  const int64_t Vs = V;
+  RShared *S = reinterpret_cast<RShared *>(smem);
+  unsigned char *p = smem + ((sizeof(RShared) + 15) & ~size_t(15));
+  c.F = reinterpret_cast<int64_t *>(p);
+  c.tail = c.F + maxn;  // unused in parallel mode
+  c.res = c.tail + maxn;
+  c.capS = c.res + maxn;
+  c.awu = c.capS + maxn;
+  REnt *L = reinterpret_cast<REnt *>(c.awu + maxn);
+  RCommit *CM = reinterpret_cast<RCommit *>(L + maxn * KT);
+  int64_t *stg_t = reinterpret_cast<int64_t *>(CM + maxn);
+  const int ntask = maxn > RWARPS ? maxn : RWARPS;
+  int32_t *stg_j = reinterpret_cast<int32_t *>(stg_t + ntask * KT);
+  int32_t *stg_s = stg_j + ntask * KT;
+  int32_t *stg_live = stg_s + ntask * KT;
+  c.awf = stg_live + ntask;
+  c.excl = c.awf + maxn;
+  int32_t *cnt = c.excl + maxn;
+  int32_t *flg = cnt + maxn;
+  int32_t *dcols = flg + maxn;
+  int32_t *inoff = dcols + maxn;    // [maxn+1] prefix of committed in-degrees
+  int32_t *outoff = inoff + maxn + 1;  // [maxn+1] prefix of committed out-degrees
+  int32_t *wsum = outoff + maxn + 1;  // [RWARPS+1] compaction prefix
+
+  // ---- init -------------------------------------------------------------------
+  if (tid == 0) {
+    S->R = 0;
+    S->live = 0;
+    S->placed = 0;
+    S->done = V == 0;
+    S->nnew = 0;
+    S->nnc = 0;
+    S->ncommit = 0;
+    S->nexcl = 0;
+    S->compact = 0;
+    S->err_status = 0;
+    S->discarded = S->excluded = S->awake = 0;
+  }
+  for (int d = tid; d < n; d += NT) {
+    c.F[d] = 0;
+    c.res[d] = 0;
+    c.capS[d] = c.cap[d];
+    c.awu[d] = 0;
+    c.awf[d] = -1;
+    c.excl[d] = 0;
+    cnt[d] = 0;
+    flg[d] = kDirty;
+  }
+  __syncthreads();
+  for (int j = tid; j < V; j += NT) {
+    int indeg = g.in_off[j + 1] - g.in_off[j];
+    c.pending[j] = indeg;
+    c.device_of[j] = -1;
+    if (indeg == 0) {
+      int s = atomicAdd(&S->R, 1);
+      c.node_s[s] = j;
+      c.rpos[j] = s;
+      c.urg_s[s] = 0;
+      c.alive_s[s] = n;
+    }
+  }
+  __syncthreads();
+  {
+    const int R = S->R;
+    for (int64_t x = tid; x < static_cast<int64_t>(R) * n; x += NT) c.Kc[(x / R) * Vs + (x % R)] = 0;
+    if (tid == 0) {
+      S->live = R;
+      S->ndirty = 0;
+      for (int q = 0; q < n; ++q) dcols[S->ndirty++] = q;
+    }
+  }
+  int minptr = 0;  // tid 0 only
+  // latency breakdown (BX_PROFILE builds): thread 0 charges phase cycles
+  const bool prof = jb.prof != nullptr;
+  int64_t pc[kProfSlots];
+  for (int i = 0; i < kProfSlots; ++i) pc[i] = 0;
+  int64_t plast = clock64();
+  const int64_t pt0 = plast;
+#define RMARK(slot)                    \
+  do {                                 \
+    if (prof && tid == 0) {            \
+      int64_t now_ = clock64();        \
+      pc[slot] += now_ - plast;        \
+      plast = now_;                    \
+    }                                  \
+  } while (0)
+
+  while (true) {
+    __syncthreads();
+    if (S->done) break;
+    if (prof && tid == 0) ++pc[P_STEPS];
+    // ---- compaction of committed (hole) slots, rarely --------------------------
+    if (S->compact) {
+      const int R = S->R;
+      const int chunk = (R + RWARPS - 1) / RWARPS;
+      const int lo = warp * chunk, hi = min(R, lo + chunk);
+      int mine = 0;
+      for (int b = lo; b < hi; b += 32) {
+        int s = b + lane;
+        bool keep = s < hi && c.device_of[c.node_s[s]] < 0;
+        mine += __popc(__ballot_sync(kFull, keep));
+      }
+      if (lane == 0) wsum[warp + 1] = mine;
+      __syncthreads();
+      if (tid == 0) {
+        wsum[0] = 0;
+        for (int w = 0; w < RWARPS; ++w) wsum[w + 1] += wsum[w];
+      }
+      __syncthreads();
+      int base = wsum[warp];
+      for (int b = lo; b < hi; b += 32) {
+        int s = b + lane;
+        bool keep = s < hi && c.device_of[c.node_s[s]] < 0;
+        unsigned m = __ballot_sync(kFull, keep);
+        if (keep) {
+          int to = base + __popc(m & ((1u << lane) - 1u));
+          int node = c.node_s[s];
+          Nb[to] = node;
+          Ub[to] = c.urg_s[s];
+          Ab[to] = c.alive_s[s];
+          c.rpos[node] = to;
+          for (int q = 0; q < n; ++q) Kb[q * Vs + to] = c.Kc[q * Vs + s];
+        }
+        base += __popc(m);
+      }
+      __syncthreads();
+      // last round's new rows follow their nodes (inserted after the rescans)
+      for (int r = tid; r < S->nnew; r += NT) jb.newl[r] = c.rpos[c.node_s[jb.newl[r]]];
+      __syncthreads();
+      // swap buffers (every thread keeps its own copy of the pointers)
+      int64_t *tK = c.Kc;
+      c.Kc = Kb;
+      Kb = tK;
+      int64_t *tU = c.urg_s;
+      c.urg_s = Ub;
+      Ub = tU;
+      int32_t *tN = c.node_s;
+      c.node_s = Nb;
+      Nb = tN;
+      int32_t *tA = c.alive_s;
+      c.alive_s = Ab;
+      Ab = tA;
+      if (tid == 0) {
+        S->R = wsum[RWARPS];
+        S->compact = 0;
+      }
+      // list entries follow their nodes
+      for (int e = tid; e < n * KT; e += NT)
+        if (e % KT < cnt[e / KT]) L[e].s = c.rpos[L[e].j];
+      __syncthreads();
+      RMARK(P_REMOVE);
+    }
+    const int R = S->R;
+    // ---- phase D: rescans of dirty columns, split over the 8 warps ------------
+    const int nd = S->ndirty;
+    if (nd > 0) {
+      const int parts = nd >= RWARPS ? 1 : RWARPS / nd;
+      for (int task = warp; task < nd * parts; task += RWARPS) {
+        const int q = dcols[task / parts], part = task % parts;
+        int64_t dt[KT];
+        int dj[KT], ds[KT], kc, live;
+        warp_topk(c, q, part * 32, 32 * parts, R, lane, dt, dj, ds, kc, live);
+        if (lane == 0) {
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            stg_t[task * KT + k] = k < kc ? dt[k] : kInf;
+            stg_j[task * KT + k] = k < kc ? dj[k] : INT32_MAX;
+            stg_s[task * KT + k] = ds[k];
+          }
+          stg_live[task] = live;
+        }
+      }
+      __syncthreads();
+      for (int ci = warp; ci < nd; ci += RWARPS) {
+        const int q = dcols[ci];
+        int64_t ct = kInf;
+        int cj = INT32_MAX, cs = -1, lv = 0;
+        if (lane < parts * KT) {
+          ct = stg_t[ci * parts * KT + lane];
+          cj = stg_j[ci * parts * KT + lane];
+          cs = stg_s[ci * parts * KT + lane];
+        }
+        if (lane < parts) lv = stg_live[ci * parts + lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lv += __shfl_xor_sync(kFull, lv, o);
+        int kc = 0;
+        REnt mine;
+        mine.j = -1;
+#pragma unroll
+        for (int r = 0; r < KT; ++r) {
+          int64_t bt = ct;
+          int64_t bj = cj;
+          warp_argmin(bt, bj);
+          if (bt == kInf) break;
+          unsigned own = __ballot_sync(kFull, cj == bj && ct == bt);
+          int bs = __shfl_sync(kFull, cs, __ffs(own) - 1);
+          if (lane == r) {
+            mine.t = bt;
+            mine.j = static_cast<int>(bj);
+            mine.s = bs;
+          }
+          ++kc;
+          if (cj == bj && ct == bt) {
+            ct = kInf;
+            cj = INT32_MAX;
+          }
+        }
+        if (lane < kc) {  // metadata of the listed nodes, fetched in parallel
+          rent_meta(mine, c, g);
+          L[q * KT + lane] = mine;
+        }
+        if (lane == 0) {
+          cnt[q] = kc;
+          flg[q] = lv <= KT ? kComplete : 0;
+        }
+      }
+    }
+    if (prof && tid == 0) pc[P_RESCANS] += nd;
+    RMARK(P_RESCAN);
+    // new rows of the last round join the clean lists (dirty ones were rescanned)
+    const int nnew = S->nnew;
+    if (nnew > 0) {
+      for (int q = warp; q < n; q += RWARPS) {
+        bool wasdirty = false;
+        for (int ci = 0; ci < nd; ++ci) wasdirty |= dcols[ci] == q;
+        if (wasdirty || c.excl[q]) continue;
+        for (int r0 = 0; r0 < nnew; r0 += 32) {
+          REnt e;
+          bool have = r0 + lane < nnew;
+          if (have) {
+            e.s = jb.newl[r0 + lane];
+            e.j = c.node_s[e.s];
+            e.t = col_key(c, q, e.s, e.j);
+            rent_meta(e, c, g);
+          }
+          for (int l = 0; l < 32 && r0 + l < nnew; ++l) {
+            REnt x;
+            x.t = __shfl_sync(kFull, e.t, l);
+            x.need = __shfl_sync(kFull, e.need, l);
+            x.k = __shfl_sync(kFull, e.k, l);
+            x.j = __shfl_sync(kFull, e.j, l);
+            x.s = __shfl_sync(kFull, e.s, l);
+            x.fav = __shfl_sync(kFull, e.fav, l);
+            x.inb = __shfl_sync(kFull, e.inb, l);
+            x.ine = __shfl_sync(kFull, e.ine, l);
+            x.outb = __shfl_sync(kFull, e.outb, l);
+            x.oute = __shfl_sync(kFull, e.oute, l);
+            if (lane == 0 && x.t != kInf) rlist_insert(L, cnt, flg, q, x);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    RMARK(P_INSERT);
+
+    // ---- phase S: the leader selects this round's commits (shared memory) -------
+    if (warp == 0) {
+      int k = 0;
+      while (true) {
+        if (S->placed + k == V) break;
+        // threshold: keys in dirty columns are >= F[q]
+        int64_t thr = kInf;
+        int64_t bt = kInf, bi = kInf;
+        for (int q = lane; q < n; q += 32) {
+          if (c.excl[q]) continue;
+          if (flg[q] & kDirty) {
+            thr = min64(thr, c.F[q]);
+            continue;
+          }
+          if (cnt[q] == 0) continue;
+          int64_t cell = (static_cast<int64_t>(L[q * KT].j) << 16) | q;
+          if (lex_less(L[q * KT].t, cell, bt, bi)) {
+            bt = L[q * KT].t;
+            bi = cell;
+          }
+        }
+        warp_argmin(bt, bi);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) thr = min64(thr, __shfl_xor_sync(kFull, thr, o));
+        if (bi == kInf) {
+          if (k == 0 && thr == kInf) {  // no live pair anywhere
+            if (lane == 0) {
+              S->err_status = kInfeasible;
+              S->err_code = E_NO_PAIR;
+              S->done = 1;
+            }
+          }
+          break;
+        }
+        if (bt >= thr) break;
+        const int q = static_cast<int>(bi & 0xffff);
+        const REnt e = L[q * KT];
+        if (c.res[q] + e.need > c.capS[q]) {
+          // discard (placers.cpp:203-219), inline: rare. With commits pending
+          // in this round, end the round first: the pair stays the minimum
+          // (every key the round adds is above it), and the exclusion scan
+          // must not see half-committed nodes.
+          if (k > 0) break;
+          int left = 0;
+          if (lane == 0) {
+            c.Kc[q * Vs + e.s] = kInf;
+            left = --c.alive_s[e.s];
+          }
+          left = __shfl_sync(kFull, left, 0);
+          if (left == 0) {
+            if (lane == 0) {
+              S->err_status = kInfeasible;
+              S->err_code = E_FITS_NONE;
+              S->err_node = e.j;
+              S->done = 1;
+            }
+            break;
+          }
+          if (lane == 0) S->discarded++;
+          if (lane == (q & 31)) rlist_remove(L, cnt, flg, q, e.j);
+          int64_t minrem = 0;
+          if (lane == 0) {
+            while (c.device_of[g.need_order[minptr]] >= 0) ++minptr;
+            minrem = c.need[g.need_order[minptr]];
+          }
+          minrem = __shfl_sync(kFull, minrem, 0);
+          if (c.res[q] + minrem > c.capS[q]) {
+            int ne = 0;
+            if (lane == 0) {
+              S->excluded++;
+              ne = ++S->nexcl;
+            }
+            ne = __shfl_sync(kFull, ne, 0);
+            int first_dead = INT32_MAX;
+            for (int s = lane; s < R; s += 32) {
+              int nd2 = c.node_s[s];
+              if (c.device_of[nd2] >= 0) continue;  // committed (hole) slot
+              if (c.Kc[q * Vs + s] != kInf) {
+                c.Kc[q * Vs + s] = kInf;
+                if (--c.alive_s[s] == 0) first_dead = min(first_dead, nd2);
+              }
+            }
+            if (ne == n) {
+              for (int x = lane; x < V; x += 32)
+                if (c.device_of[x] < 0) first_dead = min(first_dead, x);
+            }
+            first_dead = warp_min_i32(first_dead);
+            if (first_dead != INT32_MAX) {
+              if (lane == 0) {
+                S->err_status = kInfeasible;
+                S->err_code = E_FITS_NONE;
+                S->err_node = first_dead;
+                S->done = 1;
+              }
+              break;
+            }
+            if (lane == 0) c.excl[q] = 1;
+          }
+          __syncwarp();
+          continue;
+        }
+        // commit (placers.cpp:221-233): bookkeeping here, global work below
+        const int64_t fin = e.t + e.k;
+        if (lane == 0) {
+          RCommit &cm = CM[k];
+          cm.t = e.t;
+          cm.fin = fin;
+          cm.j = e.j;
+          cm.q = q;
+          cm.s = e.s;
+          cm.inb = e.inb;
+          cm.ine = e.ine;
+          cm.outb = e.outb;
+          cm.oute = e.oute;
+          c.F[q] = fin;
+          c.res[q] += e.need;
+        }
+        ++k;
+        __syncwarp();
+        for (int qq = lane; qq < n; qq += 32) {
+          if (qq == q) flg[qq] |= kDirty;
+          else rlist_remove(L, cnt, flg, qq, e.j);
+        }
+        __syncwarp();
+        if (c.sct) {
+          // awake reservations (placers.cpp:235-254); one commit per round
+          if (lane == 0) {
+            c.awf[q] = -1;
+            for (int qq = 0; qq < n; ++qq)
+              if (c.awf[qq] == e.j) {
+                c.awf[qq] = -1;
+                flg[qq] |= kDirty;
+              }
+            int h = e.fav;
+            if (h >= 0 && c.device_of[h] < 0) {
+              c.awf[q] = h;
+              c.awu[q] = fin + c.cmax;
+              S->awake++;
+            }
+          }
+          __syncwarp();
+          break;
+        }
+      }
+      // prefix sums of the committed nodes' degrees; dirty column list
+      if (lane == 0) {
+        S->ncommit = k;
+        inoff[0] = outoff[0] = 0;
+        for (int i = 0; i < k; ++i) {
+          inoff[i + 1] = inoff[i] + (CM[i].ine - CM[i].inb);
+          outoff[i + 1] = outoff[i] + (CM[i].oute - CM[i].outb);
+        }
+        int ndc = 0;
+        for (int q = 0; q < n; ++q)
+          if ((flg[q] & kDirty) && !c.excl[q]) dcols[ndc++] = q;
+        S->ndirty = ndc;
+        S->nnew = 0;
+        S->nnc = 0;
+      }
+    }
+    __syncthreads();
+    RMARK(P_ARGMIN);
+    if (S->done && S->err_status) break;
+    const int kc = S->ncommit;
+    if (prof && tid == 0) pc[P_COMMITS] += kc;
+    const int placed0 = S->placed;
+    // ---- phase B: commit bookkeeping, cache arrivals, readiness (all warps) -----
+    for (int i = warp; i < kc; i += RWARPS) {
+      const RCommit cm = CM[i];
+      if (lane == 0) {
+        c.device_of[cm.j] = cm.q;
+        c.start[cm.j] = cm.t;
+        c.finish[cm.j] = cm.fin;
+        c.cseq[placed0 + i] = cm.j;
+      }
+      for (int q = lane; q < n; q += 32) c.Kc[q * Vs + cm.s] = kInf;  // slot becomes a hole
+    }
+    {
+      const int nin = inoff[kc];
+      for (int w = tid; w < nin; w += NT) {
+        int i = 0;
+        while (inoff[i + 1] <= w) ++i;
+        const RCommit &cm = CM[i];
+        const int x = cm.inb + (w - inoff[i]);
+        if (c.pdev[x] != cm.q) {
+          const int par = c.in_src[x];
+          int64_t *slot = c.cache + static_cast<int64_t>(par) * n + cm.q;
+          if (*slot < 0) {  // commit_schedulable_time, parallel mode
+            *slot = c.pfin[x] + c.in_c[x];
+            int a = atomicAdd(&S->nnc, 1);
+            c.nc[a] = par;
+            jb.ncw[a] = i;
+          }
+        }
+      }
+      const int nout = outoff[kc];
+      for (int w = tid; w < nout; w += NT) {
+        int i = 0;
+        while (outoff[i + 1] <= w) ++i;
+        const RCommit &cm = CM[i];
+        const int y = cm.outb + (w - outoff[i]);
+        const int child = c.out_dst[y];
+        const int x = c.inpos[y];
+        c.pdev[x] = cm.q;
+        c.pfin[x] = cm.fin;
+        __threadfence_block();
+        if (atomicSub(&c.pending[child], 1) == 1) {
+          int s = atomicAdd(&S->R, 1);
+          c.node_s[s] = child;
+          c.rpos[child] = s;
+          jb.newl[atomicAdd(&S->nnew, 1)] = s;
+        }
+      }
+    }
+    __syncthreads();
+    RMARK(P_COMMIT);
+    // ---- phase C: new key rows + cached-consumer re-keys (all warps) ------------
+    {
+      const int nn = S->nnew;
+      const int nexcl = S->nexcl;
+      const int Rnow = S->R;
+      const int R0 = Rnow - nn;
+      int32_t gen = 0;
+      for (int64_t w = tid; w < static_cast<int64_t>(nn) * n; w += NT) {
+        const int r = static_cast<int>(w / n), q = static_cast<int>(w % n);
+        const int s = jb.newl[r];
+        const int ch = c.node_s[s];
+        c.Kc[q * Vs + s] = c.excl[q] ? kInf : key_of(c, ch, q, gen);
+        if (q == 0) {
+          c.alive_s[s] = n - nexcl;
+          c.urg_s[s] = c.sct ? urgency_e(c, ch) : 0;
+        }
+      }
+      const int nnc = S->nnc;
+      for (int a = warp; a < nnc; a += RWARPS) {
+        const int par = c.nc[a];
+        const int q = CM[jb.ncw[a]].q;
+        for (int y = g.out_off[par] + lane; y < g.out_off[par + 1]; y += 32) {
+          const int cc = c.out_dst[y];
+          if (c.pending[cc] != 0 || c.device_of[cc] >= 0) continue;
+          const int s = c.rpos[cc];
+          if (s >= R0) continue;  // new rows were keyed after the cache update
+          if (c.Kc[q * Vs + s] == kInf) continue;
+          c.Kc[q * Vs + s] = key_of(c, cc, q, gen);
+        }
+      }
+      if (tid == 0) {
+        S->placed += kc;
+        S->live += nn - kc;
+        if (S->placed == V) S->done = 1;
+        // holes dominate the slot range: compact next round
+        if (S->R - S->live > 1024 && S->R - S->live > S->live) S->compact = 1;
+      }
+    }
+    RMARK(P_ROWS);
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  if (S->err_status) {
+    if (lane == 0) set_err(jb.err, S->err_status, S->err_code, S->err_node, 0);
+    return;
+  }
+  emit_exec_order(c, jb, c.excl, lane);
+  if (lane == 0) {
+    jb.stats[0] = S->discarded;
+    jb.stats[1] = S->excluded;
+    jb.stats[2] = S->awake;
+    set_err(jb.err, kOk, E_NONE, 0, 0);
+    if (prof) {
+      pc[P_TOTAL] = clock64() - pt0;
+      for (int i = 0; i < kProfSlots; ++i) jb.prof[i] = pc[i];
+    }
+  }
+#undef RMARK
+}
+
+static size_t rounds_smem(int maxn) {
+  const int ntask = maxn > RWARPS ? maxn : RWARPS;
+  return ((sizeof(RShared) + 15) & ~size_t(15)) + 5 * 8 * size_t(maxn) + sizeof(REnt) * KT * maxn +
+         sizeof(RCommit) * maxn + size_t(ntask) * KT * 16 + 4 * size_t(ntask) +
+         4 * (7 * size_t(maxn) + 2) + 4 * (RWARPS + 1) + 64;  // awf excl cnt flg dcols inoff outoff wsum
+}
+
+void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
+                   int maxn, bool prof, cudaStream_t s) {
+  (void)prof;
+  const size_t sm = rounds_smem(maxn);
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(k_place_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  k_place_rounds<<<njobs, RWARPS * 32, sm, s>>>(jobs, order, njobs, graphs, preps, maxn);
+}
+
+
+// Few, large problems get a CTA each: parallel comm mode runs the round
+// kernel (rounds.cu), sequential mode the 8-warp list kernel. Many problems
+// run one warp each (four per CTA) for throughput.
 void launch_list(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                 int maxn, bool prof, cudaStream_t s) {
-  constexpr int W = 4;
-  int blocks = (njobs + W - 1) / W;
-  size_t sm = static_cast<size_t>(W) * maxn * kListSmemPerDevice;
-  if (prof) {
-    if (sm > 48 * 1024)
-      cudaFuncSetAttribute(k_place_list<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    k_place_list<W, true><<<blocks, 32 * W, sm, s>>>(jobs, order, njobs, graphs, preps, maxn);
+                 int maxn, bool prof, bool wide, cudaStream_t s) {
+  if (wide) {
+    if (prof) launch_w<8, true>(jobs, order, njobs, graphs, preps, maxn, 1, s);
+    else launch_w<8, false>(jobs, order, njobs, graphs, preps, maxn, 1, s);
+    launch_rounds(jobs, order, njobs, graphs, preps, maxn, prof, s);
   } else {
-    if (sm > 48 * 1024)
-      cudaFuncSetAttribute(k_place_list<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    k_place_list<W, false><<<blocks, 32 * W, sm, s>>>(jobs, order, njobs, graphs, preps, maxn);
+    if (prof) launch_w<1, true>(jobs, order, njobs, graphs, preps, maxn, 0, s);
+    else launch_w<1, false>(jobs, order, njobs, graphs, preps, maxn, 0, s);
   }
 }
 

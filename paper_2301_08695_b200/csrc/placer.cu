@@ -43,7 +43,10 @@ __global__ void k_prep_edges(DGraph g, DPrep pr, int write_src) {
       neg = 1;
       b = 0;
     }
-    if (write_src) g.in_src[x] = g.esrc[e];
+    if (write_src) {
+      g.in_src[x] = g.esrc[e];
+      g.inpos[e] = x;
+    }
     int64_t c = comm_time_exact(pr.ic, pr.pb, b);
     pr.in_c[x] = c;
     best = c > best ? c : best;
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_place_topo(const DJob *jobs, in
 
 // ------------------------------------------------------------ launch ----
 void launch_list(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                 int maxn, bool prof, cudaStream_t s);
+                 int maxn, bool prof, bool wide, cudaStream_t s);
 
 void launch_prep(const DGraph &g, const DPrep &pr, bool first, cudaStream_t s) {
   if (first) {
@@ -285,10 +288,10 @@ cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bi
 }
 
 void launch_placers(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                    int maxn, bool any_topo, bool any_list, bool prof, cudaStream_t s) {
+                    int maxn, bool any_topo, bool any_list, bool prof, bool wide, cudaStream_t s) {
   // one warp per job, 4 jobs per CTA, jobs in longest-first order so the
   // largest problems start in the first wave
-  if (any_list) launch_list(jobs, order, njobs, graphs, preps, maxn, prof, s);
+  if (any_list) launch_list(jobs, order, njobs, graphs, preps, maxn, prof, wide, s);
   if (any_topo) {
     constexpr int W = 4;
     k_place_topo<W><<<(njobs + W - 1) / W, 32 * W, static_cast<size_t>(W) * maxn * 56, s>>>(jobs, njobs, graphs,

@@ -22,6 +22,11 @@ struct Ctx {
   int32_t *pending, *alive_s, *node_s, *rpos, *device_of, *cseq, *nc;
   int64_t *scv;
   int32_t *scg;
+  // per in-CSR slot x of a ready node: its parent's device and finish time,
+  // written when the parent commits (inpos maps out-edge -> in-CSR slot)
+  int32_t *pdev;
+  int64_t *pfin;
+  const int32_t *inpos;
   // shared memory, per warp
   int64_t *F, *tail, *res, *capS, *awu;
   int32_t *awf, *excl;

@@ -1,0 +1,75 @@
+"""Single-graph placement latency: GPU (device-resident, CUDA events around
+the placer kernel) vs the compiled reference (one host core, run_placer's
+scope), with a bit-exact check of the two placements.
+
+python tools/latency_table.py [names...]      (default: the standard set)
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+
+import paper_2301_08695_b200 as bx  # noqa: E402
+from paper_2301_08695_b200 import workloads as W  # noqa: E402
+
+CASES = {
+    "layered100k_x4": (lambda: W.layered_dag_fast(100, 1000, 3), 4, "m-etf", 1.2),
+    "layered100k_x8": (lambda: W.layered_dag_fast(100, 1000, 3), 8, "m-etf", 1.2),
+    "layered100k_x64": (lambda: W.layered_dag_fast(100, 1000, 3), 64, "m-etf", 1.2),
+    "grid100k_x8": (lambda: W.grid_chain(6250, 16, 4), 8, "m-etf", 1.2),
+    "wide100k_x16": (lambda: W.wide_random(100000, 5), 16, "m-etf", 1.2),
+    "layered100k_x4_sct": (lambda: W.layered_dag_fast(100, 1000, 3), 4, "m-sct", 1.2),
+    "c4_layered1M_x64": (lambda: W.layered_dag_fast(1000, 1000, 1), 64, "m-etf", 1.5),
+}
+
+
+def fav_first(esrc, edst, V):
+    fav = np.full(V, -1, np.int32)
+    claimed = np.zeros(V, bool)
+    for s, d in zip(esrc.tolist(), edst.tolist()):
+        if fav[s] < 0 and not claimed[d]:
+            fav[s] = d
+            claimed[d] = True
+    return fav
+
+
+def run(name, cpu=True, reps=3):
+    mk, n, algo, f = CASES[name]
+    g = mk()
+    m = W.as_meta_dict(g)
+    gg = bx.MetaGraph.from_dict(m)
+    cm = bx.CommModel(*W.COMM_TEST)
+    caps = np.full(n, W.bench_capacity(g, n, f), np.int64)
+    fav = fav_first(g["esrc"], g["edst"], g["V"]) if algo == "m-sct" else None
+    plan = bx.Plan([gg], [bx.Job(0, algo, caps, cm, fav)])
+    plan.upload()
+    ms = []
+    for _ in range(reps + 1):
+        plan.place()
+        ms.append(plan.kernel_ms())
+    plan.download()
+    p = plan.result(0)
+    row = {"case": name, "V": gg.V, "E": gg.E, "n": n, "algo": algo, "gpu_kernel_ms": min(ms[1:]),
+           "gpu_ms_all": [round(x, 2) for x in ms[1:]]}
+    if cpu:
+        from oracle import Ref
+        rg = Ref.graph(W.as_ref_base(g), -1)
+        t0 = time.time()
+        o = Ref.place(rg, 2 if algo == "m-sct" else 1, caps, W.COMM_TEST, fav)
+        row["cpu_ref_ms"] = o.wall_ns / 1e6
+        row["cpu_wall_s"] = round(time.time() - t0, 2)
+        row["bit_exact"] = bool(np.array_equal(o.device_of, p.device_of) and np.array_equal(o.start_us, p.start_us)
+                                and np.array_equal(o.exec_order, p.exec_order_flat))
+        row["speedup"] = row["cpu_ref_ms"] / row["gpu_kernel_ms"]
+    plan.close()
+    return row
+
+
+if __name__ == "__main__":
+    names = [a for a in sys.argv[1:] if not a.startswith("-")] or list(CASES)
+    cpu = "--no-cpu" not in sys.argv
+    for nm in names:
+        print(json.dumps(run(nm, cpu=cpu)), flush=True)

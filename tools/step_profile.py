@@ -38,8 +38,9 @@ for gi in range(len(cases)):
     ms = plan.kernel_ms()
     pr = plan.profile(0)
     steps = max(pr["commits"], 1)
+    rounds = max(pr["steps"], 1)
     row = {"graph": cases[gi][0]["name"], "V": graphs[gi].V, "n": len(jobs[gi].capacity), "kernel_ms": ms,
-           "us_per_commit": ms * 1e3 / steps, "steps": pr["steps"], "rescans": pr["rescans"],
+           "us_per_commit": ms * 1e3 / steps, "steps_or_rounds": pr["steps"], "commits_per_round": round(steps / rounds, 2), "rescans": pr["rescans"],
            "cycles_per_commit": {k: round(pr[k] / steps, 1) for k in bx.Plan.PROFILE_FIELDS[:11]}}
     res.append(row)
     print(json.dumps(row), flush=True)
