@@ -111,6 +111,48 @@ def cpu_reference(graphs, jobs, sample_idx, threads, steps=1):
     return rates, st, chk
 
 
+def per_graph(bx, W, cpu=True):
+    """Placement wall time per graph (the metric's first half): a 100k-op
+    random layered DAG (C4 family, 100 layers x 1000), 4 devices, m-ETF,
+    comm_model_test.json. GPU = placer kernel on device-resident inputs
+    (CUDA events, best of 3 after a warm-up) and end to end through the C ABI
+    (upload + place + download); CPU = the compiled reference place_metf on
+    one host core (run_placer's scope), same graph, bit-exact compared."""
+    import time as _t
+    g = W.layered_dag_fast(100, 1000, 3)
+    gg = bx.MetaGraph.from_dict(W.as_meta_dict(g))
+    cm = bx.CommModel(*W.COMM_TEST)
+    caps = np.full(4, W.bench_capacity(g, 4, 1.2), np.int64)
+    plan = bx.Plan([gg], [bx.Job(0, "m-etf", caps, cm)])
+    plan.upload()
+    ks = []
+    for _ in range(4):
+        plan.place()
+        ks.append(plan.kernel_ms())
+    e2e = []
+    for _ in range(2):
+        t0 = _t.perf_counter()
+        plan.upload()
+        plan.place()
+        plan.download()
+        e2e.append((_t.perf_counter() - t0) * 1e3)
+    p = plan.result(0)
+    out = {"workload": "layered DAG 100 x 1000 (V=100k, E=%d), 4 devices, m-etf, parallel comm" % gg.E,
+           "gpu_kernel_ms": min(ks[1:]), "gpu_e2e_ms": min(e2e)}
+    plan.close()
+    if cpu:
+        from oracle import Ref
+        rg = Ref.graph(W.as_ref_base(g), -1)
+        o = Ref.place(rg, 1, caps, W.COMM_TEST)
+        out["cpu_ref_ms"] = o.wall_ns / 1e6
+        out["cpu_cores"] = 1
+        out["bit_exact"] = bool(np.array_equal(o.device_of, p.device_of) and np.array_equal(o.start_us, p.start_us)
+                                and np.array_equal(o.exec_order, p.exec_order_flat))
+        out["speedup_kernel"] = out["cpu_ref_ms"] / out["gpu_kernel_ms"]
+        out["speedup_e2e"] = out["cpu_ref_ms"] / out["gpu_e2e_ms"]
+    return out
+
+
 def sample_indices(jobs, count):
     stride = max(1, len(jobs) // count)
     return list(range(0, len(jobs), stride))[:count]
@@ -125,6 +167,7 @@ def main():
     ap.add_argument("--graphs", type=int, default=64)
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-graph", action="store_true")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -302,6 +345,13 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    pg = None
+    if rank == 0 and world == 1 and not args.no_per_graph:
+        try:
+            pg = per_graph(bx, W, cpu=not args.no_cpu_baseline)
+        except Exception as e:
+            pg = {"error": str(e)}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -314,7 +364,7 @@ def main():
                              "algorithmic_bytes_per_launch": abytes, "peak_source": peak_src,
                              "note": "latency-bound dependent scheduling chain; bytes = 40V+16E per problem"},
                 "cpu_baseline": cpu, "parity_vs_reference": parity, "infeasible_problems": infeasible,
-                "gather_ms": gather_ms, "clocks": clk.summary()}
+                "gather_ms": gather_ms, "clocks": clk.summary(), "per_graph": pg}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -151,6 +151,13 @@ int bx_plan_place(bx_plan *plan, void *stream);
  * `stream`. Returns BX_OK if the copy worked; per-job status is in out[i]. */
 int bx_plan_download(bx_plan *plan, void *stream, bx_placement *out);
 
+/* The outputs of every job live in one device region that bx_plan_download
+ * copies (one cudaMemcpyAsync) into a pinned host mirror owned by the plan;
+ * `out` may be NULL to skip the per-job copies into caller buffers. This
+ * returns a zero-copy view of job `job` inside that mirror (valid until the
+ * next download or destroy). */
+int bx_plan_result_view(bx_plan *plan, int32_t job, bx_placement *view);
+
 /* Number of kernel launches the last bx_plan_place issued. */
 int bx_plan_launch_count(const bx_plan *plan);
 

@@ -138,6 +138,7 @@ def lib():
         L.bx_plan_upload.argtypes = [_vp, _vp]
         L.bx_plan_place.argtypes = [_vp, _vp]
         L.bx_plan_download.argtypes = [_vp, _vp, C.POINTER(_Placement)]
+        L.bx_plan_result_view.argtypes = [_vp, i32, C.POINTER(_Placement)]
         L.bx_plan_launch_count.argtypes = [_vp]
         L.bx_plan_kernel_ms.argtypes = [_vp]
         L.bx_plan_kernel_ms.restype = C.c_float
@@ -153,7 +154,7 @@ def lib():
 
 
 EXPORTED = ["bx_version", "bx_last_error", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
-            "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download",
+            "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download", "bx_plan_result_view",
             "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_profile", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
             "bx_simulate", "bx_round_extract"]
 
@@ -285,17 +286,7 @@ class Plan:
         rc = lib().bx_plan_create(len(graphs), self._gc, len(jobs), self._jc, device, C.byref(h), msg, 512)
         _raise(rc, msg.value.decode())
         self.h = h
-        # host output buffers (pinned by numpy allocation; plain pageable)
         self.out = (_Placement * len(jobs))()
-        self._bufs = []
-        for i, j in enumerate(jobs):
-            V = graphs[j.graph].V
-            n = len(j.capacity)
-            b = (np.zeros(max(V, 1), np.int32), np.zeros(max(V, 1), np.int64),
-                 np.zeros(max(V, 1), np.int32), np.zeros(n + 1, np.int32))
-            self._bufs.append(b)
-            self.out[i].device_of, self.out[i].start_us = _ptr(b[0]), _ptr(b[1])
-            self.out[i].exec_order, self.out[i].exec_off = _ptr(b[2]), _ptr(b[3])
 
     def close(self):
         if getattr(self, "h", None):
@@ -334,8 +325,11 @@ class Plan:
         return float(lib().bx_plan_kernel_ms(self.h))
 
     def download(self, stream=None):
-        rc = lib().bx_plan_download(self.h, stream, self.out)
-        _raise(rc, "bx_plan_download failed")
+        """One device->pinned-host copy of every job's placement."""
+        rc = lib().bx_plan_download(self.h, stream, None)
+        _raise(rc, "bx_plan_download failed: " + lib().bx_last_error().decode())
+        for i in range(len(self.jobs)):
+            lib().bx_plan_result_view(self.h, i, C.byref(self.out[i]))
 
     def result(self, i: int, copy=True) -> Placement:
         """Placement of job i; raises the job's reference error."""
@@ -343,9 +337,16 @@ class Plan:
         _raise(o.status, o.msg.decode())
         j = self.jobs[i]
         V = self.graphs[j.graph].V
-        b = self._bufs[i]
-        f = (lambda a: a.copy()) if copy else (lambda a: a)
-        return Placement(j.algo, f(b[0][:V]), f(b[1][:V]), f(b[2][:V]), f(b[3]), tuple(o.stats))
+        n = len(j.capacity)
+
+        def view(ptr, ctype, count):
+            if count == 0:
+                return np.zeros(0, np.int32 if ctype is C.c_int32 else np.int64)
+            a = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(count,))
+            return a.copy() if copy else a
+
+        return Placement(j.algo, view(o.device_of, C.c_int32, V), view(o.start_us, C.c_int64, V),
+                         view(o.exec_order, C.c_int32, V), view(o.exec_off, C.c_int32, n + 1), tuple(o.stats))
 
     def status(self, i: int) -> tuple[int, str]:
         return self.out[i].status, self.out[i].msg.decode()

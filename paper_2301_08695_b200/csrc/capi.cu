@@ -22,8 +22,9 @@ void launch_prep(const DGraph &g, const DPrep &pr, bool first, cudaStream_t s);
 void launch_kahn(DGraph *graphs_dev, int32_t *const *queues_dev, int ngraphs, cudaStream_t s);
 cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bit, cudaStream_t s);
 void launch_extract(const XCtx &c, cudaStream_t s);
-void launch_placers(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                    int maxn, bool any_topo, bool any_list, bool prof, bool wide, cudaStream_t s);
+void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_bpar, int n_bseq, int njobs,
+                    const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo, bool prof,
+                    cudaStream_t s_small, cudaStream_t s_big);
 void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, cudaStream_t s);
 }  // namespace bx
 
@@ -56,9 +57,10 @@ std::string fmt(const char *f, ...) {
 // Bump allocator over one device pool.
 struct Layout {
   size_t off = 0;
+  size_t align = 256;
   template <typename T>
   size_t take(size_t count) {
-    off = (off + 255) & ~size_t(255);
+    off = (off + align - 1) & ~(align - 1);
     size_t at = off;
     off += std::max<size_t>(count, 1) * sizeof(T);
     return at;
@@ -102,15 +104,36 @@ struct bx_plan {
   DGraph *dg_dev = nullptr;
   DPrep *dp_dev = nullptr;
   DJob *dj_dev = nullptr;
-  int32_t *order_dev = nullptr;     // jobs by descending V*n (longest first)
+  int32_t *order_dev = nullptr;     // launch lists: small | big parallel | big sequential
+  int n_small = 0, n_bpar = 0, n_bseq = 0;
+  cudaStream_t s2 = nullptr;        // big problems run beside the small ones
+  cudaEvent_t fork = nullptr, join = nullptr;
   int32_t **queues_dev = nullptr;
   void *sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
-  std::vector<HostCopy> uploads;
+  std::vector<HostCopy> uploads;     // graph arrays: straight from the caller
+  struct Staged {
+    size_t off;
+    const void *src;
+    size_t bytes;
+  };
+  std::vector<Staged> staged;        // job inputs: packed into host_in, one copy
+  struct OOff {
+    size_t dev, start, eo, eoff, stats, err;
+  };
+  struct IOff {
+    size_t cap, fav;
+  };
+  std::vector<OOff> out_off;
+  std::vector<IOff> in_off;
+  size_t in_bytes = 0, out_bytes = 0;
+  char *dev_in = nullptr, *dev_out = nullptr;  // regions inside pool
+  void *host_in = nullptr, *host_out = nullptr;  // pinned mirrors
+  std::vector<int32_t> res_status;   // decoded by the last download
+  std::vector<std::string> res_msg;
   std::vector<Fill> fills;
   int maxn = 1;
   int64_t max_vn = 0;               // largest V*n over list-placer jobs
-  bool wide = false;                // CTA-per-problem kernels (few large problems)
   bool any_topo = false, any_list = false;
   int launches = 0;
   cudaEvent_t ev[2] = {nullptr, nullptr};  // brackets the placer kernel(s)
@@ -185,11 +208,16 @@ void bx_plan_destroy(bx_plan *plan) {
   if (!plan) return;
   cudaSetDevice(plan->device);
   if (plan->pool) cudaFree(plan->pool);
+  if (plan->host_in) cudaFreeHost(plan->host_in);
+  if (plan->host_out) cudaFreeHost(plan->host_out);
   if (plan->sim_pool) cudaFree(plan->sim_pool);
   if (plan->sort_tmp) cudaFree(plan->sort_tmp);
   if (plan->prof) cudaFree(plan->prof);
   if (plan->ev[0]) cudaEventDestroy(plan->ev[0]);
   if (plan->ev[1]) cudaEventDestroy(plan->ev[1]);
+  if (plan->fork) cudaEventDestroy(plan->fork);
+  if (plan->join) cudaEventDestroy(plan->join);
+  if (plan->s2) cudaStreamDestroy(plan->s2);
   delete plan;
 }
 
@@ -282,23 +310,31 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   };
   // Few large list-placer problems run the CTA-wide kernels (one problem per
   // CTA); many run one warp each. Decided here because the round kernel
-  // needs double-buffered slot arrays.
-  int64_t list_jobs = 0, vn_max = 0;
+  // needs double-buffered slot arrays. A job is "big" (CTA-wide kernels) when
+  // V*n >= 2^17, or >= 2^15 in a plan of at most 148 list jobs; at most 120
+  // big jobs (the largest), so the small ones keep SMs to run on.
+  std::vector<int32_t> list_ids;
   for (int i = 0; i < njobs; ++i)
-    if (jobs[i].algo != BX_ALGO_MTOPO) {
-      ++list_jobs;
-      vn_max = std::max(vn_max, int64_t(graphs[jobs[i].graph].V) * std::max(jobs[i].n, 1));
-    }
-  const bool wide_plan = list_jobs > 0 && list_jobs <= 148 && vn_max >= (int64_t(1) << 15);
-  P->wide = wide_plan;
+    if (jobs[i].algo != BX_ALGO_MTOPO) list_ids.push_back(i);
+  auto vn = [&](int i) { return int64_t(graphs[jobs[i].graph].V) * std::max(jobs[i].n, 1); };
+  std::stable_sort(list_ids.begin(), list_ids.end(), [&](int a, int b) { return vn(a) > vn(b); });
+  const int64_t big_min = list_ids.size() <= 148 ? (int64_t(1) << 15) : (int64_t(1) << 17);
+  std::vector<char> big(njobs, 0);
+  for (size_t r = 0; r < list_ids.size() && r < 120; ++r)
+    if (vn(list_ids[r]) >= big_min) big[list_ids[r]] = 1;
+  // job inputs (capacities, favourites) and outputs live in two contiguous
+  // regions so an end-to-end step moves them with one copy each way, through
+  // pinned host mirrors
+  Layout LI, LO;
+  LI.align = LO.align = 8;
   std::vector<JOff> jo(njobs);
   for (int i = 0; i < njobs; ++i) {
     const bx_job &J = jobs[i];
     const int64_t V = graphs[J.graph].V;
     const int64_t n = std::max(J.n, 1);
     JOff &o = jo[i];
-    o.cap = L.take<int64_t>(n);
-    o.fav = L.take<int32_t>(V);
+    o.cap = LI.take<int64_t>(n);
+    o.fav = LI.take<int32_t>(J.algo == BX_ALGO_MSCT && J.fav_child ? V : 1);
     o.K = L.take<int64_t>(V * n);
     o.cache = L.take<int64_t>(V * n);
     o.dead = L.take<uint8_t>(V * n);
@@ -314,6 +350,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     o.scg = L.take<int32_t>(32 * n);
     o.pdev = L.take<int32_t>(graphs[J.graph].E);
     {
+      const bool wide_plan = big[i] != 0;
       const int64_t Vr = wide_plan ? V : 1;
       o.K2 = L.take<int64_t>(Vr * (wide_plan ? n : 1));
       o.urgent2 = L.take<int64_t>(Vr);
@@ -323,26 +360,33 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
       o.newl = L.take<int32_t>(Vr);
     }
     o.pfin = L.take<int64_t>(graphs[J.graph].E);
-    o.device_of = L.take<int32_t>(V);
-    o.start = L.take<int64_t>(V);
-    o.exec_order = L.take<int32_t>(V);
-    o.exec_off = L.take<int32_t>(n + 1);
-    o.stats = L.take<int64_t>(3);
-    o.err = L.take<DErr>(1);
+    o.stats = LO.take<int64_t>(3);
+    o.err = LO.take<DErr>(1);
+    o.start = LO.take<int64_t>(V);
+    o.device_of = LO.take<int32_t>(V);
+    o.exec_order = LO.take<int32_t>(V);
+    o.exec_off = LO.take<int32_t>(n + 1);
   }
   size_t tables = L.take<DGraph>(ngraphs);
   size_t ptables = L.take<DPrep>(P->nprep);
   size_t jtables = L.take<DJob>(njobs);
   size_t qtables = L.take<int32_t *>(ngraphs);
-  size_t otable = L.take<int32_t>(njobs);
+  size_t otable = L.take<int32_t>(3 * size_t(njobs) + 3);
+  const size_t in_at = L.take<char>(LI.off), out_at = L.take<char>(LO.off);
+  P->in_bytes = LI.off;
+  P->out_bytes = LO.off;
   P->pool_bytes = L.off;
   cudaError_t ce = cudaMalloc(&P->pool, P->pool_bytes);
+  if (ce == cudaSuccess) ce = cudaHostAlloc(&P->host_in, std::max<size_t>(P->in_bytes, 8), cudaHostAllocDefault);
+  if (ce == cudaSuccess) ce = cudaHostAlloc(&P->host_out, std::max<size_t>(P->out_bytes, 8), cudaHostAllocDefault);
   if (ce != cudaSuccess) {
     put_msg(msg, msglen, fmt("cudaMalloc of %zu bytes failed: %s", P->pool_bytes, cudaGetErrorString(ce)));
     delete P;
     return BX_RUNTIME;
   }
   void *pool = P->pool;
+  P->dev_in = at<char>(pool, in_at);
+  P->dev_out = at<char>(pool, out_at);
 
   P->dg.resize(ngraphs);
   std::vector<int32_t *> queues(ngraphs);
@@ -435,7 +479,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     d.n = J.n;
     d.mode = J.cm.mode == BX_COMM_PARALLEL ? 1 : 0;
     d.skip = 0;
-    d.cap = at<int64_t>(pool, o.cap);
+    d.cap = reinterpret_cast<int64_t *>(P->dev_in + o.cap);
     d.fav = nullptr;
     d.K = at<int64_t>(pool, o.K);
     d.cache = at<int64_t>(pool, o.cache);
@@ -458,12 +502,14 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     d.ncw = at<int32_t>(pool, o.ncw);
     d.newl = at<int32_t>(pool, o.newl);
     d.pfin = at<int64_t>(pool, o.pfin);
-    d.device_of = at<int32_t>(pool, o.device_of);
-    d.start = at<int64_t>(pool, o.start);
-    d.exec_order = at<int32_t>(pool, o.exec_order);
-    d.exec_off = at<int32_t>(pool, o.exec_off);
-    d.stats = at<int64_t>(pool, o.stats);
-    d.err = at<DErr>(pool, o.err);
+    d.device_of = reinterpret_cast<int32_t *>(P->dev_out + o.device_of);
+    d.start = reinterpret_cast<int64_t *>(P->dev_out + o.start);
+    d.exec_order = reinterpret_cast<int32_t *>(P->dev_out + o.exec_order);
+    d.exec_off = reinterpret_cast<int32_t *>(P->dev_out + o.exec_off);
+    d.stats = reinterpret_cast<int64_t *>(P->dev_out + o.stats);
+    d.err = reinterpret_cast<DErr *>(P->dev_out + o.err);
+    P->out_off.push_back({o.device_of, o.start, o.exec_order, o.exec_off, o.stats, o.err});
+    P->in_off.push_back({o.cap, o.fav});
     d.prof = P->prof ? P->prof + static_cast<size_t>(kProfSlots) * i : nullptr;
     // host-side validation in the reference's order
     std::string why;
@@ -488,11 +534,11 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     P->host_status[i] = st;
     P->host_msg[i] = why;
     d.skip = st != 0;
-    if (J.n > 0) P->uploads.push_back({const_cast<int64_t *>(d.cap), J.capacity, 8 * size_t(J.n)});
+    if (J.n > 0) P->staged.push_back({P->in_off[i].cap, J.capacity, 8 * size_t(J.n)});
     if (!d.skip) {
       if (J.algo == BX_ALGO_MSCT && J.fav_child && J.fav_len == G.V && G.V > 0) {
-        d.fav = at<int32_t>(pool, o.fav);
-        P->uploads.push_back({const_cast<int32_t *>(d.fav), J.fav_child, 4 * size_t(V)});
+        d.fav = reinterpret_cast<int32_t *>(P->dev_in + o.fav);
+        P->staged.push_back({P->in_off[i].fav, J.fav_child, 4 * size_t(V)});
       }
       if (J.algo == BX_ALGO_MTOPO) {
         P->any_topo = true;
@@ -512,13 +558,27 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   P->queues_dev = at<int32_t *>(pool, qtables);
   P->order_dev = at<int32_t>(pool, otable);
   {
-    std::vector<int32_t> ord(njobs);
-    for (int i = 0; i < njobs; ++i) ord[i] = i;
-    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
-      return int64_t(graphs[jobs[a].graph].V) * jobs[a].n > int64_t(graphs[jobs[b].graph].V) * jobs[b].n;
-    });
-    BX_CUDA(cudaMemcpy(P->order_dev, ord.data(), 4 * size_t(njobs), cudaMemcpyHostToDevice), msg, msglen);
+    // three launch lists, each longest-first: small (one warp per job),
+    // big parallel-mode (round kernel), big sequential-mode (8-warp kernel)
+    std::vector<int32_t> small, bpar, bseq;
+    for (int i : list_ids) {
+      if (P->dj[i].skip) continue;
+      if (!big[i]) small.push_back(i);
+      else if (jobs[i].cm.mode == BX_COMM_PARALLEL) bpar.push_back(i);
+      else bseq.push_back(i);
+    }
+    std::vector<int32_t> all(small);
+    all.insert(all.end(), bpar.begin(), bpar.end());
+    all.insert(all.end(), bseq.begin(), bseq.end());
+    P->n_small = static_cast<int>(small.size());
+    P->n_bpar = static_cast<int>(bpar.size());
+    P->n_bseq = static_cast<int>(bseq.size());
+    if (!all.empty())
+      BX_CUDA(cudaMemcpy(P->order_dev, all.data(), 4 * all.size(), cudaMemcpyHostToDevice), msg, msglen);
   }
+  BX_CUDA(cudaStreamCreateWithFlags(&P->s2, cudaStreamNonBlocking), msg, msglen);
+  BX_CUDA(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming), msg, msglen);
+  BX_CUDA(cudaEventCreateWithFlags(&P->join, cudaEventDisableTiming), msg, msglen);
   // descriptor tables are static: copy once
   BX_CUDA(cudaMemcpy(P->dg_dev, P->dg.data(), sizeof(DGraph) * ngraphs, cudaMemcpyHostToDevice), msg, msglen);
   BX_CUDA(cudaMemcpy(P->dp_dev, P->dp.data(), sizeof(DPrep) * P->nprep, cudaMemcpyHostToDevice), msg, msglen);
@@ -547,6 +607,12 @@ int bx_plan_upload(bx_plan *P, void *stream) {
   for (const HostCopy &c : P->uploads) {
     if (cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return BX_RUNTIME;
   }
+  // the previous upload of host_in may still be in flight on this stream
+  if (cudaStreamSynchronize(s) != cudaSuccess) return BX_RUNTIME;
+  for (const auto &st : P->staged) std::memcpy(static_cast<char *>(P->host_in) + st.off, st.src, st.bytes);
+  if (P->in_bytes &&
+      cudaMemcpyAsync(P->dev_in, P->host_in, P->in_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return BX_RUNTIME;
   return BX_OK;
 }
 
@@ -579,9 +645,20 @@ int bx_plan_place(bx_plan *P, void *stream) {
   launch_kahn(P->dg_dev, P->queues_dev, P->ngraphs, s);
   P->launches += 1;
   cudaEventRecord(P->ev[0], s);
-  launch_placers(P->dj_dev, P->order_dev, P->njobs, P->dg_dev, P->dp_dev, P->maxn, P->any_topo, P->any_list, P->prof != nullptr, P->wide, s);
+  const bool fork = P->n_small > 0 && (P->n_bpar + P->n_bseq) > 0;
+  cudaStream_t sb = fork ? P->s2 : s;
+  if (fork) {
+    cudaEventRecord(P->fork, s);
+    cudaStreamWaitEvent(P->s2, P->fork, 0);
+  }
+  launch_placers(P->dj_dev, P->order_dev, P->n_small, P->n_bpar, P->n_bseq, P->njobs, P->dg_dev, P->dp_dev,
+                 P->maxn, P->any_topo, P->prof != nullptr, s, sb);
+  if (fork) {
+    cudaEventRecord(P->join, P->s2);
+    cudaStreamWaitEvent(s, P->join, 0);
+  }
   cudaEventRecord(P->ev[1], s);
-  P->launches += (P->any_topo ? 1 : 0) + (P->any_list ? 1 : 0);
+  P->launches += (P->any_topo ? 1 : 0) + (P->n_small > 0) + (P->n_bpar > 0) + (P->n_bseq > 0);
   return launch_status();
 }
 
@@ -621,74 +698,96 @@ static std::string cycle_message(const bx_plan *P, int g, cudaStream_t s) {
   return m + "} remain";
 }
 
+// Device -> pinned host mirror (one copy), then per-job status decode; with
+// `out` non-null the arrays are also copied into the caller's buffers.
 int bx_plan_download(bx_plan *P, void *stream, bx_placement *out) {
   cudaSetDevice(P->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  std::vector<DErr> errs(P->njobs);
-  std::vector<int64_t> stats(3 * static_cast<size_t>(P->njobs));
-  for (int i = 0; i < P->njobs; ++i) {
-    const DJob &d = P->dj[i];
-    const int V = P->hg[d.graph].V;
-    if (cudaMemcpyAsync(&errs[i], d.err, sizeof(DErr), cudaMemcpyDeviceToHost, s) != cudaSuccess) return BX_RUNTIME;
-    if (d.skip) continue;
-    cudaMemcpyAsync(&stats[3 * i], d.stats, 24, cudaMemcpyDeviceToHost, s);
-    if (V > 0) {
-      cudaMemcpyAsync(out[i].device_of, d.device_of, 4 * size_t(V), cudaMemcpyDeviceToHost, s);
-      cudaMemcpyAsync(out[i].start_us, d.start, 8 * size_t(V), cudaMemcpyDeviceToHost, s);
-      cudaMemcpyAsync(out[i].exec_order, d.exec_order, 4 * size_t(V), cudaMemcpyDeviceToHost, s);
-    }
-    cudaMemcpyAsync(out[i].exec_off, d.exec_off, 4 * size_t(d.n + 1), cudaMemcpyDeviceToHost, s);
-  }
-  cudaError_t ce = cudaStreamSynchronize(s);
+  cudaError_t ce = cudaSuccess;
+  if (P->out_bytes) ce = cudaMemcpyAsync(P->host_out, P->dev_out, P->out_bytes, cudaMemcpyDeviceToHost, s);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+  P->res_status.assign(P->njobs, 0);
+  P->res_msg.assign(P->njobs, "");
   if (ce != cudaSuccess) {
+    g_last_error = std::string("download: ") + cudaGetErrorString(ce);
     for (int i = 0; i < P->njobs; ++i) {
-      out[i].status = BX_RUNTIME;
-      put_msg(out[i].msg, sizeof out[i].msg, std::string("CUDA error: ") + cudaGetErrorString(ce));
+      P->res_status[i] = BX_RUNTIME;
+      P->res_msg[i] = g_last_error;
+      if (out) {
+        out[i].status = BX_RUNTIME;
+        put_msg(out[i].msg, sizeof out[i].msg, g_last_error);
+      }
     }
     return BX_RUNTIME;
   }
+  const char *H = static_cast<const char *>(P->host_out);
   for (int i = 0; i < P->njobs; ++i) {
     const DJob &d = P->dj[i];
-    bx_placement &o = out[i];
-    o.stats[0] = o.stats[1] = o.stats[2] = 0;
-    if (d.skip) {
-      o.status = P->host_status[i];
-      put_msg(o.msg, sizeof o.msg, P->host_msg[i]);
-      continue;
-    }
-    const DErr &e = errs[i];
-    o.status = e.status;
+    const bx_plan::OOff &o = P->out_off[i];
+    int status;
     std::string m;
-    switch (e.code) {
-      case E_NONE:
-        break;
-      case E_FITS_NONE:
-        m = "node " + std::to_string(e.a) + " fits on no device";
-        break;
-      case E_NO_PAIR:
-        m = "no schedulable (node, device) pair remains";
-        break;
-      case E_CYCLE:
-        m = cycle_message(P, d.graph, s);
-        break;
-      case E_NEG_BYTES:
-        m = "comm_time: negative byte count";
-        break;
-      case E_TOPO_CAP:
-        m = "m-topo per-device cap " + std::to_string(e.a) + " bytes exceeds the smallest device capacity " +
-            std::to_string(e.b) + "; use m-etf or m-sct for tight memory limits";
-        break;
-      default:
-        m = "internal error code " + std::to_string(e.code);
-        o.status = BX_RUNTIME;
+    if (d.skip) {
+      status = P->host_status[i];
+      m = P->host_msg[i];
+    } else {
+      const DErr &e = *reinterpret_cast<const DErr *>(H + o.err);
+      status = e.status;
+      switch (e.code) {
+        case E_NONE:
+          break;
+        case E_FITS_NONE:
+          m = "node " + std::to_string(e.a) + " fits on no device";
+          break;
+        case E_NO_PAIR:
+          m = "no schedulable (node, device) pair remains";
+          break;
+        case E_CYCLE:
+          m = cycle_message(P, d.graph, s);
+          break;
+        case E_NEG_BYTES:
+          m = "comm_time: negative byte count";
+          break;
+        case E_TOPO_CAP:
+          m = "m-topo per-device cap " + std::to_string(e.a) + " bytes exceeds the smallest device capacity " +
+              std::to_string(e.b) + "; use m-etf or m-sct for tight memory limits";
+          break;
+        default:
+          m = "internal error code " + std::to_string(e.code);
+          status = BX_RUNTIME;
+      }
     }
-    put_msg(o.msg, sizeof o.msg, m);
-    if (o.status == 0) {
-      o.stats[0] = stats[3 * i];
-      o.stats[1] = stats[3 * i + 1];
-      o.stats[2] = stats[3 * i + 2];
-    }
+    P->res_status[i] = status;
+    P->res_msg[i] = m;
+    if (!out) continue;
+    bx_placement &r = out[i];
+    r.status = status;
+    put_msg(r.msg, sizeof r.msg, m);
+    const int64_t *st = reinterpret_cast<const int64_t *>(H + o.stats);
+    for (int k = 0; k < 3; ++k) r.stats[k] = status == 0 && !d.skip ? st[k] : 0;
+    if (status != 0 || d.skip) continue;
+    const int V = P->hg[d.graph].V;
+    if (r.device_of) std::memcpy(r.device_of, H + o.dev, 4 * size_t(V));
+    if (r.start_us) std::memcpy(r.start_us, H + o.start, 8 * size_t(V));
+    if (r.exec_order) std::memcpy(r.exec_order, H + o.eo, 4 * size_t(V));
+    if (r.exec_off) std::memcpy(r.exec_off, H + o.eoff, 4 * size_t(d.n + 1));
   }
+  return BX_OK;
+}
+
+// Zero-copy view of job `job`'s placement inside the plan's pinned host
+// mirror (valid until the next bx_plan_download or bx_plan_destroy).
+int bx_plan_result_view(bx_plan *P, int32_t job, bx_placement *view) {
+  if (job < 0 || job >= P->njobs || P->res_status.empty()) return BX_VALIDATION;
+  const bx_plan::OOff &o = P->out_off[job];
+  char *H = static_cast<char *>(P->host_out);
+  view->device_of = reinterpret_cast<int32_t *>(H + o.dev);
+  view->start_us = reinterpret_cast<int64_t *>(H + o.start);
+  view->exec_order = reinterpret_cast<int32_t *>(H + o.eo);
+  view->exec_off = reinterpret_cast<int32_t *>(H + o.eoff);
+  view->status = P->res_status[job];
+  put_msg(view->msg, sizeof view->msg, P->res_msg[job]);
+  const int64_t *st = reinterpret_cast<const int64_t *>(H + o.stats);
+  for (int k = 0; k < 3; ++k) view->stats[k] = view->status == 0 && !P->dj[job].skip ? st[k] : 0;
   return BX_OK;
 }
 

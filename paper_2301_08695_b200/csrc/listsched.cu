@@ -1483,19 +1483,18 @@ void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGra
 }
 
 
-// Few, large problems get a CTA each: parallel comm mode runs the round
-// kernel (rounds.cu), sequential mode the 8-warp list kernel. Many problems
-// run one warp each (four per CTA) for throughput.
-void launch_list(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                 int maxn, bool prof, bool wide, cudaStream_t s) {
-  if (wide) {
-    if (prof) launch_w<8, true>(jobs, order, njobs, graphs, preps, maxn, 1, s);
-    else launch_w<8, false>(jobs, order, njobs, graphs, preps, maxn, 1, s);
-    launch_rounds(jobs, order, njobs, graphs, preps, maxn, prof, s);
-  } else {
-    if (prof) launch_w<1, true>(jobs, order, njobs, graphs, preps, maxn, 0, s);
-    else launch_w<1, false>(jobs, order, njobs, graphs, preps, maxn, 0, s);
-  }
+// Launch lists come from bx_plan_create: small problems one warp each,
+// big sequential-mode problems an 8-warp CTA each.
+void launch_small(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
+                  int maxn, bool prof, cudaStream_t s) {
+  if (prof) launch_w<1, true>(jobs, order, njobs, graphs, preps, maxn, 0, s);
+  else launch_w<1, false>(jobs, order, njobs, graphs, preps, maxn, 0, s);
+}
+
+void launch_big_seq(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
+                    int maxn, bool prof, cudaStream_t s) {
+  if (prof) launch_w<8, true>(jobs, order, njobs, graphs, preps, maxn, 0, s);
+  else launch_w<8, false>(jobs, order, njobs, graphs, preps, maxn, 0, s);
 }
 
 }  // namespace bx

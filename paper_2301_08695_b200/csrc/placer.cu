@@ -264,8 +264,12 @@ __global__ void __launch_bounds__(32 * kWarps) k_place_topo(const DJob *jobs, in
 }
 
 // ------------------------------------------------------------ launch ----
-void launch_list(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                 int maxn, bool prof, bool wide, cudaStream_t s);
+void launch_small(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
+                  int maxn, bool prof, cudaStream_t s);
+void launch_big_seq(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
+                    int maxn, bool prof, cudaStream_t s);
+void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
+                   int maxn, bool prof, cudaStream_t s);
 
 void launch_prep(const DGraph &g, const DPrep &pr, bool first, cudaStream_t s) {
   if (first) {
@@ -287,15 +291,18 @@ cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bi
                                          s);
 }
 
-void launch_placers(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                    int maxn, bool any_topo, bool any_list, bool prof, bool wide, cudaStream_t s) {
-  // one warp per job, 4 jobs per CTA, jobs in longest-first order so the
-  // largest problems start in the first wave
-  if (any_list) launch_list(jobs, order, njobs, graphs, preps, maxn, prof, wide, s);
+void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_bpar, int n_bseq, int njobs,
+                    const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo, bool prof,
+                    cudaStream_t s_small, cudaStream_t s_big) {
+  // big problems (CTA-wide kernels) on s_big, beside the small ones (one
+  // warp per job, four per CTA) on s_small; every list is longest-first
+  if (n_bpar) launch_rounds(jobs, order + n_small, n_bpar, graphs, preps, maxn, prof, s_big);
+  if (n_bseq) launch_big_seq(jobs, order + n_small + n_bpar, n_bseq, graphs, preps, maxn, prof, s_big);
+  if (n_small) launch_small(jobs, order, n_small, graphs, preps, maxn, prof, s_small);
   if (any_topo) {
     constexpr int W = 4;
-    k_place_topo<W><<<(njobs + W - 1) / W, 32 * W, static_cast<size_t>(W) * maxn * 56, s>>>(jobs, njobs, graphs,
-                                                                                            preps, maxn);
+    k_place_topo<W><<<(njobs + W - 1) / W, 32 * W, static_cast<size_t>(W) * maxn * 56, s_small>>>(
+        jobs, njobs, graphs, preps, maxn);
   }
 }
 

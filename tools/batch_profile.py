@@ -1,0 +1,37 @@
+"""Which problems bound the C5 batch? Runs the sweep plan with BX_PROFILE=1
+and prints the longest jobs (SM cycles per job from clock64) by family/n."""
+import collections
+import os
+import sys
+
+os.environ["BX_PROFILE"] = "1"
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+
+import paper_2301_08695_b200 as bx  # noqa: E402
+from paper_2301_08695_b200 import sweep  # noqa: E402
+from paper_2301_08695_b200 import workloads as W  # noqa: E402
+
+graphs, jobs = sweep.rank_sweep(0, int(sys.argv[1]) if len(sys.argv) > 1 else 64)
+mgs = [bx.MetaGraph.from_dict(W.as_meta_dict(g)) for g in graphs]
+cm = bx.CommModel(*W.COMM_TEST)
+plan = bx.Plan(mgs, [bx.Job(gi, "m-etf", np.full(n, cap, np.int64), cm) for gi, n, cap in jobs])
+plan.upload()
+plan.place()
+plan.download()
+print("kernel ms", plan.kernel_ms())
+rows = []
+for i, (gi, n, cap) in enumerate(jobs):
+    pr = plan.profile(i)
+    rows.append((pr["total"], graphs[gi]["name"], graphs[gi]["V"], n, pr["commits"], pr["steps"]))
+rows.sort(reverse=True)
+clk = 1.965e9
+for r in rows[:15]:
+    print(f"{r[0]/clk*1e3:8.1f} ms  {r[1]:>16s} V={r[2]:6d} n={r[3]:3d} commits={r[4]} steps/rounds={r[5]}"
+          f"  us/commit={r[0]/clk*1e6/max(r[4],1):.2f}")
+fam = collections.defaultdict(list)
+for r in rows:
+    fam[(r[1].rstrip('0123456789x'), r[3])].append(r[0] / clk * 1e3)
+for k in sorted(fam):
+    v = fam[k]
+    print(k, f"max {max(v):.1f} ms mean {np.mean(v):.1f} ms")

@@ -21,6 +21,12 @@ if which == "sweep-big":
 elif which == "c4":
     g = W.layered_dag_fast(1000, 1000, 1)
     cases = [(g, 64)]
+elif which == "n64":
+    g = W.layered_dag_fast(100, 100, 3)
+    cases = [(g, 16), (g, 32), (g, 64)]
+elif which == "grid":
+    g = W.grid_chain(6250, 16, 4)
+    cases = [(g, 8)]
 else:
     g = W.layered_dag_fast(100, 1000, 1)
     cases = [(g, 4), (g, 8)]
