@@ -2,7 +2,7 @@
  *
  * Plain C, plain pointers and sizes; no CUDA or torch types cross this line.
  * Every entry point replaces one function of the reference C++ placer API
- * (namespace dagsched, /root/reference/proj/include/dagsched/*.hpp); the
+ * (namespace dagsched, /root/reference/proj/include/dagsched/<name>.hpp); the
  * citation sits above each declaration. INTEGRATION.md shows the bindings
  * (C++ shim, ctypes) a maintainer of the reference would add.
  *
@@ -121,6 +121,48 @@ int bx_comm_time(const bx_comm *cm, int64_t bytes, int64_t *out_us);
 int bx_build_adjacency(int32_t V, int32_t E, const int32_t *esrc,
                        const int32_t *edst, int32_t *in_off, int32_t *in_edge,
                        int32_t *out_off, char *msg, int msglen);
+
+/* ---- ingest: base graph -> GroupedGraph (host C++) ----------------------
+ * A ProfiledGraph (graph.hpp:10-40) as arrays. Colocation groups are given
+ * as integer labels (equal label = same colocation_group string; -1 none);
+ * coplace_pair as has_pair + peer id. Node/edge order is free. */
+typedef struct {
+  int32_t nodes;
+  const int64_t *id, *compute_us, *temp_bytes, *perm_bytes, *out_bytes; /* [nodes] */
+  const int32_t *coloc_label;   /* [nodes] or NULL */
+  const uint8_t *has_pair;      /* [nodes] or NULL */
+  const int64_t *coplace_peer;  /* [nodes] or NULL */
+  int32_t edges;
+  const int64_t *src, *dst, *tensor_bytes; /* [edges], node ids */
+} bx_base_graph;
+
+/* Base-node view of a grouping (GroupedGraph::group_of / MetaNode::members,
+ * MetaEdge::base_count). */
+typedef struct {
+  int32_t base_nodes;
+  const int64_t *base_ids;        /* [base_nodes] ascending (make_graph order) */
+  const int32_t *group_of;        /* [base_nodes] base index -> meta index */
+  const int32_t *members;         /* concatenated base indices per meta node */
+  const int32_t *member_off;      /* [V+1] */
+  const int32_t *edge_base_count; /* [E] */
+} bx_grouping;
+
+#define BX_PIPE_SINGLETON (-1)    /* singleton_groups only */
+#define BX_PIPE_COLOCATION 0      /* apply_colocation */
+#define BX_PIPE_COPLACEMENT 2     /* + apply_coplacement */
+#define BX_PIPE_FUSION 4          /* + fuse_operators */
+
+typedef struct bx_grouped bx_grouped;
+
+/* make_graph (graph.cpp:99-194) then build_grouped (bench.cpp:43-49):
+ * singleton groups, colocation (transforms.cpp:329-351), optional
+ * co-placement (:353-388) and fusion (:390-444). Validation / CycleError
+ * texts are the reference's; status BX_VALIDATION on failure. */
+int bx_grouped_create(const bx_base_graph *base, int32_t pipeline, bx_grouped **out, char *msg, int msglen);
+/* Views into the grouped graph (valid until destroy): the meta graph ready
+ * for bx_plan_create / bx_place, and the base-node grouping. */
+int bx_grouped_view(const bx_grouped *grouped, bx_graph *meta, bx_grouping *grouping);
+void bx_grouped_destroy(bx_grouped *grouped);
 
 /* ---- plans: device-resident batches of placement problems --------------
  * A plan owns device copies of `ngraphs` graphs and `njobs` jobs plus the

@@ -93,6 +93,18 @@ class _Graph(C.Structure):
                 ("in_off", _vp), ("in_edge", _vp), ("out_off", _vp), ("first_id", _vp)]
 
 
+class _BaseGraph(C.Structure):
+    _fields_ = [("nodes", C.c_int32), ("id", _vp), ("compute_us", _vp), ("temp_bytes", _vp),
+                ("perm_bytes", _vp), ("out_bytes", _vp), ("coloc_label", _vp), ("has_pair", _vp),
+                ("coplace_peer", _vp), ("edges", C.c_int32), ("src", _vp), ("dst", _vp),
+                ("tensor_bytes", _vp)]
+
+
+class _Grouping(C.Structure):
+    _fields_ = [("base_nodes", C.c_int32), ("base_ids", _vp), ("group_of", _vp), ("members", _vp),
+                ("member_off", _vp), ("edge_base_count", _vp)]
+
+
 class _Comm(C.Structure):
     _fields_ = [("intercept_us", C.c_double), ("us_per_byte", C.c_double), ("mode", C.c_int32)]
 
@@ -148,6 +160,10 @@ def lib():
         L.bx_place.argtypes = [C.POINTER(_Graph), C.POINTER(_Job), C.POINTER(_Placement)]
         L.bx_simulate.argtypes = [C.POINTER(_Graph), i32, _vp, C.POINTER(_Comm), i32, _vp, _vp, _vp,
                                   C.POINTER(_SimReport)]
+        L.bx_grouped_create.argtypes = [C.POINTER(_BaseGraph), i32, C.POINTER(_vp), cp, C.c_int]
+        L.bx_grouped_view.argtypes = [_vp, C.POINTER(_Graph), C.POINTER(_Grouping)]
+        L.bx_grouped_destroy.argtypes = [_vp]
+        L.bx_grouped_destroy.restype = None
         L.bx_round_extract.argtypes = [i32, i32, _vp, _vp, _vp, C.c_double, _vp, _vp, _vp, cp, C.c_int]
         _lib = L
     return _lib
@@ -156,7 +172,7 @@ def lib():
 EXPORTED = ["bx_version", "bx_last_error", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
             "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download", "bx_plan_result_view",
             "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_profile", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
-            "bx_simulate", "bx_round_extract"]
+            "bx_simulate", "bx_round_extract", "bx_grouped_create", "bx_grouped_view", "bx_grouped_destroy"]
 
 
 def _ptr(a):
@@ -378,6 +394,58 @@ class Plan:
             out.append(SimReport(r.makespan_us, b[0][:V], b[1], b[2], b[3], r.transfer_count,
                                  r.transfer_bytes, r.duplicate_transfers, r.cache_hits))
         return out
+
+
+# ---- ingest: make_graph + build_grouped (host C++, csrc/ingest.cpp) --------
+PIPE_SINGLETON, PIPE_COLOCATION, PIPE_COPLACEMENT, PIPE_FUSION = -1, 0, 2, 4
+
+
+def _arr(ptr, ctype, count, dt):
+    if count == 0:
+        return np.zeros(0, dt)
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(count,)).astype(dt, copy=True)
+
+
+def build_grouped(base: dict, coplacement: bool = True, fusion: bool = True, singleton: bool = False):
+    """make_graph (graph.cpp:99-194) + build_grouped (bench.cpp:43-49).
+
+    `base` holds node arrays id, k, temp, perm, out, optional coloc (int
+    label, -1 none), has_pair + pair (peer id), and edge arrays src, dst,
+    bytes (node ids). Returns (MetaGraph, grouping dict with base_ids,
+    group_of, members, member_off, edge_base_count). Raises the reference's
+    ValidationError / CycleError texts."""
+    n = len(base["id"])
+    keep = {k: _c(base[k], np.int64) for k in ("id", "k", "temp", "perm", "out", "src", "dst", "bytes")}
+    coloc = base.get("coloc")
+    keep["coloc"] = None if coloc is None else _c(coloc, np.int32)
+    hp = base.get("has_pair")
+    keep["has_pair"] = None if hp is None else _c(hp, np.uint8)
+    keep["pair"] = None if hp is None else _c(base["pair"], np.int64)
+    g = _BaseGraph(n, _ptr(keep["id"]), _ptr(keep["k"]), _ptr(keep["temp"]), _ptr(keep["perm"]),
+                   _ptr(keep["out"]), _ptr(keep["coloc"]), _ptr(keep["has_pair"]), _ptr(keep["pair"]),
+                   len(keep["src"]), _ptr(keep["src"]), _ptr(keep["dst"]), _ptr(keep["bytes"]))
+    pipe = PIPE_SINGLETON if singleton else (PIPE_COPLACEMENT if coplacement else 0) | (PIPE_FUSION if fusion else 0)
+    h = _vp()
+    msg = C.create_string_buffer(4096)
+    rc = lib().bx_grouped_create(C.byref(g), pipe, C.byref(h), msg, 4096)
+    _raise(rc, msg.value.decode())
+    try:
+        mg = _Graph()
+        gp = _Grouping()
+        lib().bx_grouped_view(h, C.byref(mg), C.byref(gp))
+        V, E, B = mg.V, mg.E, gp.base_nodes
+        i64, i32 = C.c_int64, C.c_int32
+        meta = MetaGraph(_arr(mg.compute_us, i64, V, np.int64), _arr(mg.temp_bytes, i64, V, np.int64),
+                         _arr(mg.perm_bytes, i64, V, np.int64), _arr(mg.out_bytes, i64, V, np.int64),
+                         _arr(mg.esrc, i32, E, np.int32), _arr(mg.edst, i32, E, np.int32),
+                         _arr(mg.tensor_bytes, i64, E, np.int64), _arr(mg.first_id, i64, V, np.int64))
+        off = _arr(gp.member_off, i32, V + 1, np.int32)
+        grouping = dict(base_ids=_arr(gp.base_ids, i64, B, np.int64), group_of=_arr(gp.group_of, i32, B, np.int32),
+                        members=_arr(gp.members, i32, int(off[-1]) if V else 0, np.int32), member_off=off,
+                        edge_base_count=_arr(gp.edge_base_count, i32, E, np.int32))
+    finally:
+        lib().bx_grouped_destroy(h)
+    return meta, grouping
 
 
 # ---- reference-shaped entry points ---------------------------------------

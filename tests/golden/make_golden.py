@@ -96,5 +96,34 @@ def main():
     print(f"{len(index)} cases ({ok} placed, {len(index) - ok} errors), {len(graphs)} graphs")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--ingest" not in sys.argv:
     main()
+
+
+def make_ingest():
+    """tests/golden/ingest.npz: reference transforms (colocation, co-placement,
+    fusion) of seeded generator graphs with colocation groups and coplace pairs."""
+    arrays, index = {}, []
+    case = 0
+    for seed, fam, cf, pf in [(21, "branchy", 0.2, 0.1), (22, "layered-chain", 0.1, 0.2),
+                              (23, "random-dag", 0.3, 0.05), (24, "branchy", 0.0, 0.3)]:
+        g = Ref.generate(fam, 220, seed, layers=5, edge_prob=0.04, colocate_edge_frac=cf, coplace_frac=pf)
+        for pipe in (-1, 0, 2, 4, 6):
+            try:
+                r = Ref.graph(g, pipe).meta()
+            except OracleError:
+                continue
+            for k in ("id", "k", "temp", "perm", "out", "coloc", "has_pair", "pair", "src", "dst", "bytes"):
+                arrays[f"c{case}_in_{k}"] = g[k]
+            for k in ("k", "temp", "perm", "out", "esrc", "edst", "ebytes", "group_of", "ecount", "member_off",
+                      "members", "first_id"):
+                arrays[f"c{case}_out_{k}"] = r[k]
+            index.append(dict(case=case, pipe=pipe, family=fam, seed=seed, V=int(r["V"])))
+            case += 1
+    np.savez_compressed(os.path.join(HERE, "ingest.npz"), **arrays)
+    json.dump(index, open(os.path.join(HERE, "ingest_index.json"), "w"), indent=0)
+    print(f"{len(index)} ingest cases")
+
+
+if __name__ == "__main__" and "--ingest" in sys.argv:
+    make_ingest()
