@@ -167,6 +167,196 @@ def sweep_graphs(seed_base: int = 0, count: int = 64, vmin: int = 1000, vmax: in
     return out
 
 
+# ---- model-shaped training graphs (configs C1-C3) ---------------------------
+class _TrainGraph:
+    """Builds a training DAG from forward layers: every
+    forward op f gets a gradient op g_f (reversed data edges plus the
+    activation edge f -> g_f, coplace_pair(f, g_f)); every layer has a weight
+    Variable colocated with its reader, and a weight-gradient op colocated
+    with its ApplyGrad (paper Fig. 3 colocation groups)."""
+
+    def __init__(self, seed):
+        self.rng = np.random.default_rng(seed)
+        self.k, self.temp, self.perm, self.out = [], [], [], []
+        self.coloc, self.pair = [], []
+        self.edges = []  # (src, dst, bytes)
+        self.fwd = []  # forward op ids in creation (topological) order
+        self.fwd_succ = {}  # forward op -> forward consumers
+        self.label = 0
+
+    def op(self, k=None, perm=0, coloc=-1, out=None, temp=None):
+        r = self.rng
+        self.k.append(int(r.integers(50, 151)) if k is None else k)
+        self.temp.append(int(r.integers(0, 64 * KIB + 1)) if temp is None else temp)
+        self.perm.append(perm)
+        self.out.append(int(r.integers(KIB, 256 * KIB + 1)) if out is None else out)
+        self.coloc.append(coloc)
+        self.pair.append(-1)
+        return len(self.k) - 1
+
+    def edge(self, s, d, nbytes=None):
+        self.edges.append((s, d, int(self.rng.integers(KIB, 64 * KIB + 1)) if nbytes is None else nbytes))
+
+    def fwd_op(self, inputs, weight=None):
+        f = self.op()
+        for i in inputs:
+            self.edge(i, f)
+            self.fwd_succ.setdefault(i, []).append(f)
+        if weight is not None:
+            self.edge(weight, f)
+        self.fwd.append(f)
+        self.fwd_succ.setdefault(f, [])
+        return f
+
+    def layer(self, inputs, sub):
+        """`sub` forward ops in a chain; the first reads a weight Variable and
+        shares its colocation_group (a Variable grouped with its ApplyGrad
+        would close a cycle through the whole pass, which the reference
+        rejects, transforms.cpp:343-349)."""
+        lab = self.label
+        self.label += 2
+        v = self.op(k=1, perm=int(self.rng.integers(64 * KIB, 4096 * KIB)), coloc=lab, out=0)
+        cur = self.fwd_op(inputs, weight=v)
+        self.coloc[cur] = lab
+        first = cur
+        for _ in range(sub - 1):
+            cur = self.fwd_op([cur])
+        self._weights = getattr(self, "_weights", []) + [(first, v, lab)]
+        return cur
+
+    def finish(self, name):
+        grad = {}
+        for f in reversed(self.fwd):
+            g = self.op()
+            grad[f] = g
+            self.edge(f, g)  # activation edge
+            for c in self.fwd_succ[f]:
+                self.edge(grad[c], g)  # gradient flows backwards
+            self.pair[f], self.pair[g] = g, f
+        for first, v, lab in getattr(self, "_weights", []):
+            wg = self.op(coloc=lab + 1)  # weight gradient + ApplyGrad colocated
+            self.edge(grad[first], wg)
+            ap = self.op(k=20, coloc=lab + 1, out=0)
+            self.edge(wg, ap)
+            self.edge(v, ap, 0)
+        V = len(self.k)
+        es = sorted(set((s, d) for s, d, _ in self.edges))
+        by = {}
+        for s, d, b in self.edges:
+            by.setdefault((s, d), b)
+        has_pair = np.array([p >= 0 for p in self.pair], np.uint8)
+        return {"name": name, "V": V, "id": np.arange(V, dtype=np.int64),
+                "k": np.array(self.k, np.int64), "temp": np.array(self.temp, np.int64),
+                "perm": np.array(self.perm, np.int64), "out": np.array(self.out, np.int64),
+                "coloc": np.array(self.coloc, np.int32), "has_pair": has_pair,
+                "pair": np.array([max(p, 0) for p in self.pair], np.int64),
+                "src": np.array([s for s, _ in es], np.int64), "dst": np.array([d for _, d in es], np.int64),
+                "bytes": np.array([by[e] for e in es], np.int64)}
+
+
+def inception_v3(seed: int = 1, sub: int = 28):
+    """C1: Inception-V3-shaped training DAG, ~7k ops: stem, 11 split ->
+    branches (4-6, depth 1-5) -> concat modules, head (branchy shape,
+    generator.cpp:59-87), with backward mirror, coplace pairs and
+    Variable/ApplyGrad colocation."""
+    t = _TrainGraph(seed)
+    x = t.fwd_op([])
+    for _ in range(5):
+        x = t.layer([x], sub)
+    for _m in range(11):
+        tails = []
+        for _b in range(int(t.rng.integers(4, 7))):
+            y = x
+            for _d in range(int(t.rng.integers(1, 4))):
+                y = t.layer([y], sub)
+            tails.append(y)
+        x = t.fwd_op(tails)  # concat
+    for _ in range(2):
+        x = t.layer([x], sub)
+    t.fwd_op([x])  # loss
+    return t.finish(f"inception_v3_s{seed}")
+
+
+def gnmt(seed: int = 1, layers: int = 4, steps: int = 40, cell_ops: int = 24):
+    """C2: GNMT-shaped 4-layer LSTM seq2seq training graph, ~18k ops at
+    sequence length 40: unrolled encoder/decoder cells (each a short op
+    chain reading the previous step and the layer below), Bahdanau-style
+    attention from every decoder step to the top encoder states, residual
+    links from layer 3 up; backward mirror with coplace pairs."""
+    t = _TrainGraph(seed)
+    enc = [[None] * steps for _ in range(layers)]
+    emb = [t.fwd_op([]) for _ in range(steps)]
+    for l in range(layers):
+        for s in range(steps):
+            ins = [emb[s] if l == 0 else enc[l - 1][s]]
+            if s > 0:
+                ins.append(enc[l][s - 1])
+            if l >= 2:
+                ins.append(enc[l - 2][s])
+            enc[l][s] = t.layer(ins, cell_ops)
+    dec_prev = [None] * layers
+    for s in range(steps):
+        x = t.fwd_op([])  # target embedding
+        att = t.fwd_op([enc[layers - 1][i] for i in range(0, steps, max(1, steps // 8))])
+        for l in range(layers):
+            ins = [x, att] if l == 0 else [x]
+            if dec_prev[l] is not None:
+                ins.append(dec_prev[l])
+            x = t.layer(ins, cell_ops)
+            dec_prev[l] = x
+        t.fwd_op([x])  # per-step softmax / loss
+    return t.finish(f"gnmt{layers}x{steps}_s{seed}")
+
+
+def transformer(seed: int = 1, enc_layers: int = 6, dec_layers: int = 6, sub: int = 8):
+    """C3: Transformer 6+6 module-level training graph (~2-3k ops):
+    attention (q/k/v projections, scores, softmax, context, output),
+    add&norm and feed-forward blocks, split into sub-ops."""
+    t = _TrainGraph(seed)
+    x = t.layer([t.fwd_op([])], sub)
+
+    def attn(q_in, kv_in):
+        q = t.layer([q_in], sub)
+        k = t.layer([kv_in], sub)
+        v = t.layer([kv_in], sub)
+        sc = t.fwd_op([q, k])
+        sm = t.fwd_op([sc])
+        ctx = t.fwd_op([sm, v])
+        o = t.layer([ctx], sub)
+        return t.fwd_op([o, q_in])  # residual add + norm
+
+    def ffn(x_in):
+        h = t.layer([x_in], sub)
+        y = t.layer([h], sub)
+        return t.fwd_op([y, x_in])
+
+    for _ in range(enc_layers):
+        x = ffn(attn(x, x))
+    memory = x
+    y = t.layer([t.fwd_op([])], sub)
+    for _ in range(dec_layers):
+        y = attn(y, y)
+        y = attn(y, memory)
+        y = ffn(y)
+    t.fwd_op([t.layer([y], sub)])
+    return t.finish(f"transformer{enc_layers}+{dec_layers}_s{seed}")
+
+
+# BASELINE.json configs[0..2] as (generator, devices, algo, pipeline, cap factor)
+CONFIGS = {
+    "C1_inception_mtopo_metf": (inception_v3, 4, ("m-topo", "m-etf"), dict(coplacement=True, fusion=True), 1.3),
+    "C1_inception_nocoplace": (inception_v3, 4, ("m-etf",), dict(coplacement=False, fusion=False), 1.3),
+    "C2_gnmt_metf_coplace": (gnmt, 4, ("m-etf",), dict(coplacement=True, fusion=True), 1.3),
+    "C3_transformer_msct_tight": (transformer, 8, ("m-sct",), dict(coplacement=True, fusion=True), 1.05),
+}
+
+
+def meta_capacity(meta, n: int, factor: float) -> int:
+    """bench_capacity (bench.cpp:77-87) on a grouped (meta) graph."""
+    nd = meta.perm + meta.out + meta.temp
+    return int(math.ceil((float(nd.sum()) / n + float(nd.max() if len(nd) else 0)) * factor))
+
+
 def need(g):
     return g["perm"] + g["out"] + g["temp"]
 

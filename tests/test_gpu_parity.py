@@ -275,3 +275,49 @@ def test_full_size_100k_properties_and_reference(bx, mode):
         _assert_same(p, o)
         ro = Ref.simulate(rg, caps, cm, 1, o.device_of, o.exec_order, o.exec_off)
         assert ro.makespan == r.makespan_us and np.array_equal(ro.start_us, r.start_us)
+
+
+def _pipe(kw):
+    return (2 if kw.get("coplacement", True) else 0) | (4 if kw.get("fusion", True) else 0)
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_model_configs_end_to_end(bx, name):
+    """BASELINE configs C1-C3 end to end through our own pipeline: host
+    ingest (make_graph + colocation/co-placement/fusion) -> GPU placer ->
+    GPU simulator, bit-exact against the reference's transforms + placer +
+    simulator on the same base graph (m-SCT with the fixed fav map)."""
+    gen, n, algos, kw, f = W.CONFIGS[name]
+    g = gen()
+    meta, grouping = bx.build_grouped(g, **kw)
+    cap = W.meta_capacity(meta, n, f)
+    cm = bx.CommModel(*W.COMM_TEST)
+    m = dict(V=meta.V, E=meta.E, esrc=meta.esrc, edst=meta.edst)
+    fav = golden_cases.fav_first(m)
+    for algo in algos:
+        fv = fav if algo == "m-sct" else None
+        try:
+            p = bx._one(meta, algo, [cap] * n, cm, fv)
+            pe = None
+        except bx.Error as e:
+            pe = (e.kind, e.msg)
+        if Ref.available():
+            rg = Ref.graph(g, _pipe(kw))
+            try:
+                o = Ref.place(rg, ALGO.index(algo), [cap] * n, W.COMM_TEST, fv)
+                oe = None
+            except OracleError as e:
+                oe = (e.kind, e.msg)
+            assert pe == oe
+            if oe is None:
+                _assert_same(p, o, stats=algo != "m-topo")
+                r = bx.simulate(meta, p, [cap] * n, cm, bx.GRAPH_STATIC)
+                ro = Ref.simulate(rg, [cap] * n, W.COMM_TEST, 0, o.device_of, o.exec_order, o.exec_off)
+                assert r.makespan_us == ro.makespan and np.array_equal(r.start_us, ro.start_us)
+                assert r.peak_bytes.tolist() == ro.peak.tolist()
+        else:
+            o = Restate.place(dict(k=meta.k, temp=meta.temp, perm=meta.perm, out=meta.out, esrc=meta.esrc,
+                                   edst=meta.edst, ebytes=meta.ebytes), ALGO.index(algo), [cap] * n,
+                              W.COMM_TEST, fv)
+            assert pe is None
+            _assert_same(p, o, stats=algo != "m-topo")

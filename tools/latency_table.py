@@ -26,6 +26,45 @@ CASES = {
 }
 
 
+def run_config(name, cpu=True, reps=3):
+    """BASELINE configs C1-C3: our ingest + GPU placer vs the reference's
+    transforms + placer (one core), same base graph."""
+    gen, n, algos, kw, f = W.CONFIGS[name]
+    g = gen()
+    import time as _t
+    t0 = _t.perf_counter()
+    meta, _ = bx.build_grouped(g, **kw)
+    ingest_ms = (_t.perf_counter() - t0) * 1e3
+    cap = W.meta_capacity(meta, n, f)
+    cm = bx.CommModel(*W.COMM_TEST)
+    rows = []
+    for algo in algos:
+        fav = fav_first(meta.esrc, meta.edst, meta.V) if algo == "m-sct" else None
+        plan = bx.Plan([meta], [bx.Job(0, algo, np.full(n, cap, np.int64), cm, fav)])
+        plan.upload()
+        ms = []
+        for _ in range(reps + 1):
+            plan.place()
+            ms.append(plan.kernel_ms())
+        plan.download()
+        st, msg = plan.status(0)
+        p = plan.result(0) if st == 0 else None
+        row = {"case": name, "algo": algo, "base_V": g["V"], "meta_V": meta.V, "meta_E": meta.E, "n": n,
+               "ingest_ms_host": round(ingest_ms, 2), "gpu_kernel_ms": min(ms[1:]), "status": st}
+        if cpu:
+            from oracle import Ref
+            pipe = (2 if kw.get("coplacement", True) else 0) | (4 if kw.get("fusion", True) else 0)
+            rg = Ref.graph(g, pipe)
+            o = Ref.place(rg, {"m-topo": 0, "m-etf": 1, "m-sct": 2}[algo], [cap] * n, W.COMM_TEST, fav)
+            row["cpu_ref_ms"] = o.wall_ns / 1e6
+            row["bit_exact"] = bool(p is not None and np.array_equal(o.device_of, p.device_of)
+                                    and np.array_equal(o.start_us, p.start_us))
+            row["speedup"] = row["cpu_ref_ms"] / row["gpu_kernel_ms"]
+        plan.close()
+        rows.append(row)
+    return rows
+
+
 def fav_first(esrc, edst, V):
     fav = np.full(V, -1, np.int32)
     claimed = np.zeros(V, bool)
@@ -72,4 +111,8 @@ if __name__ == "__main__":
     names = [a for a in sys.argv[1:] if not a.startswith("-")] or list(CASES)
     cpu = "--no-cpu" not in sys.argv
     for nm in names:
-        print(json.dumps(run(nm, cpu=cpu)), flush=True)
+        if nm in W.CONFIGS:
+            for r in run_config(nm, cpu=cpu):
+                print(json.dumps(r), flush=True)
+        else:
+            print(json.dumps(run(nm, cpu=cpu)), flush=True)
