@@ -187,8 +187,9 @@ __device__ void warp_topk(const Ctx &c, int q, int s0, int step, int R, int lane
 #pragma unroll
   for (int r = 0; r < KT; ++r) {
     int64_t bt = lt[0];
-    int64_t bj = lj[0];
-    warp_argmin(bt, bj);
+    unsigned bju = static_cast<unsigned>(lj[0]);
+    warp_argmin_u(bt, bju);
+    const int64_t bj = static_cast<int>(bju);
     int bs = __shfl_sync(kFull, ls[0], __ffs(__ballot_sync(kFull, lj[0] == bj && lt[0] == bt)) - 1);
     dt[r] = bt;
     dj[r] = static_cast<int>(bj);
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
   Tops T;
   int64_t *stg_t = nullptr;
   int32_t *stg_j = nullptr, *stg_s = nullptr, *stg_live = nullptr;
-  int32_t *s_R, *s_done;
+  int32_t *s_R, *s_done, *s_rq;
   {
     const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 16;
     unsigned char *base = smem + static_cast<size_t>(pslot) * per;
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     }
     s_R = p32;
     s_done = p32 + 1;
+    s_rq = p32 + 2;  // the one column the group rescans next (-1: none)
   }
   const int V = c.V, n = c.n;
   const int64_t Vs = V;
@@ -407,6 +409,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     if (lane == 0) {
       *s_R = R;
       *s_done = V == 0;
+      *s_rq = -1;
     }
   }
 
@@ -422,109 +425,120 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     if (*s_done) break;
     int R = *s_R;
     if (kProf) ++prof[P_STEPS];
-    // ---- refresh dirty columns (every warp of the group) -------------------
-    for (int q0 = 0; q0 < n; q0 += 32) {
-      int q = q0 + lane;
-      unsigned m = __ballot_sync(kFull, q < n && (T.flg[q] & kDirty) && !c.excl[q]);
-      while (m) {
-        int qq = q0 + __ffs(m) - 1;
-        m &= m - 1;
-        int64_t dt[KT];
-        int dj[KT], ds[KT], cnt, live;
-        warp_topk(c, qq, gw * 32, 32 * kW, R, lane, dt, dj, ds, cnt, live);
-        if (kProf) ++prof[P_RESCANS];
-        if (lane == 0) {
-          if (kW == 1) {
+    // ---- rescan the column the leader asked for (every warp of the group) --
+    const int rq = *s_rq;
+    if (rq >= 0) {
+      const int qq = rq;
+      int64_t dt[KT];
+      int dj[KT], ds[KT], cnt, live;
+      warp_topk(c, qq, gw * 32, 32 * kW, R, lane, dt, dj, ds, cnt, live);
+      if (kProf) ++prof[P_RESCANS];
+      if (lane == 0) {
+        if (kW == 1) {
 #pragma unroll
-            for (int k = 0; k < KT; ++k) {
-              T.t[qq * KT + k] = dt[k];
-              T.j[qq * KT + k] = dj[k];
-              T.s[qq * KT + k] = ds[k];
-            }
-            T.cnt[qq] = cnt;
-            T.flg[qq] = live <= KT ? kComplete : 0;
-          } else {
-#pragma unroll
-            for (int k = 0; k < KT; ++k) {
-              stg_t[(qq * kW + gw) * KT + k] = k < cnt ? dt[k] : kInf;
-              stg_j[(qq * kW + gw) * KT + k] = k < cnt ? dj[k] : INT32_MAX;
-              stg_s[(qq * kW + gw) * KT + k] = ds[k];
-            }
-            stg_live[qq * kW + gw] = live;
+          for (int k = 0; k < KT; ++k) {
+            T.t[qq * KT + k] = dt[k];
+            T.j[qq * KT + k] = dj[k];
+            T.s[qq * KT + k] = ds[k];
           }
+          T.cnt[qq] = cnt;
+          T.flg[qq] = live <= KT ? kComplete : 0;
+        } else {
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            stg_t[gw * KT + k] = k < cnt ? dt[k] : kInf;
+            stg_j[gw * KT + k] = k < cnt ? dj[k] : INT32_MAX;
+            stg_s[gw * KT + k] = ds[k];
+          }
+          stg_live[gw] = live;
         }
       }
-    }
-    if (kW > 1) {
-      __syncthreads();
-      if (!leader) continue;
-      // merge the group's partial lists (kW*KT <= 32 candidates per column)
-      for (int q0 = 0; q0 < n; q0 += 32) {
-        int q = q0 + lane;
-        unsigned m = __ballot_sync(kFull, q < n && (T.flg[q] & kDirty) && !c.excl[q]);
-        while (m) {
-          int qq = q0 + __ffs(m) - 1;
-          m &= m - 1;
-          int64_t ct = kInf;
-          int cj = INT32_MAX, cs = -1, lv = 0;
-          if (lane < kW * KT) {
-            ct = stg_t[qq * kW * KT + lane];
-            cj = stg_j[qq * kW * KT + lane];
-            cs = stg_s[qq * kW * KT + lane];
-          }
-          if (lane < kW) lv = stg_live[qq * kW + lane];
+      if (kW > 1) {
+        __syncthreads();
+        if (!leader) continue;
+        // merge the group's partial lists (kW*KT <= 32 candidates)
+        int64_t ct = kInf;
+        int cj = INT32_MAX, cs = -1, lv = 0;
+        if (lane < kW * KT) {
+          ct = stg_t[lane];
+          cj = stg_j[lane];
+          cs = stg_s[lane];
+        }
+        if (lane < kW) lv = stg_live[lane];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) lv += __shfl_xor_sync(kFull, lv, o);
-          int cnt = 0;
+        for (int o = 16; o > 0; o >>= 1) lv += __shfl_xor_sync(kFull, lv, o);
+        int mc = 0;
 #pragma unroll
-          for (int r = 0; r < KT; ++r) {
-            int64_t bt = ct;
-            int64_t bj = cj;
-            warp_argmin(bt, bj);
-            if (bt == kInf) break;
-            unsigned own = __ballot_sync(kFull, cj == bj && ct == bt);
-            int bs = __shfl_sync(kFull, cs, __ffs(own) - 1);
-            if (lane == 0) {
-              T.t[qq * KT + r] = bt;
-              T.j[qq * KT + r] = static_cast<int>(bj);
-              T.s[qq * KT + r] = bs;
-            }
-            ++cnt;
-            if (cj == bj && ct == bt) {
-              ct = kInf;
-              cj = INT32_MAX;
-            }
-          }
+        for (int r = 0; r < KT; ++r) {
+          int64_t bt2 = ct;
+          unsigned bju2 = static_cast<unsigned>(cj);
+          warp_argmin_u(bt2, bju2);
+          const int64_t bj2 = static_cast<int>(bju2);
+          if (bt2 == kInf) break;
+          unsigned own = __ballot_sync(kFull, cj == bj2 && ct == bt2);
+          int bs = __shfl_sync(kFull, cs, __ffs(own) - 1);
           if (lane == 0) {
-            T.cnt[qq] = cnt;
-            T.flg[qq] = lv <= KT ? kComplete : 0;
+            T.t[qq * KT + r] = bt2;
+            T.j[qq * KT + r] = static_cast<int>(bj2);
+            T.s[qq * KT + r] = bs;
+          }
+          ++mc;
+          if (cj == bj2 && ct == bt2) {
+            ct = kInf;
+            cj = INT32_MAX;
           }
         }
+        if (lane == 0) {
+          T.cnt[qq] = mc;
+          T.flg[qq] = lv <= KT ? kComplete : 0;
+        }
       }
+      if (lane == 0) *s_rq = -1;
+    } else if (kW > 1 && !leader) {
+      continue;
     }
     __syncwarp();
     BX_MARK(P_RESCAN);
 
-    // ---- leader only from here: argmin over column heads (key, node, device)
-    int64_t bt = kInf, bi = kInf;
+    // ---- leader only from here: argmin over the clean column heads (key,
+    // node, device). A dirty column's keys are all >= F[q], so it only has to
+    // be rescanned when F[q] does not exceed the best clean head.
+    // cell = node * n + device orders (node, device) lexicographically
+    int64_t bt = kInf, df = kInf;
+    unsigned bi = 0xffffffffu, dq = 0xffffffffu;
     for (int q = lane; q < n; q += 32) {
-      if (c.excl[q] || T.cnt[q] == 0) continue;
+      if (c.excl[q]) continue;
+      if (T.flg[q] & kDirty) {
+        if (c.F[q] < df) {  // ascending q per lane: first minimum wins
+          df = c.F[q];
+          dq = q;
+        }
+        continue;
+      }
+      if (T.cnt[q] == 0) continue;
       int64_t t = T.t[q * KT];
-      int64_t cell = (static_cast<int64_t>(T.j[q * KT]) << 16) | q;
-      if (lex_less(t, cell, bt, bi)) {
+      unsigned cell = static_cast<unsigned>(T.j[q * KT]) * static_cast<unsigned>(n) + q;
+      if (t < bt || (t == bt && cell < bi)) {
         bt = t;
         bi = cell;
       }
     }
-    warp_argmin(bt, bi);
-    if (bi == kInf) {
+    warp_argmin_u(bt, bi);
+    warp_argmin_u(df, dq);
+    if (dq != 0xffffffffu && !(bt < df)) {
+      if (lane == 0) *s_rq = static_cast<int>(dq);
+      __syncwarp();
+      BX_MARK(P_ARGMIN);
+      continue;
+    }
+    if (bi == 0xffffffffu) {
       err_status = kInfeasible;
       err_code = E_NO_PAIR;
       if (lane == 0) *s_done = 1;
       continue;
     }
-    const int j = static_cast<int>(bi >> 16);
-    const int p = static_cast<int>(bi & 0xffff);
+    const int j = static_cast<int>(bi / static_cast<unsigned>(n));
+    const int p = static_cast<int>(bi % static_cast<unsigned>(n));
     const int64_t t = bt;
     const int sj = T.s[p * KT];
     BX_MARK(P_ARGMIN);
@@ -1126,8 +1140,9 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
 #pragma unroll
         for (int r = 0; r < KT; ++r) {
           int64_t bt = ct;
-          int64_t bj = cj;
-          warp_argmin(bt, bj);
+          unsigned bju = static_cast<unsigned>(cj);
+          warp_argmin_u(bt, bju);
+          const int64_t bj = static_cast<int>(bju);
           if (bt == kInf) break;
           unsigned own = __ballot_sync(kFull, cj == bj && ct == bt);
           int bs = __shfl_sync(kFull, cs, __ffs(own) - 1);
@@ -1158,9 +1173,9 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
     const int nnew = S->nnew;
     if (nnew > 0) {
       for (int q = warp; q < n; q += RWARPS) {
-        bool wasdirty = false;
+        bool wasdirty = false;  // rescanned this phase: already includes the new rows
         for (int ci = 0; ci < nd; ++ci) wasdirty |= dcols[ci] == q;
-        if (wasdirty || c.excl[q]) continue;
+        if (wasdirty || c.excl[q] || (flg[q] & kDirty)) continue;
         for (int r0 = 0; r0 < nnew; r0 += 32) {
           REnt e;
           bool have = r0 + lane < nnew;
@@ -1197,7 +1212,8 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
         if (S->placed + k == V) break;
         // threshold: keys in dirty columns are >= F[q]
         int64_t thr = kInf;
-        int64_t bt = kInf, bi = kInf;
+        int64_t bt = kInf;
+        unsigned bi = 0xffffffffu, dummy = 0;
         for (int q = lane; q < n; q += 32) {
           if (c.excl[q]) continue;
           if (flg[q] & kDirty) {
@@ -1205,16 +1221,15 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
             continue;
           }
           if (cnt[q] == 0) continue;
-          int64_t cell = (static_cast<int64_t>(L[q * KT].j) << 16) | q;
-          if (lex_less(L[q * KT].t, cell, bt, bi)) {
+          unsigned cell = static_cast<unsigned>(L[q * KT].j) * static_cast<unsigned>(n) + q;
+          if (L[q * KT].t < bt || (L[q * KT].t == bt && cell < bi)) {
             bt = L[q * KT].t;
             bi = cell;
           }
         }
-        warp_argmin(bt, bi);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) thr = min64(thr, __shfl_xor_sync(kFull, thr, o));
-        if (bi == kInf) {
+        warp_argmin_u(bt, bi);
+        warp_argmin_u(thr, dummy);
+        if (bi == 0xffffffffu) {
           if (k == 0 && thr == kInf) {  // no live pair anywhere
             if (lane == 0) {
               S->err_status = kInfeasible;
@@ -1225,7 +1240,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
           break;
         }
         if (bt >= thr) break;
-        const int q = static_cast<int>(bi & 0xffff);
+        const int q = static_cast<int>(bi % static_cast<unsigned>(n));
         const REnt e = L[q * KT];
         if (c.res[q] + e.need > c.capS[q]) {
           // discard (placers.cpp:203-219), inline: rare. With commits pending
@@ -1334,6 +1349,13 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
           break;
         }
       }
+      // only dirty columns that could beat the best clean head get rescanned
+      // (their keys are all >= F[q]); the others stay dirty, lists stale
+      int64_t tb = kInf;
+      for (int q = lane; q < n; q += 32)
+        if (!c.excl[q] && !(flg[q] & kDirty) && cnt[q] > 0) tb = min64(tb, L[q * KT].t);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tb = min64(tb, __shfl_xor_sync(kFull, tb, o));
       // prefix sums of the committed nodes' degrees; dirty column list
       if (lane == 0) {
         S->ncommit = k;
@@ -1344,7 +1366,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
         }
         int ndc = 0;
         for (int q = 0; q < n; ++q)
-          if ((flg[q] & kDirty) && !c.excl[q]) dcols[ndc++] = q;
+          if ((flg[q] & kDirty) && !c.excl[q] && !(tb < c.F[q])) dcols[ndc++] = q;
         S->ndirty = ndc;
         S->nnew = 0;
         S->nnc = 0;

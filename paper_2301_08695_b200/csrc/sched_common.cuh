@@ -144,6 +144,20 @@ __device__ __forceinline__ void warp_argmin(int64_t &t, int64_t &idx) {
   }
 }
 
+// Lexicographic (key, id) warp argmin for non-negative int64 keys and 32-bit
+// ids with three REDUX instructions instead of 20 shuffles: min of the key's
+// high word, then of the low word among lanes holding that high word, then
+// of the id among lanes holding the minimum key. Every lane gets the result.
+__device__ __forceinline__ void warp_argmin_u(int64_t &t, unsigned &id) {
+  const unsigned long long u = static_cast<unsigned long long>(t);
+  const unsigned hi = static_cast<unsigned>(u >> 32), lo = static_cast<unsigned>(u);
+  const unsigned mhi = __reduce_min_sync(kFull, hi);
+  const unsigned mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xffffffffu);
+  const bool win = hi == mhi && lo == mlo;
+  id = __reduce_min_sync(kFull, win ? id : 0xffffffffu);
+  t = static_cast<int64_t>((static_cast<unsigned long long>(mhi) << 32) | mlo);
+}
+
 __device__ __forceinline__ int64_t warp_max64(int64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = max64(v, __shfl_xor_sync(kFull, v, o));
