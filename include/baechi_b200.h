@@ -231,6 +231,22 @@ int bx_simulate(const bx_graph *graph, int32_t n, const int64_t *capacity,
                 const int32_t *exec_order, const int32_t *exec_off,
                 bx_sim_report *out);
 
+/* LpSolution (lp.hpp:47-53) bookkeeping + SctLp row-class counts (:33-38). */
+typedef struct {
+  int32_t iterations;
+  double rel_gap;
+  double w;            /* unscaled objective after re-tightening the starts */
+  int32_t num_rows, completion_rows, precedence_rows, child_rows, parent_rows, bound_rows;
+} bx_lp_info;
+
+/* bx_lp_solve == build_lp + solve_relaxed (lp.hpp:45-59, lp.cpp:14-278) on a
+ * meta graph: the same Mehrotra IPM (scaling, start point, eta, stopping
+ * rule, 200-iteration cap), normal equations factored on the GPU (cuSOLVER
+ * sparse Cholesky). x [E] (clipped to [0,1]) and s [V] (nullable) are the
+ * unscaled solution. BX_SOLVER with the reference's text on failure. */
+int bx_lp_solve(const bx_graph *graph, const bx_comm *cm, double tolerance, double *x, double *s,
+                bx_lp_info *info, char *msg, int msglen);
+
 /* bx_round_extract == round_and_extract (lp.hpp:88-90, lp.cpp:280-326) on
  * the device (K3): x[E] per meta edge, threshold in (0, 0.5).
  * stats2 = {favorite_edges, repaired_nodes}. */

@@ -105,6 +105,12 @@ class _Grouping(C.Structure):
                 ("member_off", _vp), ("edge_base_count", _vp)]
 
 
+class _LpInfo(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("rel_gap", C.c_double), ("w", C.c_double),
+                ("num_rows", C.c_int32), ("completion_rows", C.c_int32), ("precedence_rows", C.c_int32),
+                ("child_rows", C.c_int32), ("parent_rows", C.c_int32), ("bound_rows", C.c_int32)]
+
+
 class _Comm(C.Structure):
     _fields_ = [("intercept_us", C.c_double), ("us_per_byte", C.c_double), ("mode", C.c_int32)]
 
@@ -164,6 +170,8 @@ def lib():
         L.bx_grouped_view.argtypes = [_vp, C.POINTER(_Graph), C.POINTER(_Grouping)]
         L.bx_grouped_destroy.argtypes = [_vp]
         L.bx_grouped_destroy.restype = None
+        L.bx_lp_solve.argtypes = [C.POINTER(_Graph), C.POINTER(_Comm), C.c_double, _vp, _vp,
+                                   C.POINTER(_LpInfo), cp, C.c_int]
         L.bx_round_extract.argtypes = [i32, i32, _vp, _vp, _vp, C.c_double, _vp, _vp, _vp, cp, C.c_int]
         _lib = L
     return _lib
@@ -172,7 +180,7 @@ def lib():
 EXPORTED = ["bx_version", "bx_last_error", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
             "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download", "bx_plan_result_view",
             "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_profile", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
-            "bx_simulate", "bx_round_extract", "bx_grouped_create", "bx_grouped_view", "bx_grouped_destroy"]
+            "bx_simulate", "bx_round_extract", "bx_grouped_create", "bx_grouped_view", "bx_grouped_destroy", "bx_lp_solve"]
 
 
 def _ptr(a):
@@ -522,6 +530,49 @@ def round_and_extract(V: int, esrc, edst, x, threshold: float = 0.1):
                                 _ptr(fp), _ptr(s2), msg, 256)
     _raise(rc, msg.value.decode())
     return fc[:V], fp[:V], (int(s2[0]), int(s2[1]))
+
+
+@dataclass
+class LpSolution:
+    """LpSolution (lp.hpp:47-53) plus SctLp row-class counts."""
+    x: np.ndarray
+    s: np.ndarray
+    w: float
+    iterations: int
+    rel_gap: float
+    rows: dict
+
+
+def solve_relaxed(gg: MetaGraph, cm: CommModel, tolerance: float = 1e-6) -> LpSolution:
+    """build_lp + solve_relaxed (lp.cpp:14-278): the reference's Mehrotra IPM,
+    normal equations factored on the GPU. Raises SolverError like the
+    reference."""
+    x = np.zeros(max(gg.E, 1), np.float64)
+    s = np.zeros(max(gg.V, 1), np.float64)
+    info = _LpInfo()
+    msg = C.create_string_buffer(512)
+    g = gg._c()
+    cmc = cm._c()
+    rc = lib().bx_lp_solve(C.byref(g), C.byref(cmc), float(tolerance), _ptr(x), _ptr(s), C.byref(info), msg, 512)
+    _raise(rc, msg.value.decode())
+    rows = dict(total=info.num_rows, completion=info.completion_rows, precedence=info.precedence_rows,
+                child=info.child_rows, parent=info.parent_rows, bound=info.bound_rows)
+    return LpSolution(x[:gg.E].copy(), s[:gg.V].copy(), info.w, info.iterations, info.rel_gap, rows)
+
+
+def sct_favorites(gg: MetaGraph, cm: CommModel, threshold: float = 0.1, tolerance: float = 1e-6):
+    """The m-SCT front half of run_placer (bench.cpp:63-70): solve the LP,
+    round at `threshold` and extract favourites (K3 on the GPU). Returns
+    (fav_child, fav_parent, (favorite_edges, repaired_nodes), LpSolution)."""
+    sol = solve_relaxed(gg, cm, tolerance)
+    fc, fp, st = round_and_extract(gg.V, gg.esrc, gg.edst, sol.x, threshold)
+    return fc, fp, st, sol
+
+
+def run_msct(gg: MetaGraph, capacity, cm: CommModel, threshold: float = 0.1, stats_out=None):
+    """run_placer(Algo::MSct) (bench.cpp:63-70): LP -> favourites -> place_msct."""
+    fc, _, _, _ = sct_favorites(gg, cm, threshold)
+    return place_msct(gg, capacity, cm, fc, stats_out=stats_out)
 
 
 def comm_time(cm: CommModel, nbytes: int) -> int:
