@@ -13,7 +13,11 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
         "l1tex__t_sector_hit_rate.pct", "launch__grid_size", "launch__block_size",
         "launch__occupancy_limit_registers", "launch__waves_per_multiprocessor",
-        "sm__inst_executed.sum", "smsp__cycles_active.avg", "launch__shared_mem_per_block"]
+        "sm__inst_executed.sum", "smsp__cycles_active.avg", "launch__shared_mem_per_block",
+        "smsp__average_warp_latency_issue_stalled", "smsp__warp_issue_stalled_long_scoreboard_per_warp_active",
+        "smsp__warp_issue_stalled_barrier_per_warp_active", "smsp__warp_issue_stalled_short_scoreboard_per_warp_active",
+        "smsp__warp_issue_stalled_membar_per_warp_active", "smsp__warp_issue_stalled_wait_per_warp_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "l1tex__t_bytes.sum", "lts__t_bytes.sum"]
 
 
 def launches(path):
