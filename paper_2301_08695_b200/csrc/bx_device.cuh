@@ -128,6 +128,15 @@ struct DSim {
   int32_t *seen;                    // [V] validation
   int64_t *dest_bytes;              // [n]
   int32_t *dest_cnt;                // [n]
+  // dataflow (parallel comm mode) workspace, K4f
+  int32_t *pos;                     // [V] position of a node in its device's exec_order
+  int32_t *psrc;                    // [E] parent of each in-CSR slot
+  int64_t *cx;                      // [E] arrival delay per in-CSR slot (-1 same device, -2 never)
+  int64_t *fin;                     // [V] finish time, -1 until published
+  int64_t *sx;                      // [V] start time per exec slot
+  int64_t *bucket;                  // [V] output bytes freed before each exec slot's start
+  int64_t *mb;                      // [V*n] max bytes per (producer, consumer device)
+  uint8_t *first;                   // [E] edge opens its (producer, device) transfer
   // outputs
   int64_t *start;                   // [V]
   int64_t *dev3n;                   // [3n] peak, busy, idle

@@ -318,7 +318,8 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     if (jobs[i].algo != BX_ALGO_MTOPO) list_ids.push_back(i);
   auto vn = [&](int i) { return int64_t(graphs[jobs[i].graph].V) * std::max(jobs[i].n, 1); };
   std::stable_sort(list_ids.begin(), list_ids.end(), [&](int a, int b) { return vn(a) > vn(b); });
-  const int64_t big_min = list_ids.size() <= 148 ? (int64_t(1) << 15) : (int64_t(1) << 17);
+  int64_t big_min = list_ids.size() <= 148 ? (int64_t(1) << 15) : (int64_t(1) << 17);
+  if (const char *e = std::getenv("BX_BIG_MIN")) big_min = std::atoll(e);  // tuning experiments
   std::vector<char> big(njobs, 0);
   for (size_t r = 0; r < list_ids.size() && r < 120; ++r)
     if (vn(list_ids[r]) >= big_min) big[list_ids[r]] = 1;
@@ -797,6 +798,7 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
   Layout L;
   struct SOff {
     size_t mem, peak, xfree, qpos, busy, cl, fin, sq, res, sent, ht, hk, seen, db, dc, start, dev3n, xfer4, mk, err;
+    size_t pos, psrc, cx, ffin, sx, bucket, mb, first;
   };
   std::vector<SOff> so(P->njobs);
   for (int i = 0; i < P->njobs; ++i) {
@@ -823,6 +825,14 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
     o.xfer4 = L.take<int64_t>(4);
     o.mk = L.take<int64_t>(1);
     o.err = L.take<DErr>(1);
+    o.pos = L.take<int32_t>(V);
+    o.psrc = L.take<int32_t>(E);
+    o.cx = L.take<int64_t>(E);
+    o.ffin = L.take<int64_t>(V);
+    o.sx = L.take<int64_t>(V);
+    o.bucket = L.take<int64_t>(V);
+    o.mb = L.take<int64_t>(V * n);
+    o.first = L.take<uint8_t>(E);
   }
   size_t tab = L.take<DSim>(P->njobs);
   BX_CUDA(cudaMalloc(&P->sim_pool, L.off), msg, msglen);
@@ -865,6 +875,14 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
     d.xfer4 = at<int64_t>(pool, o.xfer4);
     d.makespan = at<int64_t>(pool, o.mk);
     d.err = at<DErr>(pool, o.err);
+    d.pos = at<int32_t>(pool, o.pos);
+    d.psrc = at<int32_t>(pool, o.psrc);
+    d.cx = at<int64_t>(pool, o.cx);
+    d.fin = at<int64_t>(pool, o.ffin);
+    d.sx = at<int64_t>(pool, o.sx);
+    d.bucket = at<int64_t>(pool, o.bucket);
+    d.mb = at<int64_t>(pool, o.mb);
+    d.first = at<uint8_t>(pool, o.first);
     P->sim_fills.push_back({d.resident, 0, size_t(V * n)});
     P->sim_fills.push_back({d.sent, 0, size_t(V * n)});
     P->sim_fills.push_back({d.err, 0, sizeof(DErr)});

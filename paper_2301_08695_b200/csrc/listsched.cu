@@ -856,36 +856,124 @@ __device__ __forceinline__ void rent_meta(REnt &e, const Ctx &c, const DGraph &g
 }
 
 // lane-owned list edits on REnt lists (lane q % 32 owns column q)
+template <int KR>
 __device__ __forceinline__ void rlist_remove(REnt *L, int32_t *cnt, int32_t *flg, int q, int j) {
   int c = cnt[q];
   int at = -1;
   for (int k = 0; k < c; ++k)
-    if (L[q * KT + k].j == j) at = k;
+    if (L[q * KR + k].j == j) at = k;
   if (at < 0) return;
-  for (int k = at; k + 1 < c; ++k) L[q * KT + k] = L[q * KT + k + 1];
+  for (int k = at; k + 1 < c; ++k) L[q * KR + k] = L[q * KR + k + 1];
   cnt[q] = --c;
   if (c == 0 && !(flg[q] & kComplete)) flg[q] |= kDirty;
 }
 
 // insert a fully built entry; returns nothing (list stays exact top-cnt)
+template <int KR>
 __device__ __forceinline__ void rlist_insert(REnt *L, int32_t *cnt, int32_t *flg, int q, const REnt &e) {
   int c = cnt[q];
   int f = flg[q];
   if (f & kDirty) return;
-  if (c == KT) {
+  if (c == KR) {
     flg[q] = f & ~kComplete;
-    if (!lex_less(e.t, e.j, L[q * KT + KT - 1].t, L[q * KT + KT - 1].j)) return;
+    if (!lex_less(e.t, e.j, L[q * KR + KR - 1].t, L[q * KR + KR - 1].j)) return;
     --c;
   } else if (!(f & kComplete)) {
-    if (c == 0 || !lex_less(e.t, e.j, L[q * KT + c - 1].t, L[q * KT + c - 1].j)) return;
+    if (c == 0 || !lex_less(e.t, e.j, L[q * KR + c - 1].t, L[q * KR + c - 1].j)) return;
   }
   int k = c;
-  while (k > 0 && lex_less(e.t, e.j, L[q * KT + k - 1].t, L[q * KT + k - 1].j)) {
-    L[q * KT + k] = L[q * KT + k - 1];
+  while (k > 0 && lex_less(e.t, e.j, L[q * KR + k - 1].t, L[q * KR + k - 1].j)) {
+    L[q * KR + k] = L[q * KR + k - 1];
     --k;
   }
-  L[q * KT + k] = e;
+  L[q * KR + k] = e;
   cnt[q] = c + 1;
+}
+
+// Exact smallest pairs of column q over this warp's share of the slots
+// (s0 + lane + k*step < R). Every lane keeps its own top-LK; a lane that saw
+// more than LK live pairs vouches only up to its LK-th pair, so the share's
+// sorted order is known exactly up to thr = the least such LK-th pair
+// (pairs are unique per column: everything a lane dropped is above it).
+// Pops lane heads while <= thr, at most KR, into out_* (lane 0 writes).
+template <int KR>
+__device__ void warp_prefix(const Ctx &c, int q, int s0, int step, int R, int lane, int64_t *out_t, int32_t *out_j,
+                            int32_t *out_s, int &cnt, int64_t &thr_t, unsigned &thr_j, int &live) {
+  constexpr int LK = 4;
+  int64_t lt[LK];
+  int lj[LK], ls[LK];
+#pragma unroll
+  for (int k = 0; k < LK; ++k) {
+    lt[k] = kInf;
+    lj[k] = INT32_MAX;
+    ls[k] = -1;
+  }
+  int seen = 0;
+  const int64_t *kcol = c.Kc + static_cast<int64_t>(q) * c.V;
+  const int64_t Fq = c.F[q];
+  const int aw = c.sct ? c.awf[q] : -1;
+  const int64_t awu = aw >= 0 ? c.awu[q] : 0;
+  constexpr int U = 4;
+  for (int base = s0 + lane; base < R; base += U * step) {
+    int64_t kv[U];
+    int nd[U];
+    int64_t ug[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int s = base + u * step;
+      kv[u] = s < R ? kcol[s] : kInf;
+      nd[u] = s < R ? c.node_s[s] : 0;
+      ug[u] = (aw >= 0 && s < R) ? c.urg_s[s] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (kv[u] == kInf) continue;
+      ++seen;
+      int64_t t = max64(kv[u], Fq);
+      if (aw >= 0 && aw != nd[u]) t = max64(t, min64(awu, ug[u]));
+      topk_insert(lt, lj, ls, t, nd[u], base + u * step);
+    }
+  }
+  int64_t tt = seen > LK ? lt[LK - 1] : kInf;
+  unsigned tj = seen > LK ? static_cast<unsigned>(lj[LK - 1]) : 0xffffffffu;
+  warp_argmin_u(tt, tj);
+  live = seen;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(kFull, live, o);
+  cnt = 0;
+  int64_t lastt = kInf;
+  unsigned lastj = 0xffffffffu;
+  for (int r = 0; r < KR; ++r) {
+    int64_t bt = lt[0];
+    unsigned bju = static_cast<unsigned>(lj[0]);
+    warp_argmin_u(bt, bju);
+    if (bt == kInf || bt > tt || (bt == tt && bju > tj)) break;
+    const bool own = lj[0] == static_cast<int>(bju) && lt[0] == bt;
+    if (own) {
+      out_t[r] = bt;
+      out_j[r] = static_cast<int>(bju);
+      out_s[r] = ls[0];
+#pragma unroll
+      for (int k = 0; k < LK - 1; ++k) {
+        lt[k] = lt[k + 1];
+        lj[k] = lj[k + 1];
+        ls[k] = ls[k + 1];
+      }
+      lt[LK - 1] = kInf;
+      lj[LK - 1] = INT32_MAX;
+      ls[LK - 1] = -1;
+    }
+    lastt = bt;
+    lastj = bju;
+    ++cnt;
+  }
+  if (cnt == KR) {  // truncated: the share is exact only up to its last pair
+    thr_t = lastt;
+    thr_j = lastj;
+  } else {
+    thr_t = tt;
+    thr_j = tj;
+  }
 }
 
 struct RShared {
@@ -894,6 +982,7 @@ struct RShared {
   int64_t discarded, excluded, awake;
 };
 
+template <int KR>
 __global__ void __launch_bounds__(RWARPS * 32, 1)
     k_place_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                    int maxn) {
@@ -958,13 +1047,16 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
   c.capS = c.res + maxn;
   c.awu = c.capS + maxn;
   REnt *L = reinterpret_cast<REnt *>(c.awu + maxn);
-  RCommit *CM = reinterpret_cast<RCommit *>(L + maxn * KT);
+  RCommit *CM = reinterpret_cast<RCommit *>(L + maxn * KR);
   int64_t *stg_t = reinterpret_cast<int64_t *>(CM + maxn);
   const int ntask = maxn > RWARPS ? maxn : RWARPS;
-  int32_t *stg_j = reinterpret_cast<int32_t *>(stg_t + ntask * KT);
-  int32_t *stg_s = stg_j + ntask * KT;
-  int32_t *stg_live = stg_s + ntask * KT;
-  c.awf = stg_live + ntask;
+  int64_t *stg_tt = stg_t + ntask * KR;  // per task: threshold of its exact prefix
+  int32_t *stg_j = reinterpret_cast<int32_t *>(stg_tt + ntask);
+  int32_t *stg_s = stg_j + ntask * KR;
+  int32_t *stg_live = stg_s + ntask * KR;
+  int32_t *stg_cnt = stg_live + ntask;
+  unsigned *stg_tj = reinterpret_cast<unsigned *>(stg_cnt + ntask);
+  c.awf = reinterpret_cast<int32_t *>(stg_tj + ntask);
   c.excl = c.awf + maxn;
   int32_t *cnt = c.excl + maxn;
   int32_t *flg = cnt + maxn;
@@ -1096,8 +1188,8 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
         S->compact = 0;
       }
       // list entries follow their nodes
-      for (int e = tid; e < n * KT; e += NT)
-        if (e % KT < cnt[e / KT]) L[e].s = c.rpos[L[e].j];
+      for (int e = tid; e < n * KR; e += NT)
+        if (e % KR < cnt[e / KR]) L[e].s = c.rpos[L[e].j];
       __syncthreads();
       RMARK(P_REMOVE);
     }
@@ -1108,62 +1200,59 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
       const int parts = nd >= RWARPS ? 1 : RWARPS / nd;
       for (int task = warp; task < nd * parts; task += RWARPS) {
         const int q = dcols[task / parts], part = task % parts;
-        int64_t dt[KT];
-        int dj[KT], ds[KT], kc, live;
-        warp_topk(c, q, part * 32, 32 * parts, R, lane, dt, dj, ds, kc, live);
+        int kc, live;
+        int64_t tt;
+        unsigned tj;
+        warp_prefix<KR>(c, q, part * 32, 32 * parts, R, lane, stg_t + task * KR, stg_j + task * KR,
+                        stg_s + task * KR, kc, tt, tj, live);
         if (lane == 0) {
-#pragma unroll
-          for (int k = 0; k < KT; ++k) {
-            stg_t[task * KT + k] = k < kc ? dt[k] : kInf;
-            stg_j[task * KT + k] = k < kc ? dj[k] : INT32_MAX;
-            stg_s[task * KT + k] = ds[k];
-          }
+          stg_cnt[task] = kc;
           stg_live[task] = live;
+          stg_tt[task] = tt;
+          stg_tj[task] = tj;
         }
       }
       __syncthreads();
       for (int ci = warp; ci < nd; ci += RWARPS) {
         const int q = dcols[ci];
-        int64_t ct = kInf;
-        int cj = INT32_MAX, cs = -1, lv = 0;
-        if (lane < parts * KT) {
-          ct = stg_t[ci * parts * KT + lane];
-          cj = stg_j[ci * parts * KT + lane];
-          cs = stg_s[ci * parts * KT + lane];
+        // merge the parts' exact prefixes up to the least threshold
+        const int tb = ci * parts;
+        int ptr = 0, cl = 0, lv = 0;
+        int64_t thr_t = kInf;
+        unsigned thr_j = 0xffffffffu;
+        if (lane < parts) {
+          cl = stg_cnt[tb + lane];
+          lv = stg_live[tb + lane];
+          thr_t = stg_tt[tb + lane];
+          thr_j = stg_tj[tb + lane];
         }
-        if (lane < parts) lv = stg_live[ci * parts + lane];
+        warp_argmin_u(thr_t, thr_j);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) lv += __shfl_xor_sync(kFull, lv, o);
         int kc = 0;
-        REnt mine;
-        mine.j = -1;
-#pragma unroll
-        for (int r = 0; r < KT; ++r) {
-          int64_t bt = ct;
-          unsigned bju = static_cast<unsigned>(cj);
-          warp_argmin_u(bt, bju);
-          const int64_t bj = static_cast<int>(bju);
-          if (bt == kInf) break;
-          unsigned own = __ballot_sync(kFull, cj == bj && ct == bt);
-          int bs = __shfl_sync(kFull, cs, __ffs(own) - 1);
-          if (lane == r) {
-            mine.t = bt;
-            mine.j = static_cast<int>(bj);
-            mine.s = bs;
+        for (int r = 0; r < KR; ++r) {
+          const bool has = lane < parts && ptr < cl;
+          const int64_t ht = has ? stg_t[(tb + lane) * KR + ptr] : kInf;
+          const unsigned hj = has ? static_cast<unsigned>(stg_j[(tb + lane) * KR + ptr]) : 0xffffffffu;
+          int64_t bt = ht;
+          unsigned bj = hj;
+          warp_argmin_u(bt, bj);
+          if (bt == kInf || bt > thr_t || (bt == thr_t && bj > thr_j)) break;
+          if (has && ht == bt && hj == bj) {
+            L[q * KR + r].t = bt;
+            L[q * KR + r].j = static_cast<int>(bj);
+            L[q * KR + r].s = stg_s[(tb + lane) * KR + ptr];
+            ++ptr;
           }
           ++kc;
-          if (cj == bj && ct == bt) {
-            ct = kInf;
-            cj = INT32_MAX;
-          }
         }
-        if (lane < kc) {  // metadata of the listed nodes, fetched in parallel
-          rent_meta(mine, c, g);
-          L[q * KT + lane] = mine;
-        }
+        __syncwarp();
+        if (lane < kc) rent_meta(L[q * KR + lane], c, g);  // listed nodes' metadata, in parallel
+        if (KR > 32)
+          for (int r = lane + 32; r < kc; r += 32) rent_meta(L[q * KR + r], c, g);
         if (lane == 0) {
           cnt[q] = kc;
-          flg[q] = lv <= KT ? kComplete : 0;
+          flg[q] = lv == kc ? kComplete : 0;
         }
       }
     }
@@ -1197,7 +1286,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
             x.ine = __shfl_sync(kFull, e.ine, l);
             x.outb = __shfl_sync(kFull, e.outb, l);
             x.oute = __shfl_sync(kFull, e.oute, l);
-            if (lane == 0 && x.t != kInf) rlist_insert(L, cnt, flg, q, x);
+            if (lane == 0 && x.t != kInf) rlist_insert<KR>(L, cnt, flg, q, x);
           }
         }
       }
@@ -1221,9 +1310,9 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
             continue;
           }
           if (cnt[q] == 0) continue;
-          unsigned cell = static_cast<unsigned>(L[q * KT].j) * static_cast<unsigned>(n) + q;
-          if (L[q * KT].t < bt || (L[q * KT].t == bt && cell < bi)) {
-            bt = L[q * KT].t;
+          unsigned cell = static_cast<unsigned>(L[q * KR].j) * static_cast<unsigned>(n) + q;
+          if (L[q * KR].t < bt || (L[q * KR].t == bt && cell < bi)) {
+            bt = L[q * KR].t;
             bi = cell;
           }
         }
@@ -1241,7 +1330,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
         }
         if (bt >= thr) break;
         const int q = static_cast<int>(bi % static_cast<unsigned>(n));
-        const REnt e = L[q * KT];
+        const REnt e = L[q * KR];
         if (c.res[q] + e.need > c.capS[q]) {
           // discard (placers.cpp:203-219), inline: rare. With commits pending
           // in this round, end the round first: the pair stays the minimum
@@ -1264,7 +1353,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
             break;
           }
           if (lane == 0) S->discarded++;
-          if (lane == (q & 31)) rlist_remove(L, cnt, flg, q, e.j);
+          if (lane == (q & 31)) rlist_remove<KR>(L, cnt, flg, q, e.j);
           int64_t minrem = 0;
           if (lane == 0) {
             while (c.device_of[g.need_order[minptr]] >= 0) ++minptr;
@@ -1326,7 +1415,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
         __syncwarp();
         for (int qq = lane; qq < n; qq += 32) {
           if (qq == q) flg[qq] |= kDirty;
-          else rlist_remove(L, cnt, flg, qq, e.j);
+          else rlist_remove<KR>(L, cnt, flg, qq, e.j);
         }
         __syncwarp();
         if (c.sct) {
@@ -1353,7 +1442,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
       // (their keys are all >= F[q]); the others stay dirty, lists stale
       int64_t tb = kInf;
       for (int q = lane; q < n; q += 32)
-        if (!c.excl[q] && !(flg[q] & kDirty) && cnt[q] > 0) tb = min64(tb, L[q * KT].t);
+        if (!c.excl[q] && !(flg[q] & kDirty) && cnt[q] > 0) tb = min64(tb, L[q * KR].t);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tb = min64(tb, __shfl_xor_sync(kFull, tb, o));
       // prefix sums of the committed nodes' degrees; dirty column list
@@ -1364,12 +1453,19 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
           inoff[i + 1] = inoff[i] + (CM[i].ine - CM[i].inb);
           outoff[i + 1] = outoff[i] + (CM[i].oute - CM[i].outb);
         }
-        int ndc = 0;
-        for (int q = 0; q < n; ++q)
-          if ((flg[q] & kDirty) && !c.excl[q] && !(tb < c.F[q])) dcols[ndc++] = q;
-        S->ndirty = ndc;
         S->nnew = 0;
         S->nnc = 0;
+      }
+      {
+        int ndc = 0;
+        for (int q0 = 0; q0 < n; q0 += 32) {
+          const int q = q0 + lane;
+          const bool want = q < n && (flg[q] & kDirty) && !c.excl[q] && !(tb < c.F[q]);
+          const unsigned m = __ballot_sync(kFull, want);
+          if (want) dcols[ndc + __popc(m & ((1u << lane) - 1u))] = q;
+          ndc += __popc(m);
+        }
+        if (lane == 0) S->ndirty = ndc;
       }
     }
     __syncthreads();
@@ -1488,20 +1584,29 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
 #undef RMARK
 }
 
-static size_t rounds_smem(int maxn) {
+static size_t rounds_smem(int maxn, int KR) {
   const int ntask = maxn > RWARPS ? maxn : RWARPS;
-  return ((sizeof(RShared) + 15) & ~size_t(15)) + 5 * 8 * size_t(maxn) + sizeof(REnt) * KT * maxn +
-         sizeof(RCommit) * maxn + size_t(ntask) * KT * 16 + 4 * size_t(ntask) +
+  return ((sizeof(RShared) + 15) & ~size_t(15)) + 5 * 8 * size_t(maxn) + sizeof(REnt) * KR * maxn +
+         sizeof(RCommit) * maxn + size_t(ntask) * (KR * 16 + 8 + 12) +
          4 * (7 * size_t(maxn) + 2) + 4 * (RWARPS + 1) + 64;  // awf excl cnt flg dcols inoff outoff wsum
 }
 
+// list length per device column: long lists when they fit (fewer rescans: the
+// columns' heads are largely the same nodes, so short lists drain together)
 void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                    int maxn, bool prof, cudaStream_t s) {
   (void)prof;
-  const size_t sm = rounds_smem(maxn);
-  if (sm > 48 * 1024)
-    cudaFuncSetAttribute(k_place_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-  k_place_rounds<<<njobs, RWARPS * 32, sm, s>>>(jobs, order, njobs, graphs, preps, maxn);
+  if (rounds_smem(maxn, 16) <= 200 * 1024) {
+    const size_t sm = rounds_smem(maxn, 16);
+    if (sm > 48 * 1024)
+      cudaFuncSetAttribute(k_place_rounds<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    k_place_rounds<16><<<njobs, RWARPS * 32, sm, s>>>(jobs, order, njobs, graphs, preps, maxn);
+  } else {
+    const size_t sm = rounds_smem(maxn, KT);
+    if (sm > 48 * 1024)
+      cudaFuncSetAttribute(k_place_rounds<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    k_place_rounds<KT><<<njobs, RWARPS * 32, sm, s>>>(jobs, order, njobs, graphs, preps, maxn);
+  }
 }
 
 

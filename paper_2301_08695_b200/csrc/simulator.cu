@@ -128,6 +128,12 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
   c.V = c.g.V;
   c.n = c.s.n;
   c.lane = lane;
+  if (c.s.mode == 1) {
+    // parallel comm mode without zero-duration nodes belongs to K4f
+    bool zero = false;
+    for (int j = lane; j < c.V; j += 32) zero |= c.g.k[j] == 0;
+    if (!__any_sync(kFullS, zero)) return;
+  }
   c.h.t = c.s.heap_t;
   c.h.k = c.s.heap_k;
   c.h.size = 0;
@@ -333,9 +339,381 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
   }
 }
 
+// ============================================================================
+// K4f — the dataflow simulator: parallel comm mode, every node k > 0.
+//
+// In parallel mode each (producer i, consumer device d) transfer leaves at
+// i's finish and takes comm_time(max bytes over i's consumers on d)
+// (simulator.cpp:156-181), so the start of node j, the next entry of its
+// device's FIFO, is
+//     start_j = max(finish of j's FIFO predecessor,
+//                   max over remote parents i of finish_i + c(i, dev j))
+// (same-device parents precede j in the FIFO or the run deadlocks, and then
+// finish before its predecessor does). Start times are therefore a longest
+// path, order-independent: one warp walks each device's FIFO, 32 entries at a
+// time, and a lane's entry is ready once every remote parent has published
+// its finish; the ready prefix is resolved by a warp max-plus scan
+// f_l = max(f_{l-1} + k_l, A_l + k_l). Walkers run in barrier rounds until
+// none moves: then either every FIFO is drained or the run is deadlocked
+// (the reference's qpos = the walkers' positions).
+//
+// Memory (simulator.cpp:66-76,121-152): a device's own start/finish events
+// alternate in FIFO order; with k > 0 every event pushed at time t is a start
+// (finishes at t were pushed earlier), so the heap pops same-time events as
+// finish < xfer < start, by node. An output freed at its last consumer's
+// finish (GraphStatic) therefore lands before the first start on its device
+// at or after that finish time: a bucket per FIFO slot, then one scan per
+// device gives the memory at every start, the peak, and the first violation
+// (min (t, node) over devices = the heap's first). Zero-duration nodes can
+// cascade same-time events out of key order; those problems and sequential
+// comm mode stay on the event-loop kernel above.
+// ============================================================================
+__device__ __forceinline__ int64_t ld_cta(const int64_t *p) {
+  int64_t v;
+  asm volatile("ld.relaxed.cta.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cta(int64_t *p, int64_t v) {
+  asm volatile("st.relaxed.cta.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(1024) k_sim_flow(const DSim *sims, int nsims, const DGraph *graphs) {
+  __shared__ unsigned long long sh_x[3];  // transfers, bytes, remote edges
+  __shared__ long long sh_mk;
+  __shared__ int sh_bad;
+  const DSim s = sims[blockIdx.x];
+  if (s.mode != 1) return;
+  const DGraph g = graphs[s.graph];
+  const int V = g.V, E = g.E, n = s.n;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  DErr *err = s.err;
+  int zero = 0;
+  for (int j = tid; j < V; j += NT) zero |= g.k[j] == 0;
+  if (__syncthreads_or(zero)) return;  // event-loop kernel
+
+  // ---- validate_placement (simulator.cpp:78-97) ------------------------------
+  for (int j = tid; j < V; j += NT) s.seen[j] = 0;
+  if (tid == 0) {
+    sh_x[0] = sh_x[1] = sh_x[2] = 0;
+    sh_mk = 0;
+    sh_bad = INT32_MAX;
+  }
+  __syncthreads();
+  int bad = 0;
+  for (int d = 0; d < n; ++d) {
+    const int o = s.exec_off[d], e = s.exec_off[d + 1];
+    for (int x = o + tid; x < e; x += NT) {
+      const int m = s.exec_order[x];
+      if (m < 0 || m >= V || s.device_of[m] != d) {
+        bad = 1;
+      } else {
+        atomicAdd(&s.seen[m], 1);
+        s.pos[m] = x - o;
+      }
+    }
+  }
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) {
+      err->status = kValidation;
+      err->code = E_SIM_EXEC;
+    }
+    return;
+  }
+  for (int j = tid; j < V; j += NT) {
+    const int d = s.device_of[j];
+    if (d < 0 || d >= n || s.seen[j] != 1) bad = 1;
+  }
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) {
+      err->status = kValidation;
+      err->code = E_SIM_ONCE;
+    }
+    return;
+  }
+
+  // ---- transfers: one per (producer, remote consumer device), max bytes ------
+  for (int j = tid; j < V; j += NT) {
+    s.fin[j] = -1;
+    s.bucket[j] = 0;
+  }
+  for (int e = tid; e < E; e += NT) {
+    const int i = g.esrc[e], dc = s.device_of[g.edst[e]];
+    if (s.device_of[i] != dc) s.mb[static_cast<int64_t>(i) * n + dc] = -1;
+  }
+  __syncthreads();
+  {
+    unsigned long long cnt = 0, rem = 0;
+    for (int e = tid; e < E; e += NT) {
+      const int i = g.esrc[e], dc = s.device_of[g.edst[e]];
+      uint8_t f = 0;
+      if (s.device_of[i] != dc) {
+        ++rem;
+        auto *slot = reinterpret_cast<unsigned long long *>(s.mb + static_cast<int64_t>(i) * n + dc);
+        f = atomicCAS(slot, ~0ull, ~0ull - 1) == ~0ull;
+        cnt += f;
+        atomicMax(reinterpret_cast<long long *>(slot), static_cast<long long>(g.ebytes[e]));
+      }
+      s.first[e] = f;
+    }
+    atomicAdd(&sh_x[0], cnt);
+    atomicAdd(&sh_x[2], rem);
+  }
+  __syncthreads();
+  {
+    unsigned long long by = 0;
+    for (int e = tid; e < E; e += NT)
+      if (s.first[e]) by += s.mb[static_cast<int64_t>(g.esrc[e]) * n + s.device_of[g.edst[e]]];
+    atomicAdd(&sh_x[1], by);
+  }
+  // per in-CSR slot: the parent and its arrival delay on the consumer's device
+  for (int x = tid; x < E; x += NT) {
+    const int e = g.in_edge[x];
+    const int i = g.esrc[e], c = g.edst[e];
+    const int di = s.device_of[i], dc = s.device_of[c];
+    s.psrc[x] = i;
+    s.cx[x] = di == dc ? (s.pos[i] < s.pos[c] ? -1 : -2)
+                       : comm_time_exact(s.ic, s.pb, s.mb[static_cast<int64_t>(i) * n + dc]);
+  }
+  // permanent memory up front, device by device in FIFO order (:209-214)
+  for (int d = warp; d < n; d += NW) {
+    const int o = s.exec_off[d], len = s.exec_off[d + 1] - o;
+    const int64_t cap = s.cap[d];
+    int64_t run = 0;
+    int vbad = INT32_MAX;
+    int64_t vmem = 0;
+    for (int b = 0; b < len; b += 32) {
+      const int p = b + lane;
+      int64_t v = p < len ? g.perm[s.exec_order[o + p]] : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        int64_t u = __shfl_up_sync(kFullS, v, off);
+        if (lane >= off) v += u;
+      }
+      const int64_t m = run + v;
+      unsigned over = __ballot_sync(kFullS, p < len && m > cap);
+      if (over && vbad == INT32_MAX) {
+        const int l = __ffs(over) - 1;
+        vbad = b + l;
+        vmem = __shfl_sync(kFullS, m, l);
+      }
+      run = __shfl_sync(kFullS, m, 31);
+    }
+    if (lane == 0) {
+      s.mem[d] = run;
+      s.qpos[d] = 0;
+      s.xfree[d] = 0;
+      s.dest_cnt[d] = vbad;  // first violating FIFO slot (perm)
+      s.dest_bytes[d] = vmem;
+      if (vbad != INT32_MAX) atomicMin(&sh_bad, d);
+    }
+  }
+  __syncthreads();
+  if (sh_bad != INT32_MAX) {
+    if (tid == 0) {
+      const int d = sh_bad;
+      err->status = kInfeasible;
+      err->code = E_SIM_MEMORY;
+      err->a = d;
+      err->b = 0;
+      err->c = s.exec_order[s.exec_off[d] + s.dest_cnt[d]];
+      err->d = s.dest_bytes[d];
+    }
+    return;
+  }
+
+  // ---- walkers ----------------------------------------------------------------
+  int64_t mk = 0;
+  while (true) {
+    int adv = 0;
+    for (int d = warp; d < n; d += NW) {
+      const int o = s.exec_off[d], len = s.exec_off[d + 1] - o;
+      int p = s.qpos[d];
+      int64_t prev = s.xfree[d];
+      while (p < len) {
+        const int idx = p + lane;
+        bool ok = false;
+        int64_t A = 0, kk = 0;
+        int j = -1;
+        if (idx < len) {
+          j = s.exec_order[o + idx];
+          kk = g.k[j];
+          ok = true;
+          const int xe = g.in_off[j + 1];
+          for (int x = g.in_off[j]; x < xe; ++x) {
+            const int64_t cc = s.cx[x];
+            if (cc == -1) continue;
+            if (cc == -2) {
+              ok = false;
+              break;
+            }
+            const int64_t f = ld_cta(s.fin + s.psrc[x]);
+            if (f < 0) {
+              ok = false;
+              break;
+            }
+            A = smax(A, f + cc);
+          }
+        }
+        const unsigned okm = __ballot_sync(kFullS, ok);
+        const int L = okm == kFullS ? 32 : __ffs(~okm) - 1;
+        if (L == 0) break;
+        int64_t al = kk, be = A + kk;  // g_l(f) = max(f + al, be), composed over lanes <= l
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int64_t a2 = __shfl_up_sync(kFullS, al, off), b2 = __shfl_up_sync(kFullS, be, off);
+          if (lane >= off) {
+            be = smax(b2 + al, be);
+            al = a2 + al;
+          }
+        }
+        const int64_t f = smax(prev + al, be);
+        if (lane < L) {
+          s.sx[o + idx] = f - kk;
+          s.start[j] = f - kk;
+          st_cta(s.fin + j, f);
+        }
+        prev = __shfl_sync(kFullS, f, L - 1);
+        p += L;
+        adv = 1;
+        if (L < 32) break;
+      }
+      if (lane == 0) {
+        s.qpos[d] = p;
+        s.xfree[d] = prev;
+      }
+      mk = smax(mk, prev);
+    }
+    if (!__syncthreads_or(adv)) break;
+  }
+  if (lane == 0) atomicMax(&sh_mk, static_cast<long long>(mk));
+
+  // ---- memory at every start ------------------------------------------------------
+  if (s.mem_mode == 0) {
+    for (int i = tid; i < V; i += NT) {
+      const int b = g.out_off[i], e = g.out_off[i + 1];
+      if (b == e) continue;  // freed at its own finish
+      int64_t lt = -1;
+      int lc = -1;
+      bool all = true;
+      for (int y = b; y < e; ++y) {
+        const int c = g.edst[y];
+        const int64_t f = s.fin[c];
+        if (f < 0) {
+          all = false;
+          break;
+        }
+        if (f > lt || (f == lt && c > lc)) {
+          lt = f;
+          lc = c;
+        }
+      }
+      if (!all) continue;
+      const int d = s.device_of[i], o = s.exec_off[d];
+      int lo = 0, hi = s.qpos[d];  // first started slot with start >= lt
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s.sx[o + mid] >= lt) hi = mid;
+        else lo = mid + 1;
+      }
+      if (lo < s.qpos[d]) atomicAdd(reinterpret_cast<unsigned long long *>(s.bucket + o + lo),
+                                    static_cast<unsigned long long>(g.outb[i]));
+    }
+  }
+  __syncthreads();
+  for (int d = warp; d < n; d += NW) {
+    const int o = s.exec_off[d], started = s.qpos[d];
+    const int64_t cap = s.cap[d];
+    int64_t run = s.mem[d], peak = run, vt = INT64_MAX, vm = 0;
+    int vj = INT32_MAX;
+    int64_t busy = 0;
+    for (int b = 0; b < started; b += 32) {
+      const int p = b + lane;
+      int64_t ch = 0, w = 0, fr = 0;
+      int j = -1;
+      if (p < started) {
+        j = s.exec_order[o + p];
+        const int64_t tmp = g.temp[j], out = g.outb[j];
+        ch = tmp + out;
+        const bool drop = s.mem_mode == 0 && g.out_off[j + 1] == g.out_off[j];
+        fr = s.bucket[o + p];
+        w = ch - tmp - (drop ? out : 0) - fr;
+        busy += g.k[j];
+      }
+      int64_t incl = w;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int64_t u = __shfl_up_sync(kFullS, incl, off);
+        if (lane >= off) incl += u;
+      }
+      const int64_t m = run + (incl - w) - fr + ch;
+      if (p < started) peak = smax(peak, m);
+      const unsigned over = __ballot_sync(kFullS, p < started && m > cap);
+      if (over && vt == INT64_MAX) {
+        const int l = __ffs(over) - 1;
+        vt = s.sx[o + b + l];
+        vj = __shfl_sync(kFullS, j, l);
+        vm = __shfl_sync(kFullS, m, l);
+      }
+      run += __shfl_sync(kFullS, incl, 31);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      peak = smax(peak, __shfl_xor_sync(kFullS, peak, off));
+      busy += __shfl_xor_sync(kFullS, busy, off);
+    }
+    if (lane == 0) {
+      s.peak[d] = peak;
+      s.dest_bytes[d] = vt;
+      s.dest_cnt[d] = vj;
+      s.xfree[d] = vm;
+      s.dev3n[3 * d + 1] = busy;
+    }
+  }
+  __syncthreads();
+  if (tid != 0) return;
+  int vd = -1;
+  for (int d = 0; d < n; ++d) {
+    const int64_t t = s.dest_bytes[d];
+    if (t == INT64_MAX) continue;
+    if (vd < 0 || t < s.dest_bytes[vd] || (t == s.dest_bytes[vd] && s.dest_cnt[d] < s.dest_cnt[vd])) vd = d;
+  }
+  if (vd >= 0) {
+    err->status = kInfeasible;
+    err->code = E_SIM_MEMORY;
+    err->a = vd;
+    err->b = s.dest_bytes[vd];
+    err->c = s.dest_cnt[vd];
+    err->d = s.xfree[vd];
+    return;
+  }
+  for (int d = 0; d < n; ++d) {
+    if (s.qpos[d] < s.exec_off[d + 1] - s.exec_off[d]) {  // deadlock (:234-246)
+      err->status = kValidation;
+      err->code = E_SIM_DEADLOCK;
+      err->a = d;
+      err->c = s.exec_order[s.exec_off[d] + s.qpos[d]];
+      return;
+    }
+  }
+  const int64_t makespan = sh_mk;
+  for (int d = 0; d < n; ++d) {
+    s.dev3n[3 * d + 0] = s.peak[d];
+    s.dev3n[3 * d + 2] = makespan - s.dev3n[3 * d + 1];
+  }
+  *s.makespan = makespan;
+  s.xfer4[0] = static_cast<int64_t>(sh_x[0]);
+  s.xfer4[1] = static_cast<int64_t>(sh_x[1]);
+  s.xfer4[2] = 0;  // a tensor is sent once per device: duplicates never arise
+  s.xfer4[3] = static_cast<int64_t>(sh_x[2] - sh_x[0]);
+  err->status = kOk;
+  err->code = E_NONE;
+}
+
 void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, cudaStream_t s) {
   constexpr int W = 4;
   k_simulate<W><<<(nsims + W - 1) / W, 32 * W, 0, s>>>(sims, nsims, graphs);
+  // one CTA per problem; a lone problem gets the widest CTA for its edge passes
+  k_sim_flow<<<nsims, nsims <= 148 ? 1024 : 256, 0, s>>>(sims, nsims, graphs);
 }
 
 // ---------------------------------------------------------------- K3 ----
