@@ -318,11 +318,18 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     if (jobs[i].algo != BX_ALGO_MTOPO) list_ids.push_back(i);
   auto vn = [&](int i) { return int64_t(graphs[jobs[i].graph].V) * std::max(jobs[i].n, 1); };
   std::stable_sort(list_ids.begin(), list_ids.end(), [&](int a, int b) { return vn(a) > vn(b); });
-  int64_t big_min = list_ids.size() <= 148 ? (int64_t(1) << 15) : (int64_t(1) << 17);
-  if (const char *e = std::getenv("BX_BIG_MIN")) big_min = std::atoll(e);  // tuning experiments
+  // A plan of at most 148 list jobs gives every parallel-mode job its own
+  // round-kernel CTA (faster per commit at every size measured,
+  // profiles/r01c_kr_sweep.txt); sequential-mode jobs go wide from 2^15.
+  const bool few = list_ids.size() <= 148;
+  int64_t big_min = few ? (int64_t(1) << 15) : (int64_t(1) << 17);
+  int64_t big_min_par = few ? 0 : big_min;
+  if (const char *e = std::getenv("BX_BIG_MIN")) big_min = big_min_par = std::atoll(e);  // tuning experiments
   std::vector<char> big(njobs, 0);
-  for (size_t r = 0; r < list_ids.size() && r < 120; ++r)
-    if (vn(list_ids[r]) >= big_min) big[list_ids[r]] = 1;
+  for (size_t r = 0; r < list_ids.size() && r < 120; ++r) {
+    const int i = list_ids[r];
+    if (vn(i) >= (jobs[i].cm.mode == BX_COMM_SEQUENTIAL ? big_min : big_min_par)) big[i] = 1;
+  }
   // job inputs (capacities, favourites) and outputs live in two contiguous
   // regions so an end-to-end step moves them with one copy each way, through
   // pinned host mirrors

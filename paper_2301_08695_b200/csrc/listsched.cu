@@ -33,16 +33,19 @@
 // else except removing the committed node from every column; so per step
 // only column p is rescanned, every other column just drops the node from
 // its top list, and new ready rows are merged into the lists.
+#include <cstdlib>
+
 #include "sched_common.cuh"
 
 namespace bx {
 
 constexpr int KT = 4;  // exact top-KT pairs kept per device column
 
-struct Tops {
-  int64_t *t;    // [n*KT] keys, ascending (key, node)
-  int32_t *j;    // [n*KT] nodes
-  int32_t *s;    // [n*KT] their ready slots
+struct Tops {      // entry k of column q at k * st + q (no bank conflicts for lane-owned columns)
+  int64_t *t;    // [KT*st] keys, ascending (key, node)
+  int32_t *j;    // [KT*st] nodes
+  int32_t *s;    // [KT*st] their ready slots
+  int st;
   int32_t *cnt;  // [n]
   int32_t *flg;  // [n] bit0 dirty, bit1 complete (list holds every live pair)
 };
@@ -215,12 +218,12 @@ __device__ __forceinline__ void list_remove(const Tops &T, int q, int j) {
   int c = T.cnt[q];
   int at = -1;
   for (int k = 0; k < c; ++k)
-    if (T.j[q * KT + k] == j) at = k;
+    if (T.j[(k) * T.st + q] == j) at = k;
   if (at < 0) return;
   for (int k = at; k + 1 < c; ++k) {
-    T.t[q * KT + k] = T.t[q * KT + k + 1];
-    T.j[q * KT + k] = T.j[q * KT + k + 1];
-    T.s[q * KT + k] = T.s[q * KT + k + 1];
+    T.t[(k) * T.st + q] = T.t[(k + 1) * T.st + q];
+    T.j[(k) * T.st + q] = T.j[(k + 1) * T.st + q];
+    T.s[(k) * T.st + q] = T.s[(k + 1) * T.st + q];
   }
   T.cnt[q] = --c;
   if (c == 0 && !(T.flg[q] & kComplete)) T.flg[q] |= kDirty;
@@ -232,22 +235,22 @@ __device__ __forceinline__ void list_insert(const Tops &T, int q, int64_t t, int
   if (f & kDirty) return;
   if (c == KT) {
     T.flg[q] = f & ~kComplete;  // a live pair now sits outside the list
-    if (!lex_less(t, j, T.t[q * KT + KT - 1], T.j[q * KT + KT - 1])) return;
+    if (!lex_less(t, j, T.t[(KT - 1) * T.st + q], T.j[(KT - 1) * T.st + q])) return;
     --c;
   } else if (!(f & kComplete)) {
     // incomplete list: only pairs that beat the last listed one are known
-    if (c == 0 || !lex_less(t, j, T.t[q * KT + c - 1], T.j[q * KT + c - 1])) return;
+    if (c == 0 || !lex_less(t, j, T.t[(c - 1) * T.st + q], T.j[(c - 1) * T.st + q])) return;
   }
   int k = c;
-  while (k > 0 && lex_less(t, j, T.t[q * KT + k - 1], T.j[q * KT + k - 1])) {
-    T.t[q * KT + k] = T.t[q * KT + k - 1];
-    T.j[q * KT + k] = T.j[q * KT + k - 1];
-    T.s[q * KT + k] = T.s[q * KT + k - 1];
+  while (k > 0 && lex_less(t, j, T.t[(k - 1) * T.st + q], T.j[(k - 1) * T.st + q])) {
+    T.t[(k) * T.st + q] = T.t[(k - 1) * T.st + q];
+    T.j[(k) * T.st + q] = T.j[(k - 1) * T.st + q];
+    T.s[(k) * T.st + q] = T.s[(k - 1) * T.st + q];
     --k;
   }
-  T.t[q * KT + k] = t;
-  T.j[q * KT + k] = j;
-  T.s[q * KT + k] = s;
+  T.t[(k) * T.st + q] = t;
+  T.j[(k) * T.st + q] = j;
+  T.s[(k) * T.st + q] = s;
   T.cnt[q] = c + 1;
 }
 
@@ -345,6 +348,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     c.res = c.tail + maxn;
     c.capS = c.res + maxn;
     c.awu = c.capS + maxn;
+    T.st = maxn;
     T.t = c.awu + maxn;
     int64_t *p64 = T.t + maxn * KT;
     if (kW > 1) {
@@ -437,9 +441,9 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
         if (kW == 1) {
 #pragma unroll
           for (int k = 0; k < KT; ++k) {
-            T.t[qq * KT + k] = dt[k];
-            T.j[qq * KT + k] = dj[k];
-            T.s[qq * KT + k] = ds[k];
+            T.t[(k) * T.st + qq] = dt[k];
+            T.j[(k) * T.st + qq] = dj[k];
+            T.s[(k) * T.st + qq] = ds[k];
           }
           T.cnt[qq] = cnt;
           T.flg[qq] = live <= KT ? kComplete : 0;
@@ -478,9 +482,9 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
           unsigned own = __ballot_sync(kFull, cj == bj2 && ct == bt2);
           int bs = __shfl_sync(kFull, cs, __ffs(own) - 1);
           if (lane == 0) {
-            T.t[qq * KT + r] = bt2;
-            T.j[qq * KT + r] = static_cast<int>(bj2);
-            T.s[qq * KT + r] = bs;
+            T.t[(r) * T.st + qq] = bt2;
+            T.j[(r) * T.st + qq] = static_cast<int>(bj2);
+            T.s[(r) * T.st + qq] = bs;
           }
           ++mc;
           if (cj == bj2 && ct == bt2) {
@@ -516,8 +520,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
         continue;
       }
       if (T.cnt[q] == 0) continue;
-      int64_t t = T.t[q * KT];
-      unsigned cell = static_cast<unsigned>(T.j[q * KT]) * static_cast<unsigned>(n) + q;
+      int64_t t = T.t[q];
+      unsigned cell = static_cast<unsigned>(T.j[q]) * static_cast<unsigned>(n) + q;
       if (t < bt || (t == bt && cell < bi)) {
         bt = t;
         bi = cell;
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     const int j = static_cast<int>(bi / static_cast<unsigned>(n));
     const int p = static_cast<int>(bi % static_cast<unsigned>(n));
     const int64_t t = bt;
-    const int sj = T.s[p * KT];
+    const int sj = T.s[p];
     BX_MARK(P_ARGMIN);
 
     if (c.mode == 0) {
@@ -686,8 +690,10 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
         c.alive_s[sj] = c.alive_s[last];
         c.rpos[mv] = sj;
       }
-      for (int e = lane; e < n * KT; e += 32)
-        if (T.j[e] == mv) T.s[e] = sj;
+      for (int e = lane; e < n * KT; e += 32) {
+        const int x = (e / n) * T.st + e % n;
+        if (T.j[x] == mv) T.s[x] = sj;
+      }
     }
     --R;
     __syncwarp();
@@ -855,38 +861,86 @@ __device__ __forceinline__ void rent_meta(REnt &e, const Ctx &c, const DGraph &g
   e.oute = g.out_off[e.j + 1];
 }
 
-// lane-owned list edits on REnt lists (lane q % 32 owns column q)
+// Per-column sorted lists in shared memory, structure of arrays, entry k of
+// column q at k * st + q: lanes that own consecutive columns touch consecutive
+// words (no bank conflicts for the lane-owned edits and the head scans).
+struct RList {
+  int64_t *t, *need, *k;
+  int32_t *j, *s, *fav, *inb, *ine, *outb, *oute;
+  int st;
+  __device__ __forceinline__ int at(int q, int kk) const { return kk * st + q; }
+  __device__ __forceinline__ REnt get(int i) const {
+    REnt e;
+    e.t = t[i];
+    e.need = need[i];
+    e.k = k[i];
+    e.j = j[i];
+    e.s = s[i];
+    e.fav = fav[i];
+    e.inb = inb[i];
+    e.ine = ine[i];
+    e.outb = outb[i];
+    e.oute = oute[i];
+    return e;
+  }
+  __device__ __forceinline__ void put(int i, const REnt &e) const {
+    t[i] = e.t;
+    need[i] = e.need;
+    k[i] = e.k;
+    j[i] = e.j;
+    s[i] = e.s;
+    fav[i] = e.fav;
+    inb[i] = e.inb;
+    ine[i] = e.ine;
+    outb[i] = e.outb;
+    oute[i] = e.oute;
+  }
+  __device__ __forceinline__ void mv(int d, int x) const {
+    t[d] = t[x];
+    need[d] = need[x];
+    k[d] = k[x];
+    j[d] = j[x];
+    s[d] = s[x];
+    fav[d] = fav[x];
+    inb[d] = inb[x];
+    ine[d] = ine[x];
+    outb[d] = outb[x];
+    oute[d] = oute[x];
+  }
+};
+
+// lane-owned list edits (lane q % 32 owns column q)
 template <int KR>
-__device__ __forceinline__ void rlist_remove(REnt *L, int32_t *cnt, int32_t *flg, int q, int j) {
+__device__ __forceinline__ void rlist_remove(const RList &L, int32_t *cnt, int32_t *flg, int q, int j) {
   int c = cnt[q];
   int at = -1;
   for (int k = 0; k < c; ++k)
-    if (L[q * KR + k].j == j) at = k;
+    if (L.j[L.at(q, k)] == j) at = k;
   if (at < 0) return;
-  for (int k = at; k + 1 < c; ++k) L[q * KR + k] = L[q * KR + k + 1];
+  for (int k = at; k + 1 < c; ++k) L.mv(L.at(q, k), L.at(q, k + 1));
   cnt[q] = --c;
   if (c == 0 && !(flg[q] & kComplete)) flg[q] |= kDirty;
 }
 
 // insert a fully built entry; returns nothing (list stays exact top-cnt)
 template <int KR>
-__device__ __forceinline__ void rlist_insert(REnt *L, int32_t *cnt, int32_t *flg, int q, const REnt &e) {
+__device__ __forceinline__ void rlist_insert(const RList &L, int32_t *cnt, int32_t *flg, int q, const REnt &e) {
   int c = cnt[q];
   int f = flg[q];
   if (f & kDirty) return;
   if (c == KR) {
     flg[q] = f & ~kComplete;
-    if (!lex_less(e.t, e.j, L[q * KR + KR - 1].t, L[q * KR + KR - 1].j)) return;
+    if (!lex_less(e.t, e.j, L.t[L.at(q, KR - 1)], L.j[L.at(q, KR - 1)])) return;
     --c;
   } else if (!(f & kComplete)) {
-    if (c == 0 || !lex_less(e.t, e.j, L[q * KR + c - 1].t, L[q * KR + c - 1].j)) return;
+    if (c == 0 || !lex_less(e.t, e.j, L.t[L.at(q, c - 1)], L.j[L.at(q, c - 1)])) return;
   }
   int k = c;
-  while (k > 0 && lex_less(e.t, e.j, L[q * KR + k - 1].t, L[q * KR + k - 1].j)) {
-    L[q * KR + k] = L[q * KR + k - 1];
+  while (k > 0 && lex_less(e.t, e.j, L.t[L.at(q, k - 1)], L.j[L.at(q, k - 1)])) {
+    L.mv(L.at(q, k), L.at(q, k - 1));
     --k;
   }
-  L[q * KR + k] = e;
+  L.put(L.at(q, k), e);
   cnt[q] = c + 1;
 }
 
@@ -1046,8 +1100,12 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
   c.res = c.tail + maxn;
   c.capS = c.res + maxn;
   c.awu = c.capS + maxn;
-  REnt *L = reinterpret_cast<REnt *>(c.awu + maxn);
-  RCommit *CM = reinterpret_cast<RCommit *>(L + maxn * KR);
+  RList L;
+  L.st = maxn;
+  L.t = c.awu + maxn;
+  L.need = L.t + maxn * KR;
+  L.k = L.need + maxn * KR;
+  RCommit *CM = reinterpret_cast<RCommit *>(L.k + maxn * KR);
   int64_t *stg_t = reinterpret_cast<int64_t *>(CM + maxn);
   const int ntask = maxn > RWARPS ? maxn : RWARPS;
   int64_t *stg_tt = stg_t + ntask * KR;  // per task: threshold of its exact prefix
@@ -1056,7 +1114,14 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
   int32_t *stg_live = stg_s + ntask * KR;
   int32_t *stg_cnt = stg_live + ntask;
   unsigned *stg_tj = reinterpret_cast<unsigned *>(stg_cnt + ntask);
-  c.awf = reinterpret_cast<int32_t *>(stg_tj + ntask);
+  L.j = reinterpret_cast<int32_t *>(stg_tj + ntask);
+  L.s = L.j + maxn * KR;
+  L.fav = L.s + maxn * KR;
+  L.inb = L.fav + maxn * KR;
+  L.ine = L.inb + maxn * KR;
+  L.outb = L.ine + maxn * KR;
+  L.oute = L.outb + maxn * KR;
+  c.awf = L.oute + maxn * KR;
   c.excl = c.awf + maxn;
   int32_t *cnt = c.excl + maxn;
   int32_t *flg = cnt + maxn;
@@ -1188,8 +1253,8 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
         S->compact = 0;
       }
       // list entries follow their nodes
-      for (int e = tid; e < n * KR; e += NT)
-        if (e % KR < cnt[e / KR]) L[e].s = c.rpos[L[e].j];
+      for (int e = tid; e < maxn * KR; e += NT)
+        if (e % maxn < n && e / maxn < cnt[e % maxn]) L.s[e] = c.rpos[L.j[e]];
       __syncthreads();
       RMARK(P_REMOVE);
     }
@@ -1239,17 +1304,19 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
           warp_argmin_u(bt, bj);
           if (bt == kInf || bt > thr_t || (bt == thr_t && bj > thr_j)) break;
           if (has && ht == bt && hj == bj) {
-            L[q * KR + r].t = bt;
-            L[q * KR + r].j = static_cast<int>(bj);
-            L[q * KR + r].s = stg_s[(tb + lane) * KR + ptr];
+            L.t[L.at(q, r)] = bt;
+            L.j[L.at(q, r)] = static_cast<int>(bj);
+            L.s[L.at(q, r)] = stg_s[(tb + lane) * KR + ptr];
             ++ptr;
           }
           ++kc;
         }
         __syncwarp();
-        if (lane < kc) rent_meta(L[q * KR + lane], c, g);  // listed nodes' metadata, in parallel
-        if (KR > 32)
-          for (int r = lane + 32; r < kc; r += 32) rent_meta(L[q * KR + r], c, g);
+        for (int r = lane; r < kc; r += 32) {  // listed nodes' metadata, in parallel
+          REnt e = L.get(L.at(q, r));
+          rent_meta(e, c, g);
+          L.put(L.at(q, r), e);
+        }
         if (lane == 0) {
           cnt[q] = kc;
           flg[q] = lv == kc ? kComplete : 0;
@@ -1310,9 +1377,9 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
             continue;
           }
           if (cnt[q] == 0) continue;
-          unsigned cell = static_cast<unsigned>(L[q * KR].j) * static_cast<unsigned>(n) + q;
-          if (L[q * KR].t < bt || (L[q * KR].t == bt && cell < bi)) {
-            bt = L[q * KR].t;
+          unsigned cell = static_cast<unsigned>(L.j[q]) * static_cast<unsigned>(n) + q;
+          if (L.t[q] < bt || (L.t[q] == bt && cell < bi)) {
+            bt = L.t[q];
             bi = cell;
           }
         }
@@ -1330,7 +1397,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
         }
         if (bt >= thr) break;
         const int q = static_cast<int>(bi % static_cast<unsigned>(n));
-        const REnt e = L[q * KR];
+        const REnt e = L.get(q);
         if (c.res[q] + e.need > c.capS[q]) {
           // discard (placers.cpp:203-219), inline: rare. With commits pending
           // in this round, end the round first: the pair stays the minimum
@@ -1442,7 +1509,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
       // (their keys are all >= F[q]); the others stay dirty, lists stale
       int64_t tb = kInf;
       for (int q = lane; q < n; q += 32)
-        if (!c.excl[q] && !(flg[q] & kDirty) && cnt[q] > 0) tb = min64(tb, L[q * KR].t);
+        if (!c.excl[q] && !(flg[q] & kDirty) && cnt[q] > 0) tb = min64(tb, L.t[q]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tb = min64(tb, __shfl_xor_sync(kFull, tb, o));
       // prefix sums of the committed nodes' degrees; dirty column list
@@ -1586,27 +1653,34 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
 
 static size_t rounds_smem(int maxn, int KR) {
   const int ntask = maxn > RWARPS ? maxn : RWARPS;
-  return ((sizeof(RShared) + 15) & ~size_t(15)) + 5 * 8 * size_t(maxn) + sizeof(REnt) * KR * maxn +
+  return ((sizeof(RShared) + 15) & ~size_t(15)) + 5 * 8 * size_t(maxn) + 52 * size_t(KR) * maxn +
          sizeof(RCommit) * maxn + size_t(ntask) * (KR * 16 + 8 + 12) +
          4 * (7 * size_t(maxn) + 2) + 4 * (RWARPS + 1) + 64;  // awf excl cnt flg dcols inoff outoff wsum
 }
 
-// list length per device column: long lists when they fit (fewer rescans: the
-// columns' heads are largely the same nodes, so short lists drain together)
+template <int KR>
+static void launch_rounds_kr(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs,
+                             const DPrep *preps, int maxn, cudaStream_t s) {
+  const size_t sm = rounds_smem(maxn, KR);
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(k_place_rounds<KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  k_place_rounds<KR><<<njobs, RWARPS * 32, sm, s>>>(jobs, order, njobs, graphs, preps, maxn);
+}
+
+// List length per device column. The columns' heads are largely the same
+// nodes, so with many devices short lists drain together and every column
+// needs a rescan every few commits; with few devices each commit rescans just
+// its own column and longer lists only cost more per rescan and per edit
+// (measured, profiles/r01c_kr_sweep.txt): 4 up to 8 devices, 8 up to 31, 16.
 void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                    int maxn, bool prof, cudaStream_t s) {
   (void)prof;
-  if (rounds_smem(maxn, 16) <= 200 * 1024) {
-    const size_t sm = rounds_smem(maxn, 16);
-    if (sm > 48 * 1024)
-      cudaFuncSetAttribute(k_place_rounds<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    k_place_rounds<16><<<njobs, RWARPS * 32, sm, s>>>(jobs, order, njobs, graphs, preps, maxn);
-  } else {
-    const size_t sm = rounds_smem(maxn, KT);
-    if (sm > 48 * 1024)
-      cudaFuncSetAttribute(k_place_rounds<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    k_place_rounds<KT><<<njobs, RWARPS * 32, sm, s>>>(jobs, order, njobs, graphs, preps, maxn);
-  }
+  int kr = maxn <= 8 ? 4 : maxn < 32 ? 8 : 16;
+  if (const char *e = std::getenv("BX_KR")) kr = std::atoi(e);  // tuning experiments
+  while (kr > 4 && rounds_smem(maxn, kr) > 200 * 1024) kr /= 2;
+  if (kr >= 16) launch_rounds_kr<16>(jobs, order, njobs, graphs, preps, maxn, s);
+  else if (kr >= 8) launch_rounds_kr<8>(jobs, order, njobs, graphs, preps, maxn, s);
+  else launch_rounds_kr<4>(jobs, order, njobs, graphs, preps, maxn, s);
 }
 
 

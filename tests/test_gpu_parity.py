@@ -173,6 +173,40 @@ def test_cuda_vs_oracle_seeded(bx, seed, g):
                         _assert_same(p, o, stats=algo != 0)
 
 
+@pytest.mark.parametrize("kr", ["4", "8", "16"])
+def test_cuda_vs_oracle_cta_kernels(bx, kr, monkeypatch):
+    """The CTA-wide kernels (round kernel for parallel comm, 8-warp list
+    kernel for sequential) forced onto small seeded problems, every list
+    length, against the C restatement."""
+    monkeypatch.setenv("BX_BIG_MIN", "0")
+    monkeypatch.setenv("BX_KR", kr)
+    for seed, g in _random_cases()[:8]:
+        m = W.as_meta_dict(g)
+        gg = _meta(bx, m)
+        fav = golden_cases.fav_first(m)
+        rng = np.random.default_rng(seed + 50)
+        for n in (1, 3, 7, 40):
+            for f in (1.0, 1.04, 1.6):
+                cap = W.bench_capacity(g, n, f)
+                caps = [int(cap * rng.uniform(0.8, 1.1)) for _ in range(n)]
+                for cm in ((5.0, 0.001, 0), (12.5, 0.002, 1), (0.0, 0.0, 1)):
+                    for algo in (1, 2):
+                        fv = fav if algo == 2 else None
+                        try:
+                            o = Restate.place(m, algo, caps, cm, fv)
+                            oe = None
+                        except OracleError as e:
+                            oe = (e.kind, e.msg)
+                        try:
+                            p = bx._one(gg, ALGO[algo], caps, bx.CommModel(*cm), fv)
+                            pe = None
+                        except bx.Error as e:
+                            pe = (e.kind, e.msg)
+                        assert oe == pe, (n, f, cm, algo)
+                        if oe is None:
+                            _assert_same(p, o)
+
+
 def test_round_extract_vs_oracle(bx):
     rng = np.random.default_rng(7)
     for trial in range(30):
