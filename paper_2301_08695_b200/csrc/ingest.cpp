@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <numeric>
 #include <queue>
 #include <stdexcept>
@@ -354,7 +355,7 @@ class Merger {
   const Meta &in_;
   std::vector<int> parent_, minm_, out_base_, in_base_, stamp_;
   int epoch_ = 0;
-  std::vector<std::unordered_map<int, Agg>> succ_, pred_;
+  std::vector<std::map<int, Agg>> succ_, pred_;
 };
 
 // meta_topo_order's acyclicity check + CycleError text (transforms.cpp:446-479)
