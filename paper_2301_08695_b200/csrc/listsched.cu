@@ -148,8 +148,29 @@ __device__ __forceinline__ void topk_insert(int64_t (&lt)[KT], int (&lj)[KT], in
 // This warp's exact top-KT of column q over slots s0 + lane + k*step < R;
 // KT rounds of warp argmin leave the result in lane 0 (dt/dj/ds, cnt) and the
 // live-pair count in every lane.
-__device__ void warp_topk(const Ctx &c, int q, int s0, int step, int R, int lane, int64_t (&dt)[KT],
-                          int (&dj)[KT], int (&ds)[KT], int &cnt, int &live) {
+// one device column's scan inputs, by value (the exact fallbacks are not
+// inlined, so they must not take the whole context by reference)
+struct ColView {
+  const int64_t *kcol;
+  const int32_t *node_s;
+  const int64_t *urg_s;
+  int64_t Fq, awu;
+  int aw;
+};
+
+__device__ __forceinline__ ColView col_view(const Ctx &c, int q) {
+  ColView v;
+  v.kcol = c.Kc + static_cast<int64_t>(q) * c.V;
+  v.node_s = c.node_s;
+  v.urg_s = c.urg_s;
+  v.Fq = c.F[q];
+  v.aw = c.sct ? c.awf[q] : -1;
+  v.awu = v.aw >= 0 ? c.awu[q] : 0;
+  return v;
+}
+
+__device__ __noinline__ void warp_topk_exact(const ColView cv, int s0, int step, int R, int lane, int64_t (&dt)[KT],
+                                             int (&dj)[KT], int (&ds)[KT], int &cnt, int &live) {
   int64_t lt[KT];
   int lj[KT], ls[KT];
 #pragma unroll
@@ -159,10 +180,10 @@ __device__ void warp_topk(const Ctx &c, int q, int s0, int step, int R, int lane
     ls[k] = -1;
   }
   live = 0;
-  const int64_t *kcol = c.Kc + static_cast<int64_t>(q) * c.V;
-  const int64_t Fq = c.F[q];
-  const int aw = c.sct ? c.awf[q] : -1;
-  const int64_t awu = aw >= 0 ? c.awu[q] : 0;
+  const int64_t *kcol = cv.kcol;
+  const int64_t Fq = cv.Fq;
+  const int aw = cv.aw;
+  const int64_t awu = cv.awu;
   constexpr int U = 4;
   for (int base = s0 + lane; base < R; base += U * step) {
     int64_t kv[U];
@@ -172,8 +193,8 @@ __device__ void warp_topk(const Ctx &c, int q, int s0, int step, int R, int lane
     for (int u = 0; u < U; ++u) {
       int s = base + u * step;
       kv[u] = s < R ? kcol[s] : kInf;
-      nd[u] = s < R ? c.node_s[s] : 0;
-      ug[u] = (aw >= 0 && s < R) ? c.urg_s[s] : 0;
+      nd[u] = s < R ? cv.node_s[s] : 0;
+      ug[u] = (aw >= 0 && s < R) ? cv.urg_s[s] : 0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -210,6 +231,126 @@ __device__ void warp_topk(const Ctx &c, int q, int s0, int step, int R, int lane
       lj[KT - 1] = INT32_MAX;
       ls[KT - 1] = -1;
     }
+  }
+}
+
+
+// ---- composite-key column scans ----------------------------------------------
+// Every key in column q is >= F[q], so (key - F[q]) << 32 | node orders the
+// column's pairs (key, node) with ONE 64-bit compare. A key more than 2^32-2
+// above F[q] saturates; `clip` reports it and the caller rescans exactly.
+constexpr unsigned long long kNoKey = ~0ull;
+
+struct Lane4 {
+  unsigned long long k[4];
+  int s[4];
+  int seen;
+  bool clip;
+};
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+  const unsigned hi = static_cast<unsigned>(v >> 32), lo = static_cast<unsigned>(v);
+  const unsigned mhi = __reduce_min_sync(kFull, hi);
+  const unsigned mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xffffffffu);
+  return (static_cast<unsigned long long>(mhi) << 32) | mlo;
+}
+
+// per-lane exact top-4 of this warp's share (slots s0 + lane + k*step < R)
+__device__ __forceinline__ void lane_top4(const Ctx &c, int q, int s0, int step, int R, int lane, Lane4 &L) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    L.k[k] = kNoKey;
+    L.s[k] = -1;
+  }
+  L.seen = 0;
+  L.clip = false;
+  const int64_t *kcol = c.Kc + static_cast<int64_t>(q) * c.V;
+  const int64_t Fq = c.F[q];
+  const int aw = c.sct ? c.awf[q] : -1;
+  const int64_t awu = aw >= 0 ? c.awu[q] : 0;
+  constexpr int U = 4;
+  for (int base = s0 + lane; base < R; base += U * step) {
+    int64_t kv[U];
+    int nd[U];
+    int64_t ug[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int s = base + u * step;
+      kv[u] = s < R ? kcol[s] : kInf;
+      nd[u] = s < R ? c.node_s[s] : 0;
+      ug[u] = (aw >= 0 && s < R) ? c.urg_s[s] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (kv[u] == kInf) continue;
+      ++L.seen;
+      int64_t t = max64(kv[u], Fq);
+      if (aw >= 0 && aw != nd[u]) t = max64(t, min64(awu, ug[u]));
+      unsigned long long d = static_cast<unsigned long long>(t - Fq);
+      if (d > 0xfffffffeull) {
+        L.clip = true;
+        d = 0xfffffffeull;
+      }
+      const unsigned long long ck = (d << 32) | static_cast<unsigned>(nd[u]);
+      if (ck < L.k[3]) {
+        L.k[3] = ck;
+        L.s[3] = base + u * step;
+#pragma unroll
+        for (int k = 3; k > 0; --k) {
+          if (L.k[k] < L.k[k - 1]) {
+            const unsigned long long a = L.k[k];
+            L.k[k] = L.k[k - 1];
+            L.k[k - 1] = a;
+            const int b = L.s[k];
+            L.s[k] = L.s[k - 1];
+            L.s[k - 1] = b;
+          }
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void lane4_pop(Lane4 &L) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    L.k[k] = L.k[k + 1];
+    L.s[k] = L.s[k + 1];
+  }
+  L.k[3] = kNoKey;
+  L.s[3] = -1;
+}
+
+// warp_topk_exact's contract through composite keys
+__device__ void warp_topk(const Ctx &c, int q, int s0, int step, int R, int lane, int64_t (&dt)[KT],
+                          int (&dj)[KT], int (&ds)[KT], int &cnt, int &live) {
+  static_assert(KT == 4, "lane lists hold 4");
+  Lane4 L;
+  lane_top4(c, q, s0, step, R, lane, L);
+  if (__any_sync(kFull, L.clip)) {
+    warp_topk_exact(col_view(c, q), s0, step, R, lane, dt, dj, ds, cnt, live);
+    return;
+  }
+  live = L.seen;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(kFull, live, o);
+  const int64_t Fq = c.F[q];
+  cnt = 0;
+#pragma unroll
+  for (int r = 0; r < KT; ++r) {
+    const unsigned long long h = warp_min_u64(L.k[0]);
+    if (h == kNoKey) {
+      dt[r] = kInf;
+      dj[r] = INT32_MAX;
+      ds[r] = -1;
+      break;
+    }
+    const bool own = L.k[0] == h;
+    dt[r] = Fq + static_cast<int64_t>(h >> 32);
+    dj[r] = static_cast<int>(h & 0xffffffffull);
+    ds[r] = __shfl_sync(kFull, L.s[0], __ffs(__ballot_sync(kFull, own)) - 1);
+    ++cnt;
+    if (own) lane4_pop(L);
   }
 }
 
@@ -951,8 +1092,9 @@ __device__ __forceinline__ void rlist_insert(const RList &L, int32_t *cnt, int32
 // (pairs are unique per column: everything a lane dropped is above it).
 // Pops lane heads while <= thr, at most KR, into out_* (lane 0 writes).
 template <int KR>
-__device__ void warp_prefix(const Ctx &c, int q, int s0, int step, int R, int lane, int64_t *out_t, int32_t *out_j,
-                            int32_t *out_s, int &cnt, int64_t &thr_t, unsigned &thr_j, int &live) {
+__device__ __noinline__ void warp_prefix_exact(const ColView cv, int s0, int step, int R, int lane, int64_t *out_t,
+                                               int32_t *out_j, int32_t *out_s, int &cnt, int64_t &thr_t,
+                                               unsigned &thr_j, int &live) {
   constexpr int LK = 4;
   int64_t lt[LK];
   int lj[LK], ls[LK];
@@ -963,10 +1105,10 @@ __device__ void warp_prefix(const Ctx &c, int q, int s0, int step, int R, int la
     ls[k] = -1;
   }
   int seen = 0;
-  const int64_t *kcol = c.Kc + static_cast<int64_t>(q) * c.V;
-  const int64_t Fq = c.F[q];
-  const int aw = c.sct ? c.awf[q] : -1;
-  const int64_t awu = aw >= 0 ? c.awu[q] : 0;
+  const int64_t *kcol = cv.kcol;
+  const int64_t Fq = cv.Fq;
+  const int aw = cv.aw;
+  const int64_t awu = cv.awu;
   constexpr int U = 4;
   for (int base = s0 + lane; base < R; base += U * step) {
     int64_t kv[U];
@@ -976,8 +1118,8 @@ __device__ void warp_prefix(const Ctx &c, int q, int s0, int step, int R, int la
     for (int u = 0; u < U; ++u) {
       int s = base + u * step;
       kv[u] = s < R ? kcol[s] : kInf;
-      nd[u] = s < R ? c.node_s[s] : 0;
-      ug[u] = (aw >= 0 && s < R) ? c.urg_s[s] : 0;
+      nd[u] = s < R ? cv.node_s[s] : 0;
+      ug[u] = (aw >= 0 && s < R) ? cv.urg_s[s] : 0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -1035,6 +1177,46 @@ struct RShared {
   int32_t err_status, err_code, err_node, pad;
   int64_t discarded, excluded, awake;
 };
+
+
+// warp_prefix_exact's contract through composite keys
+template <int KR>
+__device__ void warp_prefix(const Ctx &c, int q, int s0, int step, int R, int lane, int64_t *out_t, int32_t *out_j,
+                            int32_t *out_s, int &cnt, int64_t &thr_t, unsigned &thr_j, int &live) {
+  Lane4 L;
+  lane_top4(c, q, s0, step, R, lane, L);
+  if (__any_sync(kFull, L.clip)) {
+    warp_prefix_exact<KR>(col_view(c, q), s0, step, R, lane, out_t, out_j, out_s, cnt, thr_t, thr_j, live);
+    return;
+  }
+  unsigned long long thr = warp_min_u64(L.seen > 4 ? L.k[3] : kNoKey);
+  live = L.seen;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(kFull, live, o);
+  const int64_t Fq = c.F[q];
+  cnt = 0;
+  unsigned long long last = kNoKey;
+  for (int r = 0; r < KR; ++r) {
+    const unsigned long long h = warp_min_u64(L.k[0]);
+    if (h == kNoKey || h > thr) break;
+    if (L.k[0] == h) {
+      out_t[r] = Fq + static_cast<int64_t>(h >> 32);
+      out_j[r] = static_cast<int>(h & 0xffffffffull);
+      out_s[r] = L.s[0];
+      lane4_pop(L);
+    }
+    last = h;
+    ++cnt;
+  }
+  if (cnt == KR) thr = last;  // truncated: exact only up to its last pair
+  if (thr == kNoKey) {
+    thr_t = kInf;
+    thr_j = 0xffffffffu;
+  } else {
+    thr_t = Fq + static_cast<int64_t>(thr >> 32);
+    thr_j = static_cast<unsigned>(thr & 0xffffffffull);
+  }
+}
 
 template <int KR>
 __global__ void __launch_bounds__(RWARPS * 32, 1)

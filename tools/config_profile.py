@@ -33,7 +33,8 @@ def cases():
                         ("layered100k_x4", lambda: W.layered_dag_fast(100, 1000, 3), 4),
                         ("wide100k_x16", lambda: W.wide_random(100000, 5), 16),
                         ("layered100k_x64", lambda: W.layered_dag_fast(100, 1000, 3), 64),
-                        ("layered100k_x16", lambda: W.layered_dag_fast(100, 1000, 3), 16)):
+                        ("layered100k_x16", lambda: W.layered_dag_fast(100, 1000, 3), 16),
+                        ("layered30k_x64", lambda: W.layered_dag_fast(30, 1000, 3), 64)):
         g = mk()
         gg = bx.MetaGraph.from_dict(W.as_meta_dict(g))
         yield name, gg, bx.Job(0, "m-etf", np.full(n, W.bench_capacity(g, n, 1.2), np.int64), cm)
