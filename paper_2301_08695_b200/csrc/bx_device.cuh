@@ -137,6 +137,13 @@ struct DSim {
   int64_t *bucket;                  // [V] output bytes freed before each exec slot's start
   int64_t *mb;                      // [V*n] max bytes per (producer, consumer device)
   uint8_t *first;                   // [E] edge opens its (producer, device) transfer
+  unsigned long long *flow8;        // [8] zero-k, bad exec, bad once, transfers, bytes, remote edges
+  int32_t *rcnt;                    // [V] remote parents per node (bit 30: never ready)
+  int32_t *rp_off;                  // [V+1] remote-parent lists by FIFO slot
+  int32_t *rp_src;                  // [E] remote parent
+  int64_t *rp_c;                    // [E] its arrival delay
+  int64_t *kx;                      // [V] compute time by FIFO slot (-1: never ready)
+  int64_t *dv;                      // [4n] per device: peak, violation t, node, memory
   // outputs
   int64_t *start;                   // [V]
   int64_t *dev3n;                   // [3n] peak, busy, idle

@@ -22,10 +22,11 @@ void launch_prep(const DGraph &g, const DPrep &pr, bool first, cudaStream_t s);
 void launch_kahn(DGraph *graphs_dev, int32_t *const *queues_dev, int ngraphs, cudaStream_t s);
 cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bit, cudaStream_t s);
 void launch_extract(const XCtx &c, cudaStream_t s);
-void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_bpar, int n_bseq, int njobs,
+void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_etf, int n_bpar, int n_bseq,
+                    int njobs,
                     const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo, bool prof,
                     cudaStream_t s_small, cudaStream_t s_big);
-void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, cudaStream_t s);
+void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn, cudaStream_t s);
 }  // namespace bx
 
 using namespace bx;
@@ -105,7 +106,7 @@ struct bx_plan {
   DPrep *dp_dev = nullptr;
   DJob *dj_dev = nullptr;
   int32_t *order_dev = nullptr;     // launch lists: small | big parallel | big sequential
-  int n_small = 0, n_bpar = 0, n_bseq = 0;
+  int n_small = 0, n_etf = 0, n_bpar = 0, n_bseq = 0;  // n_etf: leading parallel m-ETF small jobs
   cudaStream_t s2 = nullptr;        // big problems run beside the small ones
   cudaEvent_t fork = nullptr, join = nullptr;
   int32_t **queues_dev = nullptr;
@@ -568,13 +569,16 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   {
     // three launch lists, each longest-first: small (one warp per job),
     // big parallel-mode (round kernel), big sequential-mode (8-warp kernel)
-    std::vector<int32_t> small, bpar, bseq;
+    std::vector<int32_t> small, sgen, bpar, bseq;
     for (int i : list_ids) {
       if (P->dj[i].skip) continue;
-      if (!big[i]) small.push_back(i);
+      const bool etf = jobs[i].cm.mode == BX_COMM_PARALLEL && P->dj[i].fav == nullptr;
+      if (!big[i]) (etf ? small : sgen).push_back(i);
       else if (jobs[i].cm.mode == BX_COMM_PARALLEL) bpar.push_back(i);
       else bseq.push_back(i);
     }
+    P->n_etf = static_cast<int>(small.size());
+    small.insert(small.end(), sgen.begin(), sgen.end());
     std::vector<int32_t> all(small);
     all.insert(all.end(), bpar.begin(), bpar.end());
     all.insert(all.end(), bseq.begin(), bseq.end());
@@ -653,20 +657,21 @@ int bx_plan_place(bx_plan *P, void *stream) {
   launch_kahn(P->dg_dev, P->queues_dev, P->ngraphs, s);
   P->launches += 1;
   cudaEventRecord(P->ev[0], s);
-  const bool fork = P->n_small > 0 && (P->n_bpar + P->n_bseq) > 0;
+  const bool fork = (P->n_small > 0 && (P->n_bpar + P->n_bseq) > 0) || (P->n_etf > 0 && P->n_small > P->n_etf);
   cudaStream_t sb = fork ? P->s2 : s;
   if (fork) {
     cudaEventRecord(P->fork, s);
     cudaStreamWaitEvent(P->s2, P->fork, 0);
   }
-  launch_placers(P->dj_dev, P->order_dev, P->n_small, P->n_bpar, P->n_bseq, P->njobs, P->dg_dev, P->dp_dev,
+  launch_placers(P->dj_dev, P->order_dev, P->n_small, P->n_etf, P->n_bpar, P->n_bseq, P->njobs, P->dg_dev,
+                 P->dp_dev,
                  P->maxn, P->any_topo, P->prof != nullptr, s, sb);
   if (fork) {
     cudaEventRecord(P->join, P->s2);
     cudaStreamWaitEvent(s, P->join, 0);
   }
   cudaEventRecord(P->ev[1], s);
-  P->launches += (P->any_topo ? 1 : 0) + (P->n_small > 0) + (P->n_bpar > 0) + (P->n_bseq > 0);
+  P->launches += (P->any_topo ? 1 : 0) + (P->n_etf > 0) + (P->n_small > P->n_etf) + (P->n_bpar > 0) + (P->n_bseq > 0);
   return launch_status();
 }
 
@@ -805,7 +810,7 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
   Layout L;
   struct SOff {
     size_t mem, peak, xfree, qpos, busy, cl, fin, sq, res, sent, ht, hk, seen, db, dc, start, dev3n, xfer4, mk, err;
-    size_t pos, psrc, cx, ffin, sx, bucket, mb, first;
+    size_t pos, psrc, cx, ffin, sx, bucket, mb, first, flow8, rcnt, rp_off, rp_src, rp_c, kx, dv;
   };
   std::vector<SOff> so(P->njobs);
   for (int i = 0; i < P->njobs; ++i) {
@@ -840,6 +845,13 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
     o.bucket = L.take<int64_t>(V);
     o.mb = L.take<int64_t>(V * n);
     o.first = L.take<uint8_t>(E);
+    o.flow8 = L.take<unsigned long long>(8);
+    o.rcnt = L.take<int32_t>(V);
+    o.rp_off = L.take<int32_t>(V + 1);
+    o.rp_src = L.take<int32_t>(E);
+    o.rp_c = L.take<int64_t>(E);
+    o.kx = L.take<int64_t>(V);
+    o.dv = L.take<int64_t>(4 * n);
   }
   size_t tab = L.take<DSim>(P->njobs);
   BX_CUDA(cudaMalloc(&P->sim_pool, L.off), msg, msglen);
@@ -890,6 +902,14 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
     d.bucket = at<int64_t>(pool, o.bucket);
     d.mb = at<int64_t>(pool, o.mb);
     d.first = at<uint8_t>(pool, o.first);
+    d.flow8 = at<unsigned long long>(pool, o.flow8);
+    d.rcnt = at<int32_t>(pool, o.rcnt);
+    d.rp_off = at<int32_t>(pool, o.rp_off);
+    d.rp_src = at<int32_t>(pool, o.rp_src);
+    d.rp_c = at<int64_t>(pool, o.rp_c);
+    d.kx = at<int64_t>(pool, o.kx);
+    d.dv = at<int64_t>(pool, o.dv);
+    P->sim_fills.push_back({d.flow8, 0, 64});
     P->sim_fills.push_back({d.resident, 0, size_t(V * n)});
     P->sim_fills.push_back({d.sent, 0, size_t(V * n)});
     P->sim_fills.push_back({d.err, 0, sizeof(DErr)});
@@ -913,7 +933,7 @@ int bx_plan_simulate(bx_plan *P, int32_t mem_mode, void *stream) {
   }
   for (const Fill &f : P->sim_fills)
     if (cudaMemsetAsync(f.ptr, f.value, f.bytes, s) != cudaSuccess) return BX_RUNTIME;
-  launch_simulate(P->ds_dev, P->njobs, P->dg_dev, s);
+  launch_simulate(P->ds_dev, P->njobs, P->dg_dev, std::max(P->maxn, 1), s);
   return launch_status();
 }
 

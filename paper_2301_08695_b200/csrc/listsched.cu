@@ -414,7 +414,10 @@ __device__ __forceinline__ void group_sync() {
   else __syncwarp();
 }
 
-template <int kW, bool kProf>
+// kEtf: compiled for parallel-comm m-ETF only (no sequential queues, no awake
+// reservations): a third of the code, which matters when ~28 warps per SM
+// run it at unrelated program counters (instruction-fetch stalls).
+template <int kW, bool kProf, bool kEtf = false>
 __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     k_place_list(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                  int maxn, int seq_only) {
@@ -447,8 +450,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
   Ctx c;
   c.V = g.V;
   c.n = jb.n;
-  c.mode = jb.mode;
-  c.sct = (jb.algo == 2 && jb.fav != nullptr);
+  c.mode = kEtf ? 1 : jb.mode;
+  c.sct = kEtf ? false : (jb.algo == 2 && jb.fav != nullptr);
   c.k = g.k;
   c.need = g.need;
   c.in_c = pr.in_c;
@@ -949,17 +952,19 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
   }
 }
 
-template <int kW, bool kProf>
+template <int kW, bool kProf, bool kEtf = false>
 static void launch_w(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                      int maxn, int seq_only, cudaStream_t s) {
+  if (njobs <= 0) return;
   const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 16;
   const int probs_per_cta = kW > 1 ? 1 : 4;
   const int threads = kW > 1 ? 32 * kW : 128;
   const int blocks = (njobs + probs_per_cta - 1) / probs_per_cta;
   const size_t sm = per * probs_per_cta;
   if (sm > 48 * 1024)
-    cudaFuncSetAttribute(k_place_list<kW, kProf>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-  k_place_list<kW, kProf><<<blocks, threads, sm, s>>>(jobs, order, njobs, graphs, preps, maxn, seq_only);
+    cudaFuncSetAttribute(k_place_list<kW, kProf, kEtf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sm));
+  k_place_list<kW, kProf, kEtf><<<blocks, threads, sm, s>>>(jobs, order, njobs, graphs, preps, maxn, seq_only);
 }
 
 // ============================================================================
@@ -1866,12 +1871,18 @@ void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGra
 }
 
 
-// Launch lists come from bx_plan_create: small problems one warp each,
+// Launch lists come from bx_plan_create: small problems one warp each (the
+// first n_etf of them parallel-comm m-ETF, on the specialised kernel),
 // big sequential-mode problems an 8-warp CTA each.
-void launch_small(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                  int maxn, bool prof, cudaStream_t s) {
-  if (prof) launch_w<1, true>(jobs, order, njobs, graphs, preps, maxn, 0, s);
-  else launch_w<1, false>(jobs, order, njobs, graphs, preps, maxn, 0, s);
+void launch_small(const DJob *jobs, const int32_t *order, int n_etf, int n_gen, const DGraph *graphs,
+                  const DPrep *preps, int maxn, bool prof, cudaStream_t s, cudaStream_t s_gen) {
+  if (prof) {
+    launch_w<1, true, true>(jobs, order, n_etf, graphs, preps, maxn, 0, s);
+    launch_w<1, true>(jobs, order + n_etf, n_gen, graphs, preps, maxn, 0, s_gen);
+  } else {
+    launch_w<1, false, true>(jobs, order, n_etf, graphs, preps, maxn, 0, s);
+    launch_w<1, false>(jobs, order + n_etf, n_gen, graphs, preps, maxn, 0, s_gen);
+  }
 }
 
 void launch_big_seq(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,

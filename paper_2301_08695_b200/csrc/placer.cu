@@ -264,8 +264,8 @@ __global__ void __launch_bounds__(32 * kWarps) k_place_topo(const DJob *jobs, in
 }
 
 // ------------------------------------------------------------ launch ----
-void launch_small(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                  int maxn, bool prof, cudaStream_t s);
+void launch_small(const DJob *jobs, const int32_t *order, int n_etf, int n_gen, const DGraph *graphs,
+                  const DPrep *preps, int maxn, bool prof, cudaStream_t s, cudaStream_t s_gen);
 void launch_big_seq(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                     int maxn, bool prof, cudaStream_t s);
 void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
@@ -291,14 +291,14 @@ cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bi
                                          s);
 }
 
-void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_bpar, int n_bseq, int njobs,
-                    const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo, bool prof,
+void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_etf, int n_bpar, int n_bseq,
+                    int njobs, const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo, bool prof,
                     cudaStream_t s_small, cudaStream_t s_big) {
   // big problems (CTA-wide kernels) on s_big, beside the small ones (one
   // warp per job, four per CTA) on s_small; every list is longest-first
   if (n_bpar) launch_rounds(jobs, order + n_small, n_bpar, graphs, preps, maxn, prof, s_big);
   if (n_bseq) launch_big_seq(jobs, order + n_small + n_bpar, n_bseq, graphs, preps, maxn, prof, s_big);
-  if (n_small) launch_small(jobs, order, n_small, graphs, preps, maxn, prof, s_small);
+  if (n_small) launch_small(jobs, order, n_etf, n_small - n_etf, graphs, preps, maxn, prof, s_small, s_big);
   if (any_topo) {
     constexpr int W = 4;
     k_place_topo<W><<<(njobs + W - 1) / W, 32 * W, static_cast<size_t>(W) * maxn * 56, s_small>>>(

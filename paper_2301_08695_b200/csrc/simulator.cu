@@ -128,12 +128,9 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
   c.V = c.g.V;
   c.n = c.s.n;
   c.lane = lane;
-  if (c.s.mode == 1) {
-    // parallel comm mode without zero-duration nodes belongs to K4f
-    bool zero = false;
-    for (int j = lane; j < c.V; j += 32) zero |= c.g.k[j] == 0;
-    if (!__any_sync(kFullS, zero)) return;
-  }
+  // parallel comm mode without zero-duration nodes belongs to K4f (its first
+  // prep pass flags zero durations)
+  if (c.s.mode == 1 && !c.s.flow8[0]) return;
   c.h.t = c.s.heap_t;
   c.h.k = c.s.heap_k;
   c.h.size = 0;
@@ -377,103 +374,211 @@ __device__ __forceinline__ void st_cta(int64_t *p, int64_t v) {
   asm volatile("st.relaxed.cta.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// K4f prep: grid-wide passes over every problem's nodes and edges
+// (blockIdx.y = problem), so a lone large problem uses the whole GPU for them.
+// Validation flags and transfer counters go to flow8; out-of-range
+// placements are only flagged here (the walker kernel reports them first).
+#define BX_SIM_STRIDE(i, N) for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (N); i += gridDim.x * blockDim.x)
+constexpr int32_t kNever = 1 << 30;  // rcnt flag: a same-device parent comes later in the FIFO
+
+__device__ __forceinline__ bool flow_skip(const DSim &s) {
+  return s.mode != 1 || s.flow8[0] || s.flow8[1] || s.flow8[2];
+}
+
+__global__ void k_sim_prep_a(const DSim *sims, const DGraph *graphs, int base) {
+  const DSim s = sims[base + blockIdx.y];
+  if (s.mode != 1) return;
+  const DGraph g = graphs[s.graph];
+  const int n = s.n;
+  int zero = 0;
+  BX_SIM_STRIDE(j, g.V) {
+    s.seen[j] = 0;
+    s.fin[j] = -1;
+    s.bucket[j] = 0;
+    s.rcnt[j] = 0;
+    zero |= g.k[j] == 0;
+  }
+  if (__syncthreads_or(zero) && threadIdx.x == 0) atomicOr(&s.flow8[0], 1ull);
+  BX_SIM_STRIDE(e, g.E) {
+    const int i = g.esrc[e], dc = s.device_of[g.edst[e]], di = s.device_of[i];
+    if (di != dc && dc >= 0 && dc < n && di >= 0 && di < n) s.mb[static_cast<int64_t>(i) * n + dc] = -1;
+  }
+}
+
+__global__ void k_sim_prep_b(const DSim *sims, const DGraph *graphs, int base) {
+  const DSim s = sims[base + blockIdx.y];
+  if (s.mode != 1) return;
+  const DGraph g = graphs[s.graph];
+  const int V = g.V, n = s.n;
+  // exec lists (simulator.cpp:84-90): range and device agreement, counts
+  int bad = 0;
+  const int total = s.exec_off[n];
+  BX_SIM_STRIDE(x, total) {
+    int lo = 0, hi = n;  // device d with exec_off[d] <= x < exec_off[d+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s.exec_off[mid] <= x) lo = mid;
+      else hi = mid;
+    }
+    const int m = s.exec_order[x];
+    if (m < 0 || m >= V || s.device_of[m] != lo) {
+      bad = 1;
+    } else {
+      atomicAdd(&s.seen[m], 1);
+      s.pos[m] = x - s.exec_off[lo];
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&s.flow8[1], 1ull);
+  // one transfer per (producer, remote consumer device), max bytes
+  unsigned long long cnt = 0, rem = 0;
+  BX_SIM_STRIDE(e, g.E) {
+    const int i = g.esrc[e], dc = s.device_of[g.edst[e]], di = s.device_of[i];
+    uint8_t f = 0;
+    if (di != dc && dc >= 0 && dc < n && di >= 0 && di < n) {
+      ++rem;
+      auto *slot = reinterpret_cast<unsigned long long *>(s.mb + static_cast<int64_t>(i) * n + dc);
+      f = atomicCAS(slot, ~0ull, ~0ull - 1) == ~0ull;
+      cnt += f;
+      atomicMax(reinterpret_cast<long long *>(slot), static_cast<long long>(g.ebytes[e]));
+    }
+    s.first[e] = f;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(kFullS, cnt, o);
+    rem += __shfl_xor_sync(kFullS, rem, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (cnt | rem)) {
+    atomicAdd(&s.flow8[3], cnt);
+    atomicAdd(&s.flow8[5], rem);
+  }
+}
+
+__global__ void k_sim_prep_c(const DSim *sims, const DGraph *graphs, int base) {
+  const DSim s = sims[base + blockIdx.y];
+  if (s.mode != 1) return;
+  const DGraph g = graphs[s.graph];
+  const int V = g.V, n = s.n;
+  int bad = 0;
+  BX_SIM_STRIDE(j, V) {
+    const int d = s.device_of[j];
+    if (d < 0 || d >= n || s.seen[j] != 1) bad = 1;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&s.flow8[2], 1ull);
+  unsigned long long by = 0;
+  BX_SIM_STRIDE(e, g.E)
+  if (s.first[e]) by += s.mb[static_cast<int64_t>(g.esrc[e]) * n + s.device_of[g.edst[e]]];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) by += __shfl_xor_sync(kFullS, by, o);
+  if ((threadIdx.x & 31) == 0 && by) atomicAdd(&s.flow8[4], by);
+  // per in-CSR slot: the arrival delay on the consumer's device; remote
+  // parents counted per consumer, a later same-device parent marks it never
+  BX_SIM_STRIDE(x, g.E) {
+    const int e = g.in_edge[x];
+    const int i = g.esrc[e], c = g.edst[e];
+    const int di = s.device_of[i], dc = s.device_of[c];
+    if (di < 0 || di >= n || dc < 0 || dc >= n) continue;  // flagged; never walked
+    if (di == dc) {
+      s.cx[x] = -1;
+      if (s.pos[i] >= s.pos[c]) atomicOr(&s.rcnt[c], kNever);
+    } else {
+      s.cx[x] = comm_time_exact(s.ic, s.pb, s.mb[static_cast<int64_t>(i) * n + dc]);
+      atomicAdd(&s.rcnt[c], 1);
+    }
+  }
+}
+
+// remote-parent list offsets in FIFO-slot order (one CTA per problem: a
+// block scan over the slots), compute times by slot
+__global__ void __launch_bounds__(1024) k_sim_prep_d(const DSim *sims, const DGraph *graphs) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  const DSim s = sims[blockIdx.x];
+  if (flow_skip(s)) return;
+  const DGraph g = graphs[s.graph];
+  const int V = g.V;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int b = 0; b < V; b += blockDim.x) {
+    const int xs = b + tid;
+    int v = 0;
+    if (xs < V) {
+      const int j = s.exec_order[xs];
+      const int rc = s.rcnt[j];
+      v = rc & (kNever - 1);
+      s.kx[xs] = (rc & kNever) ? -1 : g.k[j];
+      s.rcnt[j] = v;  // becomes the fill cursor
+    }
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(kFullS, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < NW ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(kFullS, w, o);
+        if (lane >= o) w += u;
+      }
+      if (lane < NW) wsum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int before = carry + (warp ? wsum[warp - 1] : 0) + incl - v;
+    if (xs < V) s.rp_off[xs] = before;
+    __syncthreads();
+    if (tid == 0) carry += wsum[NW - 1];
+    __syncthreads();
+  }
+  if (tid == 0) s.rp_off[V] = carry;
+}
+
+__global__ void k_sim_prep_e(const DSim *sims, const DGraph *graphs, int base) {
+  const DSim s = sims[base + blockIdx.y];
+  if (flow_skip(s)) return;
+  const DGraph g = graphs[s.graph];
+  BX_SIM_STRIDE(x, g.E) {
+    const int64_t cc = s.cx[x];
+    if (cc < 0) continue;
+    const int e = g.in_edge[x];
+    const int i = g.esrc[e], c = g.edst[e];
+    const int xs = s.exec_off[s.device_of[c]] + s.pos[c];
+    const int slot = s.rp_off[xs] + atomicSub(&s.rcnt[c], 1) - 1;
+    s.rp_src[slot] = i;
+    s.rp_c[slot] = cc;
+  }
+}
+
+constexpr int kWalkSpin = 64;
+
+// K4f walkers: validation verdicts, permanent memory, then the FIFO walk.
 __global__ void __launch_bounds__(1024) k_sim_flow(const DSim *sims, int nsims, const DGraph *graphs) {
-  __shared__ unsigned long long sh_x[3];  // transfers, bytes, remote edges
   __shared__ long long sh_mk;
   __shared__ int sh_bad;
   const DSim s = sims[blockIdx.x];
   if (s.mode != 1) return;
   const DGraph g = graphs[s.graph];
-  const int V = g.V, E = g.E, n = s.n;
-  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  const int n = s.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
   DErr *err = s.err;
-  int zero = 0;
-  for (int j = tid; j < V; j += NT) zero |= g.k[j] == 0;
-  if (__syncthreads_or(zero)) return;  // event-loop kernel
-
-  // ---- validate_placement (simulator.cpp:78-97) ------------------------------
-  for (int j = tid; j < V; j += NT) s.seen[j] = 0;
+  if (s.flow8[0]) return;  // zero-duration nodes: event-loop kernel
+  // validate_placement (simulator.cpp:78-97), decided by its first failing check
+  if (s.flow8[1] || s.flow8[2]) {
+    if (tid == 0) {
+      err->status = kValidation;
+      err->code = s.flow8[1] ? E_SIM_EXEC : E_SIM_ONCE;
+    }
+    return;
+  }
   if (tid == 0) {
-    sh_x[0] = sh_x[1] = sh_x[2] = 0;
     sh_mk = 0;
     sh_bad = INT32_MAX;
   }
   __syncthreads();
-  int bad = 0;
-  for (int d = 0; d < n; ++d) {
-    const int o = s.exec_off[d], e = s.exec_off[d + 1];
-    for (int x = o + tid; x < e; x += NT) {
-      const int m = s.exec_order[x];
-      if (m < 0 || m >= V || s.device_of[m] != d) {
-        bad = 1;
-      } else {
-        atomicAdd(&s.seen[m], 1);
-        s.pos[m] = x - o;
-      }
-    }
-  }
-  if (__syncthreads_or(bad)) {
-    if (tid == 0) {
-      err->status = kValidation;
-      err->code = E_SIM_EXEC;
-    }
-    return;
-  }
-  for (int j = tid; j < V; j += NT) {
-    const int d = s.device_of[j];
-    if (d < 0 || d >= n || s.seen[j] != 1) bad = 1;
-  }
-  if (__syncthreads_or(bad)) {
-    if (tid == 0) {
-      err->status = kValidation;
-      err->code = E_SIM_ONCE;
-    }
-    return;
-  }
-
-  // ---- transfers: one per (producer, remote consumer device), max bytes ------
-  for (int j = tid; j < V; j += NT) {
-    s.fin[j] = -1;
-    s.bucket[j] = 0;
-  }
-  for (int e = tid; e < E; e += NT) {
-    const int i = g.esrc[e], dc = s.device_of[g.edst[e]];
-    if (s.device_of[i] != dc) s.mb[static_cast<int64_t>(i) * n + dc] = -1;
-  }
-  __syncthreads();
-  {
-    unsigned long long cnt = 0, rem = 0;
-    for (int e = tid; e < E; e += NT) {
-      const int i = g.esrc[e], dc = s.device_of[g.edst[e]];
-      uint8_t f = 0;
-      if (s.device_of[i] != dc) {
-        ++rem;
-        auto *slot = reinterpret_cast<unsigned long long *>(s.mb + static_cast<int64_t>(i) * n + dc);
-        f = atomicCAS(slot, ~0ull, ~0ull - 1) == ~0ull;
-        cnt += f;
-        atomicMax(reinterpret_cast<long long *>(slot), static_cast<long long>(g.ebytes[e]));
-      }
-      s.first[e] = f;
-    }
-    atomicAdd(&sh_x[0], cnt);
-    atomicAdd(&sh_x[2], rem);
-  }
-  __syncthreads();
-  {
-    unsigned long long by = 0;
-    for (int e = tid; e < E; e += NT)
-      if (s.first[e]) by += s.mb[static_cast<int64_t>(g.esrc[e]) * n + s.device_of[g.edst[e]]];
-    atomicAdd(&sh_x[1], by);
-  }
-  // per in-CSR slot: the parent and its arrival delay on the consumer's device
-  for (int x = tid; x < E; x += NT) {
-    const int e = g.in_edge[x];
-    const int i = g.esrc[e], c = g.edst[e];
-    const int di = s.device_of[i], dc = s.device_of[c];
-    s.psrc[x] = i;
-    s.cx[x] = di == dc ? (s.pos[i] < s.pos[c] ? -1 : -2)
-                       : comm_time_exact(s.ic, s.pb, s.mb[static_cast<int64_t>(i) * n + dc]);
-  }
   // permanent memory up front, device by device in FIFO order (:209-214)
   for (int d = warp; d < n; d += NW) {
     const int o = s.exec_off[d], len = s.exec_off[d + 1] - o;
@@ -529,34 +634,44 @@ __global__ void __launch_bounds__(1024) k_sim_flow(const DSim *sims, int nsims, 
       const int o = s.exec_off[d], len = s.exec_off[d + 1] - o;
       int p = s.qpos[d];
       int64_t prev = s.xfree[d];
+      int spins = 0;
       while (p < len) {
-        const int idx = p + lane;
+        const int idx = p + lane, xs = o + idx;
         bool ok = false;
         int64_t A = 0, kk = 0;
         int j = -1;
         if (idx < len) {
-          j = s.exec_order[o + idx];
-          kk = g.k[j];
-          ok = true;
-          const int xe = g.in_off[j + 1];
-          for (int x = g.in_off[j]; x < xe; ++x) {
-            const int64_t cc = s.cx[x];
-            if (cc == -1) continue;
-            if (cc == -2) {
-              ok = false;
-              break;
-            }
-            const int64_t f = ld_cta(s.fin + s.psrc[x]);
-            if (f < 0) {
-              ok = false;
-              break;
-            }
-            A = smax(A, f + cc);
+          kk = s.kx[xs];
+          j = s.exec_order[xs];
+          int r = s.rp_off[xs];
+          const int re = s.rp_off[xs + 1];
+          ok = kk >= 0;
+          for (; ok && r + 1 < re; r += 2) {  // two remote parents per step
+            const int i0 = s.rp_src[r], i1 = s.rp_src[r + 1];
+            const int64_t c0 = s.rp_c[r], c1 = s.rp_c[r + 1];
+            const int64_t f0 = ld_cta(s.fin + i0), f1 = ld_cta(s.fin + i1);
+            ok = f0 >= 0 && f1 >= 0;
+            A = smax(A, smax(f0 + c0, f1 + c1));
+          }
+          if (ok && r < re) {
+            const int64_t f0 = ld_cta(s.fin + s.rp_src[r]);
+            ok = f0 >= 0;
+            A = smax(A, f0 + s.rp_c[r]);
           }
         }
         const unsigned okm = __ballot_sync(kFullS, ok);
         const int L = okm == kFullS ? 32 : __ffs(~okm) - 1;
-        if (L == 0) break;
+        if (L == 0) {
+          // the other walkers of this CTA publish as they go: poll a while
+          // before ending the round (fewer barrier rounds; exactness never
+          // depends on it, the barrier round decides termination)
+          if (++spins <= kWalkSpin) {
+            __nanosleep(200);
+            continue;
+          }
+          break;
+        }
+        spins = 0;
         int64_t al = kk, be = A + kk;  // g_l(f) = max(f + al, be), composed over lanes <= l
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -568,7 +683,7 @@ __global__ void __launch_bounds__(1024) k_sim_flow(const DSim *sims, int nsims, 
         }
         const int64_t f = smax(prev + al, be);
         if (lane < L) {
-          s.sx[o + idx] = f - kk;
+          s.sx[xs] = f - kk;
           s.start[j] = f - kk;
           st_cta(s.fin + j, f);
         }
@@ -586,104 +701,157 @@ __global__ void __launch_bounds__(1024) k_sim_flow(const DSim *sims, int nsims, 
     if (!__syncthreads_or(adv)) break;
   }
   if (lane == 0) atomicMax(&sh_mk, static_cast<long long>(mk));
+  __syncthreads();
+  if (tid == 0) *s.makespan = sh_mk;
+}
 
-  // ---- memory at every start ------------------------------------------------------
-  if (s.mem_mode == 0) {
-    for (int i = tid; i < V; i += NT) {
-      const int b = g.out_off[i], e = g.out_off[i + 1];
-      if (b == e) continue;  // freed at its own finish
-      int64_t lt = -1;
-      int lc = -1;
-      bool all = true;
-      for (int y = b; y < e; ++y) {
-        const int c = g.edst[y];
-        const int64_t f = s.fin[c];
-        if (f < 0) {
-          all = false;
-          break;
-        }
-        if (f > lt || (f == lt && c > lc)) {
-          lt = f;
-          lc = c;
-        }
+// GraphStatic: an output is freed at its last consumer's finish, before the
+// first start on its device at or after that time (grid-wide).
+__global__ void k_sim_free(const DSim *sims, const DGraph *graphs, int base) {
+  const DSim s = sims[base + blockIdx.y];
+  if (flow_skip(s) || s.mem_mode != 0 || s.err->status) return;
+  const DGraph g = graphs[s.graph];
+  BX_SIM_STRIDE(i, g.V) {
+    const int b = g.out_off[i], e = g.out_off[i + 1];
+    if (b == e) continue;  // freed at its own finish
+    int64_t lt = -1;
+    int lc = -1;
+    bool all = true;
+    for (int y = b; y < e; ++y) {
+      const int c = g.edst[y];
+      const int64_t f = s.fin[c];
+      if (f < 0) {
+        all = false;
+        break;
       }
-      if (!all) continue;
-      const int d = s.device_of[i], o = s.exec_off[d];
-      int lo = 0, hi = s.qpos[d];  // first started slot with start >= lt
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (s.sx[o + mid] >= lt) hi = mid;
-        else lo = mid + 1;
+      if (f > lt || (f == lt && c > lc)) {
+        lt = f;
+        lc = c;
       }
-      if (lo < s.qpos[d]) atomicAdd(reinterpret_cast<unsigned long long *>(s.bucket + o + lo),
-                                    static_cast<unsigned long long>(g.outb[i]));
     }
+    if (!all) continue;
+    const int d = s.device_of[i], o = s.exec_off[d], started = s.qpos[d];
+    int lo = 0, hi = started;  // first started slot with start >= lt
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s.sx[o + mid] >= lt) hi = mid;
+      else lo = mid + 1;
+    }
+    if (lo < started)
+      atomicAdd(reinterpret_cast<unsigned long long *>(s.bucket + o + lo), static_cast<unsigned long long>(g.outb[i]));
+  }
+}
+
+// memory at every start of one device (CTA per (device, problem)): block
+// scans over the started FIFO slots; peak, first violation, busy time.
+__global__ void __launch_bounds__(1024) k_sim_mem(const DSim *sims, const DGraph *graphs, int base) {
+  __shared__ long long wsum[32];
+  __shared__ long long s_carry, s_peak, s_busy, s_vm;
+  __shared__ int s_vp, s_vj;
+  const DSim s = sims[base + blockIdx.y];
+  const int d = blockIdx.x;
+  if (d >= s.n || flow_skip(s) || s.err->status) return;
+  const DGraph g = graphs[s.graph];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
+  const int o = s.exec_off[d], started = s.qpos[d];
+  const int64_t cap = s.cap[d];
+  if (tid == 0) {
+    s_carry = s.mem[d];
+    s_peak = s.mem[d];
+    s_busy = 0;
+    s_vp = INT32_MAX;
   }
   __syncthreads();
-  for (int d = warp; d < n; d += NW) {
-    const int o = s.exec_off[d], started = s.qpos[d];
-    const int64_t cap = s.cap[d];
-    int64_t run = s.mem[d], peak = run, vt = INT64_MAX, vm = 0;
-    int vj = INT32_MAX;
-    int64_t busy = 0;
-    for (int b = 0; b < started; b += 32) {
-      const int p = b + lane;
-      int64_t ch = 0, w = 0, fr = 0;
-      int j = -1;
-      if (p < started) {
-        j = s.exec_order[o + p];
-        const int64_t tmp = g.temp[j], out = g.outb[j];
-        ch = tmp + out;
-        const bool drop = s.mem_mode == 0 && g.out_off[j + 1] == g.out_off[j];
-        fr = s.bucket[o + p];
-        w = ch - tmp - (drop ? out : 0) - fr;
-        busy += g.k[j];
-      }
-      int64_t incl = w;
+  int64_t peak = 0, busy = 0;
+  for (int b = 0; b < started; b += blockDim.x) {
+    const int p = b + tid;
+    int64_t ch = 0, w = 0, fr = 0;
+    int j = -1;
+    if (p < started) {
+      j = s.exec_order[o + p];
+      const int64_t tmp = g.temp[j], out = g.outb[j];
+      ch = tmp + out;
+      const bool drop = s.mem_mode == 0 && g.out_off[j + 1] == g.out_off[j];
+      fr = s.bucket[o + p];
+      w = ch - tmp - (drop ? out : 0) - fr;
+      busy += g.k[j];
+    }
+    long long incl = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const long long u = __shfl_up_sync(kFullS, incl, off);
+      if (lane >= off) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      long long x = lane < NW ? wsum[lane] : 0;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
-        const int64_t u = __shfl_up_sync(kFullS, incl, off);
-        if (lane >= off) incl += u;
+        const long long u = __shfl_up_sync(kFullS, x, off);
+        if (lane >= off) x += u;
       }
-      const int64_t m = run + (incl - w) - fr + ch;
-      if (p < started) peak = smax(peak, m);
-      const unsigned over = __ballot_sync(kFullS, p < started && m > cap);
-      if (over && vt == INT64_MAX) {
-        const int l = __ffs(over) - 1;
-        vt = s.sx[o + b + l];
-        vj = __shfl_sync(kFullS, j, l);
-        vm = __shfl_sync(kFullS, m, l);
-      }
-      run += __shfl_sync(kFullS, incl, 31);
+      if (lane < NW) wsum[lane] = x;
     }
+    __syncthreads();
+    const int64_t m = s_carry + (warp ? wsum[warp - 1] : 0) + (incl - w) - fr + ch;
+    if (p < started) {
+      peak = smax(peak, m);
+      if (m > cap) atomicMin(&s_vp, p);
+    }
+    __syncthreads();
+    if (p == s_vp) {  // the run stops at its first violation
+      s_vm = m;
+      s_vj = j;
+    }
+    if (tid == 0) s_carry += wsum[NW - 1];
+    const bool stop = s_vp != INT32_MAX;
+    __syncthreads();
+    if (stop) break;
+  }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      peak = smax(peak, __shfl_xor_sync(kFullS, peak, off));
-      busy += __shfl_xor_sync(kFullS, busy, off);
-    }
-    if (lane == 0) {
-      s.peak[d] = peak;
-      s.dest_bytes[d] = vt;
-      s.dest_cnt[d] = vj;
-      s.xfree[d] = vm;
-      s.dev3n[3 * d + 1] = busy;
-    }
+  for (int off = 16; off > 0; off >>= 1) {
+    peak = smax(peak, __shfl_xor_sync(kFullS, peak, off));
+    busy += __shfl_xor_sync(kFullS, busy, off);
+  }
+  if (lane == 0) {
+    atomicMax(&s_peak, static_cast<long long>(peak));
+    atomicAdd(reinterpret_cast<unsigned long long *>(&s_busy), static_cast<unsigned long long>(busy));
   }
   __syncthreads();
   if (tid != 0) return;
+  s.dv[4 * d + 0] = s_peak;
+  s.dev3n[3 * d + 1] = s_busy;
+  if (s_vp == INT32_MAX) {
+    s.dv[4 * d + 1] = INT64_MAX;
+    return;
+  }
+  s.dv[4 * d + 1] = s.sx[o + s_vp];
+  s.dv[4 * d + 2] = s_vj;
+  s.dv[4 * d + 3] = s_vm;
+}
+
+// the verdict: first violation (min (t, node) over devices), deadlock, or the report
+__global__ void k_sim_report(const DSim *sims, int nsims) {
+  const int sid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sid >= nsims) return;
+  const DSim s = sims[sid];
+  if (flow_skip(s) || s.err->status) return;
+  DErr *err = s.err;
+  const int n = s.n;
   int vd = -1;
   for (int d = 0; d < n; ++d) {
-    const int64_t t = s.dest_bytes[d];
+    const int64_t t = s.dv[4 * d + 1];
     if (t == INT64_MAX) continue;
-    if (vd < 0 || t < s.dest_bytes[vd] || (t == s.dest_bytes[vd] && s.dest_cnt[d] < s.dest_cnt[vd])) vd = d;
+    if (vd < 0 || t < s.dv[4 * vd + 1] || (t == s.dv[4 * vd + 1] && s.dv[4 * d + 2] < s.dv[4 * vd + 2])) vd = d;
   }
   if (vd >= 0) {
     err->status = kInfeasible;
     err->code = E_SIM_MEMORY;
     err->a = vd;
-    err->b = s.dest_bytes[vd];
-    err->c = s.dest_cnt[vd];
-    err->d = s.xfree[vd];
+    err->b = s.dv[4 * vd + 1];
+    err->c = s.dv[4 * vd + 2];
+    err->d = s.dv[4 * vd + 3];
     return;
   }
   for (int d = 0; d < n; ++d) {
@@ -695,25 +863,42 @@ __global__ void __launch_bounds__(1024) k_sim_flow(const DSim *sims, int nsims, 
       return;
     }
   }
-  const int64_t makespan = sh_mk;
+  const int64_t makespan = *s.makespan;
   for (int d = 0; d < n; ++d) {
-    s.dev3n[3 * d + 0] = s.peak[d];
+    s.dev3n[3 * d + 0] = s.dv[4 * d + 0];
     s.dev3n[3 * d + 2] = makespan - s.dev3n[3 * d + 1];
   }
-  *s.makespan = makespan;
-  s.xfer4[0] = static_cast<int64_t>(sh_x[0]);
-  s.xfer4[1] = static_cast<int64_t>(sh_x[1]);
+  s.xfer4[0] = static_cast<int64_t>(s.flow8[3]);
+  s.xfer4[1] = static_cast<int64_t>(s.flow8[4]);
   s.xfer4[2] = 0;  // a tensor is sent once per device: duplicates never arise
-  s.xfer4[3] = static_cast<int64_t>(sh_x[2] - sh_x[0]);
+  s.xfer4[3] = static_cast<int64_t>(s.flow8[5] - s.flow8[3]);
   err->status = kOk;
   err->code = E_NONE;
 }
 
-void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, cudaStream_t s) {
+void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn, cudaStream_t s) {
+  // K4f: grid-wide passes (blockIdx.y = problem), then one CTA per problem
+  // for the walkers, per device for the memory scans; K4 takes the problems
+  // K4f leaves (sequential comm, zero-duration nodes) after the first pass
+  const unsigned gx = nsims <= 16 ? 148 : nsims <= 148 ? 16 : 2;
+  auto grid = [&](auto kern, unsigned x, int threads) {
+    for (int b = 0; b < nsims; b += 65535) {
+      const dim3 g(x, static_cast<unsigned>(nsims - b < 65535 ? nsims - b : 65535));
+      kern<<<g, threads, 0, s>>>(sims, graphs, b);
+    }
+  };
+  grid(k_sim_prep_a, gx, 256);
   constexpr int W = 4;
   k_simulate<W><<<(nsims + W - 1) / W, 32 * W, 0, s>>>(sims, nsims, graphs);
-  // one CTA per problem; a lone problem gets the widest CTA for its edge passes
-  k_sim_flow<<<nsims, nsims <= 148 ? 1024 : 256, 0, s>>>(sims, nsims, graphs);
+  grid(k_sim_prep_b, gx, 256);
+  grid(k_sim_prep_c, gx, 256);
+  const int cta = nsims <= 148 ? 1024 : 256;
+  k_sim_prep_d<<<nsims, cta, 0, s>>>(sims, graphs);
+  grid(k_sim_prep_e, gx, 256);
+  k_sim_flow<<<nsims, cta, 0, s>>>(sims, nsims, graphs);
+  grid(k_sim_free, gx, 256);
+  grid(k_sim_mem, static_cast<unsigned>(maxn), cta);
+  k_sim_report<<<(nsims + 127) / 128, 128, 0, s>>>(sims, nsims);
 }
 
 // ---------------------------------------------------------------- K3 ----

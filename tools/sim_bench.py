@@ -1,28 +1,45 @@
-"""K4 simulator timing on a 100k-op placement vs the reference simulate()."""
-import json, sys, time
-sys.path.insert(0, ".")
-import numpy as np
-import torch
-import paper_2301_08695_b200 as bx
-from paper_2301_08695_b200 import workloads as W
-from oracle import Ref
+"""K4 simulator timing on a 100k-op placement vs the reference simulate():
+device time of bx_plan_simulate (CUDA events on its stream) and the wall time
+including the report download."""
+import json
+import sys
+import time
 
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2301_08695_b200 as bx  # noqa: E402
+from oracle import Ref  # noqa: E402
+from paper_2301_08695_b200 import workloads as W  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 g = W.layered_dag_fast(100, 1000, 3)
 gg = bx.MetaGraph.from_dict(W.as_meta_dict(g))
 cm = bx.CommModel(*W.COMM_TEST)
-caps = np.full(4, W.bench_capacity(g, 4, 1.2), np.int64)
+caps = np.full(n, W.bench_capacity(g, n, 1.2), np.int64)
 plan = bx.Plan([gg], [bx.Job(0, "m-etf", caps, cm)])
-plan.upload(); plan.place(); plan.download()
+plan.upload()
+plan.place()
+plan.download()
 p = plan.result(0)
+st = torch.cuda.current_stream()
 for mm in (1, 0):
-    ts = []
-    for _ in range(3):
-        torch.cuda.synchronize(); t0 = time.perf_counter()
-        plan.simulate(mm); reps = plan.sim_download()
-        ts.append((time.perf_counter() - t0) * 1e3)
+    dev, wall = [], []
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(st)
+        plan.simulate(mm, st.cuda_stream)
+        e1.record(st)
+        reps = plan.sim_download(st.cuda_stream)
+        wall.append((time.perf_counter() - t0) * 1e3)
+        dev.append(e0.elapsed_time(e1))
     r = reps[0]
     rg = Ref.graph(W.as_ref_base(g), -1)
     o = Ref.simulate(rg, caps, W.COMM_TEST, mm, p.device_of, p.exec_order_flat, p.exec_off)
-    print(json.dumps({"mem_mode": mm, "gpu_sim_ms": min(ts), "cpu_ref_sim_ms": o.wall_ns / 1e6,
+    print(json.dumps({"n": n, "mem_mode": mm, "gpu_sim_device_ms": min(dev[1:]), "gpu_sim_wall_ms": min(wall[1:]),
+                      "cpu_ref_sim_ms": o.wall_ns / 1e6,
                       "same": bool(o.makespan == r.makespan_us and np.array_equal(o.start_us, r.start_us)
-                                   and o.peak.tolist() == r.peak_bytes.tolist())}))
+                                   and o.peak.tolist() == r.peak_bytes.tolist())}), flush=True)
