@@ -40,6 +40,9 @@
 namespace bx {
 
 constexpr int KT = 4;  // exact top-KT pairs kept per device column
+#ifndef BX_SCAN_U
+#define BX_SCAN_U 4  // column-scan loads in flight per lane
+#endif
 
 struct Tops {      // entry k of column q at k * st + q (no bank conflicts for lane-owned columns)
   int64_t *t;    // [KT*st] keys, ascending (key, node)
@@ -268,7 +271,7 @@ __device__ __forceinline__ void lane_top4(const Ctx &c, int q, int s0, int step,
   const int64_t Fq = c.F[q];
   const int aw = c.sct ? c.awf[q] : -1;
   const int64_t awu = aw >= 0 ? c.awu[q] : 0;
-  constexpr int U = 4;
+  constexpr int U = BX_SCAN_U;
   for (int base = s0 + lane; base < R; base += U * step) {
     int64_t kv[U];
     int nd[U];
@@ -1009,63 +1012,65 @@ __device__ __forceinline__ void rent_meta(REnt &e, const Ctx &c, const DGraph &g
 
 // Per-column sorted lists in shared memory, structure of arrays, entry k of
 // column q at k * st + q: lanes that own consecutive columns touch consecutive
-// words (no bank conflicts for the lane-owned edits and the head scans).
+// words (no bank conflicts for the lane-owned edits and the head scans). The
+// sorted order holds (t, j, handle); a node's metadata sits at its handle
+// (h * st + q) and never moves, so list edits shift three words, not ten.
 struct RList {
   int64_t *t, *need, *k;
-  int32_t *j, *s, *fav, *inb, *ine, *outb, *oute;
+  int32_t *j, *h, *s, *fav, *inb, *ine, *outb, *oute;
+  int32_t *hmask;  // [st] handles in use per column
   int st;
   __device__ __forceinline__ int at(int q, int kk) const { return kk * st + q; }
-  __device__ __forceinline__ REnt get(int i) const {
+  __device__ __forceinline__ REnt get(int q, int kk) const {
+    const int i = at(q, kk), m = h[i] * st + q;
     REnt e;
     e.t = t[i];
-    e.need = need[i];
-    e.k = k[i];
     e.j = j[i];
-    e.s = s[i];
-    e.fav = fav[i];
-    e.inb = inb[i];
-    e.ine = ine[i];
-    e.outb = outb[i];
-    e.oute = oute[i];
+    e.need = need[m];
+    e.k = k[m];
+    e.s = s[m];
+    e.fav = fav[m];
+    e.inb = inb[m];
+    e.ine = ine[m];
+    e.outb = outb[m];
+    e.oute = oute[m];
     return e;
   }
-  __device__ __forceinline__ void put(int i, const REnt &e) const {
-    t[i] = e.t;
-    need[i] = e.need;
-    k[i] = e.k;
-    j[i] = e.j;
-    s[i] = e.s;
-    fav[i] = e.fav;
-    inb[i] = e.inb;
-    ine[i] = e.ine;
-    outb[i] = e.outb;
-    oute[i] = e.oute;
+  __device__ __forceinline__ void put_meta(int q, int hh, const REnt &e) const {
+    const int m = hh * st + q;
+    need[m] = e.need;
+    k[m] = e.k;
+    s[m] = e.s;
+    fav[m] = e.fav;
+    inb[m] = e.inb;
+    ine[m] = e.ine;
+    outb[m] = e.outb;
+    oute[m] = e.oute;
   }
   __device__ __forceinline__ void mv(int d, int x) const {
     t[d] = t[x];
-    need[d] = need[x];
-    k[d] = k[x];
     j[d] = j[x];
-    s[d] = s[x];
-    fav[d] = fav[x];
-    inb[d] = inb[x];
-    ine[d] = ine[x];
-    outb[d] = outb[x];
-    oute[d] = oute[x];
+    h[d] = h[x];
   }
 };
 
 // lane-owned list edits (lane q % 32 owns column q)
 template <int KR>
-__device__ __forceinline__ void rlist_remove(const RList &L, int32_t *cnt, int32_t *flg, int q, int j) {
+// returns true when the column just turned dirty (emptied, incomplete)
+__device__ __forceinline__ bool rlist_remove(const RList &L, int32_t *cnt, int32_t *flg, int q, int j) {
   int c = cnt[q];
   int at = -1;
   for (int k = 0; k < c; ++k)
     if (L.j[L.at(q, k)] == j) at = k;
-  if (at < 0) return;
+  if (at < 0) return false;
+  L.hmask[q] &= ~(1u << L.h[L.at(q, at)]);
   for (int k = at; k + 1 < c; ++k) L.mv(L.at(q, k), L.at(q, k + 1));
   cnt[q] = --c;
-  if (c == 0 && !(flg[q] & kComplete)) flg[q] |= kDirty;
+  if (c == 0 && !(flg[q] & kComplete)) {
+    flg[q] |= kDirty;
+    return true;
+  }
+  return false;
 }
 
 // insert a fully built entry; returns nothing (list stays exact top-cnt)
@@ -1078,15 +1083,22 @@ __device__ __forceinline__ void rlist_insert(const RList &L, int32_t *cnt, int32
     flg[q] = f & ~kComplete;
     if (!lex_less(e.t, e.j, L.t[L.at(q, KR - 1)], L.j[L.at(q, KR - 1)])) return;
     --c;
+    L.hmask[q] &= ~(1u << L.h[L.at(q, KR - 1)]);  // the dropped tail frees its handle
   } else if (!(f & kComplete)) {
     if (c == 0 || !lex_less(e.t, e.j, L.t[L.at(q, c - 1)], L.j[L.at(q, c - 1)])) return;
   }
+  const unsigned used = static_cast<unsigned>(L.hmask[q]);
+  const int hh = __ffs(~used) - 1;
+  L.hmask[q] = static_cast<int32_t>(used | (1u << hh));
+  L.put_meta(q, hh, e);
   int k = c;
   while (k > 0 && lex_less(e.t, e.j, L.t[L.at(q, k - 1)], L.j[L.at(q, k - 1)])) {
     L.mv(L.at(q, k), L.at(q, k - 1));
     --k;
   }
-  L.put(L.at(q, k), e);
+  L.t[L.at(q, k)] = e.t;
+  L.j[L.at(q, k)] = e.j;
+  L.h[L.at(q, k)] = hh;
   cnt[q] = c + 1;
 }
 
@@ -1302,13 +1314,15 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
   int32_t *stg_cnt = stg_live + ntask;
   unsigned *stg_tj = reinterpret_cast<unsigned *>(stg_cnt + ntask);
   L.j = reinterpret_cast<int32_t *>(stg_tj + ntask);
-  L.s = L.j + maxn * KR;
+  L.h = L.j + maxn * KR;
+  L.s = L.h + maxn * KR;
   L.fav = L.s + maxn * KR;
   L.inb = L.fav + maxn * KR;
   L.ine = L.inb + maxn * KR;
   L.outb = L.ine + maxn * KR;
   L.oute = L.outb + maxn * KR;
-  c.awf = L.oute + maxn * KR;
+  L.hmask = L.oute + maxn * KR;
+  c.awf = L.hmask + maxn;
   c.excl = c.awf + maxn;
   int32_t *cnt = c.excl + maxn;
   int32_t *flg = cnt + maxn;
@@ -1441,7 +1455,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
       }
       // list entries follow their nodes
       for (int e = tid; e < maxn * KR; e += NT)
-        if (e % maxn < n && e / maxn < cnt[e % maxn]) L.s[e] = c.rpos[L.j[e]];
+        if (e % maxn < n && e / maxn < cnt[e % maxn]) L.s[L.h[e] * maxn + e % maxn] = c.rpos[L.j[e]];
       __syncthreads();
       RMARK(P_REMOVE);
     }
@@ -1493,20 +1507,24 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
           if (has && ht == bt && hj == bj) {
             L.t[L.at(q, r)] = bt;
             L.j[L.at(q, r)] = static_cast<int>(bj);
-            L.s[L.at(q, r)] = stg_s[(tb + lane) * KR + ptr];
+            L.h[L.at(q, r)] = r;
+            L.s[L.at(q, r)] = stg_s[(tb + lane) * KR + ptr];  // handle r: meta row r
             ++ptr;
           }
           ++kc;
         }
         __syncwarp();
         for (int r = lane; r < kc; r += 32) {  // listed nodes' metadata, in parallel
-          REnt e = L.get(L.at(q, r));
+          REnt e;
+          e.j = L.j[L.at(q, r)];
+          e.s = L.s[L.at(q, r)];
           rent_meta(e, c, g);
-          L.put(L.at(q, r), e);
+          L.put_meta(q, r, e);
         }
         if (lane == 0) {
           cnt[q] = kc;
           flg[q] = lv == kc ? kComplete : 0;
+          L.hmask[q] = static_cast<int32_t>(kc >= 32 ? 0xffffffffu : (1u << kc) - 1u);
         }
       }
     }
@@ -1551,18 +1569,22 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
     // ---- phase S: the leader selects this round's commits (shared memory) -------
     if (warp == 0) {
       int k = 0;
+      // threshold: keys in dirty columns are >= F[q]; a commit lowers it to
+      // its finish (its column turns dirty), nothing in the round raises it
+      // except an exclusion, where the stale lower value is only conservative
+      int64_t thr = kInf;
+      {
+        unsigned dummy = 0;
+        for (int q = lane; q < n; q += 32)
+          if (!c.excl[q] && (flg[q] & kDirty)) thr = min64(thr, c.F[q]);
+        warp_argmin_u(thr, dummy);
+      }
       while (true) {
         if (S->placed + k == V) break;
-        // threshold: keys in dirty columns are >= F[q]
-        int64_t thr = kInf;
         int64_t bt = kInf;
-        unsigned bi = 0xffffffffu, dummy = 0;
+        unsigned bi = 0xffffffffu;
         for (int q = lane; q < n; q += 32) {
-          if (c.excl[q]) continue;
-          if (flg[q] & kDirty) {
-            thr = min64(thr, c.F[q]);
-            continue;
-          }
+          if (c.excl[q] || (flg[q] & kDirty)) continue;
           if (cnt[q] == 0) continue;
           unsigned cell = static_cast<unsigned>(L.j[q]) * static_cast<unsigned>(n) + q;
           if (L.t[q] < bt || (L.t[q] == bt && cell < bi)) {
@@ -1571,7 +1593,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
           }
         }
         warp_argmin_u(bt, bi);
-        warp_argmin_u(thr, dummy);
+        RMARK(P_REKEY);  // (profile builds) phase S: head argmin
         if (bi == 0xffffffffu) {
           if (k == 0 && thr == kInf) {  // no live pair anywhere
             if (lane == 0) {
@@ -1584,7 +1606,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
         }
         if (bt >= thr) break;
         const int q = static_cast<int>(bi % static_cast<unsigned>(n));
-        const REnt e = L.get(q);
+        const REnt e = L.get(q, 0);
         if (c.res[q] + e.need > c.capS[q]) {
           // discard (placers.cpp:203-219), inline: rare. With commits pending
           // in this round, end the round first: the pair stays the minimum
@@ -1607,7 +1629,8 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
             break;
           }
           if (lane == 0) S->discarded++;
-          if (lane == (q & 31)) rlist_remove<KR>(L, cnt, flg, q, e.j);
+          const bool emptied = lane == (q & 31) && rlist_remove<KR>(L, cnt, flg, q, e.j);
+          if (__any_sync(kFull, emptied)) thr = min64(thr, c.F[q]);  // its keys are >= F[q]
           int64_t minrem = 0;
           if (lane == 0) {
             while (c.device_of[g.need_order[minptr]] >= 0) ++minptr;
@@ -1649,6 +1672,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
           __syncwarp();
           continue;
         }
+        RMARK(P_READY);  // (profile builds) phase S: candidate fetch + memory test
         // commit (placers.cpp:221-233): bookkeeping here, global work below
         const int64_t fin = e.t + e.k;
         if (lane == 0) {
@@ -1665,13 +1689,23 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
           c.F[q] = fin;
           c.res[q] += e.need;
         }
+        thr = min64(thr, fin);
         ++k;
         __syncwarp();
-        for (int qq = lane; qq < n; qq += 32) {
-          if (qq == q) flg[qq] |= kDirty;
-          else rlist_remove<KR>(L, cnt, flg, qq, e.j);
+        {
+          int64_t te = kInf;  // columns emptied by the removal turn dirty too
+          for (int qq = lane; qq < n; qq += 32) {
+            if (qq == q) flg[qq] |= kDirty;
+            else if (rlist_remove<KR>(L, cnt, flg, qq, e.j) && !c.excl[qq]) te = min64(te, c.F[qq]);
+          }
+          if (__any_sync(kFull, te != kInf)) {
+            unsigned dummy = 0;
+            warp_argmin_u(te, dummy);
+            thr = min64(thr, te);
+          }
         }
         __syncwarp();
+        RMARK(P_CACHE);  // (profile builds) phase S: bookkeeping + list removals
         if (c.sct) {
           // awake reservations (placers.cpp:235-254); one commit per round
           if (lane == 0) {
@@ -1700,15 +1734,32 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tb = min64(tb, __shfl_xor_sync(kFull, tb, o));
       // prefix sums of the committed nodes' degrees; dirty column list
-      if (lane == 0) {
-        S->ncommit = k;
-        inoff[0] = outoff[0] = 0;
-        for (int i = 0; i < k; ++i) {
-          inoff[i + 1] = inoff[i] + (CM[i].ine - CM[i].inb);
-          outoff[i + 1] = outoff[i] + (CM[i].oute - CM[i].outb);
+      {
+        int ci = 0, co = 0;
+        for (int b = 0; b < k; b += 32) {
+          const int i = b + lane;
+          int vi = i < k ? CM[i].ine - CM[i].inb : 0, vo = i < k ? CM[i].oute - CM[i].outb : 0;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int ui = __shfl_up_sync(kFull, vi, o), uo = __shfl_up_sync(kFull, vo, o);
+            if (lane >= o) {
+              vi += ui;
+              vo += uo;
+            }
+          }
+          if (i < k) {
+            inoff[i + 1] = ci + vi;
+            outoff[i + 1] = co + vo;
+          }
+          ci += __shfl_sync(kFull, vi, 31);
+          co += __shfl_sync(kFull, vo, 31);
         }
-        S->nnew = 0;
-        S->nnc = 0;
+        if (lane == 0) {
+          S->ncommit = k;
+          inoff[0] = outoff[0] = 0;
+          S->nnew = 0;
+          S->nnc = 0;
+        }
       }
       {
         int ndc = 0;
@@ -1721,6 +1772,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
         }
         if (lane == 0) S->ndirty = ndc;
       }
+      RMARK(P_DISCARD);  // (profile builds) phase S: round tail
     }
     __syncthreads();
     RMARK(P_ARGMIN);
@@ -1840,7 +1892,7 @@ __global__ void __launch_bounds__(RWARPS * 32, 1)
 
 static size_t rounds_smem(int maxn, int KR) {
   const int ntask = maxn > RWARPS ? maxn : RWARPS;
-  return ((sizeof(RShared) + 15) & ~size_t(15)) + 5 * 8 * size_t(maxn) + 52 * size_t(KR) * maxn +
+  return ((sizeof(RShared) + 15) & ~size_t(15)) + 5 * 8 * size_t(maxn) + 56 * size_t(KR) * maxn + 4 * size_t(maxn) +
          sizeof(RCommit) * maxn + size_t(ntask) * (KR * 16 + 8 + 12) +
          4 * (7 * size_t(maxn) + 2) + 4 * (RWARPS + 1) + 64;  // awf excl cnt flg dcols inoff outoff wsum
 }
