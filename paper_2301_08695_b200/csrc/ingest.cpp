@@ -17,6 +17,7 @@
 // epoch-stamped DFS instead of std::set / std::map where order is not
 // observable.
 #include <algorithm>
+#include <climits>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -182,7 +183,11 @@ class Merger {
     int64_t bytes = 0;
     int count = 0;
   };
-  explicit Merger(const Meta &in) : in_(in) {
+  // levels: with `track_levels` (merges that keep the meta graph acyclic:
+  // co-placement and fusion) every live root carries a topological potential
+  // lvl(u) < lvl(v) for every edge u -> v, kept valid across merges; a path
+  // search toward b then never enters a root with lvl >= lvl(b).
+  explicit Merger(const Meta &in, bool track_levels = false) : in_(in), track_(track_levels) {
     const int n = in.V();
     parent_.resize(n);
     minm_.resize(n);
@@ -201,6 +206,19 @@ class Merger {
       pred_[d][s] = Agg{in.ebytes[e], in.ecount[e]};
       out_base_[s] += in.ecount[e];
       in_base_[d] += in.ecount[e];
+    }
+    if (track_) {  // longest-path levels (Kahn); a cyclic input disables pruning
+      lvl_.assign(n, 0);
+      std::vector<int> indeg(n, 0), q;
+      for (int g = 0; g < n; ++g) indeg[g] = static_cast<int>(pred_[g].size());
+      for (int g = 0; g < n; ++g)
+        if (!indeg[g]) q.push_back(g);
+      for (size_t h = 0; h < q.size(); ++h)
+        for (const auto &kv : succ_[q[h]]) {
+          lvl_[kv.first] = std::max(lvl_[kv.first], lvl_[q[h]] + 1);
+          if (--indeg[kv.first] == 0) q.push_back(kv.first);
+        }
+      if (static_cast<int>(q.size()) != n) track_ = false;
     }
   }
   int find(int g) {
@@ -260,6 +278,21 @@ class Merger {
     succ_[l].clear();
     pred_[l].clear();
     parent_[l] = s;
+    if (track_) {
+      // the merged root sits at the higher level; successors that fall at or
+      // below it are raised, transitively (merges here never close a cycle)
+      lvl_[s] = std::max(lvl_[s], lvl_[l]);
+      std::vector<int> work{s};
+      while (!work.empty()) {
+        const int u = work.back();
+        work.pop_back();
+        for (const auto &kv : succ_[u])
+          if (lvl_[kv.first] <= lvl_[u]) {
+            lvl_[kv.first] = lvl_[u] + 1;
+            work.push_back(kv.first);
+          }
+      }
+    }
     return s;
   }
 
@@ -283,12 +316,16 @@ class Merger {
   bool path_besides_edge(int a, int b) {
     a = find(a);
     b = find(b);
+    // with levels, only roots strictly below lvl(b) can lie on a path to b
+    const int cut = track_ ? lvl_[b] : INT32_MAX;
+    if (track_ && lvl_[a] >= cut) return false;
+    auto wanted = [&](int t) { return t == b || !track_ || lvl_[t] < cut; };
     ++epoch_;
     std::vector<int> stack;
     stamp_[a] = epoch_;
     for (const auto &kv : succ_[a]) {
       if (kv.first == b) continue;
-      if (stamp_[kv.first] != epoch_) {
+      if (stamp_[kv.first] != epoch_ && wanted(kv.first)) {
         stamp_[kv.first] = epoch_;
         stack.push_back(kv.first);
       }
@@ -298,7 +335,7 @@ class Merger {
       stack.pop_back();
       if (u == b) return true;
       for (const auto &kv : succ_[u])
-        if (stamp_[kv.first] != epoch_) {
+        if (stamp_[kv.first] != epoch_ && wanted(kv.first)) {
           stamp_[kv.first] = epoch_;
           stack.push_back(kv.first);
         }
@@ -353,7 +390,8 @@ class Merger {
 
  private:
   const Meta &in_;
-  std::vector<int> parent_, minm_, out_base_, in_base_, stamp_;
+  bool track_;
+  std::vector<int> parent_, minm_, out_base_, in_base_, stamp_, lvl_;
   int epoch_ = 0;
   std::vector<std::map<int, Agg>> succ_, pred_;
 };
@@ -401,7 +439,7 @@ Meta apply_colocation(const Meta &gg, const Base &b) {
 }
 
 Meta apply_coplacement(const Meta &gg, const Base &b) {
-  Merger mg(gg);
+  Merger mg(gg, true);
   for (int i = 0; i < b.n; ++i) {
     if (!b.has_pair[i]) continue;
     int peer = b.index_of(b.pair[i]);
@@ -427,7 +465,7 @@ Meta apply_coplacement(const Meta &gg, const Base &b) {
 }
 
 Meta fuse_operators(const Meta &gg, const Base &b) {
-  Merger mg(gg);
+  Merger mg(gg, true);
   // affinity classes over base nodes: colocation label or coplace pair
   std::vector<int> par(b.n);
   std::iota(par.begin(), par.end(), 0);

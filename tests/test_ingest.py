@@ -116,3 +116,22 @@ def test_ingest_golden_vectors():
                                              "ecount", "member_off", "members", "first_id")}
         r["V"], r["E"] = len(r["k"]), len(r["esrc"])
         _cmp(m, gr, r)
+
+
+@pytest.mark.skipif(not Ref.available(), reason="reference not compiled on this host")
+@pytest.mark.parametrize("fam,V,frac,coloc", [("layered-chain", 12000, 0.05, 0.0), ("branchy", 6000, 0.2, 0.05),
+                                               ("layered-chain", 8000, 0.3, 0.02)])
+def test_ingest_at_scale_matches_reference(fam, V, frac, coloc):
+    """Level-pruned co-placement path checks and fusion at thousands of
+    nodes: identical meta graphs and groupings to the reference transforms."""
+    g = Ref.generate(fam, V, 77, layers=60, coplace_frac=frac, colocate_edge_frac=coloc)
+    for pipe in (2, 6):
+        try:
+            r = Ref.graph(g, pipe).meta()
+        except OracleError as e:
+            with pytest.raises(bx.ValidationError) as ei:
+                bx.build_grouped(g, **PIPES[pipe])
+            assert ei.value.msg == e.msg
+            continue
+        m, gr = bx.build_grouped(g, **PIPES[pipe])
+        _cmp(m, gr, r)
