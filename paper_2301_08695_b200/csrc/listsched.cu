@@ -695,7 +695,11 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     BX_MARK(P_ARGMIN);
 
     if (c.mode == 0) {
-      // lazy re-key of the winner (placers.cpp:198-202)
+      // lazy re-key of the winner (placers.cpp:198-202). Queue tails only
+      // grow, so stored keys are lower bounds; a grown key is re-placed in
+      // column p's list, like the reference's re-push (:199-201) — the list
+      // stays an exact prefix (the entry drops out if it now sorts past an
+      // incomplete list's tail), so no column rescan follows.
       int64_t fresh = 0;
       if (lane == 0) fresh = key_of(c, j, p, gen);
       fresh = __shfl_sync(kFull, fresh, 0);
@@ -707,7 +711,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
       if (key != t) {
         if (lane == 0) {
           c.Kc[p * Vs + sj] = fresh;
-          T.flg[p] |= kDirty;
+          list_remove(T, p, j);
+          list_insert(T, p, key, j, sj);
         }
         __syncwarp();
         BX_MARK(P_REKEY);

@@ -199,16 +199,11 @@ __global__ void __launch_bounds__(32 * kWarps) k_place_topo(const DJob *jobs, in
         bpos = s;
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      int b2 = __shfl_xor_sync(kFull, best, o);
-      int p2 = __shfl_xor_sync(kFull, bpos, o);
-      if (b2 < best) {
-        best = b2;
-        bpos = p2;
-      }
-    }
-    if (lane == 0) {
+    // one REDUX for the minimum node; its lane (ids are unique) moves the
+    // last ready slot into the hole
+    const int mine = best;
+    best = static_cast<int>(__reduce_min_sync(kFull, static_cast<unsigned>(best)));
+    if (mine == best) {
       order[cnt] = best;
       jb.ready[bpos] = jb.ready[R - 1];
     }
@@ -245,8 +240,75 @@ __global__ void __launch_bounds__(32 * kWarps) k_place_topo(const DJob *jobs, in
       used += b;
     }
     for (int d = dev + 1; d <= n; ++d) jb.exec_off[d] = V;
-    // schedule estimate (placers.cpp:350-362); placement is fixed up front,
-    // so every device_of is set before the fold runs
+  }
+  __syncwarp();
+  if (c.mode == 1) {
+    // schedule estimate, parallel comm (placers.cpp:350-362), warp-parallel:
+    // a remote parent's tensor lands on p at finish + c_e of the edge to its
+    // FIRST consumer on p in topo order (later consumers hit that cache
+    // entry), and every parent precedes its child in topo order, so device d
+    // (a contiguous topo chunk) depends only on devices < d and on its own
+    // predecessor: walk the devices in order, 32 nodes at a time, with a
+    // max-plus scan f_l = max(f_{l-1} + k_l, A_l + k_l).
+    int32_t *tpos = jb.pending;  // free after Kahn
+    for (int x = lane; x < V; x += 32) tpos[order[x]] = x;
+    __syncwarp();
+    for (int y = lane; y < g.E; y += 32) {  // y = edge id = out-CSR slot
+      const int i = g.esrc[y], j = g.edst[y], pj = jb.device_of[j];
+      if (jb.device_of[i] != pj) jb.cache[static_cast<int64_t>(i) * n + pj] = INT64_MAX;
+    }
+    __syncwarp();
+    for (int y = lane; y < g.E; y += 32) {
+      const int i = g.esrc[y], j = g.edst[y], pj = jb.device_of[j];
+      if (jb.device_of[i] != pj)
+        atomicMin(reinterpret_cast<long long *>(jb.cache + static_cast<int64_t>(i) * n + pj),
+                  (static_cast<long long>(tpos[j]) << 32) | g.inpos[y]);
+    }
+    __syncwarp();
+    for (int d = 0; d < n; ++d) {
+      const int o = jb.exec_off[d], len = jb.exec_off[d + 1] - o;
+      int64_t prev = 0;
+      for (int b = 0; b < len; b += 32) {
+        const int idx = b + lane;
+        int64_t A = 0, kk = 0;
+        int j = -1;
+        if (idx < len) {
+          j = order[o + idx];
+          kk = g.k[j];
+          for (int x = g.in_off[j]; x < g.in_off[j + 1]; ++x) {
+            const int i = g.in_src[x];
+            if (jb.device_of[i] == d) continue;  // earlier on this device: covered by the chain
+            const int first = static_cast<int>(jb.cache[static_cast<int64_t>(i) * n + d] & 0xffffffffll);
+            A = max64(A, jb.finish[i] + pr.in_c[first]);
+          }
+        }
+        int64_t al = kk, be = A + kk;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int64_t a2 = __shfl_up_sync(kFull, al, off), b2 = __shfl_up_sync(kFull, be, off);
+          if (lane >= off) {
+            be = max64(b2 + al, be);
+            al = a2 + al;
+          }
+        }
+        const int64_t f = max64(prev + al, be);
+        if (idx < len) {
+          jb.start[j] = f - kk;
+          jb.finish[j] = f;
+        }
+        prev = __shfl_sync(kFull, f, 31);
+        __syncwarp();
+      }
+    }
+    if (lane == 0) {
+      jb.stats[0] = jb.stats[1] = jb.stats[2] = 0;
+      set_err(jb.err, kOk, E_NONE, 0, 0);
+    }
+    return;
+  }
+  if (lane == 0) {
+    // schedule estimate (placers.cpp:350-362), sequential comm: the queue
+    // tails make it a fold in topo order; every device_of is set before it
     for (int x = 0; x < V; ++x) {
       int j = order[x];
       int p = jb.device_of[j];

@@ -38,6 +38,13 @@ def cases():
         g = mk()
         gg = bx.MetaGraph.from_dict(W.as_meta_dict(g))
         yield name, gg, bx.Job(0, "m-etf", np.full(n, W.bench_capacity(g, n, 1.2), np.int64), cm)
+    cms = bx.CommModel(5.0, 0.001, 0)  # sequential comm (the survey probe's model)
+    for name, mk, n in (("seq_layered100k_x8", lambda: W.layered_dag_fast(100, 1000, 3), 8),
+                        ("seq_wide100k_x16", lambda: W.wide_random(100000, 5), 16),
+                        ("seq_layered20k_x8", lambda: W.layered_dag_fast(20, 1000, 3), 8)):
+        g = mk()
+        gg = bx.MetaGraph.from_dict(W.as_meta_dict(g))
+        yield name, gg, bx.Job(0, "m-etf", np.full(n, W.bench_capacity(g, n, 1.2), np.int64), cms)
 
 
 def main():

@@ -23,7 +23,12 @@ CASES = {
     "wide100k_x16": (lambda: W.wide_random(100000, 5), 16, "m-etf", 1.2),
     "layered100k_x4_sct": (lambda: W.layered_dag_fast(100, 1000, 3), 4, "m-sct", 1.2),
     "c4_layered1M_x64": (lambda: W.layered_dag_fast(1000, 1000, 1), 64, "m-etf", 1.5),
+    # sequential comm mode (queues on both endpoints), the survey probe's model {5 us, 0.001 us/B}
+    "seq_layered100k_x4": (lambda: W.layered_dag_fast(100, 1000, 3), 4, "m-etf", 1.2),
+    "seq_layered100k_x8": (lambda: W.layered_dag_fast(100, 1000, 3), 8, "m-etf", 1.2),
+    "seq_wide100k_x16": (lambda: W.wide_random(100000, 5), 16, "m-etf", 1.2),
 }
+COMM_SEQ = (5.0, 0.001, 0)
 
 
 def run_config(name, cpu=True, reps=3):
@@ -80,7 +85,8 @@ def run(name, cpu=True, reps=3):
     g = mk()
     m = W.as_meta_dict(g)
     gg = bx.MetaGraph.from_dict(m)
-    cm = bx.CommModel(*W.COMM_TEST)
+    cmt = COMM_SEQ if name.startswith("seq_") else W.COMM_TEST
+    cm = bx.CommModel(*cmt)
     caps = np.full(n, W.bench_capacity(g, n, f), np.int64)
     fav = fav_first(g["esrc"], g["edst"], g["V"]) if algo == "m-sct" else None
     plan = bx.Plan([gg], [bx.Job(0, algo, caps, cm, fav)])
@@ -97,7 +103,7 @@ def run(name, cpu=True, reps=3):
         from oracle import Ref
         rg = Ref.graph(W.as_ref_base(g), -1)
         t0 = time.time()
-        o = Ref.place(rg, 2 if algo == "m-sct" else 1, caps, W.COMM_TEST, fav)
+        o = Ref.place(rg, 2 if algo == "m-sct" else 1, caps, cmt, fav)
         row["cpu_ref_ms"] = o.wall_ns / 1e6
         row["cpu_wall_s"] = round(time.time() - t0, 2)
         row["bit_exact"] = bool(np.array_equal(o.device_of, p.device_of) and np.array_equal(o.start_us, p.start_us)
