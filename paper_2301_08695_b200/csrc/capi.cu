@@ -355,8 +355,8 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     o.nc = L.take<int32_t>(V);
     o.finish = L.take<int64_t>(V);
     o.urgent = L.take<int64_t>(V);
-    o.scv = L.take<int64_t>(32 * n);
-    o.scg = L.take<int32_t>(32 * n);
+    o.scv = L.take<int64_t>(256 * n);  // per lane of up to 8 warps
+    o.scg = L.take<int32_t>(256 * n);
     o.pdev = L.take<int32_t>(graphs[J.graph].E);
     {
       const bool wide_plan = big[i] != 0;
@@ -558,7 +558,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     }
     P->fills.push_back({d.cache, 0xff, 8 * size_t(V * n)});
     P->fills.push_back({d.dead, 0, size_t(V * n)});
-    P->fills.push_back({d.sc_gen, 0, 4 * size_t(32 * n)});
+    P->fills.push_back({d.sc_gen, 0, 4 * size_t(256 * n)});
     P->fills.push_back({d.err, 0, sizeof(DErr)});
   }
   P->dg_dev = at<DGraph>(pool, tables);

@@ -399,7 +399,7 @@ __device__ __forceinline__ void list_insert(const Tops &T, int q, int64_t t, int
 }
 
 // bytes of shared memory per device column per problem
-constexpr int kSmemPerDevice = 5 * 8 + KT * 8 + 2 * 4 + 2 * KT * 4 + 2 * 4;
+constexpr int kSmemPerDevice = 5 * 8 + 2 * KT * 8 + 2 * 4 + 2 * KT * 4 + 3 * 4;
 __host__ __device__ constexpr int stage_bytes_per_device(int w) { return w > 1 ? w * (KT * 16 + 4) : 0; }
 
 #define BX_MARK(slot)                 \
@@ -478,8 +478,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
   c.device_of = jb.device_of;
   c.cseq = jb.cseq;
   c.nc = jb.nc;
-  c.scv = jb.sc_val + static_cast<int64_t>(lane) * jb.n;
-  c.scg = jb.sc_gen + static_cast<int64_t>(lane) * jb.n;
+  c.scv = jb.sc_val + static_cast<int64_t>(threadIdx.x & (32 * kW - 1)) * jb.n;  // per lane of the group
+  c.scg = jb.sc_gen + static_cast<int64_t>(threadIdx.x & (32 * kW - 1)) * jb.n;
   c.pdev = jb.pdev;
   c.pfin = jb.pfin;
   c.inpos = g.inpos;
@@ -487,6 +487,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
   int64_t *stg_t = nullptr;
   int32_t *stg_j = nullptr, *stg_s = nullptr, *stg_live = nullptr;
   int32_t *s_R, *s_done, *s_rq;
+  int64_t *nk;   // [KT*st] sequential mode: re-keyed list entries
+  int32_t *vst;  // [st] sequential mode: commit count + 1 at which the column's list was re-keyed
   {
     const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 16;
     unsigned char *base = smem + static_cast<size_t>(pslot) * per;
@@ -497,7 +499,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     c.awu = c.capS + maxn;
     T.st = maxn;
     T.t = c.awu + maxn;
-    int64_t *p64 = T.t + maxn * KT;
+    nk = T.t + maxn * KT;
+    int64_t *p64 = nk + maxn * KT;
     if (kW > 1) {
       stg_t = p64;
       p64 += static_cast<size_t>(maxn) * kW * KT;
@@ -509,7 +512,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     T.s = T.j + maxn * KT;
     T.cnt = T.s + maxn * KT;
     T.flg = T.cnt + maxn;
-    p32 = T.flg + maxn;
+    vst = T.flg + maxn;
+    p32 = vst + maxn;
     if (kW > 1) {
       stg_j = p32;
       stg_s = stg_j + maxn * kW * KT;
@@ -535,6 +539,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
       c.excl[d] = 0;
       T.cnt[d] = 0;
       T.flg[d] = kDirty;
+      vst[d] = 0;
     }
     // per-node init + initial ready slots (sources), keys 0 (dev_free = 0)
     int R = 0;
@@ -582,6 +587,15 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
       const int qq = rq;
       int64_t dt[KT];
       int dj[KT], ds[KT], cnt, live;
+      if (c.mode == 0) {
+        // sequential comm: refresh the column's stored keys to exact ones
+        // for the current queue tails first (every lane of the group keys
+        // its slots with its own scratch), so the rescanned list is exact and
+        // its head commits without a re-key
+        for (int s2 = gw * 32 + lane; s2 < R; s2 += 32 * kW)
+          if (c.Kc[qq * Vs + s2] != kInf) c.Kc[qq * Vs + s2] = key_of(c, c.node_s[s2], qq, gen);
+        group_sync<kW>();
+      }
       warp_topk(c, qq, gw * 32, 32 * kW, R, lane, dt, dj, ds, cnt, live);
       if (kProf) ++prof[P_RESCANS];
       if (lane == 0) {
@@ -594,6 +608,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
           }
           T.cnt[qq] = cnt;
           T.flg[qq] = live <= KT ? kComplete : 0;
+          vst[qq] = c.mode == 0 ? placed + 1 : 0;  // exact keys (refreshed above)
         } else {
 #pragma unroll
           for (int k = 0; k < KT; ++k) {
@@ -642,6 +657,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
         if (lane == 0) {
           T.cnt[qq] = mc;
           T.flg[qq] = lv <= KT ? kComplete : 0;
+          vst[qq] = c.mode == 0 ? placed + 1 : 0;  // exact keys (refreshed above)
         }
       }
       if (lane == 0) *s_rq = -1;
@@ -694,32 +710,77 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     const int sj = T.s[p];
     BX_MARK(P_ARGMIN);
 
-    if (c.mode == 0) {
-      // lazy re-key of the winner (placers.cpp:198-202). Queue tails only
-      // grow, so stored keys are lower bounds; a grown key is re-placed in
-      // column p's list, like the reference's re-push (:199-201) — the list
-      // stays an exact prefix (the entry drops out if it now sorts past an
-      // incomplete list's tail), so no column rescan follows.
-      int64_t fresh = 0;
-      if (lane == 0) fresh = key_of(c, j, p, gen);
-      fresh = __shfl_sync(kFull, fresh, 0);
-      int64_t key = fresh;
-      if (c.sct) {
-        int aw = c.awf[p];
-        if (aw >= 0 && aw != j) key = max64(key, min64(c.awu[p], c.urg_s[sj]));
-      }
-      if (key != t) {
-        if (lane == 0) {
-          c.Kc[p * Vs + sj] = fresh;
-          list_remove(T, p, j);
-          list_insert(T, p, key, j, sj);
+    if (c.mode == 0 && vst[p] != placed + 1) {
+      // lazy re-key (placers.cpp:198-202). Queue tails only grow, so stored
+      // keys are lower bounds and the winner may commit only once its key is
+      // exact for the current tails. Batched: the warp re-keys every listed
+      // entry of every column not yet re-keyed since the last commit (lanes
+      // over (column, entry) items, each with its own scratch tails); then
+      // each column's owner keeps the entries that still sort no later than
+      // the list's old tail (everything unlisted has a stored key past it,
+      // so they stay an exact prefix; the rest drop out with their keys
+      // written back, the reference's re-push) and marks the list re-keyed.
+      const int items = n * KT;
+      for (int it = lane; it < items; it += 32) {
+        const int q = it % n, k = it / n;
+        if (c.excl[q] || (T.flg[q] & kDirty) || vst[q] == placed + 1 || k >= T.cnt[q]) continue;
+        const int x = k * T.st + q;
+        const int hj = T.j[x], hs = T.s[x];
+        const int64_t fresh = key_of(c, hj, q, gen);
+        int64_t key = fresh;
+        if (c.sct) {
+          const int aw = c.awf[q];
+          if (aw >= 0 && aw != hj) key = max64(key, min64(c.awu[q], c.urg_s[hs]));
         }
-        __syncwarp();
-        BX_MARK(P_REKEY);
-        continue;
+        nk[x] = key;
+        c.Kc[q * Vs + hs] = fresh;
       }
+      __syncwarp();
+      for (int q = lane; q < n; q += 32) {
+        if (c.excl[q] || (T.flg[q] & kDirty) || vst[q] == placed + 1) continue;
+        const int cn = T.cnt[q];
+        if (cn == 0) continue;
+        const bool complete = (T.flg[q] & kComplete) != 0;
+        const int64_t ot = T.t[(cn - 1) * T.st + q];
+        const int oj = T.j[(cn - 1) * T.st + q];
+        int64_t et[KT];
+        int ej[KT], es[KT];
+        int kept = 0;
+#pragma unroll
+        for (int k = 0; k < KT; ++k) {
+          if (k >= cn) break;
+          const int x = k * T.st + q;
+          const int64_t t2 = nk[x];
+          const int j2 = T.j[x];
+          if (complete || !lex_less(ot, oj, t2, j2)) {  // (t2, j2) <= old tail
+            int m = kept++;
+            while (m > 0 && lex_less(t2, j2, et[m - 1], ej[m - 1])) {
+              et[m] = et[m - 1];
+              ej[m] = ej[m - 1];
+              es[m] = es[m - 1];
+              --m;
+            }
+            et[m] = t2;
+            ej[m] = j2;
+            es[m] = T.s[x];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < KT; ++k) {
+          if (k >= kept) break;
+          T.t[k * T.st + q] = et[k];
+          T.j[k * T.st + q] = ej[k];
+          T.s[k * T.st + q] = es[k];
+        }
+        T.cnt[q] = kept;
+        if (kept == 0 && !complete) T.flg[q] |= kDirty;
+        else vst[q] = placed + 1;
+      }
+      __syncwarp();
       BX_MARK(P_REKEY);
+      continue;
     }
+    if (c.mode == 0) BX_MARK(P_REKEY);
 
     const int64_t needj = c.need[j];
     if (c.res[p] + needj > c.capS[p]) {
