@@ -322,12 +322,18 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   // A plan of at most 148 list jobs gives every parallel-mode job its own
   // round-kernel CTA (faster per commit at every size measured,
   // profiles/r01c_kr_sweep.txt); sequential-mode jobs go wide from 2^15.
+  // In a many-job sweep parallel-mode jobs all stay on the warp kernel: a
+  // round CTA holds a whole SM's register file, and the sweep ran 14.0k
+  // placements/s with none of them vs 13.2k with the 120 largest
+  // (profiles/r01d_seq_policy.txt).
   const bool few = list_ids.size() <= 148;
   int64_t big_min = few ? (int64_t(1) << 15) : (int64_t(1) << 17);
-  int64_t big_min_par = few ? 0 : big_min;
+  int64_t big_min_par = few ? 0 : INT64_MAX;
   if (const char *e = std::getenv("BX_BIG_MIN")) big_min = big_min_par = std::atoll(e);  // tuning experiments
   std::vector<char> big(njobs, 0);
-  for (size_t r = 0; r < list_ids.size() && r < 120; ++r) {
+  size_t big_max = 120;
+  if (const char *e = std::getenv("BX_BIG_MAX")) big_max = static_cast<size_t>(std::atoll(e));  // tuning experiments
+  for (size_t r = 0; r < list_ids.size() && r < big_max; ++r) {
     const int i = list_ids[r];
     if (vn(i) >= (jobs[i].cm.mode == BX_COMM_SEQUENTIAL ? big_min : big_min_par)) big[i] = 1;
   }

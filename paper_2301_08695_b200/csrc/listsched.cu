@@ -40,6 +40,12 @@
 namespace bx {
 
 constexpr int KT = 4;  // exact top-KT pairs kept per device column
+#ifndef BX_XR_MODE
+// sequential comm, when a rescan keys its column exactly first: 0 never,
+// 1 after a re-key dropped an entry, 2 after one emptied the list, 3 always,
+// 4 always beyond 4 devices (measured, profiles/r01d_seq_policy.txt)
+#define BX_XR_MODE 4
+#endif
 #ifndef BX_SCAN_U
 #define BX_SCAN_U 4  // column-scan loads in flight per lane
 #endif
@@ -399,7 +405,7 @@ __device__ __forceinline__ void list_insert(const Tops &T, int q, int64_t t, int
 }
 
 // bytes of shared memory per device column per problem
-constexpr int kSmemPerDevice = 5 * 8 + 2 * KT * 8 + 2 * 4 + 2 * KT * 4 + 3 * 4;
+constexpr int kSmemPerDevice = 5 * 8 + 2 * KT * 8 + 2 * 4 + 2 * KT * 4 + 4 * 4;
 __host__ __device__ constexpr int stage_bytes_per_device(int w) { return w > 1 ? w * (KT * 16 + 4) : 0; }
 
 #define BX_MARK(slot)                 \
@@ -489,6 +495,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
   int32_t *s_R, *s_done, *s_rq;
   int64_t *nk;   // [KT*st] sequential mode: re-keyed list entries
   int32_t *vst;  // [st] sequential mode: commit count + 1 at which the column's list was re-keyed
+  int32_t *xr;   // [st] sequential mode: the column's stored keys proved stale -> exact rescan
   {
     const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 16;
     unsigned char *base = smem + static_cast<size_t>(pslot) * per;
@@ -513,7 +520,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     T.cnt = T.s + maxn * KT;
     T.flg = T.cnt + maxn;
     vst = T.flg + maxn;
-    p32 = vst + maxn;
+    xr = vst + maxn;
+    p32 = xr + maxn;
     if (kW > 1) {
       stg_j = p32;
       stg_s = stg_j + maxn * kW * KT;
@@ -540,6 +548,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
       T.cnt[d] = 0;
       T.flg[d] = kDirty;
       vst[d] = 0;
+      xr[d] = 0;
     }
     // per-node init + initial ready slots (sources), keys 0 (dev_free = 0)
     int R = 0;
@@ -587,11 +596,12 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
       const int qq = rq;
       int64_t dt[KT];
       int dj[KT], ds[KT], cnt, live;
-      if (c.mode == 0) {
-        // sequential comm: refresh the column's stored keys to exact ones
-        // for the current queue tails first (every lane of the group keys
-        // its slots with its own scratch), so the rescanned list is exact and
-        // its head commits without a re-key
+      const bool exact = c.mode == 0 && (BX_XR_MODE == 3 || (BX_XR_MODE == 4 ? n > 4 : xr[qq] != 0));
+      if (exact) {
+        // sequential comm, a column whose stored keys proved stale: refresh
+        // them to exact keys for the current queue tails first (every lane of
+        // the group keys its slots with its own scratch), so the rescanned
+        // list is exact and its head commits without a re-key
         for (int s2 = gw * 32 + lane; s2 < R; s2 += 32 * kW)
           if (c.Kc[qq * Vs + s2] != kInf) c.Kc[qq * Vs + s2] = key_of(c, c.node_s[s2], qq, gen);
         group_sync<kW>();
@@ -608,7 +618,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
           }
           T.cnt[qq] = cnt;
           T.flg[qq] = live <= KT ? kComplete : 0;
-          vst[qq] = c.mode == 0 ? placed + 1 : 0;  // exact keys (refreshed above)
+          vst[qq] = exact ? placed + 1 : 0;  // exact keys (refreshed above)
+          xr[qq] = 0;
         } else {
 #pragma unroll
           for (int k = 0; k < KT; ++k) {
@@ -657,7 +668,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
         if (lane == 0) {
           T.cnt[qq] = mc;
           T.flg[qq] = lv <= KT ? kComplete : 0;
-          vst[qq] = c.mode == 0 ? placed + 1 : 0;  // exact keys (refreshed above)
+          vst[qq] = exact ? placed + 1 : 0;  // exact keys (refreshed above)
+          xr[qq] = 0;
         }
       }
       if (lane == 0) *s_rq = -1;
@@ -773,6 +785,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
           T.s[k * T.st + q] = es[k];
         }
         T.cnt[q] = kept;
+        // stale lower bounds: the column's next rescan keys it exactly
+        if (BX_XR_MODE == 1 ? kept < cn : BX_XR_MODE == 2 ? kept == 0 : BX_XR_MODE >= 3) xr[q] = 1;
         if (kept == 0 && !complete) T.flg[q] |= kDirty;
         else vst[q] = placed + 1;
       }
@@ -1302,7 +1316,10 @@ __device__ void warp_prefix(const Ctx &c, int q, int s0, int step, int R, int la
 }
 
 template <int KR>
-__global__ void __launch_bounds__(RWARPS * 32, 1)
+#ifndef BX_ROUNDS_MINB
+#define BX_ROUNDS_MINB 1  // resident round CTAs per SM the register budget allows
+#endif
+__global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
     k_place_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                    int maxn) {
   extern __shared__ __align__(16) unsigned char smem[];
