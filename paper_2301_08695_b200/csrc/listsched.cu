@@ -1065,8 +1065,9 @@ static void launch_w(const DJob *jobs, const int32_t *order, int njobs, const DG
 // column), then the whole CTA does the global-memory work of all of them at
 // once: cache arrivals, readiness, new key rows, cached-consumer re-keys, and
 // the rescans of the touched columns.
-// m-SCT commits one pair per round (a lifted reservation may lower keys in
-// another column); discards and exclusions are handled inline by the leader.
+// m-SCT: a lifted awake reservation may lower keys in another column, which
+// then turns dirty and lowers the round's threshold to its F; discards and
+// exclusions are handled inline by the leader.
 // ============================================================================
 constexpr int RWARPS = 8;
 
@@ -1790,13 +1791,19 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
         __syncwarp();
         RMARK(P_CACHE);  // (profile builds) phase S: bookkeeping + list removals
         if (c.sct) {
-          // awake reservations (placers.cpp:235-254); one commit per round
+          // awake reservations (placers.cpp:235-254). A lifted reservation
+          // can lower keys in its column: that column turns dirty and lowers
+          // the threshold to its F (its keys stay >= F), so the round goes
+          // on exactly; a new reservation only touches column q (dirty).
+          // h is j's child, so it cannot have committed earlier this round.
+          int64_t tl = kInf;
           if (lane == 0) {
             c.awf[q] = -1;
             for (int qq = 0; qq < n; ++qq)
               if (c.awf[qq] == e.j) {
                 c.awf[qq] = -1;
                 flg[qq] |= kDirty;
+                if (!c.excl[qq]) tl = min64(tl, c.F[qq]);
               }
             int h = e.fav;
             if (h >= 0 && c.device_of[h] < 0) {
@@ -1805,8 +1812,8 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
               S->awake++;
             }
           }
+          thr = min64(thr, __shfl_sync(kFull, tl, 0));
           __syncwarp();
-          break;
         }
       }
       // only dirty columns that could beat the best clean head get rescanned
