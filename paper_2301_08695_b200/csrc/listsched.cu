@@ -1069,7 +1069,10 @@ static void launch_w(const DJob *jobs, const int32_t *order, int njobs, const DG
 // then turns dirty and lowers the round's threshold to its F; discards and
 // exclusions are handled inline by the leader.
 // ============================================================================
-constexpr int RWARPS = 8;
+#ifndef BX_RWARPS
+#define BX_RWARPS 8
+#endif
+constexpr int RWARPS = BX_RWARPS;  // warps per round-kernel CTA
 
 struct REnt {
   int64_t t, need, k;

@@ -2,12 +2,16 @@
 // solve_relaxed (:124-278) restated in C++17. The interior-point iteration
 // (Mehrotra predictor-corrector on G z <= h, same scaling f = 100/max coef,
 // same strictly feasible start, eta, tolerances and 200-iteration cap) runs on
-// the host; the normal equations (G^T W G + reg I) dz = r are factored and
-// solved on the GPU with cuSOLVER's sparse Cholesky (fill-reducing reorder),
-// the analogue of the reference's Eigen SimplicialLDLT. Eigen3 is absent from
+// the host; the normal equations (G^T W G + reg I) dz = r are factored on the
+// GPU once per iteration and solved for both the predictor and the corrector:
+// dense Cholesky (cuSOLVER potrf/potrs, FP64) up to kDenseMax variables —
+// the w column couples every completion row, so the factor fills in anyway —
+// and cuSOLVER's sparse Cholesky with fill-reducing reorder beyond, the
+// analogues of the reference's Eigen SimplicialLDLT. Eigen3 is absent from
 // the image, so parity with the reference is at the reference tests'
 // tolerance (test_lp.cpp), not bit level.
 #include <cuda_runtime.h>
+#include <cusolverDn.h>
 #include <cusolverSp.h>
 #include <cusparse.h>
 
@@ -158,37 +162,86 @@ Normal normal_pattern(const std::vector<Row> &G, int nvars) {
   return N;
 }
 
+constexpr int kDenseMax = 24576;  // 4.8 GB of FP64 factor at the limit
+
+__global__ void k_scatter_dense(int nnz, const int *rowidx, const int *colind, const double *val, double *A, int m) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += gridDim.x * blockDim.x)
+    A[static_cast<size_t>(colind[i]) * m + rowidx[i]] = val[i];  // column-major; the pattern is symmetric
+}
+
 struct Chol {  // device side of the normal-equation solves
   cusolverSpHandle_t h = nullptr;
+  cusolverDnHandle_t hd = nullptr;
   cusparseMatDescr_t d = nullptr;
-  int *rowptr = nullptr, *colind = nullptr;
-  double *val = nullptr, *b = nullptr, *x = nullptr;
-  int m = 0, nnz = 0, reorder = 3;
+  int *rowptr = nullptr, *colind = nullptr, *rowidx = nullptr, *dinfo = nullptr;
+  double *val = nullptr, *b = nullptr, *x = nullptr, *A = nullptr, *work = nullptr;
+  int m = 0, nnz = 0, reorder = 3, lwork = 0;
+  bool dense = false;
   ~Chol() {
     if (h) cusolverSpDestroy(h);
+    if (hd) cusolverDnDestroy(hd);
     if (d) cusparseDestroyMatDescr(d);
     cudaFree(rowptr);
     cudaFree(colind);
+    cudaFree(rowidx);
+    cudaFree(dinfo);
     cudaFree(val);
     cudaFree(b);
     cudaFree(x);
+    cudaFree(A);
+    cudaFree(work);
   }
   void init(const Normal &N) {
     m = N.m;
     nnz = static_cast<int>(N.colind.size());
-    if (cusolverSpCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw std::runtime_error("cusolverSpCreate failed");
-    cusparseCreateMatDescr(&d);
-    cusparseSetMatType(d, CUSPARSE_MATRIX_TYPE_GENERAL);
-    cusparseSetMatIndexBase(d, CUSPARSE_INDEX_BASE_ZERO);
+    dense = m <= kDenseMax;
     if (cudaMalloc(&rowptr, 4 * size_t(m + 1)) || cudaMalloc(&colind, 4 * size_t(nnz)) ||
         cudaMalloc(&val, 8 * size_t(nnz)) || cudaMalloc(&b, 8 * size_t(m)) || cudaMalloc(&x, 8 * size_t(m)))
       throw std::runtime_error("cudaMalloc failed for the normal equations");
     cudaMemcpy(rowptr, N.rowptr.data(), 4 * size_t(m + 1), cudaMemcpyHostToDevice);
     cudaMemcpy(colind, N.colind.data(), 4 * size_t(nnz), cudaMemcpyHostToDevice);
+    if (dense) {
+      std::vector<int> ri(nnz);
+      for (int r = 0; r < m; ++r)
+        for (int q = N.rowptr[r]; q < N.rowptr[r + 1]; ++q) ri[q] = r;
+      if (cusolverDnCreate(&hd) != CUSOLVER_STATUS_SUCCESS) throw std::runtime_error("cusolverDnCreate failed");
+      if (cudaMalloc(&rowidx, 4 * size_t(nnz)) || cudaMalloc(&A, 8 * size_t(m) * size_t(m)) ||
+          cudaMalloc(&dinfo, sizeof(int)))
+        throw std::runtime_error("cudaMalloc failed for the dense normal equations");
+      cudaMemcpy(rowidx, ri.data(), 4 * size_t(nnz), cudaMemcpyHostToDevice);
+      if (cusolverDnDpotrf_bufferSize(hd, CUBLAS_FILL_MODE_LOWER, m, A, m, &lwork) != CUSOLVER_STATUS_SUCCESS ||
+          cudaMalloc(&work, 8 * size_t(std::max(lwork, 1))))
+        throw std::runtime_error("potrf workspace");
+    } else {
+      if (cusolverSpCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw std::runtime_error("cusolverSpCreate failed");
+      cusparseCreateMatDescr(&d);
+      cusparseSetMatType(d, CUSPARSE_MATRIX_TYPE_GENERAL);
+      cusparseSetMatIndexBase(d, CUSPARSE_INDEX_BASE_ZERO);
+    }
   }
-  void load(const std::vector<double> &v) { cudaMemcpy(val, v.data(), 8 * size_t(nnz), cudaMemcpyHostToDevice); }
+  // new values for this iteration; the dense path factors here, once
+  void load(const std::vector<double> &v) {
+    cudaMemcpy(val, v.data(), 8 * size_t(nnz), cudaMemcpyHostToDevice);
+    if (!dense) return;
+    cudaMemset(A, 0, 8 * size_t(m) * size_t(m));
+    const int blocks = std::min((nnz + 255) / 256, 4096);
+    k_scatter_dense<<<std::max(blocks, 1), 256>>>(nnz, rowidx, colind, val, A, m);
+    int info = 0;
+    if (cusolverDnDpotrf(hd, CUBLAS_FILL_MODE_LOWER, m, A, m, work, lwork, dinfo) != CUSOLVER_STATUS_SUCCESS ||
+        cudaMemcpy(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess || info != 0)
+      throw SolverFail("normal-equation factorization failed");
+  }
   void solve(const std::vector<double> &rhs, std::vector<double> &out) {
     cudaMemcpy(b, rhs.data(), 8 * size_t(m), cudaMemcpyHostToDevice);
+    out.resize(m);
+    if (dense) {
+      int info = 0;
+      if (cusolverDnDpotrs(hd, CUBLAS_FILL_MODE_LOWER, m, 1, A, m, b, m, dinfo) != CUSOLVER_STATUS_SUCCESS ||
+          cudaMemcpy(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess || info != 0)
+        throw SolverFail("normal-equation factorization failed");
+      cudaMemcpy(out.data(), b, 8 * size_t(m), cudaMemcpyDeviceToHost);
+      return;
+    }
     int singular = -1;
     cusolverStatus_t st = cusolverSpDcsrlsvchol(h, m, nnz, d, val, rowptr, colind, b, 1e-14, reorder, x, &singular);
     if (st != CUSOLVER_STATUS_SUCCESS && reorder != 1) {  // older ordering codes only
@@ -196,7 +249,6 @@ struct Chol {  // device side of the normal-equation solves
       st = cusolverSpDcsrlsvchol(h, m, nnz, d, val, rowptr, colind, b, 1e-14, reorder, x, &singular);
     }
     if (st != CUSOLVER_STATUS_SUCCESS || singular >= 0) throw SolverFail("normal-equation factorization failed");
-    out.resize(m);
     cudaMemcpy(out.data(), x, 8 * size_t(m), cudaMemcpyDeviceToHost);
   }
 };

@@ -29,6 +29,21 @@ clk = 1.965e9
 for r in rows[:15]:
     print(f"{r[0]/clk*1e3:8.1f} ms  {r[1]:>16s} V={r[2]:6d} n={r[3]:3d} commits={r[4]} steps/rounds={r[5]}"
           f"  us/commit={r[0]/clk*1e6/max(r[4],1):.2f}")
+# phase breakdown (SM cycles per commit) summed over all jobs, and over the 64 longest
+tot = collections.Counter()
+top = collections.Counter()
+order = sorted(range(len(jobs)), key=lambda i: -plan.profile(i)["total"])
+for rank, i in enumerate(order):
+    pr = plan.profile(i)
+    for k in bx.Plan.PROFILE_FIELDS[:11]:
+        tot[k] += pr[k]
+        if rank < 64:
+            top[k] += pr[k]
+    tot["commits"] += pr["commits"]
+    if rank < 64:
+        top["commits"] += pr["commits"]
+for name, c in (("all jobs", tot), ("64 longest", top)):
+    print(name, {k: round(c[k] / max(c["commits"], 1)) for k in bx.Plan.PROFILE_FIELDS[:11] if c[k]})
 fam = collections.defaultdict(list)
 for r in rows:
     fam[(r[1].rstrip('0123456789x'), r[3])].append(r[0] / clk * 1e3)
