@@ -130,3 +130,67 @@ def test_sim_flow_full_size_vs_event_loop(bx):
         assert [r.transfer_count, r.transfer_bytes, r.duplicate_transfers, r.cache_hits] == [
             o.transfer_count, o.transfer_bytes, o.duplicate_transfers, o.cache_hits]
     plan.close()
+
+
+def test_sim_many_devices_and_tiny_graphs(bx):
+    """Walker warps owning several devices (n = 40 > 32 warps) and degenerate
+    graphs (one node, isolated nodes, empty device FIFOs)."""
+    rng = np.random.default_rng(5)
+    g = W.layered_dag(10, 30, 3)
+    m = W.as_meta_dict(g)
+    gg = bx.MetaGraph.from_dict(m)
+    need = m["perm"] + m["out"] + m["temp"]
+    for trial in range(4):
+        pl = _placement(bx, m, 40, rng, deadlock=trial == 3)
+        tot_d = np.bincount(pl.device_of, weights=need, minlength=40).astype(np.int64)
+        for caps in (tot_d + 1, tot_d // 2 + 1):
+            for mm in (0, 1):
+                _check(bx, m, gg, pl, [int(c) for c in caps], (12.5, 0.002, 1), mm)
+    one = dict(V=1, E=0, k=np.array([7], np.int64), temp=np.array([3], np.int64), perm=np.array([5], np.int64),
+               out=np.array([2], np.int64), esrc=np.zeros(0, np.int32), edst=np.zeros(0, np.int32),
+               ebytes=np.zeros(0, np.int64))
+    iso = dict(V=3, E=0, k=np.array([4, 9, 1], np.int64), temp=np.zeros(3, np.int64), perm=np.ones(3, np.int64),
+               out=np.ones(3, np.int64), esrc=np.zeros(0, np.int32), edst=np.zeros(0, np.int32),
+               ebytes=np.zeros(0, np.int64))
+    for mg, n in ((one, 1), (one, 3), (iso, 2), (iso, 5)):
+        gm = bx.MetaGraph.from_dict(mg)
+        pl = _placement(bx, mg, n, rng)
+        for mm in (0, 1):
+            _check(bx, mg, gm, pl, [100] * n, (12.5, 0.002, 1), mm)
+
+
+def test_sim_batched_plan_vs_restatement(bx):
+    """A many-job plan (> 148 problems: 256-thread walker CTAs, several
+    devices per warp at n = 16) placed and simulated on the device, every
+    report against the C restatement."""
+    graphs = W.sweep_graphs(3, 8, 800, 3000)
+    jobs = [(gi, n, W.bench_capacity(graphs[gi], n, f)) for gi in range(len(graphs)) for n in (2, 5, 16)
+            for f in (1.05, 1.3, 1.6, 2.0, 3.0, 4.0, 5.0)]
+    assert len(jobs) > 148
+    cmt = W.COMM_TEST
+    mgs = [bx.MetaGraph.from_dict(W.as_meta_dict(g)) for g in graphs]
+    plan = bx.Plan(mgs, [bx.Job(gi, "m-etf", np.full(n, cap, np.int64), bx.CommModel(*cmt)) for gi, n, cap in jobs])
+    plan.upload()
+    plan.place()
+    plan.download()
+    for mm in (0, 1):
+        plan.simulate(mm)
+        reps = plan.sim_download()
+        for i, (gi, n, cap) in enumerate(jobs):
+            st, _ = plan.status(i)
+            if st:
+                continue
+            p = plan.result(i)
+            m = W.as_meta_dict(graphs[gi])
+            try:
+                o = Restate.simulate(m, [cap] * n, cmt, mm, p.device_of, p.exec_order_flat, p.exec_off)
+            except OracleError as e:
+                assert reps[i] == (e.kind, e.msg), i
+                continue
+            r = reps[i]
+            assert not isinstance(r, tuple), (i, r)
+            assert r.makespan_us == o.makespan and np.array_equal(r.start_us, o.start_us), i
+            assert r.peak_bytes.tolist() == o.peak.tolist(), i
+            assert [r.transfer_count, r.transfer_bytes, r.cache_hits] == [o.transfer_count, o.transfer_bytes,
+                                                                          o.cache_hits], i
+    plan.close()
