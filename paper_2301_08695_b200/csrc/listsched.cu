@@ -796,7 +796,23 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     }
     if (c.mode == 0) BX_MARK(P_REKEY);
 
-    const int64_t needj = c.need[j];
+    // the winner's metadata and the last ready slot (swap-removed on a
+    // commit; nothing before the swap writes it in a commit step), all
+    // independent loads issued together
+    const int64_t needj = c.need[j], kj = c.k[j];
+    const int ib = c.in_off[j], ie = c.in_off[j + 1], ob = c.out_off[j], oe = c.out_off[j + 1];
+    const int last = R - 1;
+    int mv = 0;
+    int64_t mv_urg = 0, mv_kc = 0;
+    int32_t mv_alive = 0;
+    if (sj != last) {
+      mv = c.node_s[last];
+      if (lane == 0) {
+        mv_urg = c.urg_s[last];
+        mv_alive = c.alive_s[last];
+      }
+      if (lane < n) mv_kc = c.Kc[lane * Vs + last];
+    }
     if (c.res[p] + needj > c.capS[p]) {
       // discard (placers.cpp:203-219)
       int left = 0;
@@ -855,16 +871,16 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     }
 
     // ---- commit (placers.cpp:221-233) ------------------------------------
-    const int64_t fin = t + c.k[j];
+    const int64_t fin = t + kj;
     int ncount = 0;
     if (c.mode == 1) {
       // commit_schedulable_time, parallel mode: every remote uncached parent
       // tensor lands on p at finish + c_e; order-free, so lanes split parents
-      for (int x0 = c.in_off[j]; x0 < c.in_off[j + 1]; x0 += 32) {
+      for (int x0 = ib; x0 < ie; x0 += 32) {
         int x = x0 + lane;
         bool fresh = false;
         int i = 0;
-        if (x < c.in_off[j + 1]) {
+        if (x < ie) {
           i = c.in_src[x];
           if (c.pdev[x] != p) {
             int64_t *slot = c.cache + static_cast<int64_t>(i) * n + p;
@@ -881,7 +897,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     } else if (lane == 0) {
       // sequential mode: the fold walks parents in ascending order on the
       // live queue tails (placers.cpp:62-69)
-      for (int x = c.in_off[j]; x < c.in_off[j + 1]; ++x) {
+      for (int x = ib; x < ie; ++x) {
         int d = c.pdev[x];
         if (d == p) continue;
         int i = c.in_src[x];
@@ -907,14 +923,13 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
     if (kProf) ++prof[P_COMMITS];
     BX_MARK(P_COMMIT);
     // swap-remove slot sj: the last slot moves in (lists follow its slot)
-    const int last = R - 1;
     if (sj != last) {
-      for (int q = lane; q < n; q += 32) c.Kc[q * Vs + sj] = c.Kc[q * Vs + last];
-      const int mv = c.node_s[last];
+      if (lane < n) c.Kc[lane * Vs + sj] = mv_kc;
+      for (int q = lane + 32; q < n; q += 32) c.Kc[q * Vs + sj] = c.Kc[q * Vs + last];
       if (lane == 0) {
         c.node_s[sj] = mv;
-        c.urg_s[sj] = c.urg_s[last];
-        c.alive_s[sj] = c.alive_s[last];
+        c.urg_s[sj] = mv_urg;
+        c.alive_s[sj] = mv_alive;
         c.rpos[mv] = sj;
       }
       for (int e = lane; e < n * KT; e += 32) {
@@ -955,11 +970,11 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
 
     // ---- readiness (placers.cpp:256-268); publish j to its children's slots
     const int R0 = R;
-    for (int base = c.out_off[j]; base < c.out_off[j + 1]; base += 32) {
+    for (int base = ob; base < oe; base += 32) {
       int y = base + lane;
       bool fresh = false;
       int child = -1;
-      if (y < c.out_off[j + 1]) {
+      if (y < oe) {
         child = c.out_dst[y];
         int x = c.inpos[y];
         c.pdev[x] = p;
