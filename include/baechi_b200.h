@@ -215,8 +215,9 @@ float bx_plan_kernel_ms(bx_plan *plan);
 int bx_plan_profile(bx_plan *plan, int32_t job, int64_t *out16);
 
 /* simulate (simulator.cpp:273-278) of every job's current device-resident
- * placement (K4), in `mem_mode`. Device-resident; use bx_plan_sim_download
- * for the reports. */
+ * placement, in `mem_mode`: K4f (FIFO walkers + max-plus scans) for parallel
+ * comm without zero-duration nodes, K4 (the reference's event heap order)
+ * otherwise. Device-resident; use bx_plan_sim_download for the reports. */
 int bx_plan_simulate(bx_plan *plan, int32_t mem_mode, void *stream);
 int bx_plan_sim_download(bx_plan *plan, void *stream, bx_sim_report *out);
 

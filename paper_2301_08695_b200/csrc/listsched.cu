@@ -46,6 +46,9 @@ constexpr int KT = 4;  // exact top-KT pairs kept per device column
 // 4 always beyond 4 devices (measured, profiles/r01d_seq_policy.txt)
 #define BX_XR_MODE 4
 #endif
+#ifndef BX_LIST_MINB
+#define BX_LIST_MINB 3  // resident 4-problem warp-kernel CTAs per SM (register budget; profiles/r01d_minb.txt)
+#endif
 #ifndef BX_SCAN_U
 #define BX_SCAN_U 4  // column-scan loads in flight per lane
 #endif
@@ -427,7 +430,7 @@ __device__ __forceinline__ void group_sync() {
 // reservations): a third of the code, which matters when ~28 warps per SM
 // run it at unrelated program counters (instruction-fetch stalls).
 template <int kW, bool kProf, bool kEtf = false>
-__global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : 7)
+__global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : BX_LIST_MINB)
     k_place_list(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                  int maxn, int seq_only) {
   extern __shared__ __align__(16) unsigned char smem[];
