@@ -335,7 +335,11 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   if (const char *e = std::getenv("BX_BIG_MAX")) big_max = static_cast<size_t>(std::atoll(e));  // tuning experiments
   for (size_t r = 0; r < list_ids.size() && r < big_max; ++r) {
     const int i = list_ids[r];
-    if (vn(i) >= (jobs[i].cm.mode == BX_COMM_SEQUENTIAL ? big_min : big_min_par)) big[i] = 1;
+    // small m-SCT problems commit one pair at a time more often (lifted
+    // reservations dirty columns), where the lone warp beats the round CTA
+    // (C3: 6.2 vs 7.2 ms); so they go wide only from 2^15 like sequential jobs
+    const bool sct = jobs[i].algo == BX_ALGO_MSCT && jobs[i].fav_child != nullptr;
+    if (vn(i) >= (jobs[i].cm.mode == BX_COMM_SEQUENTIAL || sct ? big_min : big_min_par)) big[i] = 1;
   }
   // job inputs (capacities, favourites) and outputs live in two contiguous
   // regions so an end-to-end step moves them with one copy each way, through

@@ -46,6 +46,9 @@ constexpr int KT = 4;  // exact top-KT pairs kept per device column
 // 4 always beyond 4 devices (measured, profiles/r01d_seq_policy.txt)
 #define BX_XR_MODE 4
 #endif
+#ifndef BX_PPC
+#define BX_PPC 4  // problems (warps) per warp-kernel CTA
+#endif
 #ifndef BX_LIST_MINB
 #define BX_LIST_MINB 3  // resident 4-problem warp-kernel CTAs per SM (register budget; profiles/r01d_minb.txt)
 #endif
@@ -430,7 +433,7 @@ __device__ __forceinline__ void group_sync() {
 // reservations): a third of the code, which matters when ~28 warps per SM
 // run it at unrelated program counters (instruction-fetch stalls).
 template <int kW, bool kProf, bool kEtf = false>
-__global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : BX_LIST_MINB)
+__global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : BX_LIST_MINB)
     k_place_list(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                  int maxn, int seq_only) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -444,7 +447,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 128, kW > 1 ? 1 : BX_LIST_M
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = kW > 1 ? warp : 0;             // warp index inside the problem's group
   const int pslot = kW > 1 ? 0 : warp;          // problem index inside the CTA
-  const int slot_id = kW > 1 ? blockIdx.x : blockIdx.x * 4 + warp;
+  const int slot_id = kW > 1 ? blockIdx.x : blockIdx.x * BX_PPC + warp;
   if (slot_id >= njobs) return;                 // uniform per problem group
   const DJob jb = jobs[order[slot_id]];
   if (jb.skip || jb.algo == 0 || (seq_only && jb.mode == 1)) return;
@@ -1058,13 +1061,21 @@ static void launch_w(const DJob *jobs, const int32_t *order, int njobs, const DG
                      int maxn, int seq_only, cudaStream_t s) {
   if (njobs <= 0) return;
   const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 16;
-  const int probs_per_cta = kW > 1 ? 1 : 4;
-  const int threads = kW > 1 ? 32 * kW : 128;
+  const int probs_per_cta = kW > 1 ? 1 : BX_PPC;
+  const int threads = kW > 1 ? 32 * kW : 32 * BX_PPC;
   const int blocks = (njobs + probs_per_cta - 1) / probs_per_cta;
   const size_t sm = per * probs_per_cta;
   if (sm > 48 * 1024)
     cudaFuncSetAttribute(k_place_list<kW, kProf, kEtf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sm));
+  // the rest of the unified L1/shared array goes to L1: just enough shared
+  // memory for the resident CTAs (+3% sweep throughput, profiles/r01d_minb.txt)
+  if (kW == 1) {
+    int pct = static_cast<int>((100 * size_t(BX_LIST_MINB) * (sm + 1024) + 228 * 1024 - 1) / (228 * 1024)) + 5;
+    if (const char *e = std::getenv("BX_CARVEOUT")) pct = std::atoi(e);  // tuning experiments
+    cudaFuncSetAttribute(k_place_list<kW, kProf, kEtf>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         pct < 100 ? pct : 100);
+  }
   k_place_list<kW, kProf, kEtf><<<blocks, threads, sm, s>>>(jobs, order, njobs, graphs, preps, maxn, seq_only);
 }
 
