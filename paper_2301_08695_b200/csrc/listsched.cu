@@ -53,7 +53,10 @@ constexpr int KT = 4;  // exact top-KT pairs kept per device column
 #define BX_LIST_MINB 3  // resident 4-problem warp-kernel CTAs per SM (register budget; profiles/r01d_minb.txt)
 #endif
 #ifndef BX_SCAN_U
-#define BX_SCAN_U 4  // column-scan loads in flight per lane
+#define BX_SCAN_U 4  // column-scan loads in flight per lane, warp kernel
+#endif
+#ifndef BX_SCAN_U_ROUNDS
+#define BX_SCAN_U_ROUNDS 8  // ... round kernel (profiles/r01e_scan_u.txt)
 #endif
 
 struct Tops {      // entry k of column q at k * st + q (no bank conflicts for lane-owned columns)
@@ -271,6 +274,7 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
 }
 
 // per-lane exact top-4 of this warp's share (slots s0 + lane + k*step < R)
+template <int U>
 __device__ __forceinline__ void lane_top4(const Ctx &c, int q, int s0, int step, int R, int lane, Lane4 &L) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -283,7 +287,7 @@ __device__ __forceinline__ void lane_top4(const Ctx &c, int q, int s0, int step,
   const int64_t Fq = c.F[q];
   const int aw = c.sct ? c.awf[q] : -1;
   const int64_t awu = aw >= 0 ? c.awu[q] : 0;
-  constexpr int U = BX_SCAN_U;
+
   for (int base = s0 + lane; base < R; base += U * step) {
     int64_t kv[U];
     int nd[U];
@@ -341,7 +345,7 @@ __device__ void warp_topk(const Ctx &c, int q, int s0, int step, int R, int lane
                           int (&dj)[KT], int (&ds)[KT], int &cnt, int &live) {
   static_assert(KT == 4, "lane lists hold 4");
   Lane4 L;
-  lane_top4(c, q, s0, step, R, lane, L);
+  lane_top4<BX_SCAN_U>(c, q, s0, step, R, lane, L);
   if (__any_sync(kFull, L.clip)) {
     warp_topk_exact(col_view(c, q), s0, step, R, lane, dt, dj, ds, cnt, live);
     return;
@@ -1314,7 +1318,7 @@ template <int KR>
 __device__ void warp_prefix(const Ctx &c, int q, int s0, int step, int R, int lane, int64_t *out_t, int32_t *out_j,
                             int32_t *out_s, int &cnt, int64_t &thr_t, unsigned &thr_j, int &live) {
   Lane4 L;
-  lane_top4(c, q, s0, step, R, lane, L);
+  lane_top4<BX_SCAN_U_ROUNDS>(c, q, s0, step, R, lane, L);
   if (__any_sync(kFull, L.clip)) {
     warp_prefix_exact<KR>(col_view(c, q), s0, step, R, lane, out_t, out_j, out_s, cnt, thr_t, thr_j, live);
     return;
@@ -2039,7 +2043,8 @@ void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGra
   int kr = maxn <= 8 ? 4 : maxn < 32 ? 8 : 16;
   if (const char *e = std::getenv("BX_KR")) kr = std::atoi(e);  // tuning experiments
   while (kr > 4 && rounds_smem(maxn, kr) > 200 * 1024) kr /= 2;
-  if (kr >= 16) launch_rounds_kr<16>(jobs, order, njobs, graphs, preps, maxn, s);
+  if (kr >= 32) launch_rounds_kr<32>(jobs, order, njobs, graphs, preps, maxn, s);
+  else if (kr >= 16) launch_rounds_kr<16>(jobs, order, njobs, graphs, preps, maxn, s);
   else if (kr >= 8) launch_rounds_kr<8>(jobs, order, njobs, graphs, preps, maxn, s);
   else launch_rounds_kr<4>(jobs, order, njobs, graphs, preps, maxn, s);
 }
