@@ -2036,11 +2036,12 @@ static void launch_rounds_kr(const DJob *jobs, const int32_t *order, int njobs, 
 // nodes, so with many devices short lists drain together and every column
 // needs a rescan every few commits; with few devices each commit rescans just
 // its own column and longer lists only cost more per rescan and per edit
-// (measured, profiles/r01c_kr_sweep.txt): 4 up to 8 devices, 8 up to 31, 16.
+// (measured, profiles/r01c_kr_sweep.txt, r01e_scan_u.txt): 4 up to 8
+// devices, 8 up to 31, 16 up to 47, 32 (100k x 64: 1.27 -> 1.07 s vs 16).
 void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                    int maxn, bool prof, cudaStream_t s) {
   (void)prof;
-  int kr = maxn <= 8 ? 4 : maxn < 32 ? 8 : 16;
+  int kr = maxn <= 8 ? 4 : maxn < 32 ? 8 : maxn < 48 ? 16 : 32;
   if (const char *e = std::getenv("BX_KR")) kr = std::atoi(e);  // tuning experiments
   while (kr > 4 && rounds_smem(maxn, kr) > 200 * 1024) kr /= 2;
   if (kr >= 32) launch_rounds_kr<32>(jobs, order, njobs, graphs, preps, maxn, s);

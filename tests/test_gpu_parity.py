@@ -173,7 +173,7 @@ def test_cuda_vs_oracle_seeded(bx, seed, g):
                         _assert_same(p, o, stats=algo != 0)
 
 
-@pytest.mark.parametrize("kr", ["4", "8", "16"])
+@pytest.mark.parametrize("kr", ["4", "8", "16", "32"])
 def test_cuda_vs_oracle_cta_kernels(bx, kr, monkeypatch):
     """The CTA-wide kernels (round kernel for parallel comm, 8-warp list
     kernel for sequential) forced onto small seeded problems, every list
