@@ -1013,9 +1013,11 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
     for (int a = 0; a < ncount; ++a) {
       int i = c.nc[a];
       for (int y = c.out_off[i] + lane; y < c.out_off[i + 1]; y += 32) {
-        int cc = c.out_dst[y];
-        if (cc == j || c.pending[cc] != 0 || c.device_of[cc] >= 0) continue;
-        int s = c.rpos[cc];
+        const int cc = c.out_dst[y];
+        // the three node loads issue together (no short-circuit chain);
+        // rpos is only trusted once the node is known ready and unplaced
+        const int pend = c.pending[cc], dv = c.device_of[cc], s = c.rpos[cc];
+        if (cc == j || pend != 0 || dv >= 0) continue;
         if (s >= R0) continue;  // new rows were keyed after the cache update
         if (c.Kc[p * Vs + s] == kInf) continue;
         c.Kc[p * Vs + s] = key_of(c, cc, p, gen);
@@ -1979,8 +1981,8 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
         const int q = CM[jb.ncw[a]].q;
         for (int y = g.out_off[par] + lane; y < g.out_off[par + 1]; y += 32) {
           const int cc = c.out_dst[y];
-          if (c.pending[cc] != 0 || c.device_of[cc] >= 0) continue;
-          const int s = c.rpos[cc];
+          const int pend = c.pending[cc], dv = c.device_of[cc], s = c.rpos[cc];  // issued together
+          if (pend != 0 || dv >= 0) continue;
           if (s >= R0) continue;  // new rows were keyed after the cache update
           if (c.Kc[q * Vs + s] == kInf) continue;
           c.Kc[q * Vs + s] = key_of(c, cc, q, gen);
