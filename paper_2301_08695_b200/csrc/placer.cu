@@ -78,14 +78,16 @@ __global__ void k_prep_nodes(DGraph g) {
 // so a level-synchronous peel finds the same residue. One CTA per graph;
 // the frontier ping-pongs through `queue` (2*V ints of scratch).
 __global__ void k_kahn(DGraph *graphs, int32_t *const *queues) {
+  // level-synchronous peel, one barrier per level: level L reads queue buffer
+  // L%2 with count s_n[L%3], appends to buffer (L+1)%2 / s_n[(L+1)%3], and
+  // clears s_n[(L+2)%3] (last read at level L-1, next written at level L+1)
   DGraph g = graphs[blockIdx.x];
   int32_t *q = queues[blockIdx.x];
-  __shared__ int s_n[2];
+  __shared__ int s_n[3];
   __shared__ int s_total;
-  int V = g.V;
+  const int V = g.V;
   if (threadIdx.x == 0) {
-    s_n[0] = 0;
-    s_n[1] = 0;
+    s_n[0] = s_n[1] = s_n[2] = 0;
     s_total = 0;
   }
   __syncthreads();
@@ -93,23 +95,23 @@ __global__ void k_kahn(DGraph *graphs, int32_t *const *queues) {
     if (g.indeg_left[j] == 0) q[atomicAdd(&s_n[0], 1)] = j;
   }
   __syncthreads();
-  int cur = 0;
-  while (true) {
-    int cnt = s_n[cur];
+  for (int L = 0;; ++L) {
+    const int cnt = s_n[L % 3];
     if (cnt == 0) break;
-    int32_t *in = q + (cur ? V : 0);
-    int32_t *out = q + (cur ? 0 : V);
-    if (threadIdx.x == 0) s_total += cnt;
+    const int32_t *in = q + ((L & 1) ? V : 0);
+    int32_t *out = q + ((L & 1) ? 0 : V);
+    int *next = &s_n[(L + 1) % 3];
+    if (threadIdx.x == 0) {
+      s_total += cnt;
+      s_n[(L + 2) % 3] = 0;
+    }
     for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
-      int u = in[x];
+      const int u = in[x];
       for (int y = g.out_off[u]; y < g.out_off[u + 1]; ++y) {
-        int v = g.edst[y];
-        if (atomicSub(&g.indeg_left[v], 1) == 1) out[atomicAdd(&s_n[cur ^ 1], 1)] = v;
+        const int v = g.edst[y];
+        if (atomicSub(&g.indeg_left[v], 1) == 1) out[atomicAdd(next, 1)] = v;
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) s_n[cur] = 0;
-    cur ^= 1;
     __syncthreads();
   }
   if (threadIdx.x == 0) g.flags[0] = s_total;
