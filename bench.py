@@ -366,6 +366,18 @@ def main():
             pg = per_graph(bx, W, cpu=not args.no_cpu_baseline)
         except Exception as e:
             pg = {"error": str(e)}
+        # BASELINE configs C1-C3 (single model-shaped graphs): GPU placer
+        # kernels (device-resident, best of 3) next to the reference placer on
+        # one core, same meta graph, bit-exact flag
+        try:
+            sys.path.insert(0, os.path.join(HERE, "tools"))
+            from latency_table import run_config
+            pg["configs"] = [
+                {k: r.get(k) for k in ("case", "algo", "meta_V", "n", "gpu_kernel_ms", "cpu_ref_ms", "bit_exact",
+                                       "speedup")}
+                for name in W.CONFIGS for r in run_config(name, cpu=not args.no_cpu_baseline)]
+        except Exception as e:
+            pg["configs"] = {"error": str(e)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
