@@ -225,23 +225,34 @@ __global__ void __launch_bounds__(32 * kWarps) k_place_topo(const DJob *jobs, in
     }
     __syncwarp();
   }
-  if (lane == 0) {
-    // balanced fill; the last device absorbs the rest (placers.cpp:337-347)
+  {
+    // balanced fill; the last device absorbs the rest (placers.cpp:337-347).
+    // The greedy is sequential, but its inputs are not: the warp loads 32
+    // nodes' needs at once and every lane replays the same greedy over them
+    // from registers, keeping the device of its own node.
     int dev = 0;
     int64_t used = 0;
-    jb.exec_off[0] = 0;
-    for (int x = 0; x < V; ++x) {
-      int j = order[x];
-      int64_t b = g.need[j];
-      if (used + b > cap && dev + 1 < n) {
-        jb.exec_off[dev + 1] = x;
-        ++dev;
-        used = 0;
+    if (lane == 0) jb.exec_off[0] = 0;
+    for (int base = 0; base < V; base += 32) {
+      const int x = base + lane;
+      const int j = x < V ? order[x] : 0;
+      const int64_t b = x < V ? g.need[j] : 0;
+      const int cntb = V - base < 32 ? V - base : 32;
+      int mine = 0;
+      for (int l = 0; l < cntb; ++l) {
+        const int64_t bl = __shfl_sync(kFull, b, l);
+        if (used + bl > cap && dev + 1 < n) {
+          if (lane == 0) jb.exec_off[dev + 1] = base + l;
+          ++dev;
+          used = 0;
+        }
+        if (l == lane) mine = dev;
+        used += bl;
       }
-      jb.device_of[j] = dev;
-      used += b;
+      if (x < V) jb.device_of[j] = mine;
     }
-    for (int d = dev + 1; d <= n; ++d) jb.exec_off[d] = V;
+    if (lane == 0)
+      for (int d = dev + 1; d <= n; ++d) jb.exec_off[d] = V;
   }
   __syncwarp();
   if (c.mode == 1) {
