@@ -14,9 +14,11 @@ from oracle import Ref  # noqa: E402
 from paper_2301_08695_b200 import workloads as W  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+seq = len(sys.argv) > 2 and sys.argv[2] == "seq"  # sequential comm: the event-loop kernel (K4)
 g = W.layered_dag_fast(100, 1000, 3)
 gg = bx.MetaGraph.from_dict(W.as_meta_dict(g))
-cm = bx.CommModel(*W.COMM_TEST)
+COMM = (5.0, 0.001, 0) if seq else W.COMM_TEST
+cm = bx.CommModel(*COMM)
 caps = np.full(n, W.bench_capacity(g, n, 1.2), np.int64)
 plan = bx.Plan([gg], [bx.Job(0, "m-etf", caps, cm)])
 plan.upload()
@@ -38,8 +40,8 @@ for mm in (1, 0):
         dev.append(e0.elapsed_time(e1))
     r = reps[0]
     rg = Ref.graph(W.as_ref_base(g), -1)
-    o = Ref.simulate(rg, caps, W.COMM_TEST, mm, p.device_of, p.exec_order_flat, p.exec_off)
-    print(json.dumps({"n": n, "mem_mode": mm, "gpu_sim_device_ms": min(dev[1:]), "gpu_sim_wall_ms": min(wall[1:]),
+    o = Ref.simulate(rg, caps, COMM, mm, p.device_of, p.exec_order_flat, p.exec_off)
+    print(json.dumps({"n": n, "comm": "sequential" if seq else "parallel", "mem_mode": mm, "gpu_sim_device_ms": min(dev[1:]), "gpu_sim_wall_ms": min(wall[1:]),
                       "cpu_ref_sim_ms": o.wall_ns / 1e6,
                       "same": bool(o.makespan == r.makespan_us and np.array_equal(o.start_us, r.start_us)
                                    and o.peak.tolist() == r.peak_bytes.tolist())}), flush=True)
