@@ -8,6 +8,8 @@
 // 128-bit compare orders them. Lane 0 owns the heap; the whole warp scans
 // in/out-edge lists (inputs_resident, the per-destination max-bytes map)
 // and the per-device tables.
+#include <cstdlib>
+
 #include "bx_device.cuh"
 
 namespace bx {
@@ -21,9 +23,14 @@ __device__ __forceinline__ int64_t pack_ev(int kind, int a, int b) {
   return (static_cast<int64_t>(kind) << 58) | (static_cast<int64_t>(a) << 20) | static_cast<int64_t>(b);
 }
 
+// The event heap starts in the warp's shared-memory slice (the live event
+// set is small: running nodes, transfers in flight, queued starts) and moves
+// to its global-memory arrays the first time it outgrows the slice.
 struct Heap {
   int64_t *t, *k;
-  int64_t size;
+  int64_t size, cap;
+  int64_t *gt, *gk;  // global arrays (capacity 2n + E + 16, never outgrown)
+  bool spilled;
   __device__ bool less(int64_t x, int64_t y) const { return t[x] < t[y] || (t[x] == t[y] && k[x] < k[y]); }
   __device__ void swap(int64_t x, int64_t y) {
     int64_t a = t[x], b = k[x];
@@ -33,6 +40,15 @@ struct Heap {
     k[y] = b;
   }
   __device__ void push(int64_t tt, int64_t kk) {
+    if (size == cap && !spilled) {
+      for (int64_t x = 0; x < size; ++x) {
+        gt[x] = t[x];
+        gk[x] = k[x];
+      }
+      t = gt;
+      k = gk;
+      spilled = true;
+    }
     int64_t i = size++;
     t[i] = tt;
     k[i] = kk;
@@ -118,7 +134,8 @@ __device__ bool charge(SimCtx &c, int dev, int64_t delta, int64_t t, int meta) {
 }
 
 template <int kWarps>
-__global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int nsims, const DGraph *graphs) {
+__global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int nsims, const DGraph *graphs,
+                                                         int sim_heap_cap) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sid = blockIdx.x * kWarps + warp;
   if (sid >= nsims) return;
@@ -131,9 +148,24 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
   // parallel comm mode without zero-duration nodes belongs to K4f (its first
   // prep pass flags zero durations)
   if (c.s.mode == 1 && !c.s.flow8[0]) return;
-  c.h.t = c.s.heap_t;
-  c.h.k = c.s.heap_k;
-  c.h.size = 0;
+  {
+    extern __shared__ int64_t sim_heap_smem[];
+    const int64_t scap = static_cast<int64_t>(sim_heap_cap);
+    c.h.gt = c.s.heap_t;
+    c.h.gk = c.s.heap_k;
+    c.h.size = 0;
+    if (scap > 0) {
+      c.h.t = sim_heap_smem + static_cast<int64_t>(warp) * 2 * scap;
+      c.h.k = c.h.t + scap;
+      c.h.cap = scap;
+      c.h.spilled = false;
+    } else {
+      c.h.t = c.h.gt;
+      c.h.k = c.h.gk;
+      c.h.cap = INT64_MAX;
+      c.h.spilled = true;
+    }
+  }
   const int V = c.V, n = c.n;
   DErr *err = c.s.err;
 
@@ -888,8 +920,22 @@ void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn
     }
   };
   grid(k_sim_prep_a, gx, 256);
-  constexpr int W = 4;
-  k_simulate<W><<<(nsims + W - 1) / W, 32 * W, 0, s>>>(sims, nsims, graphs);
+  int force_cap = -1;  // tests: a tiny shared-memory heap exercises the spill to global memory
+  if (const char *e = std::getenv("BX_SIM_HEAP_CAP")) force_cap = std::atoi(e);
+  if (force_cap >= 0) {
+    const size_t sm = 2 * sizeof(int64_t) * static_cast<size_t>(force_cap > 0 ? force_cap : 1);
+    k_simulate<1><<<nsims, 32, sm, s>>>(sims, nsims, graphs, force_cap);
+  } else if (nsims <= 148) {  // a few problems: one per CTA, a 12k-event shared-memory heap each
+    constexpr int kCap = 12288;
+    const size_t sm = 2 * sizeof(int64_t) * kCap;
+    cudaFuncSetAttribute(k_simulate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    k_simulate<1><<<nsims, 32, sm, s>>>(sims, nsims, graphs, kCap);
+  } else {
+    constexpr int W = 4, kCap = 1024;
+    const size_t sm = 2 * sizeof(int64_t) * kCap * W;
+    cudaFuncSetAttribute(k_simulate<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    k_simulate<W><<<(nsims + W - 1) / W, 32 * W, sm, s>>>(sims, nsims, graphs, kCap);
+  }
   grid(k_sim_prep_b, gx, 256);
   grid(k_sim_prep_c, gx, 256);
   const int cta = nsims <= 148 ? 1024 : 256;

@@ -194,3 +194,26 @@ def test_sim_batched_plan_vs_restatement(bx):
             assert [r.transfer_count, r.transfer_bytes, r.cache_hits] == [o.transfer_count, o.transfer_bytes,
                                                                           o.cache_hits], i
     plan.close()
+
+
+@pytest.mark.parametrize("cap", ["0", "3"])
+def test_event_heap_spill(bx, monkeypatch, cap):
+    """The event-loop kernel's heap starting in a 3-entry shared-memory slice
+    (spills to global memory at once) or in global memory outright: same
+    reports and errors, sequential comm and zero-duration nodes."""
+    monkeypatch.setenv("BX_SIM_HEAP_CAP", cap)
+    rng = np.random.default_rng(9)
+    for g in (W.layered_dag(6, 10, 1), W.branchy(5, 2)):
+        m = W.as_meta_dict(g)
+        k = m["k"].copy()
+        k[rng.random(len(k)) < 0.3] = 0
+        for mg in (m, dict(m, k=k)):
+            gg = bx.MetaGraph.from_dict(mg)
+            need = mg["perm"] + mg["out"] + mg["temp"]
+            for n in (2, 5):
+                pl = _placement(bx, mg, n, rng)
+                tot_d = np.bincount(pl.device_of, weights=need, minlength=n).astype(np.int64)
+                for caps in (tot_d + 1, tot_d // 3 + 1):
+                    for cm in ((5.0, 0.001, 0), (12.5, 0.002, 1)):
+                        for mm in (0, 1):
+                            _check(bx, mg, gg, pl, [int(c) for c in caps], cm, mm)
