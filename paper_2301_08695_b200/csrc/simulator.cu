@@ -268,15 +268,20 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
         c.s.qpos[dev]++;
         c.s.finished[j] = 1;
         c.s.mem[dev] -= c.g.temp[j];
-        if (c.s.mem_mode == 0) {
-          if (c.s.consumers_left[j] == 0) c.s.mem[dev] -= c.g.outb[j];
-          for (int x = c.g.in_off[j]; x < c.g.in_off[j + 1]; ++x) {
-            int i = c.g.esrc[c.g.in_edge[x]];
-            if (--c.s.consumers_left[i] == 0) c.s.mem[c.s.device_of[i]] -= c.g.outb[i];
-          }
-        }
+        if (c.s.mem_mode == 0 && c.s.consumers_left[j] == 0) c.s.mem[dev] -= c.g.outb[j];
       }
       __syncwarp();
+      if (c.s.mem_mode == 0) {
+        // parents whose last consumer this was free their outputs; only
+        // decrements, checked at starts, so the lanes may take them in any order
+        for (int x = c.g.in_off[j] + lane; x < c.g.in_off[j + 1]; x += 32) {
+          const int i = c.g.esrc[c.g.in_edge[x]];
+          if (atomicSub(&c.s.consumers_left[i], 1) == 1)
+            atomicAdd(reinterpret_cast<unsigned long long *>(&c.s.mem[c.s.device_of[i]]),
+                      static_cast<unsigned long long>(-c.g.outb[i]));
+        }
+        __syncwarp();
+      }
       // destinations: max bytes per remote consumer device
       int remote = 0;
       for (int y = c.g.out_off[j] + lane; y < c.g.out_off[j + 1]; y += 32) {
