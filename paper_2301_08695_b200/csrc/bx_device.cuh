@@ -144,6 +144,7 @@ struct DSim {
   int64_t *rp_c;                    // [E] its arrival delay
   int64_t *kx;                      // [V] compute time by FIFO slot (-1: never ready)
   int64_t *dv;                      // [4n] per device: peak, violation t, node, memory
+  int32_t *ninp;                    // [V] K4: inputs of a node not yet resident on its device
   // outputs
   int64_t *start;                   // [V]
   int64_t *dev3n;                   // [3n] peak, busy, idle

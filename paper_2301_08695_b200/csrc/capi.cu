@@ -820,7 +820,7 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
   Layout L;
   struct SOff {
     size_t mem, peak, xfree, qpos, busy, cl, fin, sq, res, sent, ht, hk, seen, db, dc, start, dev3n, xfer4, mk, err;
-    size_t pos, psrc, cx, ffin, sx, bucket, mb, first, flow8, rcnt, rp_off, rp_src, rp_c, kx, dv;
+    size_t pos, psrc, cx, ffin, sx, bucket, mb, first, flow8, rcnt, rp_off, rp_src, rp_c, kx, dv, ninp;
   };
   std::vector<SOff> so(P->njobs);
   for (int i = 0; i < P->njobs; ++i) {
@@ -862,6 +862,7 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
     o.rp_c = L.take<int64_t>(E);
     o.kx = L.take<int64_t>(V);
     o.dv = L.take<int64_t>(4 * n);
+    o.ninp = L.take<int32_t>(V);
   }
   size_t tab = L.take<DSim>(P->njobs);
   BX_CUDA(cudaMalloc(&P->sim_pool, L.off), msg, msglen);
@@ -919,6 +920,7 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
     d.rp_c = at<int64_t>(pool, o.rp_c);
     d.kx = at<int64_t>(pool, o.kx);
     d.dv = at<int64_t>(pool, o.dv);
+    d.ninp = at<int32_t>(pool, o.ninp);
     P->sim_fills.push_back({d.flow8, 0, 64});
     P->sim_fills.push_back({d.resident, 0, size_t(V * n)});
     P->sim_fills.push_back({d.sent, 0, size_t(V * n)});

@@ -85,7 +85,19 @@ struct SimCtx {
   int lane;
 };
 
-// inputs_resident (simulator.cpp:100-111), warp-cooperative.
+// inputs_resident (simulator.cpp:100-111) as a counter: ninp[j] starts at
+// j's in-edge count and drops when a same-device parent finishes or a
+// parent's tensor lands on j's device (each (parent, device) transfer is sent
+// exactly once), so the test at try_start is one load instead of a scan.
+__device__ __forceinline__ void inputs_landed(const SimCtx &c, int i, int dev) {
+  for (int y = c.g.out_off[i] + c.lane; y < c.g.out_off[i + 1]; y += 32) {
+    const int ch = c.g.edst[y];
+    if (c.s.device_of[ch] == dev) atomicSub(&c.s.ninp[ch], 1);
+  }
+  __syncwarp();
+}
+
+// inputs_resident (simulator.cpp:100-111), warp-cooperative scan (reference form).
 __device__ bool inputs_resident(const SimCtx &c, int j) {
   int dev = c.s.device_of[j];
   bool ok = true;
@@ -105,7 +117,7 @@ __device__ void try_start(SimCtx &c, int dev, int64_t now) {
   if (q >= len) return;
   int j = c.s.exec_order[c.s.exec_off[dev] + q];
   if (c.s.start_q[j]) return;
-  if (!inputs_resident(c, j)) return;
+  if (c.s.ninp[j] != 0) return;
   __syncwarp();
   if (c.lane == 0) {
     c.s.start_q[j] = 1;
@@ -213,6 +225,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
   }
   for (int j = lane; j < V; j += 32) {
     c.s.consumers_left[j] = c.g.out_off[j + 1] - c.g.out_off[j];
+    c.s.ninp[j] = c.g.in_off[j + 1] - c.g.in_off[j];
     c.s.finished[j] = 0;
     c.s.start_q[j] = 0;
     c.s.start[j] = 0;
@@ -325,11 +338,13 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
       hits += remote - distinct;
       c.h.size = __shfl_sync(kFullS, c.h.size, 0);
       __syncwarp();
+      inputs_landed(c, j, dev);  // same-device consumers now hold j's output
       try_start(c, dev, t);
     } else {
       // run_xfer_done (:186-190)
       if (lane == 0) c.s.resident[static_cast<int64_t>(a) * n + b] = 1;
       __syncwarp();
+      inputs_landed(c, a, b);
       try_start(c, b, t);
     }
   }
