@@ -8,6 +8,7 @@
 // 128-bit compare orders them. Lane 0 owns the heap; the whole warp scans
 // in/out-edge lists (inputs_resident, the per-destination max-bytes map)
 // and the per-device tables.
+#include <algorithm>
 #include <cstdlib>
 
 #include "bx_device.cuh"
@@ -147,7 +148,7 @@ __device__ bool charge(SimCtx &c, int dev, int64_t delta, int64_t t, int meta) {
 
 template <int kWarps>
 __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int nsims, const DGraph *graphs,
-                                                         int sim_heap_cap) {
+                                                         int sim_heap_cap, int dev_slots) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sid = blockIdx.x * kWarps + warp;
   if (sid >= nsims) return;
@@ -163,6 +164,19 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
   {
     extern __shared__ int64_t sim_heap_smem[];
     const int64_t scap = static_cast<int64_t>(sim_heap_cap);
+    // per-device state in this warp's shared-memory slice (after all heaps)
+    // when the roster fits: every event reads and writes it on lane 0's chain
+    if (dev_slots >= c.n && dev_slots > 0) {
+      int64_t *base = sim_heap_smem + static_cast<int64_t>(kWarps) * 2 * scap +
+                      static_cast<int64_t>(warp) * 6 * dev_slots;
+      c.s.mem = base;
+      c.s.peak = base + dev_slots;
+      c.s.xfree = base + 2 * dev_slots;
+      c.s.dest_bytes = base + 3 * dev_slots;
+      c.s.qpos = reinterpret_cast<int32_t *>(base + 4 * dev_slots);
+      c.s.dest_cnt = c.s.qpos + dev_slots;
+      c.s.busy = reinterpret_cast<uint8_t *>(base + 5 * dev_slots);
+    }
     c.h.gt = c.s.heap_t;
     c.h.gk = c.s.heap_k;
     c.h.size = 0;
@@ -942,19 +956,25 @@ void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn
   grid(k_sim_prep_a, gx, 256);
   int force_cap = -1;  // tests: a tiny shared-memory heap exercises the spill to global memory
   if (const char *e = std::getenv("BX_SIM_HEAP_CAP")) force_cap = std::atoi(e);
+  // per-device state goes to shared memory when it fits beside the heaps
+  constexpr size_t kSmemBudget = 200 * 1024;
+  int dev_slots = maxn;
+  if (6 * sizeof(int64_t) * size_t(dev_slots) * 4 + 2 * sizeof(int64_t) * 1024 * 4 > kSmemBudget) dev_slots = 0;
+  const size_t dev_bytes = 6 * sizeof(int64_t) * static_cast<size_t>(dev_slots);
   if (force_cap >= 0) {
-    const size_t sm = 2 * sizeof(int64_t) * static_cast<size_t>(force_cap > 0 ? force_cap : 1);
-    k_simulate<1><<<nsims, 32, sm, s>>>(sims, nsims, graphs, force_cap);
-  } else if (nsims <= 148) {  // a few problems: one per CTA, a 12k-event shared-memory heap each
-    constexpr int kCap = 12288;
-    const size_t sm = 2 * sizeof(int64_t) * kCap;
+    const size_t sm = 2 * sizeof(int64_t) * static_cast<size_t>(force_cap) + dev_bytes;
     cudaFuncSetAttribute(k_simulate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    k_simulate<1><<<nsims, 32, sm, s>>>(sims, nsims, graphs, kCap);
+    k_simulate<1><<<nsims, 32, sm, s>>>(sims, nsims, graphs, force_cap, dev_slots);
+  } else if (nsims <= 148) {  // a few problems: one per CTA, a 12k-event shared-memory heap each
+    const int kCap = static_cast<int>(std::min<size_t>(12288, (kSmemBudget - dev_bytes) / (2 * sizeof(int64_t))));
+    const size_t sm = 2 * sizeof(int64_t) * kCap + dev_bytes;
+    cudaFuncSetAttribute(k_simulate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    k_simulate<1><<<nsims, 32, sm, s>>>(sims, nsims, graphs, kCap, dev_slots);
   } else {
     constexpr int W = 4, kCap = 1024;
-    const size_t sm = 2 * sizeof(int64_t) * kCap * W;
+    const size_t sm = (2 * sizeof(int64_t) * kCap + dev_bytes) * W;
     cudaFuncSetAttribute(k_simulate<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    k_simulate<W><<<(nsims + W - 1) / W, 32 * W, sm, s>>>(sims, nsims, graphs, kCap);
+    k_simulate<W><<<(nsims + W - 1) / W, 32 * W, sm, s>>>(sims, nsims, graphs, kCap, dev_slots);
   }
   grid(k_sim_prep_b, gx, 256);
   grid(k_sim_prep_c, gx, 256);
