@@ -5,9 +5,10 @@
 // K4: one warp per (graph, placement) problem. Events are processed in the
 // reference's heap order (t, kind{finish 0 < xfer_done 1 < start 2}, a, b)
 // (simulator.cpp:14-24); the heap stores (t, packed(kind, a, b)) pairs so one
-// 128-bit compare orders them. Lane 0 owns the heap; the whole warp scans
-// in/out-edge lists (inputs_resident, the per-destination max-bytes map)
-// and the per-device tables.
+// 128-bit compare orders them. Lane 0 owns the heap; the whole warp scans the
+// out-edge lists (input-residency counters, the per-destination max bytes,
+// GraphStatic releases). K4f (further down) replaces the event loop for
+// parallel comm mode without zero-duration nodes.
 #include <algorithm>
 #include <cstdlib>
 
@@ -96,18 +97,6 @@ __device__ __forceinline__ void inputs_landed(const SimCtx &c, int i, int dev) {
     if (c.s.device_of[ch] == dev) atomicSub(&c.s.ninp[ch], 1);
   }
   __syncwarp();
-}
-
-// inputs_resident (simulator.cpp:100-111), warp-cooperative scan (reference form).
-__device__ bool inputs_resident(const SimCtx &c, int j) {
-  int dev = c.s.device_of[j];
-  bool ok = true;
-  for (int x = c.g.in_off[j] + c.lane; x < c.g.in_off[j + 1]; x += 32) {
-    int i = c.g.esrc[c.g.in_edge[x]];
-    if (!c.s.finished[i]) ok = false;
-    else if (c.s.device_of[i] != dev && !c.s.resident[static_cast<int64_t>(i) * c.n + dev]) ok = false;
-  }
-  return __all_sync(kFullS, ok);
 }
 
 // try_start (simulator.cpp:113-119). Warp-uniform control flow; lane 0 pushes.
