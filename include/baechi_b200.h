@@ -175,6 +175,24 @@ typedef struct bx_plan bx_plan;
 int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs,
                    const bx_job *jobs, int32_t device, bx_plan **out,
                    char *msg, int msglen);
+
+/* Kernel-dispatch options of a plan (bx_plan_create uses the defaults).
+ * Results never depend on them — every kernel is bit-exact — only speed
+ * does; tests use them to drive each kernel over the same cases. Zero-
+ * initialise and set what you need; 0 / -1 mean "default". */
+typedef struct {
+  int32_t no_small_frontier; /* 1: never try the small-frontier kernel (K2s) */
+  int32_t wide_min_vn;       /* >= 0: V*n from which list jobs take the CTA-wide kernels; -1 default */
+  int32_t wide_max_jobs;     /* > 0: at most this many CTA-wide jobs (default 120) */
+  int32_t list_len;          /* 4/8/16/32: round-kernel column list length; 0 default */
+  int32_t profile;           /* 1: clock64-instrumented placer (bx_plan_profile) */
+  int32_t sim_heap_cap;      /* >= 0: shared-memory event heap slice of K4; -1 default */
+} bx_plan_options;
+
+int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs,
+                      const bx_job *jobs, int32_t device,
+                      const bx_plan_options *options, bx_plan **out,
+                      char *msg, int msglen);
 void bx_plan_destroy(bx_plan *plan);
 
 /* Host -> device copy of every graph/job input, enqueued on `stream`
@@ -203,12 +221,21 @@ int bx_plan_result_view(bx_plan *plan, int32_t job, bx_placement *view);
 /* Number of kernel launches the last bx_plan_place issued. */
 int bx_plan_launch_count(const bx_plan *plan);
 
+/* Which kernel placed job `job` in the last bx_plan_place (waits for it). */
+#define BX_KERNEL_NONE (-1)          /* host validation failed: never launched */
+#define BX_KERNEL_MTOPO 0            /* k_place_topo */
+#define BX_KERNEL_WARP 1             /* k_place_list<1>: one warp per problem */
+#define BX_KERNEL_ROUNDS 2           /* k_place_rounds: CTA per problem, parallel comm */
+#define BX_KERNEL_CTA_SEQ 3          /* k_place_list<8>: CTA per problem, sequential comm */
+#define BX_KERNEL_SMALL_FRONTIER 4   /* k_place_small: one warp, shared-memory state (smallsched.cu) */
+int bx_plan_job_kernel(bx_plan *plan, int32_t job);
+
 /* Device time (ms) of the placer kernel(s) of the last bx_plan_place,
  * measured with CUDA events on the plan's stream; waits for it. */
 float bx_plan_kernel_ms(bx_plan *plan);
 
-/* Per-step latency breakdown of job `job` (plans created with the
- * environment variable BX_PROFILE=1 run a clock64-instrumented placer):
+/* Per-step latency breakdown of job `job` (plans created with
+ * bx_plan_options.profile = 1 run a clock64-instrumented placer):
  * 16 int64 = SM cycles in rescan, argmin, rekey, discard, commit, remove,
  * ready, rows, cache, insert, emit, then counts steps, commits, rescans,
  * and the total cycles of the job. */
@@ -231,6 +258,11 @@ int bx_simulate(const bx_graph *graph, int32_t n, const int64_t *capacity,
                 const bx_comm *cm, int32_t mem_mode, const int32_t *device_of,
                 const int32_t *exec_order, const int32_t *exec_off,
                 bx_sim_report *out);
+/* bx_simulate with plan options (tests: sim_heap_cap). */
+int bx_simulate_ex(const bx_graph *graph, int32_t n, const int64_t *capacity,
+                   const bx_comm *cm, int32_t mem_mode, const int32_t *device_of,
+                   const int32_t *exec_order, const int32_t *exec_off,
+                   const bx_plan_options *options, bx_sim_report *out);
 
 /* LpSolution (lp.hpp:47-53) bookkeeping + SctLp row-class counts (:33-38). */
 typedef struct {

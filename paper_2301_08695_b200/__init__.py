@@ -120,6 +120,21 @@ class _Job(C.Structure):
                 ("cm", _Comm), ("fav_child", _vp), ("fav_len", C.c_int32)]
 
 
+class _PlanOptions(C.Structure):
+    _fields_ = [("no_small_frontier", C.c_int32), ("wide_min_vn", C.c_int32), ("wide_max_jobs", C.c_int32),
+                ("list_len", C.c_int32), ("profile", C.c_int32), ("sim_heap_cap", C.c_int32)]
+
+
+def _options(opts):
+    """bx_plan_options from a dict (keys = field names); None = defaults."""
+    o = _PlanOptions(0, -1, 0, 0, 0, -1)
+    for k, v in (opts or {}).items():
+        if k not in dict(_PlanOptions._fields_):
+            raise ValueError(f"unknown plan option {k!r}")
+        setattr(o, k, int(v))
+    return o
+
+
 class _Placement(C.Structure):
     _fields_ = [("device_of", _vp), ("start_us", _vp), ("exec_order", _vp), ("exec_off", _vp),
                 ("stats", C.c_int64 * 3), ("status", C.c_int32), ("msg", C.c_char * 256)]
@@ -151,6 +166,8 @@ def lib():
         L.bx_build_adjacency.argtypes = [i32, i32, _vp, _vp, _vp, _vp, _vp, cp, C.c_int]
         L.bx_plan_create.argtypes = [i32, C.POINTER(_Graph), i32, C.POINTER(_Job), i32,
                                      C.POINTER(_vp), cp, C.c_int]
+        L.bx_plan_create_ex.argtypes = [i32, C.POINTER(_Graph), i32, C.POINTER(_Job), i32,
+                                        C.POINTER(_PlanOptions), C.POINTER(_vp), cp, C.c_int]
         L.bx_plan_destroy.argtypes = [_vp]
         L.bx_plan_destroy.restype = None
         L.bx_plan_upload.argtypes = [_vp, _vp]
@@ -158,6 +175,9 @@ def lib():
         L.bx_plan_download.argtypes = [_vp, _vp, C.POINTER(_Placement)]
         L.bx_plan_result_view.argtypes = [_vp, i32, C.POINTER(_Placement)]
         L.bx_plan_launch_count.argtypes = [_vp]
+        L.bx_plan_job_kernel.argtypes = [_vp, i32]
+        L.bx_simulate_ex.argtypes = [C.POINTER(_Graph), i32, _vp, C.POINTER(_Comm), i32, _vp, _vp, _vp,
+                                     C.POINTER(_PlanOptions), C.POINTER(_SimReport)]
         L.bx_plan_kernel_ms.argtypes = [_vp]
         L.bx_plan_kernel_ms.restype = C.c_float
         L.bx_plan_profile.argtypes = [_vp, i32, _vp]
@@ -178,6 +198,7 @@ def lib():
 
 
 EXPORTED = ["bx_version", "bx_last_error", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
+            "bx_plan_create_ex", "bx_plan_job_kernel", "bx_simulate_ex",
             "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download", "bx_plan_result_view",
             "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_profile", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
             "bx_simulate", "bx_round_extract", "bx_grouped_create", "bx_grouped_view", "bx_grouped_destroy", "bx_lp_solve"]
@@ -292,7 +313,9 @@ class Plan:
     CUDA stream with inputs already resident, ``download`` copies the
     placements back (synchronising the stream)."""
 
-    def __init__(self, graphs: list[MetaGraph], jobs: list[Job], device: int = 0):
+    def __init__(self, graphs: list[MetaGraph], jobs: list[Job], device: int = 0, options: dict | None = None):
+        """``options``: bx_plan_options fields (kernel dispatch; results never
+        depend on them)."""
         self.graphs = graphs
         self.jobs = jobs
         self._keep = []
@@ -307,7 +330,9 @@ class Plan:
         self._jc = (_Job * len(jobs))(*jc)
         h = _vp()
         msg = C.create_string_buffer(512)
-        rc = lib().bx_plan_create(len(graphs), self._gc, len(jobs), self._jc, device, C.byref(h), msg, 512)
+        self._opt = _options(options)
+        rc = lib().bx_plan_create_ex(len(graphs), self._gc, len(jobs), self._jc, device, C.byref(self._opt),
+                                     C.byref(h), msg, 512)
         _raise(rc, msg.value.decode())
         self.h = h
         self.out = (_Placement * len(jobs))()
@@ -334,14 +359,20 @@ class Plan:
     def launch_count(self) -> int:
         return lib().bx_plan_launch_count(self.h)
 
+    KERNELS = {-1: "none", 0: "m-topo", 1: "warp", 2: "rounds", 3: "cta-seq", 4: "small-frontier"}
+
+    def job_kernel(self, i: int) -> str:
+        """Which kernel placed job i in the last place()."""
+        return self.KERNELS[lib().bx_plan_job_kernel(self.h, i)]
+
     PROFILE_FIELDS = ("rescan", "argmin", "rekey", "discard", "commit", "remove", "ready", "rows", "cache",
                       "insert", "emit", "steps", "commits", "rescans", "total")
 
     def profile(self, i: int) -> dict:
-        """Latency breakdown of job i (plan built with BX_PROFILE=1)."""
+        """Latency breakdown of job i (plan built with options={"profile": 1})."""
         out = np.zeros(16, np.int64)
         rc = lib().bx_plan_profile(self.h, i, _ptr(out))
-        _raise(rc, "no profile: create the plan with BX_PROFILE=1")
+        _raise(rc, "no profile: create the plan with options={'profile': 1}")
         return dict(zip(self.PROFILE_FIELDS, out.tolist()))
 
     def kernel_ms(self) -> float:
@@ -457,7 +488,22 @@ def build_grouped(base: dict, coplacement: bool = True, fusion: bool = True, sin
 
 
 # ---- reference-shaped entry points ---------------------------------------
-def _one(gg: MetaGraph, algo: str, capacity, cm: CommModel, fav=None, stats_out=None) -> Placement:
+def _one(gg: MetaGraph, algo: str, capacity, cm: CommModel, fav=None, stats_out=None,
+         options: dict | None = None) -> Placement:
+    if options is not None:  # a one-job plan with explicit dispatch options
+        plan = Plan([gg], [Job(0, algo, capacity, cm, fav)], options=options)
+        try:
+            plan.upload()
+            plan.place()
+            plan.download()
+            st, msg = plan.status(0)
+            _raise(st, msg)
+            p = plan.result(0)
+        finally:
+            plan.close()
+        if stats_out is not None:
+            stats_out[:] = list(p.stats)
+        return p
     cap = _c(capacity, np.int64)
     favc = None if fav is None else _c(fav, np.int32)
     job = _Job(0, ALGOS[algo], len(cap), _ptr(cap), cm._c(), _ptr(favc), 0 if favc is None else len(favc))
@@ -487,7 +533,7 @@ def place_msct(gg: MetaGraph, capacity, cm: CommModel, fav_child=None, stats_out
 
 
 def simulate(gg: MetaGraph, placement: Placement, capacity, cm: CommModel,
-             mem_mode: int = TRAINING_PERSISTENT) -> SimReport:
+             mem_mode: int = TRAINING_PERSISTENT, options: dict | None = None) -> SimReport:
     cap = _c(capacity, np.int64)
     n = len(cap)
     V = gg.V
@@ -500,8 +546,9 @@ def simulate(gg: MetaGraph, placement: Placement, capacity, cm: CommModel,
         raise ValidationError("placement does not match graph or roster")
     g = gg._c()
     cmc = cm._c()
-    lib().bx_simulate(C.byref(g), n, _ptr(cap), C.byref(cmc), mem_mode, _ptr(dev), _ptr(eo), _ptr(off),
-                      C.byref(rep))
+    opt = _options(options)
+    lib().bx_simulate_ex(C.byref(g), n, _ptr(cap), C.byref(cmc), mem_mode, _ptr(dev), _ptr(eo), _ptr(off),
+                         C.byref(opt), C.byref(rep))
     _raise(rep.status, rep.msg.decode())
     return SimReport(rep.makespan_us, b[0][:V].copy(), b[1][:n].copy(), b[2][:n].copy(), b[3][:n].copy(),
                      rep.transfer_count, rep.transfer_bytes, rep.duplicate_transfers, rep.cache_hits)

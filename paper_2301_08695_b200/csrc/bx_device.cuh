@@ -67,7 +67,8 @@ struct DGraph {
   int32_t *in_src;
   int32_t *inpos;       // [E] in-CSR slot of each edge (out-CSR order = edge order)
   int32_t *indeg_left;  // Kahn residue (cycle message)
-  int32_t *flags;       // [0] peeled count, [1] negative-bytes flag
+  int32_t *flags;       // [0] peeled count, [1] negative-bytes flag, [2] negative compute time
+  int64_t *ksum;        // sum of compute times (K2s int32 time bound)
 };
 
 struct DPrep {
@@ -75,6 +76,11 @@ struct DPrep {
   double ic, pb;
   int64_t *in_c;   // [E] comm_time of the in-CSR slot's edge
   int64_t *cmax;   // max_comm_time (cost_model.cpp:234-240)
+  // K2s (small-frontier kernel) extras, filled by k_prep_small when a job needs them
+  int32_t *in_c32;    // [E] in_c as int32 (valid when *cbad == 0)
+  int32_t *nu;        // [V] index of a producer whose out-edges carry different comm times, else -1
+  int32_t *nu_count;  // number of such producers
+  int32_t *cbad;      // some comm time outside [0, 2^30)
 };
 
 struct DJob {
@@ -101,6 +107,11 @@ struct DJob {
   int64_t *stats;
   DErr *err;
   int64_t *prof;  // [kProfSlots] per-phase SM cycles when built with profiling, else null
+  // K2s: set to 1 when the small-frontier kernel placed the job (or reported
+  // its error); the general kernels then skip it. Null: not a K2s job.
+  int32_t *sdone;
+  int32_t nucap;  // K2s shared-memory slots reserved for non-uniform producers
+  int32_t maxin;  // largest in-degree of the graph (K2s list sizing)
 };
 
 // Per-step latency breakdown slots (clock64 cycles summed over the run, lane 0).

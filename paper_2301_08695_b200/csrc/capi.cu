@@ -23,10 +23,13 @@ void launch_kahn(DGraph *graphs_dev, int32_t *const *queues_dev, int ngraphs, cu
 cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bit, cudaStream_t s);
 void launch_extract(const XCtx &c, cudaStream_t s);
 void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_etf, int n_bpar, int n_bseq,
-                    int njobs,
-                    const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo, bool prof,
-                    cudaStream_t s_small, cudaStream_t s_big);
-void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn, cudaStream_t s);
+                    int njobs, const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo, bool prof,
+                    int list_len, cudaStream_t s_small, cudaStream_t s_big);
+void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn, int force_cap, cudaStream_t s);
+void launch_prep_small(const DGraph &g, const DPrep &pr, cudaStream_t s);
+void launch_small_frontier(const DJob *jobs, const int32_t *order, int n_etf, int n_sct, const DGraph *graphs,
+                           const DPrep *preps, size_t smem, bool prof, cudaStream_t s);
+size_t small_smem_bytes_host(int V, int n, int nucap, int nccap);
 }  // namespace bx
 
 using namespace bx;
@@ -89,6 +92,7 @@ struct Fill {  // one memset
 
 struct bx_plan {
   int device = 0;
+  bx_plan_options opt{0, -1, 0, 0, 0, -1};
   int ngraphs = 0, njobs = 0, nprep = 0;
   std::vector<bx_graph> hg;
   std::vector<bx_job> hj;
@@ -107,6 +111,11 @@ struct bx_plan {
   DJob *dj_dev = nullptr;
   int32_t *order_dev = nullptr;     // launch lists: small | big parallel | big sequential
   int n_small = 0, n_etf = 0, n_bpar = 0, n_bseq = 0;  // n_etf: leading parallel m-ETF small jobs
+  int n_sf_etf = 0, n_sf_sct = 0;   // small-frontier (K2s) jobs, launched first
+  size_t sf_smem = 0;
+  int32_t *sf_order_dev = nullptr;
+  std::vector<char> prep_small;     // prep index -> K2s extras needed
+  std::vector<int> job_kernel;      // BX_KERNEL_* of the general kernel each job is queued on
   cudaStream_t s2 = nullptr;        // big problems run beside the small ones
   cudaEvent_t fork = nullptr, join = nullptr;
   int32_t **queues_dev = nullptr;
@@ -224,6 +233,11 @@ void bx_plan_destroy(bx_plan *plan) {
 
 int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const bx_job *jobs, int32_t device,
                    bx_plan **out, char *msg, int msglen) {
+  return bx_plan_create_ex(ngraphs, graphs, njobs, jobs, device, nullptr, out, msg, msglen);
+}
+
+int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const bx_job *jobs, int32_t device,
+                      const bx_plan_options *options, bx_plan **out, char *msg, int msglen) {
   *out = nullptr;
   int ndev = bx_device_count();
   if (ndev <= 0) {
@@ -238,6 +252,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   auto *P = new (std::nothrow) bx_plan();
   if (!P) return BX_RUNTIME;
   P->device = device;
+  if (options) P->opt = *options;
   P->ngraphs = ngraphs;
   P->njobs = njobs;
   P->hg.assign(graphs, graphs + ngraphs);
@@ -266,7 +281,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   Layout L;
   struct GOff {
     size_t k, temp, perm, outb, esrc, edst, ebytes, in_off, in_edge, out_off, need, need_order, iota, need_keys,
-        in_src, inpos, indeg_left, flags, queue;
+        in_src, inpos, indeg_left, flags, queue, ksum;
   };
   std::vector<GOff> go(ngraphs);
   size_t max_sort_V = 0;
@@ -291,10 +306,15 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     o.inpos = L.take<int32_t>(G.E);
     o.indeg_left = L.take<int32_t>(G.V);
     o.flags = L.take<int32_t>(4);
+    o.ksum = L.take<int64_t>(1);
     o.queue = L.take<int32_t>(2 * static_cast<size_t>(G.V));
     max_sort_V = std::max(max_sort_V, static_cast<size_t>(G.V));
   }
   std::vector<std::pair<size_t, size_t>> po(P->nprep);  // in_c, cmax
+  struct POff {
+    size_t c32, nu, cnt;
+  };
+  std::vector<POff> pso(P->nprep);
   std::vector<int> prep_graph(P->nprep);
   std::vector<std::pair<double, double>> prep_cm(P->nprep);
   for (auto &kv : prep_of) {
@@ -304,10 +324,13 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     prep_cm[pi] = {std::get<1>(kv.first), std::get<2>(kv.first)};
     po[pi].first = L.take<int64_t>(graphs[g].E);
     po[pi].second = L.take<int64_t>(1);
+    pso[pi].c32 = L.take<int32_t>(graphs[g].E);
+    pso[pi].nu = L.take<int32_t>(graphs[g].V);
+    pso[pi].cnt = L.take<int32_t>(2);
   }
   struct JOff {
     size_t cap, fav, K, cache, dead, pending, alive, ready, rpos, cseq, nc, finish, urgent, scv, scg, pdev, pfin, K2, urgent2, ready2, alive2, ncw, newl, device_of,
-        start, exec_order, exec_off, stats, err;
+        start, exec_order, exec_off, stats, err, sdone;
   };
   // Few large list-placer problems run the CTA-wide kernels (one problem per
   // CTA); many run one warp each. Decided here because the round kernel
@@ -329,10 +352,10 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   const bool few = list_ids.size() <= 148;
   int64_t big_min = few ? (int64_t(1) << 15) : (int64_t(1) << 17);
   int64_t big_min_par = few ? 0 : INT64_MAX;
-  if (const char *e = std::getenv("BX_BIG_MIN")) big_min = big_min_par = std::atoll(e);  // tuning experiments
+  if (P->opt.wide_min_vn >= 0) big_min = big_min_par = P->opt.wide_min_vn;
   std::vector<char> big(njobs, 0);
   size_t big_max = 120;
-  if (const char *e = std::getenv("BX_BIG_MAX")) big_max = static_cast<size_t>(std::atoll(e));  // tuning experiments
+  if (P->opt.wide_max_jobs > 0) big_max = static_cast<size_t>(P->opt.wide_max_jobs);
   for (size_t r = 0; r < list_ids.size() && r < big_max; ++r) {
     const int i = list_ids[r];
     // small m-SCT problems commit one pair at a time more often (lifted
@@ -379,6 +402,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
       o.newl = L.take<int32_t>(Vr);
     }
     o.pfin = L.take<int64_t>(graphs[J.graph].E);
+    o.sdone = L.take<int32_t>(1);
     o.stats = LO.take<int64_t>(3);
     o.err = LO.take<DErr>(1);
     o.start = LO.take<int64_t>(V);
@@ -391,6 +415,7 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   size_t jtables = L.take<DJob>(njobs);
   size_t qtables = L.take<int32_t *>(ngraphs);
   size_t otable = L.take<int32_t>(3 * size_t(njobs) + 3);
+  size_t sftable = L.take<int32_t>(size_t(njobs) + 1);
   const size_t in_at = L.take<char>(LI.off), out_at = L.take<char>(LO.off);
   P->in_bytes = LI.off;
   P->out_bytes = LO.off;
@@ -433,6 +458,8 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     d.inpos = at<int32_t>(pool, o.inpos);
     d.indeg_left = at<int32_t>(pool, o.indeg_left);
     d.flags = at<int32_t>(pool, o.flags);
+    d.ksum = at<int64_t>(pool, o.ksum);
+    P->fills.push_back({d.ksum, 0, 8});
     queues[g] = at<int32_t>(pool, o.queue);
     auto up = [&](const void *dev, const void *host, size_t bytes) {
       if (bytes) P->uploads.push_back({const_cast<void *>(dev), host, bytes});
@@ -476,13 +503,34 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     d.in_c = at<int64_t>(pool, po[pi].first);
     d.cmax = at<int64_t>(pool, po[pi].second);
     P->fills.push_back({d.cmax, 0, 8});
+    d.in_c32 = at<int32_t>(pool, pso[pi].c32);
+    d.nu = at<int32_t>(pool, pso[pi].nu);
+    d.nu_count = at<int32_t>(pool, pso[pi].cnt);
+    d.cbad = d.nu_count + 1;
     if (!graph_seen[d.graph]) {
       graph_seen[d.graph] = 1;
       P->prep_first[pi] = 1;
     }
   }
+  // small-frontier kernel (K2s, smallsched.cu) eligibility inputs per graph:
+  // largest in-degree and the producers whose out-edges carry different byte
+  // counts (an upper bound of those with different comm times)
+  std::vector<int> g_maxin(ngraphs, 0), g_nu(ngraphs, 0);
+  for (int g = 0; g < ngraphs; ++g) {
+    const bx_graph &G = graphs[g];
+    for (int v = 0; v < G.V; ++v) g_maxin[g] = std::max(g_maxin[g], G.in_off[v + 1] - G.in_off[v]);
+    for (int v = 0; v < G.V; ++v) {
+      const int b = G.out_off[v], e = G.out_off[v + 1];
+      for (int y = b + 1; y < e; ++y)
+        if (G.tensor_bytes[y] != G.tensor_bytes[b]) {
+          ++g_nu[g];
+          break;
+        }
+    }
+  }
+  P->prep_small.assign(P->nprep, 0);
   P->dj.resize(njobs);
-  if (std::getenv("BX_PROFILE") && std::getenv("BX_PROFILE")[0] == '1') {
+  if (P->opt.profile == 1) {
     BX_CUDA(cudaMalloc(&P->prof, sizeof(int64_t) * kProfSlots * size_t(njobs)), msg, msglen);
     BX_CUDA(cudaMemset(P->prof, 0, sizeof(int64_t) * kProfSlots * size_t(njobs)), msg, msglen);
   }
@@ -570,12 +618,42 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
     P->fills.push_back({d.dead, 0, size_t(V * n)});
     P->fills.push_back({d.sc_gen, 0, 4 * size_t(256 * n)});
     P->fills.push_back({d.err, 0, sizeof(DErr)});
+    // K2s: parallel-comm list jobs of single-graph-sized plans whose per-node
+    // state fits one SM's shared memory; the kernel re-checks the value
+    // bounds on the device and leaves the job to the general kernels if any
+    // fails (or its frontier outgrows 256 pairs)
+    d.sdone = nullptr;
+    d.nucap = g_nu[J.graph];
+    d.maxin = g_maxin[J.graph];
+    if (!d.skip && few && J.algo != BX_ALGO_MTOPO && J.cm.mode == BX_COMM_PARALLEL && J.n <= 32 && G.V > 0 &&
+        G.V < (1 << 26) && !P->opt.no_small_frontier && P->opt.wide_min_vn < 0) {
+      const size_t sm = small_smem_bytes_host(G.V, J.n, d.nucap, std::max(1024, d.maxin));
+      if (sm <= 200 * 1024) {
+        d.sdone = at<int32_t>(pool, o.sdone);
+        P->fills.push_back({d.sdone, 0, 4});
+        P->sf_smem = std::max(P->sf_smem, sm);
+        P->prep_small[job_prep[i]] = 1;
+      }
+    }
   }
   P->dg_dev = at<DGraph>(pool, tables);
   P->dp_dev = at<DPrep>(pool, ptables);
   P->dj_dev = at<DJob>(pool, jtables);
   P->queues_dev = at<int32_t *>(pool, qtables);
   P->order_dev = at<int32_t>(pool, otable);
+  P->sf_order_dev = at<int32_t>(pool, sftable);
+  {
+    std::vector<int32_t> sfe, sfs;
+    for (int i = 0; i < njobs; ++i) {
+      if (!P->dj[i].sdone) continue;
+      (P->dj[i].algo == BX_ALGO_MSCT && P->dj[i].fav ? sfs : sfe).push_back(i);
+    }
+    P->n_sf_etf = static_cast<int>(sfe.size());
+    P->n_sf_sct = static_cast<int>(sfs.size());
+    sfe.insert(sfe.end(), sfs.begin(), sfs.end());
+    if (!sfe.empty())
+      BX_CUDA(cudaMemcpy(P->sf_order_dev, sfe.data(), 4 * sfe.size(), cudaMemcpyHostToDevice), msg, msglen);
+  }
   {
     // three launch lists, each longest-first: small (one warp per job),
     // big parallel-mode (round kernel), big sequential-mode (8-warp kernel)
@@ -587,6 +665,13 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
       else if (jobs[i].cm.mode == BX_COMM_PARALLEL) bpar.push_back(i);
       else bseq.push_back(i);
     }
+    P->job_kernel.assign(njobs, BX_KERNEL_NONE);
+    for (int i = 0; i < njobs; ++i)
+      if (!P->dj[i].skip && jobs[i].algo == BX_ALGO_MTOPO) P->job_kernel[i] = BX_KERNEL_MTOPO;
+    for (int i : small) P->job_kernel[i] = BX_KERNEL_WARP;
+    for (int i : sgen) P->job_kernel[i] = BX_KERNEL_WARP;
+    for (int i : bpar) P->job_kernel[i] = BX_KERNEL_ROUNDS;
+    for (int i : bseq) P->job_kernel[i] = BX_KERNEL_CTA_SEQ;
     P->n_etf = static_cast<int>(small.size());
     small.insert(small.end(), sgen.begin(), sgen.end());
     std::vector<int32_t> all(small);
@@ -654,6 +739,13 @@ int bx_plan_place(bx_plan *P, void *stream) {
     launch_prep(g, P->dp[pi], P->prep_first[pi] != 0, s);
     P->launches += (P->prep_first[pi] && g.V > 0 ? 1 : 0) + (g.E > 0 ? 1 : 0);
   }
+  for (int pi = 0; pi < P->nprep; ++pi) {
+    if (!P->prep_small[pi]) continue;
+    const DGraph &g = P->dg[P->dp[pi].graph];
+    cudaMemsetAsync(P->dp[pi].nu_count, 0, 8, s);
+    launch_prep_small(g, P->dp[pi], s);
+    P->launches += 1;
+  }
   for (int g = 0; g < P->ngraphs; ++g) {
     if (P->dg[g].V == 0) continue;
     size_t bytes = P->sort_tmp_bytes;
@@ -667,6 +759,11 @@ int bx_plan_place(bx_plan *P, void *stream) {
   launch_kahn(P->dg_dev, P->queues_dev, P->ngraphs, s);
   P->launches += 1;
   cudaEventRecord(P->ev[0], s);
+  if (P->n_sf_etf + P->n_sf_sct > 0) {
+    launch_small_frontier(P->dj_dev, P->sf_order_dev, P->n_sf_etf, P->n_sf_sct, P->dg_dev, P->dp_dev, P->sf_smem,
+                          P->prof != nullptr, s);
+    P->launches += (P->n_sf_etf > 0) + (P->n_sf_sct > 0);
+  }
   const bool fork = (P->n_small > 0 && (P->n_bpar + P->n_bseq) > 0) || (P->n_etf > 0 && P->n_small > P->n_etf);
   cudaStream_t sb = fork ? P->s2 : s;
   if (fork) {
@@ -675,7 +772,7 @@ int bx_plan_place(bx_plan *P, void *stream) {
   }
   launch_placers(P->dj_dev, P->order_dev, P->n_small, P->n_etf, P->n_bpar, P->n_bseq, P->njobs, P->dg_dev,
                  P->dp_dev,
-                 P->maxn, P->any_topo, P->prof != nullptr, s, sb);
+                 P->maxn, P->any_topo, P->prof != nullptr, P->opt.list_len, s, sb);
   if (fork) {
     cudaEventRecord(P->join, P->s2);
     cudaStreamWaitEvent(s, P->join, 0);
@@ -686,6 +783,17 @@ int bx_plan_place(bx_plan *P, void *stream) {
 }
 
 int bx_plan_launch_count(const bx_plan *P) { return P->launches; }
+
+int bx_plan_job_kernel(bx_plan *P, int32_t job) {
+  if (job < 0 || job >= P->njobs) return BX_KERNEL_NONE;
+  if (P->dj[job].sdone) {
+    int32_t done = 0;
+    cudaSetDevice(P->device);
+    if (cudaMemcpy(&done, P->dj[job].sdone, 4, cudaMemcpyDeviceToHost) == cudaSuccess && done)
+      return BX_KERNEL_SMALL_FRONTIER;
+  }
+  return P->job_kernel[job];
+}
 
 int bx_plan_profile(bx_plan *P, int32_t job, int64_t *out16) {
   cudaSetDevice(P->device);
@@ -945,7 +1053,7 @@ int bx_plan_simulate(bx_plan *P, int32_t mem_mode, void *stream) {
   }
   for (const Fill &f : P->sim_fills)
     if (cudaMemsetAsync(f.ptr, f.value, f.bytes, s) != cudaSuccess) return BX_RUNTIME;
-  launch_simulate(P->ds_dev, P->njobs, P->dg_dev, std::max(P->maxn, 1), s);
+  launch_simulate(P->ds_dev, P->njobs, P->dg_dev, std::max(P->maxn, 1), P->opt.sim_heap_cap, s);
   return launch_status();
 }
 
@@ -1040,6 +1148,12 @@ int bx_place(const bx_graph *graph, const bx_job *job, bx_placement *out) {
 
 int bx_simulate(const bx_graph *graph, int32_t n, const int64_t *capacity, const bx_comm *cm, int32_t mem_mode,
                 const int32_t *device_of, const int32_t *exec_order, const int32_t *exec_off, bx_sim_report *out) {
+  return bx_simulate_ex(graph, n, capacity, cm, mem_mode, device_of, exec_order, exec_off, nullptr, out);
+}
+
+int bx_simulate_ex(const bx_graph *graph, int32_t n, const int64_t *capacity, const bx_comm *cm, int32_t mem_mode,
+                   const int32_t *device_of, const int32_t *exec_order, const int32_t *exec_off,
+                   const bx_plan_options *options, bx_sim_report *out) {
   if (n <= 0) {
     out->status = BX_VALIDATION;
     put_msg(out->msg, sizeof out->msg, "placement does not match graph or roster");
@@ -1053,15 +1167,16 @@ int bx_simulate(const bx_graph *graph, int32_t n, const int64_t *capacity, const
   j.capacity = capacity;
   j.cm = *cm;
   bx_plan *P = nullptr;
-  int rc = bx_plan_create(1, graph, 1, &j, 0, &P, out->msg, sizeof out->msg);
+  int rc = bx_plan_create_ex(1, graph, 1, &j, 0, options, &P, out->msg, sizeof out->msg);
   if (rc) {
     out->status = rc;
     return rc;
   }
   const DJob &d = P->dj[0];
   const int V = graph->V;
-  int total = exec_off[n] - exec_off[0];
-  if (exec_off[0] != 0 || total != V) {
+  bool offsets_ok = exec_off[0] == 0 && exec_off[n] == V;
+  for (int dv = 0; dv < n && offsets_ok; ++dv) offsets_ok = exec_off[dv] <= exec_off[dv + 1];
+  if (!offsets_ok) {
     // lists that cannot hold every node exactly once never reach the device
     // buffers (sized V); the verdict is validate_placement's own
     // (simulator.cpp:78-97), decided by its first failing check
@@ -1069,7 +1184,7 @@ int bx_simulate(const bx_graph *graph, int32_t n, const int64_t *capacity, const
     out->status = BX_VALIDATION;
     const char *why = "placement must assign every node exactly once";
     for (int dv = 0; dv < n; ++dv)
-      for (int x = exec_off[dv]; x < exec_off[dv + 1]; ++x) {
+      for (int x = std::max(exec_off[dv], 0); x < exec_off[dv + 1] && x < V; ++x) {
         int m = exec_order[x];
         if (m < 0 || m >= V || device_of[m] != dv) why = "exec_order disagrees with assignments";
       }

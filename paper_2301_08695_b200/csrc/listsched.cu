@@ -455,6 +455,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
   if (slot_id >= njobs) return;                 // uniform per problem group
   const DJob jb = jobs[order[slot_id]];
   if (jb.skip || jb.algo == 0 || (seq_only && jb.mode == 1)) return;
+  if (jb.sdone && *jb.sdone) return;  // placed by the small-frontier kernel (smallsched.cu)
   const DGraph g = graphs[jb.graph];
   const DPrep pr = preps[jb.prep];
   // acyclicity then byte-count validation, in the reference's order
@@ -1078,7 +1079,6 @@ static void launch_w(const DJob *jobs, const int32_t *order, int njobs, const DG
   // memory for the resident CTAs (+3% sweep throughput, profiles/r01d_minb.txt)
   if (kW == 1) {
     int pct = static_cast<int>((100 * size_t(BX_LIST_MINB) * (sm + 1024) + 228 * 1024 - 1) / (228 * 1024)) + 5;
-    if (const char *e = std::getenv("BX_CARVEOUT")) pct = std::atoi(e);  // tuning experiments
     cudaFuncSetAttribute(k_place_list<kW, kProf, kEtf>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          pct < 100 ? pct : 100);
   }
@@ -1368,6 +1368,7 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
   if (blockIdx.x >= njobs) return;
   const DJob jb = jobs[order[blockIdx.x]];
   if (jb.skip || jb.algo == 0 || jb.mode != 1) return;
+  if (jb.sdone && *jb.sdone) return;  // placed by the small-frontier kernel (smallsched.cu)
   const DGraph g = graphs[jb.graph];
   const DPrep pr = preps[jb.prep];
   if (g.flags[0] != g.V || g.flags[1]) {
@@ -2041,10 +2042,9 @@ static void launch_rounds_kr(const DJob *jobs, const int32_t *order, int njobs, 
 // (measured, profiles/r01c_kr_sweep.txt, r01e_scan_u.txt): 4 up to 8
 // devices, 8 up to 31, 16 up to 47, 32 (100k x 64: 1.27 -> 1.07 s vs 16).
 void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                   int maxn, bool prof, cudaStream_t s) {
-  (void)prof;
+                   int maxn, int list_len, cudaStream_t s) {
   int kr = maxn <= 8 ? 4 : maxn < 32 ? 8 : maxn < 48 ? 16 : 32;
-  if (const char *e = std::getenv("BX_KR")) kr = std::atoi(e);  // tuning experiments
+  if (list_len > 0) kr = list_len;  // bx_plan_options.list_len (tests drive every length)
   while (kr > 4 && rounds_smem(maxn, kr) > 200 * 1024) kr /= 2;
   if (kr >= 32) launch_rounds_kr<32>(jobs, order, njobs, graphs, preps, maxn, s);
   else if (kr >= 16) launch_rounds_kr<16>(jobs, order, njobs, graphs, preps, maxn, s);

@@ -63,13 +63,27 @@ __global__ void k_prep_edges(DGraph g, DPrep pr, int write_src) {
   }
 }
 
-// need[j] = perm + out + temp (reserve_bytes, placers.hpp:43-45).
+// need[j] = perm + out + temp (reserve_bytes, placers.hpp:43-45); the sum of
+// compute times and a negative-time flag (the small-frontier kernel's bounds).
 __global__ void k_prep_nodes(DGraph g) {
+  unsigned long long ks = 0;
+  int neg = 0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < g.V; j += gridDim.x * blockDim.x) {
     int64_t v = g.perm[j] + g.outb[j] + g.temp[j];
     g.need[j] = v;
     g.iota[j] = j;
     g.indeg_left[j] = g.in_off[j + 1] - g.in_off[j];
+    const int64_t k = g.k[j];
+    if (k < 0) neg = 1;
+    else ks += static_cast<unsigned long long>(k);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ks += __shfl_xor_sync(kFull, ks, o);
+    neg |= __shfl_xor_sync(kFull, neg, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (ks) atomicAdd(reinterpret_cast<unsigned long long *>(g.ksum), ks);
+    if (neg) atomicOr(&g.flags[2], 1);
   }
 }
 
@@ -344,7 +358,7 @@ void launch_small(const DJob *jobs, const int32_t *order, int n_etf, int n_gen, 
 void launch_big_seq(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                     int maxn, bool prof, cudaStream_t s);
 void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
-                   int maxn, bool prof, cudaStream_t s);
+                   int maxn, int list_len, cudaStream_t s);
 
 void launch_prep(const DGraph &g, const DPrep &pr, bool first, cudaStream_t s) {
   if (first) {
@@ -368,10 +382,10 @@ cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bi
 
 void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_etf, int n_bpar, int n_bseq,
                     int njobs, const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo, bool prof,
-                    cudaStream_t s_small, cudaStream_t s_big) {
+                    int list_len, cudaStream_t s_small, cudaStream_t s_big) {
   // big problems (CTA-wide kernels) on s_big, beside the small ones (one
   // warp per job, four per CTA) on s_small; every list is longest-first
-  if (n_bpar) launch_rounds(jobs, order + n_small, n_bpar, graphs, preps, maxn, prof, s_big);
+  if (n_bpar) launch_rounds(jobs, order + n_small, n_bpar, graphs, preps, maxn, list_len, s_big);
   if (n_bseq) launch_big_seq(jobs, order + n_small + n_bpar, n_bseq, graphs, preps, maxn, prof, s_big);
   if (n_small) launch_small(jobs, order, n_etf, n_small - n_etf, graphs, preps, maxn, prof, s_small, s_big);
   if (any_topo) {

@@ -931,7 +931,7 @@ __global__ void k_sim_report(const DSim *sims, int nsims) {
   err->code = E_NONE;
 }
 
-void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn, cudaStream_t s) {
+void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn, int force_cap, cudaStream_t s) {
   // K4f: grid-wide passes (blockIdx.y = problem), then one CTA per problem
   // for the walkers, per device for the memory scans; K4 takes the problems
   // K4f leaves (sequential comm, zero-duration nodes) after the first pass
@@ -943,8 +943,8 @@ void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn
     }
   };
   grid(k_sim_prep_a, gx, 256);
-  int force_cap = -1;  // tests: a tiny shared-memory heap exercises the spill to global memory
-  if (const char *e = std::getenv("BX_SIM_HEAP_CAP")) force_cap = std::atoi(e);
+  // force_cap >= 0 (bx_plan_options.sim_heap_cap, tests): a tiny shared-memory
+  // heap exercises the spill to global memory
   // per-device state goes to shared memory when it fits beside the heaps
   constexpr size_t kSmemBudget = 200 * 1024;
   int dev_slots = maxn;

@@ -174,12 +174,11 @@ def test_cuda_vs_oracle_seeded(bx, seed, g):
 
 
 @pytest.mark.parametrize("kr", ["4", "8", "16", "32"])
-def test_cuda_vs_oracle_cta_kernels(bx, kr, monkeypatch):
+def test_cuda_vs_oracle_cta_kernels(bx, kr):
     """The CTA-wide kernels (round kernel for parallel comm, 8-warp list
     kernel for sequential) forced onto small seeded problems, every list
     length, against the C restatement."""
-    monkeypatch.setenv("BX_BIG_MIN", "0")
-    monkeypatch.setenv("BX_KR", kr)
+    opts = {"wide_min_vn": 0, "list_len": int(kr)}
     for seed, g in _random_cases()[:8]:
         m = W.as_meta_dict(g)
         gg = _meta(bx, m)
@@ -198,7 +197,7 @@ def test_cuda_vs_oracle_cta_kernels(bx, kr, monkeypatch):
                         except OracleError as e:
                             oe = (e.kind, e.msg)
                         try:
-                            p = bx._one(gg, ALGO[algo], caps, bx.CommModel(*cm), fv)
+                            p = bx._one(gg, ALGO[algo], caps, bx.CommModel(*cm), fv, options=opts)
                             pe = None
                         except bx.Error as e:
                             pe = (e.kind, e.msg)

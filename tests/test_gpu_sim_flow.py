@@ -58,14 +58,14 @@ def _graphs():
     return out
 
 
-def _check(bx, m, gg, pl, caps, cm, mm):
+def _check(bx, m, gg, pl, caps, cm, mm, options=None):
     try:
         o = Restate.simulate(m, caps, cm, mm, pl.device_of, pl.exec_order_flat, pl.exec_off)
         oe = None
     except OracleError as e:
         oe = (e.kind, e.msg)
     try:
-        r = bx.simulate(gg, pl, caps, bx.CommModel(*cm), mm)
+        r = bx.simulate(gg, pl, caps, bx.CommModel(*cm), mm, options=options)
         re = None
     except bx.Error as e:
         re = (e.kind, e.msg)
@@ -197,11 +197,10 @@ def test_sim_batched_plan_vs_restatement(bx):
 
 
 @pytest.mark.parametrize("cap", ["0", "3"])
-def test_event_heap_spill(bx, monkeypatch, cap):
+def test_event_heap_spill(bx, cap):
     """The event-loop kernel's heap starting in a 3-entry shared-memory slice
     (spills to global memory at once) or in global memory outright: same
     reports and errors, sequential comm and zero-duration nodes."""
-    monkeypatch.setenv("BX_SIM_HEAP_CAP", cap)
     rng = np.random.default_rng(9)
     for g in (W.layered_dag(6, 10, 1), W.branchy(5, 2)):
         m = W.as_meta_dict(g)
@@ -216,4 +215,5 @@ def test_event_heap_spill(bx, monkeypatch, cap):
                 for caps in (tot_d + 1, tot_d // 3 + 1):
                     for cm in ((5.0, 0.001, 0), (12.5, 0.002, 1)):
                         for mm in (0, 1):
-                            _check(bx, mg, gg, pl, [int(c) for c in caps], cm, mm)
+                            _check(bx, mg, gg, pl, [int(c) for c in caps], cm, mm,
+                                   options={"sim_heap_cap": int(cap)})

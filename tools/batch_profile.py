@@ -1,10 +1,9 @@
-"""Which problems bound the C5 batch? Runs the sweep plan with BX_PROFILE=1
+"""Which problems bound the C5 batch? Runs the sweep plan with options={"profile": 1}
 and prints the longest jobs (SM cycles per job from clock64) by family/n."""
 import collections
 import os
 import sys
 
-os.environ["BX_PROFILE"] = "1"
 sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
 
@@ -15,7 +14,7 @@ from paper_2301_08695_b200 import workloads as W  # noqa: E402
 graphs, jobs = sweep.rank_sweep(0, int(sys.argv[1]) if len(sys.argv) > 1 else 64)
 mgs = [bx.MetaGraph.from_dict(W.as_meta_dict(g)) for g in graphs]
 cm = bx.CommModel(*W.COMM_TEST)
-plan = bx.Plan(mgs, [bx.Job(gi, "m-etf", np.full(n, cap, np.int64), cm) for gi, n, cap in jobs])
+plan = bx.Plan(mgs, [bx.Job(gi, "m-etf", np.full(n, cap, np.int64), cm) for gi, n, cap in jobs], options={"profile": 1})
 plan.upload()
 plan.place()
 plan.download()

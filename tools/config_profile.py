@@ -1,14 +1,13 @@
 """Per-commit latency breakdown (clock64 phases) of the list placer on the
 BASELINE configs and the 100k single-graph cases, for both the warp kernel and
-the round kernel (forced through BX_BIG_MIN).
+the round kernel (forced through plan options).
 
-BX_PROFILE=1 python tools/config_profile.py [case ...]
+python tools/config_profile.py [case ...]
 """
 import json
 import os
 import sys
 
-os.environ.setdefault("BX_PROFILE", "1")
 sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
 
@@ -52,18 +51,23 @@ def main():
     for name, gg, job in cases():
         if want and name not in want:
             continue
-        kerns = os.environ.get("CP_KERNELS", "warp,rounds").split(",")
-        for kern, big_min in (("warp", str(1 << 62)), ("rounds", "0")):
+        kerns = os.environ.get("CP_KERNELS", "small,warp,rounds").split(",")
+        # small: the small-frontier kernel (phases: argmin = keys + selection,
+        # commit = cache arrivals + readiness, remove, rows, cache = re-keys;
+        # steps = rounds)
+        for kern, opts in (("small", {}), ("warp", {"wide_min_vn": (1 << 31) - 1}), ("rounds", {"wide_min_vn": 0})):
             if kern not in kerns:
                 continue
-            os.environ["BX_BIG_MIN"] = big_min
-            plan = bx.Plan([gg], [job])
+            plan = bx.Plan([gg], [job], options=dict(opts, profile=1))
             plan.upload()
             ms = []
             for _ in range(3):
                 plan.place()
                 ms.append(plan.kernel_ms())
             pr = plan.profile(0)
+            if kern == "small" and plan.job_kernel(0) != "small-frontier":
+                plan.close()
+                continue
             commits = max(pr["commits"], 1)
             row = {"case": name, "kernel": kern, "V": gg.V, "n": len(job.capacity), "algo": job.algo,
                    "kernel_ms": round(min(ms), 3), "us_per_commit": round(min(ms) * 1e3 / commits, 3),

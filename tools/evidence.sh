@@ -4,7 +4,7 @@
 # and full captures of the dominant kernels. Outputs in gpurun_out/ev_*.
 set -u
 O=gpurun_out
-export BX_PROFILE=0
+
 timeout 1200 python -m pytest tests -q -m gpu > $O/ev_tests.log 2>&1; echo "tests rc=$?"; tail -2 $O/ev_tests.log
 timeout 600 python bench.py > $O/ev_bench.log 2>&1; echo "bench rc=$?"
 timeout 1500 python tools/latency_table.py layered100k_x4 layered100k_x8 layered100k_x64 grid100k_x8 wide100k_x16 \

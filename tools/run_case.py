@@ -1,6 +1,7 @@
 """Run one placement case once (for ncu captures): python tools/run_case.py CASE [reps]
 CASE is a CONFIGS name or grid100k_x8 / layered100k_x4 / wide100k_x16.
-BX_BIG_MIN selects the kernel (0: round kernel, huge: warp kernel)."""
+RC_KERNEL=small|rounds|warp selects the kernel (default: the plan's own dispatch)."""
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -13,7 +14,9 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 for nm, gg, job in CP.cases():
     if nm != name:
         continue
-    plan = bx.Plan([gg], [job])
+    kern = os.environ.get("RC_KERNEL", "")
+    opts = {"small": None, "rounds": {"wide_min_vn": 0}, "warp": {"wide_min_vn": (1 << 31) - 1}}.get(kern)
+    plan = bx.Plan([gg], [job], options=opts)
     plan.upload()
     for _ in range(reps):
         plan.place()

@@ -1,13 +1,12 @@
 """Per-step latency breakdown of the list placer (clock64 instrumentation).
 
-BX_PROFILE=1 python tools/step_profile.py [workload]
+python tools/step_profile.py [workload]
 Prints, per job, the SM cycles per committed step spent in each phase.
 """
 import json
 import os
 import sys
 
-os.environ["BX_PROFILE"] = "1"
 sys.path.insert(0, ".")
 import numpy as np
 import paper_2301_08695_b200 as bx
@@ -37,7 +36,7 @@ for gi, (g, n) in enumerate(cases):
     jobs.append(bx.Job(gi, "m-etf", np.full(n, W.bench_capacity(g, n, 1.3), np.int64), cm))
 res = []
 for gi in range(len(cases)):
-    plan = bx.Plan([graphs[gi]], [bx.Job(0, "m-etf", jobs[gi].capacity, cm)])
+    plan = bx.Plan([graphs[gi]], [bx.Job(0, "m-etf", jobs[gi].capacity, cm)], options={"profile": 1})
     plan.upload()
     plan.place()
     plan.download()
