@@ -187,6 +187,7 @@ typedef struct {
   int32_t list_len;          /* 4/8/16/32: round-kernel column list length; 0 default */
   int32_t profile;           /* 1: clock64-instrumented placer (bx_plan_profile) */
   int32_t sim_heap_cap;      /* >= 0: shared-memory event heap slice of K4; -1 default */
+  int32_t sim_trace;         /* 1: simulations record SimOptions::record_trace events (bx_plan_sim_trace) */
 } bx_plan_options;
 
 int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs,
@@ -287,6 +288,104 @@ int bx_round_extract(int32_t V, int32_t E, const int32_t *esrc,
                      const int32_t *edst, const double *x, double threshold,
                      int32_t *fav_child, int32_t *fav_parent, int32_t *stats2,
                      char *msg, int msglen);
+
+/* ---- partial-schedule queries ---------------------------------------------
+ * PlacerState (placers.hpp:49-60) flattened: mode is PlacerState::mode (the
+ * queue discipline of the estimate), cache_arrival is [V*n] row-major by
+ * meta node, -1 = absent. */
+typedef struct {
+  int32_t V, n, mode;             /* mode: BX_COMM_* */
+  const int64_t *dev_free;        /* [n] */
+  const int64_t *xfer_tail;       /* [n] */
+  const int32_t *device_of;       /* [V] -1 = unplaced */
+  const int64_t *finish_us;       /* [V] */
+  const int64_t *cache_arrival;   /* [V*n] */
+} bx_placer_state;
+
+/* schedulable_time (placers.hpp:66-67, placers.cpp:43-91) of `count` (node,
+ * device) queries against one partial schedule, evaluated on the GPU (one
+ * thread per query): out[i] = earliest start of node[i] on device[i]. The
+ * state is not modified (the sequential-mode queue tails are folded on a
+ * private copy, as the reference's estimate does). In sequential mode an
+ * uncached remote parent must be placed (the reference indexes its queue). */
+int bx_schedulable_time(const bx_graph *graph, const bx_comm *cm, const bx_placer_state *state, int32_t count,
+                        const int32_t *node, const int32_t *device, int64_t *out, char *msg, int msglen);
+
+/* critical_path_us (simulator.cpp:296-309): the compute-weighted longest
+ * path of the meta graph (a level-synchronous peel on the GPU). Cyclic
+ * graphs fail with meta_topo_order's CycleError text (BX_VALIDATION). */
+int bx_critical_path_us(const bx_graph *graph, int64_t *out_us, char *msg, int msglen);
+
+/* ---- simulator trace (SimOptions::record_trace, simulator.hpp:19-37) ------ */
+#define BX_TRACE_START 0
+#define BX_TRACE_FINISH 1
+#define BX_TRACE_XFER_BEGIN 2
+#define BX_TRACE_XFER_END 3
+typedef struct {
+  int64_t time_us;
+  int32_t device;
+  int32_t event;   /* BX_TRACE_* ("start" | "finish" | "xfer_begin" | "xfer_end") */
+  int64_t node;    /* base node id of the meta node's first member */
+} bx_trace_event;
+
+/* bx_simulate with record_trace: `trace` receives SimReport::trace in the
+ * reference's processing order (at most trace_cap events; *trace_len = the
+ * number recorded, 2V + 2E bounds it). */
+int bx_simulate_trace(const bx_graph *graph, int32_t n, const int64_t *capacity, const bx_comm *cm,
+                      int32_t mem_mode, const int32_t *device_of, const int32_t *exec_order,
+                      const int32_t *exec_off, bx_sim_report *out, bx_trace_event *trace, int64_t trace_cap,
+                      int64_t *trace_len);
+/* The trace of job `job` of a plan created with bx_plan_options.sim_trace. */
+int bx_plan_sim_trace(bx_plan *plan, int32_t job, bx_trace_event *out, int64_t cap, int64_t *len);
+/* trace_to_csv (simulator.cpp:311-324): header "time_us,device,event,node",
+ * rows stable-sorted by time. Writes a NUL-terminated string into buf when
+ * buflen >= *needed (else BX_VALIDATION and only *needed is set). */
+int bx_trace_to_csv(const bx_trace_event *trace, int64_t count, char *buf, int64_t buflen, int64_t *needed);
+
+/* ---- interchange IO (host C++, csrc/jsonio.cpp) ----------------------------
+ * JSON texts are read in one schema-directed pass (no DOM) with the
+ * reference's validation order and messages; emitted texts are
+ * byte-identical to nlohmann's dump(2) + "\n" as the reference writes them.
+ * Emitters write a NUL-terminated string into buf when buflen >= *needed,
+ * else return BX_VALIDATION with only *needed set. */
+
+/* parse_comm_model / load_comm_model / save_comm_model (cost_model.cpp:71-134). */
+int bx_comm_model_parse(const char *text, int64_t len, bx_comm *out, char *msg, int msglen);
+int bx_comm_model_load(const char *path, bx_comm *out, char *msg, int msglen);
+int bx_comm_model_to_json(const bx_comm *cm, char *buf, int64_t buflen, int64_t *needed);
+
+/* parse_graph / load_graph (graph.cpp:196-281) up to, not including,
+ * make_graph: the parsed base graph (file order) with its node names and
+ * colocation groups as labels (labels index the sorted distinct group
+ * strings). bx_grouped_create runs make_graph + the transforms on the view. */
+typedef struct bx_json_graph bx_json_graph;
+int bx_graph_parse(const char *text, int64_t len, bx_json_graph **out, char *msg, int msglen);
+int bx_graph_load(const char *path, bx_json_graph **out, char *msg, int msglen);
+int bx_json_graph_view(const bx_json_graph *g, bx_base_graph *base, const char *const **names,
+                       const char *const **groups, int32_t *ngroups);
+void bx_json_graph_destroy(bx_json_graph *g);
+/* graph_to_json (graph.cpp:283-309) of a ProfiledGraph: nodes by ascending
+ * id, edges by (src, dst). names [nodes] / groups [labels] may be NULL. */
+int bx_graph_to_json(const bx_base_graph *g, const char *const *names, const char *const *groups, char *buf,
+                     int64_t buflen, int64_t *needed);
+
+/* placement_to_json / placement_from_json (placers.cpp:367-432). The
+ * grouping is the GroupedGraph's (bx_grouped_view). to_json writes one row
+ * per base member of every meta node in exec order with its simulated
+ * start; from_json fills device_of/start_us [V] and exec lists (file order). */
+int bx_placement_to_json(const bx_grouping *grouping, const char *algorithm, int32_t n, const int32_t *exec_order,
+                         const int32_t *exec_off, const int64_t *sim_start_us, int64_t makespan_us,
+                         const int64_t *peak_bytes, char *buf, int64_t buflen, int64_t *needed);
+int bx_placement_from_json(const bx_grouping *grouping, int32_t V, const char *text, int64_t len, int32_t n,
+                           char *algorithm, int algolen, int32_t *device_of, int64_t *start_us,
+                           int32_t *exec_order, int32_t *exec_off, char *msg, int msglen);
+
+/* Binary CSR sidecar of a meta graph: save, and load into an owned copy
+ * whose bx_graph view feeds bx_plan_create directly (adjacency checked). */
+typedef struct bx_bin_graph bx_bin_graph;
+int bx_graph_save_bin(const bx_graph *graph, const char *path, char *msg, int msglen);
+int bx_graph_load_bin(const char *path, bx_bin_graph **out, bx_graph *view, char *msg, int msglen);
+void bx_bin_graph_destroy(bx_bin_graph *g);
 
 #ifdef __cplusplus
 }

@@ -138,8 +138,92 @@ class Ref:
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_void_p, cp, ip]
+            i64p, vp = C.POINTER(C.c_int64), C.c_void_p
+            L.ref_simulate_trace_csv.argtypes = [vp, C.c_int32, _i64p, C.c_double, C.c_double, C.c_int32,
+                                                 C.c_int32, _i32p, _i32p, _i32p, vp, C.c_int64, i64p, i64p,
+                                                 cp, ip]
+            L.ref_graph_json_roundtrip.argtypes = [cp, C.c_int64, vp, C.c_int64, i64p, cp, ip]
+            L.ref_graph_to_json.argtypes = [vp, vp, C.c_int64, i64p]
+            L.ref_comm_model_roundtrip.argtypes = [cp, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                                   C.POINTER(C.c_int32), vp, C.c_int64, i64p, cp, ip]
+            L.ref_placement_to_json.argtypes = [vp, cp, C.c_int32, _i32p, _i32p, _i32p, _i64p, C.c_int64, _i64p,
+                                                vp, C.c_int64, i64p]
+            L.ref_placement_from_json.argtypes = [vp, cp, C.c_int64, C.c_int32, cp, ip, _i32p, _i64p, _i32p,
+                                                  _i32p, cp, ip]
             cls._lib = L
         return cls._lib
+
+    @staticmethod
+    def _text(call):
+        """Two-phase string result: call(buf, buflen, needed_ptr) -> rc."""
+        need = C.c_int64(0)
+        rc = call(None, 0, C.byref(need))
+        if need.value <= 0:
+            return rc, ""
+        buf = C.create_string_buffer(need.value)
+        rc = call(buf, need.value, C.byref(need))
+        return rc, buf.value.decode("utf-8")
+
+    @classmethod
+    def simulate_trace_csv(cls, rg, caps, cm, mem_mode, device_of, exec_order, exec_off):
+        """simulate(record_trace) + trace_to_csv -> (csv text, event count)."""
+        caps = _a(caps, np.int64)
+        err = C.create_string_buffer(4096)
+        ev = C.c_int64()
+        args = (_a(device_of, np.int32), _a(exec_order, np.int32), _a(exec_off, np.int32))
+        rc, text = cls._text(lambda b, bl, nd: cls.lib().ref_simulate_trace_csv(
+            rg.h, len(caps), caps, cm[0], cm[1], cm[2], mem_mode, *args, b, bl, nd, C.byref(ev), err, 4096))
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return text, ev.value
+
+    @classmethod
+    def graph_json_roundtrip(cls, text: str) -> str:
+        """parse_graph(text) -> graph_to_json."""
+        raw = text.encode("utf-8")
+        err = C.create_string_buffer(4096)
+        rc, out = cls._text(lambda b, bl, nd: cls.lib().ref_graph_json_roundtrip(raw, len(raw), b, bl, nd, err,
+                                                                                 4096))
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return out
+
+    @classmethod
+    def graph_to_json(cls, rg) -> str:
+        return cls._text(lambda b, bl, nd: cls.lib().ref_graph_to_json(rg.h, b, bl, nd))[1]
+
+    @classmethod
+    def comm_model_roundtrip(cls, text: str):
+        """parse_comm_model(text) -> ((ic, pb, mode), save_comm_model text)."""
+        raw = text.encode("utf-8")
+        err = C.create_string_buffer(4096)
+        ic, pb, md = C.c_double(), C.c_double(), C.c_int32()
+        rc, out = cls._text(lambda b, bl, nd: cls.lib().ref_comm_model_roundtrip(
+            raw, len(raw), C.byref(ic), C.byref(pb), C.byref(md), b, bl, nd, err, 4096))
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return (ic.value, pb.value, md.value), out
+
+    @classmethod
+    def placement_to_json(cls, rg, algorithm, device_of, exec_order, exec_off, sim_start, makespan, peaks) -> str:
+        off = _a(exec_off, np.int32)
+        args = (_a(device_of, np.int32), _a(exec_order, np.int32), off, _a(sim_start, np.int64), int(makespan),
+                _a(peaks, np.int64))
+        return cls._text(lambda b, bl, nd: cls.lib().ref_placement_to_json(
+            rg.h, algorithm.encode(), len(off) - 1, *args, b, bl, nd))[1]
+
+    @classmethod
+    def placement_from_json(cls, rg, text: str, n: int):
+        V = rg.sizes()[2]
+        raw = text.encode("utf-8")
+        algo = C.create_string_buffer(256)
+        dev, st = np.zeros(max(V, 1), np.int32), np.zeros(max(V, 1), np.int64)
+        eo, off = np.zeros(max(V, 1), np.int32), np.zeros(n + 1, np.int32)
+        err = C.create_string_buffer(4096)
+        rc = cls.lib().ref_placement_from_json(rg.h, raw, len(raw), n, algo, 256, dev, st, eo, off, err, 4096)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return algo.value.decode(), Placement(dev[:V], st[:V], eo[:V], off)
 
     # ---- graphs ----------------------------------------------------------
     class Graph:

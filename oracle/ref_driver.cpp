@@ -17,6 +17,10 @@
 //   schedulable_time        proj/src/placers.cpp:83
 //   simulate                proj/src/simulator.cpp:273
 //   critical_path_us        proj/src/simulator.cpp:296
+//   trace_to_csv            proj/src/simulator.cpp:311
+//   parse_graph/graph_to_json         proj/src/graph.cpp:196-309
+//   parse/save_comm_model             proj/src/cost_model.cpp:71-134
+//   placement_to_json/_from_json      proj/src/placers.cpp:367-432
 //   generate_graph          proj/src/generator.cpp:173
 // The pipeline composition mirrors build_grouped (proj/src/bench.cpp:43-49)
 // and the sweep's capacity rule bench_capacity (proj/src/bench.cpp:77-87);
@@ -27,6 +31,9 @@
 #include <omp.h>
 
 #include <chrono>
+#include <cstdio>
+#include <fstream>
+#include <sstream>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -489,6 +496,93 @@ int ref_generate(int32_t family, int32_t node_count, int32_t branching,
       dst[e] = g.edges[e].dst;
       bytes[e] = g.edges[e].tensor_bytes;
     }
+  });
+}
+
+// Copies a string result into a caller buffer (two-phase: needed first).
+static int put_text(const std::string& s, char* buf, int64_t buflen, int64_t* needed) {
+  *needed = static_cast<int64_t>(s.size()) + 1;
+  if (!buf || buflen < *needed) return 1;
+  std::memcpy(buf, s.data(), s.size());
+  buf[s.size()] = '\0';
+  return 0;
+}
+
+// simulate with SimOptions{record_trace = true}, then trace_to_csv.
+int ref_simulate_trace_csv(void* h, int32_t n, const int64_t* caps, double intercept, double per_byte, int32_t mode,
+                           int32_t mem_mode, const int32_t* device_of, const int32_t* exec_order,
+                           const int32_t* exec_off, char* buf, int64_t buflen, int64_t* needed, int64_t* events,
+                           char* err, int errlen) {
+  auto* rg = static_cast<RefGraph*>(h);
+  *needed = 0;
+  return guarded(err, errlen, [&] {
+    SimOptions opt;
+    opt.record_trace = true;
+    Placement p = import_placement(rg->gg, n, device_of, exec_order, exec_off);
+    SimReport r = simulate(rg->gg, p, make_roster(n, caps), make_cm(intercept, per_byte, mode),
+                           mem_mode == 1 ? MemoryMode::TrainingPersistent : MemoryMode::GraphStatic, opt);
+    *events = static_cast<int64_t>(r.trace.size());
+    put_text(trace_to_csv(r.trace), buf, buflen, needed);
+  });
+}
+
+// parse_graph(text) then graph_to_json of the result.
+int ref_graph_json_roundtrip(const char* text, int64_t len, char* buf, int64_t buflen, int64_t* needed, char* err,
+                             int errlen) {
+  *needed = 0;
+  return guarded(err, errlen, [&] {
+    ProfiledGraph g = parse_graph(std::string(text, static_cast<size_t>(len)));
+    put_text(graph_to_json(g), buf, buflen, needed);
+  });
+}
+
+// graph_to_json of a handle's base graph (names "n<id>", groups "g<label>").
+int ref_graph_to_json(void* h, char* buf, int64_t buflen, int64_t* needed) {
+  return put_text(graph_to_json(*static_cast<RefGraph*>(h)->base), buf, buflen, needed);
+}
+
+// parse_comm_model(text) then save_comm_model's text (written to a temp file
+// by the reference and read back).
+int ref_comm_model_roundtrip(const char* text, int64_t len, double* ic, double* pb, int32_t* mode, char* buf,
+                             int64_t buflen, int64_t* needed, char* err, int errlen) {
+  *needed = 0;
+  return guarded(err, errlen, [&] {
+    CommModel cm = parse_comm_model(std::string(text, static_cast<size_t>(len)));
+    *ic = cm.intercept_us;
+    *pb = cm.us_per_byte;
+    *mode = cm.mode == CommMode::Parallel ? 1 : 0;
+    char path[] = "/tmp/bx_cm_XXXXXX";
+    int fd = mkstemp(path);
+    if (fd >= 0) close(fd);
+    save_comm_model(cm, path);
+    std::ifstream in(path);
+    std::ostringstream b;
+    b << in.rdbuf();
+    std::remove(path);
+    put_text(b.str(), buf, buflen, needed);
+  });
+}
+
+// placement_to_json of an external placement with a simulated report.
+int ref_placement_to_json(void* h, const char* algorithm, int32_t n, const int32_t* device_of,
+                          const int32_t* exec_order, const int32_t* exec_off, const int64_t* sim_start,
+                          int64_t makespan, const int64_t* peaks, char* buf, int64_t buflen, int64_t* needed) {
+  auto* rg = static_cast<RefGraph*>(h);
+  Placement p = import_placement(rg->gg, n, device_of, exec_order, exec_off);
+  p.algorithm = algorithm;
+  std::vector<micros_t> st(sim_start, sim_start + rg->gg.node_count());
+  std::vector<bytes_t> pk(peaks, peaks + n);
+  return put_text(placement_to_json(rg->gg, p, st, makespan, pk), buf, buflen, needed);
+}
+
+int ref_placement_from_json(void* h, const char* text, int64_t len, int32_t n, char* algorithm, int algolen,
+                            int32_t* device_of, int64_t* start, int32_t* exec_order, int32_t* exec_off, char* err,
+                            int errlen) {
+  auto* rg = static_cast<RefGraph*>(h);
+  return guarded(err, errlen, [&] {
+    Placement p = placement_from_json(rg->gg, std::string(text, static_cast<size_t>(len)), n);
+    put(algorithm, algolen, p.algorithm);
+    export_placement(p, device_of, start, exec_order, exec_off);
   });
 }
 

@@ -14,6 +14,12 @@ reference              here
 ``verify_placement``   :func:`verify_placement` (simulator.hpp:64-67)
 ``round_and_extract``  :func:`round_and_extract` (lp.hpp:88-90)
 ``comm_time``          :func:`comm_time`    (cost_model.hpp:29)
+``schedulable_time``   :func:`schedulable_time` (placers.hpp:66-67)
+``critical_path_us``   :func:`critical_path_us` (simulator.hpp:69)
+``trace_to_csv``       :func:`trace_to_csv` (simulator.hpp:71)
+``parse_comm_model``   :func:`parse_comm_model` / ``load_comm_model`` / ``save_comm_model``
+``parse_graph``        :func:`parse_graph` / ``load_graph`` / :func:`graph_to_json`
+``placement_to_json``  :func:`placement_to_json` / :func:`placement_from_json`
 ``max_comm_time``      :func:`max_comm_time` (cost_model.hpp:71)
 ``ValidationError``..  same names (errors.hpp:10-51)
 =====================  ==============================================
@@ -122,12 +128,22 @@ class _Job(C.Structure):
 
 class _PlanOptions(C.Structure):
     _fields_ = [("no_small_frontier", C.c_int32), ("wide_min_vn", C.c_int32), ("wide_max_jobs", C.c_int32),
-                ("list_len", C.c_int32), ("profile", C.c_int32), ("sim_heap_cap", C.c_int32)]
+                ("list_len", C.c_int32), ("profile", C.c_int32), ("sim_heap_cap", C.c_int32),
+                ("sim_trace", C.c_int32)]
+
+
+class _PlacerState(C.Structure):
+    _fields_ = [("V", C.c_int32), ("n", C.c_int32), ("mode", C.c_int32), ("dev_free", _vp), ("xfer_tail", _vp),
+                ("device_of", _vp), ("finish_us", _vp), ("cache_arrival", _vp)]
+
+
+class _TraceEvent(C.Structure):
+    _fields_ = [("time_us", C.c_int64), ("device", C.c_int32), ("event", C.c_int32), ("node", C.c_int64)]
 
 
 def _options(opts):
     """bx_plan_options from a dict (keys = field names); None = defaults."""
-    o = _PlanOptions(0, -1, 0, 0, 0, -1)
+    o = _PlanOptions(0, -1, 0, 0, 0, -1, 0)
     for k, v in (opts or {}).items():
         if k not in dict(_PlanOptions._fields_):
             raise ValueError(f"unknown plan option {k!r}")
@@ -193,6 +209,31 @@ def lib():
         L.bx_lp_solve.argtypes = [C.POINTER(_Graph), C.POINTER(_Comm), C.c_double, _vp, _vp,
                                    C.POINTER(_LpInfo), cp, C.c_int]
         L.bx_round_extract.argtypes = [i32, i32, _vp, _vp, _vp, C.c_double, _vp, _vp, _vp, cp, C.c_int]
+        i64p = C.POINTER(i64)
+        L.bx_schedulable_time.argtypes = [C.POINTER(_Graph), C.POINTER(_Comm), C.POINTER(_PlacerState), i32, _vp,
+                                          _vp, _vp, cp, C.c_int]
+        L.bx_critical_path_us.argtypes = [C.POINTER(_Graph), i64p, cp, C.c_int]
+        L.bx_simulate_trace.argtypes = [C.POINTER(_Graph), i32, _vp, C.POINTER(_Comm), i32, _vp, _vp, _vp,
+                                        C.POINTER(_SimReport), _vp, i64, i64p]
+        L.bx_plan_sim_trace.argtypes = [_vp, i32, _vp, i64, i64p]
+        L.bx_trace_to_csv.argtypes = [_vp, i64, _vp, i64, i64p]
+        L.bx_comm_model_parse.argtypes = [cp, i64, C.POINTER(_Comm), cp, C.c_int]
+        L.bx_comm_model_load.argtypes = [cp, C.POINTER(_Comm), cp, C.c_int]
+        L.bx_comm_model_to_json.argtypes = [C.POINTER(_Comm), _vp, i64, i64p]
+        L.bx_graph_parse.argtypes = [cp, i64, C.POINTER(_vp), cp, C.c_int]
+        L.bx_graph_load.argtypes = [cp, C.POINTER(_vp), cp, C.c_int]
+        L.bx_json_graph_view.argtypes = [_vp, C.POINTER(_BaseGraph), C.POINTER(_vp), C.POINTER(_vp),
+                                         C.POINTER(i32)]
+        L.bx_json_graph_destroy.argtypes = [_vp]
+        L.bx_json_graph_destroy.restype = None
+        L.bx_graph_to_json.argtypes = [C.POINTER(_BaseGraph), _vp, _vp, _vp, i64, i64p]
+        L.bx_placement_to_json.argtypes = [C.POINTER(_Grouping), cp, i32, _vp, _vp, _vp, i64, _vp, _vp, i64, i64p]
+        L.bx_placement_from_json.argtypes = [C.POINTER(_Grouping), i32, cp, i64, i32, cp, C.c_int, _vp, _vp, _vp,
+                                             _vp, cp, C.c_int]
+        L.bx_graph_save_bin.argtypes = [C.POINTER(_Graph), cp, cp, C.c_int]
+        L.bx_graph_load_bin.argtypes = [cp, C.POINTER(_vp), C.POINTER(_Graph), cp, C.c_int]
+        L.bx_bin_graph_destroy.argtypes = [_vp]
+        L.bx_bin_graph_destroy.restype = None
         _lib = L
     return _lib
 
@@ -201,7 +242,11 @@ EXPORTED = ["bx_version", "bx_last_error", "bx_device_count", "bx_comm_time", "b
             "bx_plan_create_ex", "bx_plan_job_kernel", "bx_simulate_ex",
             "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download", "bx_plan_result_view",
             "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_profile", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
-            "bx_simulate", "bx_round_extract", "bx_grouped_create", "bx_grouped_view", "bx_grouped_destroy", "bx_lp_solve"]
+            "bx_simulate", "bx_round_extract", "bx_grouped_create", "bx_grouped_view", "bx_grouped_destroy", "bx_lp_solve",
+            "bx_schedulable_time", "bx_critical_path_us", "bx_simulate_trace", "bx_plan_sim_trace", "bx_trace_to_csv",
+            "bx_comm_model_parse", "bx_comm_model_load", "bx_comm_model_to_json", "bx_graph_parse", "bx_graph_load",
+            "bx_json_graph_view", "bx_json_graph_destroy", "bx_graph_to_json", "bx_placement_to_json",
+            "bx_placement_from_json", "bx_graph_save_bin", "bx_graph_load_bin", "bx_bin_graph_destroy"]
 
 
 def _ptr(a):
@@ -284,6 +329,18 @@ class Placement:
 
 
 @dataclass
+class TraceEvent:
+    """TraceEvent (simulator.hpp:18-23)."""
+    time_us: int
+    device: int
+    event: str  # start | finish | xfer_begin | xfer_end
+    node: int
+
+
+TRACE_EVENTS = ("start", "finish", "xfer_begin", "xfer_end")
+
+
+@dataclass
 class SimReport:
     """SimReport (simulator.hpp:25-34)."""
     makespan_us: int
@@ -295,6 +352,7 @@ class SimReport:
     transfer_bytes: int
     duplicate_transfers: int
     cache_hits: int
+    trace: list = field(default_factory=list)
 
 
 @dataclass
@@ -533,7 +591,9 @@ def place_msct(gg: MetaGraph, capacity, cm: CommModel, fav_child=None, stats_out
 
 
 def simulate(gg: MetaGraph, placement: Placement, capacity, cm: CommModel,
-             mem_mode: int = TRAINING_PERSISTENT, options: dict | None = None) -> SimReport:
+             mem_mode: int = TRAINING_PERSISTENT, options: dict | None = None,
+             record_trace: bool = False) -> SimReport:
+    """simulate (simulator.hpp:53-55); record_trace = SimOptions::record_trace."""
     cap = _c(capacity, np.int64)
     n = len(cap)
     V = gg.V
@@ -547,11 +607,21 @@ def simulate(gg: MetaGraph, placement: Placement, capacity, cm: CommModel,
     g = gg._c()
     cmc = cm._c()
     opt = _options(options)
-    lib().bx_simulate_ex(C.byref(g), n, _ptr(cap), C.byref(cmc), mem_mode, _ptr(dev), _ptr(eo), _ptr(off),
-                         C.byref(opt), C.byref(rep))
+    trace = []
+    if record_trace:
+        cap_ev = 2 * V + 2 * gg.E + 4
+        tb = (_TraceEvent * cap_ev)()
+        tl = C.c_int64()
+        lib().bx_simulate_trace(C.byref(g), n, _ptr(cap), C.byref(cmc), mem_mode, _ptr(dev), _ptr(eo), _ptr(off),
+                                C.byref(rep), tb, cap_ev, C.byref(tl))
+        trace = [TraceEvent(tb[i].time_us, tb[i].device, TRACE_EVENTS[tb[i].event], tb[i].node)
+                 for i in range(min(tl.value, cap_ev))]
+    else:
+        lib().bx_simulate_ex(C.byref(g), n, _ptr(cap), C.byref(cmc), mem_mode, _ptr(dev), _ptr(eo), _ptr(off),
+                             C.byref(opt), C.byref(rep))
     _raise(rep.status, rep.msg.decode())
     return SimReport(rep.makespan_us, b[0][:V].copy(), b[1][:n].copy(), b[2][:n].copy(), b[3][:n].copy(),
-                     rep.transfer_count, rep.transfer_bytes, rep.duplicate_transfers, rep.cache_hits)
+                     rep.transfer_count, rep.transfer_bytes, rep.duplicate_transfers, rep.cache_hits, trace)
 
 
 def verify_placement(gg, placement, capacity, cm, mem_mode=TRAINING_PERSISTENT):
@@ -637,3 +707,220 @@ def max_comm_time(gg: MetaGraph, cm: CommModel) -> int:
 
 def device_count() -> int:
     return lib().bx_device_count()
+
+
+# ---- partial-schedule queries (placers.hpp:49-67, simulator.hpp:69) --------
+class PlacerState:
+    """PlacerState (placers.hpp:49-60): dev_free / xfer_tail [n], device_of /
+    finish_us [V], cache_arrival [V*n] (-1 absent); initialised as the
+    reference's constructor does (placers.cpp:31-37)."""
+
+    def __init__(self, meta_count: int, device_count: int, mode: int):
+        self.mode = int(mode)
+        self.dev_free = np.zeros(device_count, np.int64)
+        self.xfer_tail = np.zeros(device_count, np.int64)
+        self.device_of = np.full(meta_count, -1, np.int32)
+        self.finish_us = np.zeros(meta_count, np.int64)
+        self.cache_arrival = np.full(meta_count * device_count, -1, np.int64)
+
+    def _c(self):
+        self._keep = [_c(a, dt) for a, dt in ((self.dev_free, np.int64), (self.xfer_tail, np.int64),
+                                              (self.device_of, np.int32), (self.finish_us, np.int64),
+                                              (self.cache_arrival, np.int64))]
+        k = self._keep
+        return _PlacerState(len(k[2]), len(k[0]), self.mode, *[_ptr(a) for a in k])
+
+
+def schedulable_times(st: PlacerState, nodes, devices, gg: MetaGraph, cm: CommModel) -> np.ndarray:
+    """schedulable_time (placers.cpp:83-91) for every (nodes[i], devices[i]),
+    evaluated on the GPU in one launch."""
+    js, ps = _c(nodes, np.int32), _c(devices, np.int32)
+    out = np.zeros(max(len(js), 1), np.int64)
+    msg = C.create_string_buffer(512)
+    g, cmc, sc = gg._c(), cm._c(), st._c()
+    rc = lib().bx_schedulable_time(C.byref(g), C.byref(cmc), C.byref(sc), len(js), _ptr(js), _ptr(ps), _ptr(out),
+                                   msg, 512)
+    _raise(rc, msg.value.decode())
+    return out[:len(js)]
+
+
+def schedulable_time(st: PlacerState, j: int, p: int, gg: MetaGraph, cm: CommModel) -> int:
+    """schedulable_time (placers.hpp:66-67): earliest start of j on p."""
+    return int(schedulable_times(st, [j], [p], gg, cm)[0])
+
+
+def critical_path_us(gg: MetaGraph) -> int:
+    """critical_path_us (simulator.cpp:296-309) on the GPU."""
+    out = C.c_int64()
+    msg = C.create_string_buffer(4096)
+    g = gg._c()
+    rc = lib().bx_critical_path_us(C.byref(g), C.byref(out), msg, 4096)
+    _raise(rc, msg.value.decode())
+    return out.value
+
+
+def _text(call) -> tuple[int, str]:
+    need = C.c_int64(0)
+    call(None, 0, C.byref(need))
+    buf = C.create_string_buffer(max(need.value, 1))
+    rc = call(buf, need.value, C.byref(need))
+    return rc, buf.value.decode("utf-8")
+
+
+def trace_to_csv(trace: list) -> str:
+    """trace_to_csv (simulator.cpp:311-324)."""
+    arr = (_TraceEvent * max(len(trace), 1))()
+    for i, ev in enumerate(trace):
+        arr[i] = _TraceEvent(ev.time_us, ev.device, TRACE_EVENTS.index(ev.event), ev.node)
+    return _text(lambda b, bl, nd: lib().bx_trace_to_csv(arr, len(trace), b, bl, nd))[1]
+
+
+# ---- interchange IO (csrc/jsonio.cpp) -------------------------------------
+def parse_comm_model(text: str) -> CommModel:
+    """parse_comm_model (cost_model.cpp:71-111)."""
+    raw = text.encode("utf-8")
+    out = _Comm()
+    msg = C.create_string_buffer(1024)
+    rc = lib().bx_comm_model_parse(raw, len(raw), C.byref(out), msg, 1024)
+    _raise(rc, msg.value.decode())
+    return CommModel(out.intercept_us, out.us_per_byte, out.mode)
+
+
+def load_comm_model(path: str) -> CommModel:
+    """load_comm_model (cost_model.cpp:113-122), e.g. comm_model_test.json."""
+    out = _Comm()
+    msg = C.create_string_buffer(1024)
+    rc = lib().bx_comm_model_load(os.fsencode(path), C.byref(out), msg, 1024)
+    _raise(rc, msg.value.decode())
+    return CommModel(out.intercept_us, out.us_per_byte, out.mode)
+
+
+def comm_model_to_json(cm: CommModel) -> str:
+    """The text save_comm_model writes (cost_model.cpp:124-134)."""
+    c = cm._c()
+    return _text(lambda b, bl, nd: lib().bx_comm_model_to_json(C.byref(c), b, bl, nd))[1]
+
+
+def save_comm_model(cm: CommModel, path: str) -> None:
+    with open(path, "w") as f:
+        f.write(comm_model_to_json(cm))
+
+
+class JsonGraph:
+    """A parsed graph file (parse_graph, graph.cpp:196-272, before
+    make_graph): ``base`` is the dict build_grouped takes, plus node names
+    and colocation group strings."""
+
+    def __init__(self, handle):
+        self.h = handle
+        bg = _BaseGraph()
+        names, groups, ng = _vp(), _vp(), C.c_int32()
+        lib().bx_json_graph_view(handle, C.byref(bg), C.byref(names), C.byref(groups), C.byref(ng))
+        n, e = bg.nodes, bg.edges
+        i64, i32, u8 = C.c_int64, C.c_int32, C.c_uint8
+        self.base = dict(id=_arr(bg.id, i64, n, np.int64), k=_arr(bg.compute_us, i64, n, np.int64),
+                         temp=_arr(bg.temp_bytes, i64, n, np.int64), perm=_arr(bg.perm_bytes, i64, n, np.int64),
+                         out=_arr(bg.out_bytes, i64, n, np.int64), coloc=_arr(bg.coloc_label, i32, n, np.int32),
+                         has_pair=_arr(bg.has_pair, u8, n, np.uint8),
+                         pair=_arr(bg.coplace_peer, i64, n, np.int64), src=_arr(bg.src, i64, e, np.int64),
+                         dst=_arr(bg.dst, i64, e, np.int64), bytes=_arr(bg.tensor_bytes, i64, e, np.int64))
+        npp = C.cast(names, C.POINTER(C.c_char_p))
+        gpp = C.cast(groups, C.POINTER(C.c_char_p))
+        self.names = [npp[i].decode("utf-8") for i in range(n)]
+        self.groups = [gpp[i].decode("utf-8") for i in range(ng.value)]
+        lib().bx_json_graph_destroy(handle)
+        self.h = None
+
+
+def parse_graph(text: str) -> JsonGraph:
+    """parse_graph (graph.cpp:196-262) up to make_graph (run by build_grouped)."""
+    raw = text.encode("utf-8")
+    h = _vp()
+    msg = C.create_string_buffer(4096)
+    rc = lib().bx_graph_parse(raw, len(raw), C.byref(h), msg, 4096)
+    _raise(rc, msg.value.decode())
+    return JsonGraph(h)
+
+
+def load_graph(path: str) -> JsonGraph:
+    h = _vp()
+    msg = C.create_string_buffer(4096)
+    rc = lib().bx_graph_load(os.fsencode(path), C.byref(h), msg, 4096)
+    _raise(rc, msg.value.decode())
+    return JsonGraph(h)
+
+
+def graph_to_json(base: dict, names=None, groups=None) -> str:
+    """graph_to_json (graph.cpp:283-309) of a base graph dict."""
+    n = len(base["id"])
+    keep = {k: _c(base[k], np.int64) for k in ("id", "k", "temp", "perm", "out", "src", "dst", "bytes")}
+    coloc = base.get("coloc")
+    keep["coloc"] = None if coloc is None else _c(coloc, np.int32)
+    hp = base.get("has_pair")
+    keep["has_pair"] = None if hp is None else _c(hp, np.uint8)
+    keep["pair"] = None if hp is None else _c(base["pair"], np.int64)
+    g = _BaseGraph(n, _ptr(keep["id"]), _ptr(keep["k"]), _ptr(keep["temp"]), _ptr(keep["perm"]),
+                   _ptr(keep["out"]), _ptr(keep["coloc"]), _ptr(keep["has_pair"]), _ptr(keep["pair"]),
+                   len(keep["src"]), _ptr(keep["src"]), _ptr(keep["dst"]), _ptr(keep["bytes"]))
+    nm = None if names is None else (C.c_char_p * max(n, 1))(*[x.encode("utf-8") for x in names])
+    gr = None if groups is None else (C.c_char_p * max(len(groups), 1))(*[x.encode("utf-8") for x in groups])
+    return _text(lambda b, bl, nd: lib().bx_graph_to_json(C.byref(g), nm, gr, b, bl, nd))[1]
+
+
+def _grouping_c(grouping: dict):
+    keep = dict(base_ids=_c(grouping["base_ids"], np.int64), group_of=_c(grouping["group_of"], np.int32),
+                members=_c(grouping["members"], np.int32), member_off=_c(grouping["member_off"], np.int32),
+                edge_base_count=_c(grouping.get("edge_base_count", np.zeros(1)), np.int32))
+    return _Grouping(len(keep["base_ids"]), _ptr(keep["base_ids"]), _ptr(keep["group_of"]), _ptr(keep["members"]),
+                     _ptr(keep["member_off"]), _ptr(keep["edge_base_count"])), keep
+
+
+def placement_to_json(grouping: dict, placement: Placement, report: SimReport) -> str:
+    """placement_to_json (placers.cpp:367-386) with a simulated report."""
+    gp, keep = _grouping_c(grouping)
+    eo, off = _c(placement.exec_order_flat, np.int32), _c(placement.exec_off, np.int32)
+    st, pk = _c(report.start_us, np.int64), _c(report.peak_bytes, np.int64)
+    algo = placement.algorithm.encode("utf-8")
+    return _text(lambda b, bl, nd: lib().bx_placement_to_json(C.byref(gp), algo, len(off) - 1, _ptr(eo), _ptr(off),
+                                                              _ptr(st), int(report.makespan_us), _ptr(pk), b,
+                                                              bl, nd))[1]
+
+
+def placement_from_json(grouping: dict, V: int, text: str, device_count: int) -> Placement:
+    """placement_from_json (placers.cpp:388-432)."""
+    gp, keep = _grouping_c(grouping)
+    raw = text.encode("utf-8")
+    algo = C.create_string_buffer(256)
+    dev, st = np.zeros(max(V, 1), np.int32), np.zeros(max(V, 1), np.int64)
+    eo, off = np.zeros(max(V, 1), np.int32), np.zeros(device_count + 1, np.int32)
+    msg = C.create_string_buffer(1024)
+    rc = lib().bx_placement_from_json(C.byref(gp), V, raw, len(raw), device_count, algo, 256, _ptr(dev), _ptr(st),
+                                      _ptr(eo), _ptr(off), msg, 1024)
+    _raise(rc, msg.value.decode())
+    return Placement(algo.value.decode(), dev[:V].copy(), st[:V].copy(), eo[:V].copy(), off.copy())
+
+
+def save_graph_bin(gg: MetaGraph, path: str) -> None:
+    """Binary CSR sidecar of a meta graph (csrc/jsonio.cpp)."""
+    msg = C.create_string_buffer(1024)
+    g = gg._c()
+    rc = lib().bx_graph_save_bin(C.byref(g), os.fsencode(path), msg, 1024)
+    _raise(rc, msg.value.decode())
+
+
+def load_graph_bin(path: str) -> MetaGraph:
+    h = _vp()
+    v = _Graph()
+    msg = C.create_string_buffer(1024)
+    rc = lib().bx_graph_load_bin(os.fsencode(path), C.byref(h), C.byref(v), msg, 1024)
+    _raise(rc, msg.value.decode())
+    try:
+        i64, i32 = C.c_int64, C.c_int32
+        V, E = v.V, v.E
+        return MetaGraph(_arr(v.compute_us, i64, V, np.int64), _arr(v.temp_bytes, i64, V, np.int64),
+                         _arr(v.perm_bytes, i64, V, np.int64), _arr(v.out_bytes, i64, V, np.int64),
+                         _arr(v.esrc, i32, E, np.int32), _arr(v.edst, i32, E, np.int32),
+                         _arr(v.tensor_bytes, i64, E, np.int64),
+                         None if not v.first_id else _arr(v.first_id, i64, V, np.int64))
+    finally:
+        lib().bx_bin_graph_destroy(h)

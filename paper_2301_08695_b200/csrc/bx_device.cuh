@@ -73,6 +73,7 @@ struct DGraph {
 
 struct DPrep {
   int32_t graph;
+  int32_t first;  // 1: the first prep of its graph derives the graph-level arrays
   double ic, pb;
   int64_t *in_c;   // [E] comm_time of the in-CSR slot's edge
   int64_t *cmax;   // max_comm_time (cost_model.cpp:234-240)
@@ -113,6 +114,14 @@ struct DJob {
   int32_t nucap;  // K2s shared-memory slots reserved for non-uniform producers
   int32_t maxin;  // largest in-degree of the graph (K2s list sizing)
 };
+
+// One chunk of a per-step workspace fill (k_fill); at most kFillChunk bytes.
+struct FillChunk {
+  void *ptr;
+  uint32_t bytes;
+  uint32_t value;
+};
+constexpr size_t kFillChunk = 64 * 1024;
 
 // Per-step latency breakdown slots (clock64 cycles summed over the run, lane 0).
 enum ProfSlot : int {
@@ -156,6 +165,11 @@ struct DSim {
   int64_t *kx;                      // [V] compute time by FIFO slot (-1: never ready)
   int64_t *dv;                      // [4n] per device: peak, violation t, node, memory
   int32_t *ninp;                    // [V] K4: inputs of a node not yet resident on its device
+  // SimOptions::record_trace (simulator.hpp:37): K4 appends (t, device,
+  // event, meta) per event in processing order; null = no trace
+  int64_t *trace;
+  int64_t trace_cap;                // events the buffer holds
+  unsigned long long *trace_n;      // events recorded
   // outputs
   int64_t *start;                   // [V]
   int64_t *dev3n;                   // [3n] peak, busy, idle

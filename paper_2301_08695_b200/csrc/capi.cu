@@ -15,12 +15,15 @@
 #include <vector>
 
 #include "../../include/baechi_b200.h"
+#include "arena.hpp"
 #include "bx_device.cuh"
 
 namespace bx {
-void launch_prep(const DGraph &g, const DPrep &pr, bool first, cudaStream_t s);
+void launch_prep_all(const DGraph *graphs_dev, const DPrep *preps_dev, int nprep, int max_ev, cudaStream_t s);
+void launch_fill(const FillChunk *table, int n, cudaStream_t s);
 void launch_kahn(DGraph *graphs_dev, int32_t *const *queues_dev, int ngraphs, cudaStream_t s);
-cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bit, cudaStream_t s);
+cudaError_t sort_needs_all(void *tmp, size_t &tmp_bytes, const int64_t *need, int64_t *keys_out, const int32_t *iota,
+                           int32_t *order_out, int total, int nseg, const int32_t *seg_off, cudaStream_t s);
 void launch_extract(const XCtx &c, cudaStream_t s);
 void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_etf, int n_bpar, int n_bseq,
                     int njobs, const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo, bool prof,
@@ -58,30 +61,6 @@ std::string fmt(const char *f, ...) {
     }                                                                                 \
   } while (0)
 
-// Bump allocator over one device pool.
-struct Layout {
-  size_t off = 0;
-  size_t align = 256;
-  template <typename T>
-  size_t take(size_t count) {
-    off = (off + align - 1) & ~(align - 1);
-    size_t at = off;
-    off += std::max<size_t>(count, 1) * sizeof(T);
-    return at;
-  }
-};
-
-template <typename T>
-T *at(void *pool, size_t off) {
-  return reinterpret_cast<T *>(static_cast<char *>(pool) + off);
-}
-
-struct HostCopy {  // one H2D or D2H copy
-  void *dst;
-  const void *src;
-  size_t bytes;
-};
-
 struct Fill {  // one memset
   void *ptr;
   int value;
@@ -92,7 +71,7 @@ struct Fill {  // one memset
 
 struct bx_plan {
   int device = 0;
-  bx_plan_options opt{0, -1, 0, 0, 0, -1};
+  bx_plan_options opt{0, -1, 0, 0, 0, -1, 0};
   int ngraphs = 0, njobs = 0, nprep = 0;
   std::vector<bx_graph> hg;
   std::vector<bx_job> hj;
@@ -100,8 +79,14 @@ struct bx_plan {
   std::vector<DPrep> dp;
   std::vector<DJob> dj;
   std::vector<int> prep_first;      // prep index -> 1 if first prep of its graph
-  std::vector<int> sort_bits;       // radix bits covering the graph's largest need
-  std::vector<int> sort_launches;   // kernels the need sort issues
+  int max_ev = 0;                   // largest max(V, E) over graphs (prep grid)
+  int total_V = 0;                  // need arrays of all graphs, concatenated (one segmented sort)
+  int64_t *need_all = nullptr, *need_keys_all = nullptr;
+  int32_t *iota_all = nullptr, *need_order_all = nullptr, *seg_off = nullptr;
+  FillChunk *fill_dev = nullptr;    // per-step fills as k_fill chunks
+  int nfill = 0;
+  FillChunk *sim_fill_dev = nullptr;
+  int nsim_fill = 0;
   std::vector<int> host_status;     // per job host-side validation result
   std::vector<std::string> host_msg;
   void *pool = nullptr;
@@ -156,7 +141,24 @@ struct bx_plan {
   int sim_mem_mode = -1;
   // external placements (bx_simulate)
   bool external = false;
+  // one-shot plans borrow pools, pinned mirrors, streams and events from
+  // the calling thread's arena (arena.hpp) instead of owning them
+  bool borrowed = false;
 };
+
+namespace bx {
+Arena &thread_arena() {
+  static thread_local std::vector<Arena *> per_device;
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    cudaGetLastError();
+    d = 0;
+  }
+  if (static_cast<int>(per_device.size()) <= d) per_device.resize(static_cast<size_t>(d) + 1, nullptr);
+  if (!per_device[d]) per_device[d] = new Arena();
+  return *per_device[d];
+}
+}  // namespace bx
 
 static thread_local std::string g_last_error;
 
@@ -217,12 +219,19 @@ int bx_build_adjacency(int32_t V, int32_t E, const int32_t *esrc, const int32_t 
 void bx_plan_destroy(bx_plan *plan) {
   if (!plan) return;
   cudaSetDevice(plan->device);
+  if (plan->borrowed) {  // pools, tables, streams and events belong to the thread's arena
+    if (plan->prof) cudaFree(plan->prof);
+    delete plan;
+    return;
+  }
   if (plan->pool) cudaFree(plan->pool);
   if (plan->host_in) cudaFreeHost(plan->host_in);
   if (plan->host_out) cudaFreeHost(plan->host_out);
   if (plan->sim_pool) cudaFree(plan->sim_pool);
   if (plan->sort_tmp) cudaFree(plan->sort_tmp);
   if (plan->prof) cudaFree(plan->prof);
+  if (plan->fill_dev) cudaFree(plan->fill_dev);
+  if (plan->sim_fill_dev) cudaFree(plan->sim_fill_dev);
   if (plan->ev[0]) cudaEventDestroy(plan->ev[0]);
   if (plan->ev[1]) cudaEventDestroy(plan->ev[1]);
   if (plan->fork) cudaEventDestroy(plan->fork);
@@ -236,8 +245,47 @@ int bx_plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const
   return bx_plan_create_ex(ngraphs, graphs, njobs, jobs, device, nullptr, out, msg, msglen);
 }
 
-int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const bx_job *jobs, int32_t device,
-                      const bx_plan_options *options, bx_plan **out, char *msg, int msglen) {
+}  // extern "C"
+
+namespace {
+// Splits fills into k_fill chunks and uploads the table: to the arena slot
+// `slot` for borrowed plans (left unowned), else to a fresh allocation.
+int upload_fills(const std::vector<Fill> &fills, Arena *A, int slot, FillChunk **dev, int *n, char *msg,
+                 int msglen) {
+  std::vector<FillChunk> t;
+  for (const Fill &f : fills) {
+    for (size_t o = 0; o < f.bytes; o += kFillChunk) {
+      const size_t b = std::min(kFillChunk, f.bytes - o);
+      t.push_back({static_cast<char *>(f.ptr) + o, static_cast<uint32_t>(b), static_cast<uint32_t>(f.value & 0xff)});
+    }
+  }
+  *n = static_cast<int>(t.size());
+  if (t.empty()) return BX_OK;
+  const size_t bytes = sizeof(FillChunk) * t.size();
+  if (A) {
+    char *pp = nullptr;
+    BX_CUDA(A->device(bytes, &pp, slot), msg, msglen);
+    *dev = nullptr;  // not owned
+    BX_CUDA(cudaMemcpy(pp, t.data(), bytes, cudaMemcpyHostToDevice), msg, msglen);
+    *dev = reinterpret_cast<FillChunk *>(pp);
+    return BX_OK;
+  }
+  BX_CUDA(cudaMalloc(reinterpret_cast<void **>(dev), bytes), msg, msglen);
+  BX_CUDA(cudaMemcpy(*dev, t.data(), bytes, cudaMemcpyHostToDevice), msg, msglen);
+  return BX_OK;
+}
+
+// Frees a half-built plan on every early return of plan_create.
+struct PlanGuard {
+  bx_plan *p = nullptr;
+  ~PlanGuard() {
+    if (p) bx_plan_destroy(p);
+  }
+};
+}  // namespace
+
+static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const bx_job *jobs, int32_t device,
+                       const bx_plan_options *options, bool borrow, bx_plan **out, char *msg, int msglen) {
   *out = nullptr;
   int ndev = bx_device_count();
   if (ndev <= 0) {
@@ -251,7 +299,11 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
   BX_CUDA(cudaSetDevice(device), msg, msglen);
   auto *P = new (std::nothrow) bx_plan();
   if (!P) return BX_RUNTIME;
+  PlanGuard guard;
+  guard.p = P;
   P->device = device;
+  P->borrowed = borrow;
+  Arena *A = borrow ? &thread_arena() : nullptr;
   if (options) P->opt = *options;
   P->ngraphs = ngraphs;
   P->njobs = njobs;
@@ -267,7 +319,6 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
     const bx_job &J = jobs[i];
     if (J.graph < 0 || J.graph >= ngraphs) {
       put_msg(msg, msglen, fmt("job %d names graph %d of %d", i, J.graph, ngraphs));
-      delete P;
       return BX_VALIDATION;
     }
     auto key = std::make_tuple(J.graph, J.cm.intercept_us, J.cm.us_per_byte);
@@ -298,10 +349,8 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
     o.in_off = L.take<int32_t>(G.V + 1);
     o.in_edge = L.take<int32_t>(G.E);
     o.out_off = L.take<int32_t>(G.V + 1);
-    o.need = L.take<int64_t>(G.V);
-    o.need_order = L.take<int32_t>(G.V);
-    o.iota = L.take<int32_t>(G.V);
-    o.need_keys = L.take<int64_t>(G.V);
+    o.need = o.need_order = o.iota = o.need_keys = static_cast<size_t>(P->total_V);  // element offsets
+    P->total_V += G.V;
     o.in_src = L.take<int32_t>(G.E);
     o.inpos = L.take<int32_t>(G.E);
     o.indeg_left = L.take<int32_t>(G.V);
@@ -309,7 +358,11 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
     o.ksum = L.take<int64_t>(1);
     o.queue = L.take<int32_t>(2 * static_cast<size_t>(G.V));
     max_sort_V = std::max(max_sort_V, static_cast<size_t>(G.V));
+    P->max_ev = std::max(P->max_ev, std::max(G.V, G.E));
   }
+  const size_t need_at = L.take<int64_t>(P->total_V), need_keys_at = L.take<int64_t>(P->total_V);
+  const size_t iota_at = L.take<int32_t>(P->total_V), need_order_at = L.take<int32_t>(P->total_V);
+  const size_t seg_at = L.take<int32_t>(size_t(ngraphs) + 1);
   std::vector<std::pair<size_t, size_t>> po(P->nprep);  // in_c, cmax
   struct POff {
     size_t c32, nu, cnt;
@@ -420,18 +473,36 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
   P->in_bytes = LI.off;
   P->out_bytes = LO.off;
   P->pool_bytes = L.off;
-  cudaError_t ce = cudaMalloc(&P->pool, P->pool_bytes);
-  if (ce == cudaSuccess) ce = cudaHostAlloc(&P->host_in, std::max<size_t>(P->in_bytes, 8), cudaHostAllocDefault);
-  if (ce == cudaSuccess) ce = cudaHostAlloc(&P->host_out, std::max<size_t>(P->out_bytes, 8), cudaHostAllocDefault);
+  cudaError_t ce;
+  if (A) {
+    char *pp = nullptr;
+    ce = A->device(P->pool_bytes, &pp, 1);
+    P->pool = pp;
+    if (ce == cudaSuccess) ce = A->pinned(std::max<size_t>(P->in_bytes, 8), &P->host_in, 0);
+    if (ce == cudaSuccess) ce = A->pinned(std::max<size_t>(P->out_bytes, 8), &P->host_out, 1);
+  } else {
+    ce = cudaMalloc(&P->pool, P->pool_bytes);
+    if (ce == cudaSuccess) ce = cudaHostAlloc(&P->host_in, std::max<size_t>(P->in_bytes, 8), cudaHostAllocDefault);
+    if (ce == cudaSuccess) ce = cudaHostAlloc(&P->host_out, std::max<size_t>(P->out_bytes, 8), cudaHostAllocDefault);
+  }
   if (ce != cudaSuccess) {
     put_msg(msg, msglen, fmt("cudaMalloc of %zu bytes failed: %s", P->pool_bytes, cudaGetErrorString(ce)));
-    delete P;
     return BX_RUNTIME;
   }
   void *pool = P->pool;
   P->dev_in = at<char>(pool, in_at);
   P->dev_out = at<char>(pool, out_at);
 
+  P->need_all = at<int64_t>(pool, need_at);
+  P->need_keys_all = at<int64_t>(pool, need_keys_at);
+  P->iota_all = at<int32_t>(pool, iota_at);
+  P->need_order_all = at<int32_t>(pool, need_order_at);
+  P->seg_off = at<int32_t>(pool, seg_at);
+  {
+    std::vector<int32_t> seg(static_cast<size_t>(ngraphs) + 1, 0);
+    for (int g = 0; g < ngraphs; ++g) seg[g + 1] = seg[g] + graphs[g].V;
+    BX_CUDA(cudaMemcpy(P->seg_off, seg.data(), 4 * seg.size(), cudaMemcpyHostToDevice), msg, msglen);
+  }
   P->dg.resize(ngraphs);
   std::vector<int32_t *> queues(ngraphs);
   for (int g = 0; g < ngraphs; ++g) {
@@ -450,10 +521,10 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
     d.in_off = at<int32_t>(pool, o.in_off);
     d.in_edge = at<int32_t>(pool, o.in_edge);
     d.out_off = at<int32_t>(pool, o.out_off);
-    d.need = at<int64_t>(pool, o.need);
-    d.need_order = at<int32_t>(pool, o.need_order);
-    d.iota = at<int32_t>(pool, o.iota);
-    d.need_keys = at<int64_t>(pool, o.need_keys);
+    d.need = at<int64_t>(pool, need_at) + o.need;
+    d.need_order = at<int32_t>(pool, need_order_at) + o.need_order;
+    d.iota = at<int32_t>(pool, iota_at) + o.iota;
+    d.need_keys = at<int64_t>(pool, need_keys_at) + o.need_keys;
     d.in_src = at<int32_t>(pool, o.in_src);
     d.inpos = at<int32_t>(pool, o.inpos);
     d.indeg_left = at<int32_t>(pool, o.indeg_left);
@@ -475,22 +546,6 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
     up(d.in_edge, G.in_edge, 4 * size_t(G.E));
     up(d.out_off, G.out_off, 4 * size_t(G.V + 1));
     P->fills.push_back({d.flags, 0, 16});
-    // largest need bounds the radix bits (needs are non-negative after
-    // make_graph validation; a negative field keeps all 64 bits)
-    int64_t mx = 0;
-    bool neg = false;
-    for (int j = 0; j < G.V; ++j) {
-      int64_t v = G.perm_bytes[j] + G.out_bytes[j] + G.temp_bytes[j];
-      if (v < 0) neg = true;
-      mx = std::max(mx, v);
-    }
-    int bits = 1;
-    while (bits < 63 && (int64_t(1) << bits) <= mx) ++bits;
-    if (neg) bits = 64;
-    P->sort_bits.push_back(bits);
-    // onesweep: histogram + exclusive sum + one pass per 8-bit digit;
-    // small inputs take the single-tile path
-    P->sort_launches.push_back(G.V <= 3072 ? 1 : 2 + (bits + 7) / 8);
   }
   P->dp.resize(P->nprep);
   P->prep_first.assign(P->nprep, 0);
@@ -507,9 +562,11 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
     d.nu = at<int32_t>(pool, pso[pi].nu);
     d.nu_count = at<int32_t>(pool, pso[pi].cnt);
     d.cbad = d.nu_count + 1;
+    d.first = 0;
     if (!graph_seen[d.graph]) {
       graph_seen[d.graph] = 1;
       P->prep_first[pi] = 1;
+      d.first = 1;
     }
   }
   // small-frontier kernel (K2s, smallsched.cu) eligibility inputs per graph:
@@ -576,6 +633,11 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
     d.stats = reinterpret_cast<int64_t *>(P->dev_out + o.stats);
     d.err = reinterpret_cast<DErr *>(P->dev_out + o.err);
     P->out_off.push_back({o.device_of, o.start, o.exec_order, o.exec_off, o.stats, o.err});
+    // a job that is never placed (host validation) or fails in the placer
+    // leaves device_of = -1 and empty exec lists, so a later simulate of it
+    // fails validation instead of walking stale lists
+    P->fills.push_back({d.device_of, 0xff, 4 * size_t(V)});
+    P->fills.push_back({d.exec_off, 0, 4 * size_t(n + 1)});
     P->in_off.push_back({o.cap, o.fav});
     d.prof = P->prof ? P->prof + static_cast<size_t>(kProfSlots) * i : nullptr;
     // host-side validation in the reference's order
@@ -683,9 +745,15 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
     if (!all.empty())
       BX_CUDA(cudaMemcpy(P->order_dev, all.data(), 4 * all.size(), cudaMemcpyHostToDevice), msg, msglen);
   }
-  BX_CUDA(cudaStreamCreateWithFlags(&P->s2, cudaStreamNonBlocking), msg, msglen);
-  BX_CUDA(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming), msg, msglen);
-  BX_CUDA(cudaEventCreateWithFlags(&P->join, cudaEventDisableTiming), msg, msglen);
+  if (A) {
+    P->s2 = A->side_stream();
+    P->fork = A->event(0, false);
+    P->join = A->event(1, false);
+  } else {
+    BX_CUDA(cudaStreamCreateWithFlags(&P->s2, cudaStreamNonBlocking), msg, msglen);
+    BX_CUDA(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming), msg, msglen);
+    BX_CUDA(cudaEventCreateWithFlags(&P->join, cudaEventDisableTiming), msg, msglen);
+  }
   // descriptor tables are static: copy once
   BX_CUDA(cudaMemcpy(P->dg_dev, P->dg.data(), sizeof(DGraph) * ngraphs, cudaMemcpyHostToDevice), msg, msglen);
   BX_CUDA(cudaMemcpy(P->dp_dev, P->dp.data(), sizeof(DPrep) * P->nprep, cudaMemcpyHostToDevice), msg, msglen);
@@ -694,18 +762,41 @@ int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, co
           msglen);
   // radix-sort scratch sized for the largest graph
   {
-    DGraph probe = {};
-    probe.V = static_cast<int32_t>(max_sort_V);
+    (void)max_sort_V;
     size_t bytes = 0;
-    sort_needs(nullptr, bytes, probe, 64, nullptr);
+    sort_needs_all(nullptr, bytes, P->need_all, P->need_keys_all, P->iota_all, P->need_order_all, P->total_V, ngraphs,
+                   P->seg_off, nullptr);
     P->sort_tmp_bytes = std::max<size_t>(bytes, 256);
-    BX_CUDA(cudaMalloc(&P->sort_tmp, P->sort_tmp_bytes), msg, msglen);
+    if (A) {
+      char *pp = nullptr;
+      BX_CUDA(A->device(P->sort_tmp_bytes, &pp, 3), msg, msglen);
+      P->sort_tmp = pp;
+    } else {
+      BX_CUDA(cudaMalloc(&P->sort_tmp, P->sort_tmp_bytes), msg, msglen);
+    }
   }
-  BX_CUDA(cudaEventCreate(&P->ev[0]), msg, msglen);
-  BX_CUDA(cudaEventCreate(&P->ev[1]), msg, msglen);
+  if (A) {
+    P->ev[0] = A->event(2, true);
+    P->ev[1] = A->event(3, true);
+  } else {
+    BX_CUDA(cudaEventCreate(&P->ev[0]), msg, msglen);
+    BX_CUDA(cudaEventCreate(&P->ev[1]), msg, msglen);
+  }
+  {
+    int rc = upload_fills(P->fills, A, 4, &P->fill_dev, &P->nfill, msg, msglen);
+    if (rc) return rc;
+  }
+  guard.p = nullptr;
   *out = P;
   put_msg(msg, msglen, "");
   return BX_OK;
+}
+
+extern "C" {
+
+int bx_plan_create_ex(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, const bx_job *jobs, int32_t device,
+                      const bx_plan_options *options, bx_plan **out, char *msg, int msglen) {
+  return plan_create(ngraphs, graphs, njobs, jobs, device, options, false, out, msg, msglen);
 }
 
 int bx_plan_upload(bx_plan *P, void *stream) {
@@ -727,34 +818,26 @@ int bx_plan_place(bx_plan *P, void *stream) {
   cudaSetDevice(P->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   P->launches = 0;
-  for (const Fill &f : P->fills) {
-    cudaError_t e = cudaMemsetAsync(f.ptr, f.value, f.bytes, s);
-    if (e != cudaSuccess) {
-      g_last_error = std::string("cudaMemsetAsync: ") + cudaGetErrorString(e);
-      return BX_RUNTIME;
-    }
-  }
-  for (int pi = 0; pi < P->nprep; ++pi) {
-    const DGraph &g = P->dg[P->dp[pi].graph];
-    launch_prep(g, P->dp[pi], P->prep_first[pi] != 0, s);
-    P->launches += (P->prep_first[pi] && g.V > 0 ? 1 : 0) + (g.E > 0 ? 1 : 0);
-  }
+  launch_fill(P->fill_dev, P->nfill, s);
+  P->launches += P->nfill > 0;
+  launch_prep_all(P->dg_dev, P->dp_dev, P->nprep, P->max_ev, s);
+  P->launches += P->nprep > 0 && P->max_ev > 0;
   for (int pi = 0; pi < P->nprep; ++pi) {
     if (!P->prep_small[pi]) continue;
     const DGraph &g = P->dg[P->dp[pi].graph];
     cudaMemsetAsync(P->dp[pi].nu_count, 0, 8, s);
     launch_prep_small(g, P->dp[pi], s);
-    P->launches += 1;
+    P->launches += 2;
   }
-  for (int g = 0; g < P->ngraphs; ++g) {
-    if (P->dg[g].V == 0) continue;
+  if (P->total_V > 0) {
     size_t bytes = P->sort_tmp_bytes;
-    cudaError_t e = sort_needs(P->sort_tmp, bytes, P->dg[g], P->sort_bits[g], s);
+    cudaError_t e = sort_needs_all(P->sort_tmp, bytes, P->need_all, P->need_keys_all, P->iota_all, P->need_order_all,
+                                   P->total_V, P->ngraphs, P->seg_off, s);
     if (e != cudaSuccess) {
       g_last_error = std::string("need sort: ") + cudaGetErrorString(e);
       return BX_RUNTIME;
     }
-    P->launches += P->sort_launches[g];
+    P->launches += 3;
   }
   launch_kahn(P->dg_dev, P->queues_dev, P->ngraphs, s);
   P->launches += 1;
@@ -928,7 +1011,7 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
   Layout L;
   struct SOff {
     size_t mem, peak, xfree, qpos, busy, cl, fin, sq, res, sent, ht, hk, seen, db, dc, start, dev3n, xfer4, mk, err;
-    size_t pos, psrc, cx, ffin, sx, bucket, mb, first, flow8, rcnt, rp_off, rp_src, rp_c, kx, dv, ninp;
+    size_t pos, psrc, cx, ffin, sx, bucket, mb, first, flow8, rcnt, rp_off, rp_src, rp_c, kx, dv, ninp, tr, trn;
   };
   std::vector<SOff> so(P->njobs);
   for (int i = 0; i < P->njobs; ++i) {
@@ -971,9 +1054,19 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
     o.kx = L.take<int64_t>(V);
     o.dv = L.take<int64_t>(4 * n);
     o.ninp = L.take<int32_t>(V);
+    // every event is a start, a finish or one end of a transfer, and a
+    // (producer, device) transfer needs a consumer edge: <= 2V + 2E events
+    o.tr = P->opt.sim_trace ? L.take<int64_t>(4 * (2 * V + 2 * E + 4)) : 0;
+    o.trn = L.take<unsigned long long>(1);
   }
   size_t tab = L.take<DSim>(P->njobs);
-  BX_CUDA(cudaMalloc(&P->sim_pool, L.off), msg, msglen);
+  if (P->borrowed) {
+    char *pp = nullptr;
+    BX_CUDA(thread_arena().device(L.off, &pp, 2), msg, msglen);
+    P->sim_pool = pp;
+  } else {
+    BX_CUDA(cudaMalloc(&P->sim_pool, L.off), msg, msglen);
+  }
   void *pool = P->sim_pool;
   P->ds.resize(P->njobs);
   for (int i = 0; i < P->njobs; ++i) {
@@ -1029,10 +1122,19 @@ static int sim_setup(bx_plan *P, char *msg, int msglen) {
     d.kx = at<int64_t>(pool, o.kx);
     d.dv = at<int64_t>(pool, o.dv);
     d.ninp = at<int32_t>(pool, o.ninp);
+    d.trace = P->opt.sim_trace ? at<int64_t>(pool, o.tr) : nullptr;
+    d.trace_cap = P->opt.sim_trace ? 2 * V + 2 * E + 4 : 0;
+    d.trace_n = at<unsigned long long>(pool, o.trn);
+    P->sim_fills.push_back({d.trace_n, 0, 8});
     P->sim_fills.push_back({d.flow8, 0, 64});
     P->sim_fills.push_back({d.resident, 0, size_t(V * n)});
     P->sim_fills.push_back({d.sent, 0, size_t(V * n)});
     P->sim_fills.push_back({d.err, 0, sizeof(DErr)});
+  }
+  {
+    int rc = upload_fills(P->sim_fills, P->borrowed ? &thread_arena() : nullptr, 5, &P->sim_fill_dev,
+                          &P->nsim_fill, msg, msglen);
+    if (rc) return rc;
   }
   P->ds_dev = at<DSim>(pool, tab);
   BX_CUDA(cudaMemcpy(P->ds_dev, P->ds.data(), sizeof(DSim) * P->njobs, cudaMemcpyHostToDevice), msg, msglen);
@@ -1051,8 +1153,7 @@ int bx_plan_simulate(bx_plan *P, int32_t mem_mode, void *stream) {
       return BX_RUNTIME;
     P->sim_mem_mode = mem_mode;
   }
-  for (const Fill &f : P->sim_fills)
-    if (cudaMemsetAsync(f.ptr, f.value, f.bytes, s) != cudaSuccess) return BX_RUNTIME;
+  launch_fill(P->sim_fill_dev, P->nsim_fill, s);
   launch_simulate(P->ds_dev, P->njobs, P->dg_dev, std::max(P->maxn, 1), P->opt.sim_heap_cap, s);
   return launch_status();
 }
@@ -1130,7 +1231,9 @@ int bx_place(const bx_graph *graph, const bx_job *job, bx_placement *out) {
   bx_job j = *job;
   j.graph = 0;
   bx_plan *P = nullptr;
-  int rc = bx_plan_create(1, graph, 1, &j, 0, &P, out->msg, sizeof out->msg);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int rc = plan_create(1, graph, 1, &j, dev, nullptr, true, &P, out->msg, sizeof out->msg);
   if (rc) {
     out->status = rc;
     return rc;
@@ -1151,9 +1254,14 @@ int bx_simulate(const bx_graph *graph, int32_t n, const int64_t *capacity, const
   return bx_simulate_ex(graph, n, capacity, cm, mem_mode, device_of, exec_order, exec_off, nullptr, out);
 }
 
-int bx_simulate_ex(const bx_graph *graph, int32_t n, const int64_t *capacity, const bx_comm *cm, int32_t mem_mode,
-                   const int32_t *device_of, const int32_t *exec_order, const int32_t *exec_off,
-                   const bx_plan_options *options, bx_sim_report *out) {
+}  // extern "C"
+
+// One-shot simulate of an external placement (bx_simulate*, bx_simulate_trace).
+static int simulate_oneshot(const bx_graph *graph, int32_t n, const int64_t *capacity, const bx_comm *cm,
+                            int32_t mem_mode, const int32_t *device_of, const int32_t *exec_order,
+                            const int32_t *exec_off, const bx_plan_options *options, bx_sim_report *out,
+                            bx_trace_event *trace, int64_t trace_cap, int64_t *trace_len) {
+  if (trace_len) *trace_len = 0;
   if (n <= 0) {
     out->status = BX_VALIDATION;
     put_msg(out->msg, sizeof out->msg, "placement does not match graph or roster");
@@ -1167,7 +1275,9 @@ int bx_simulate_ex(const bx_graph *graph, int32_t n, const int64_t *capacity, co
   j.capacity = capacity;
   j.cm = *cm;
   bx_plan *P = nullptr;
-  int rc = bx_plan_create_ex(1, graph, 1, &j, 0, options, &P, out->msg, sizeof out->msg);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int rc = plan_create(1, graph, 1, &j, dev, options, true, &P, out->msg, sizeof out->msg);
   if (rc) {
     out->status = rc;
     return rc;
@@ -1199,12 +1309,54 @@ int bx_simulate_ex(const bx_graph *graph, int32_t n, const int64_t *capacity, co
   if (!rc) cudaMemcpy(d.exec_off, exec_off, 4 * size_t(n + 1), cudaMemcpyHostToDevice);
   if (!rc) rc = bx_plan_simulate(P, mem_mode, nullptr);
   if (!rc) rc = bx_plan_sim_download(P, nullptr, out);
+  if (!rc && trace) rc = bx_plan_sim_trace(P, 0, trace, trace_cap, trace_len);
   if (rc) {
     out->status = rc;
     put_msg(out->msg, sizeof out->msg, "CUDA failure in bx_simulate");
   }
   bx_plan_destroy(P);
   return rc ? rc : out->status;
+}
+
+extern "C" {
+
+int bx_simulate_ex(const bx_graph *graph, int32_t n, const int64_t *capacity, const bx_comm *cm, int32_t mem_mode,
+                   const int32_t *device_of, const int32_t *exec_order, const int32_t *exec_off,
+                   const bx_plan_options *options, bx_sim_report *out) {
+  return simulate_oneshot(graph, n, capacity, cm, mem_mode, device_of, exec_order, exec_off, options, out, nullptr, 0,
+                          nullptr);
+}
+
+int bx_simulate_trace(const bx_graph *graph, int32_t n, const int64_t *capacity, const bx_comm *cm, int32_t mem_mode,
+                      const int32_t *device_of, const int32_t *exec_order, const int32_t *exec_off,
+                      bx_sim_report *out, bx_trace_event *trace, int64_t trace_cap, int64_t *trace_len) {
+  bx_plan_options o{0, -1, 0, 0, 0, -1, 1};
+  return simulate_oneshot(graph, n, capacity, cm, mem_mode, device_of, exec_order, exec_off, &o, out, trace,
+                          trace_cap, trace_len);
+}
+
+int bx_plan_sim_trace(bx_plan *P, int32_t job, bx_trace_event *out, int64_t cap, int64_t *len) {
+  cudaSetDevice(P->device);
+  *len = 0;
+  if (!P->sim_pool || job < 0 || job >= P->njobs || !P->ds[job].trace) return BX_VALIDATION;
+  const DSim &d = P->ds[job];
+  unsigned long long cnt = 0;
+  if (cudaMemcpy(&cnt, d.trace_n, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return BX_RUNTIME;
+  const int64_t have = std::min<int64_t>(static_cast<int64_t>(cnt), d.trace_cap);
+  const int64_t m = std::min<int64_t>(have, cap);
+  std::vector<int64_t> raw(4 * static_cast<size_t>(m));
+  if (m > 0 && cudaMemcpy(raw.data(), d.trace, 32 * size_t(m), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return BX_RUNTIME;
+  const bx_graph &G = P->hg[d.graph];
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t meta = raw[4 * i + 3];
+    out[i].time_us = raw[4 * i];
+    out[i].device = static_cast<int32_t>(raw[4 * i + 1]);
+    out[i].event = static_cast<int32_t>(raw[4 * i + 2]);
+    out[i].node = G.first_id ? G.first_id[meta] : meta;  // base_id(meta), simulator.cpp:56-58
+  }
+  *len = have;
+  return have > cap ? BX_VALIDATION : BX_OK;
 }
 
 int bx_round_extract(int32_t V, int32_t E, const int32_t *esrc, const int32_t *edst, const double *x,

@@ -33,10 +33,10 @@ namespace bx {
 // Per (graph, comm model): in-CSR gather of src + comm_time per slot, and
 // c_max. Bytes per edge: 4 (in_edge) + 4 (esrc) + 8 (ebytes) read, 4 + 8
 // written.
-__global__ void k_prep_edges(DGraph g, DPrep pr, int write_src) {
+__device__ __forceinline__ void prep_edges(const DGraph &g, const DPrep &pr, int write_src, int tid, int nthreads) {
   int64_t best = 0;
   int neg = 0;
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.E; x += gridDim.x * blockDim.x) {
+  for (int x = tid; x < g.E; x += nthreads) {
     int e = g.in_edge[x];
     int64_t b = g.ebytes[e];
     if (b < 0) {
@@ -65,10 +65,10 @@ __global__ void k_prep_edges(DGraph g, DPrep pr, int write_src) {
 
 // need[j] = perm + out + temp (reserve_bytes, placers.hpp:43-45); the sum of
 // compute times and a negative-time flag (the small-frontier kernel's bounds).
-__global__ void k_prep_nodes(DGraph g) {
+__device__ __forceinline__ void prep_nodes(const DGraph &g, int tid, int nthreads) {
   unsigned long long ks = 0;
   int neg = 0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < g.V; j += gridDim.x * blockDim.x) {
+  for (int j = tid; j < g.V; j += nthreads) {
     int64_t v = g.perm[j] + g.outb[j] + g.temp[j];
     g.need[j] = v;
     g.iota[j] = j;
@@ -84,6 +84,39 @@ __global__ void k_prep_nodes(DGraph g) {
   if ((threadIdx.x & 31) == 0) {
     if (ks) atomicAdd(reinterpret_cast<unsigned long long *>(g.ksum), ks);
     if (neg) atomicOr(&g.flags[2], 1);
+  }
+}
+
+// Every prepared (graph, comm model) of a plan in one launch: blockIdx.y is
+// the prep; the first prep of each graph also derives the graph-level node
+// arrays and the in-CSR source gather.
+__global__ void k_prep_all(const DGraph *graphs, const DPrep *preps) {
+  const DPrep pr = preps[blockIdx.y];
+  const DGraph g = graphs[pr.graph];
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  prep_edges(g, pr, pr.first, tid, nth);
+  if (pr.first) prep_nodes(g, tid, nth);
+}
+
+// Per-step zero / 0xff fills of a plan's workspace (key caches, dead flags,
+// error records, output offsets, ...) in one launch instead of one memset per
+// array: the host splits every fill into chunks of at most kFillChunk bytes
+// (chunk starts stay 16-byte aligned), each CTA stores its chunks with 16-byte
+// vector stores.
+__global__ void __launch_bounds__(256) k_fill(const FillChunk *__restrict__ t, int n) {
+  for (int c = blockIdx.x; c < n; c += gridDim.x) {
+    const FillChunk f = t[c];
+    unsigned char *p = reinterpret_cast<unsigned char *>(f.ptr);
+    const unsigned v8 = f.value & 0xffu;
+    const unsigned w = v8 * 0x01010101u;
+    const uint4 w4 = make_uint4(w, w, w, w);
+    const size_t head = (16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15;
+    const size_t pre = head < f.bytes ? head : f.bytes;
+    for (size_t i = threadIdx.x; i < pre; i += blockDim.x) p[i] = static_cast<unsigned char>(v8);
+    const size_t body = (f.bytes - pre) >> 4;
+    uint4 *q = reinterpret_cast<uint4 *>(p + pre);
+    for (size_t i = threadIdx.x; i < body; i += blockDim.x) q[i] = w4;
+    for (size_t i = pre + (body << 4) + threadIdx.x; i < f.bytes; i += blockDim.x) p[i] = static_cast<unsigned char>(v8);
   }
 }
 
@@ -360,24 +393,32 @@ void launch_big_seq(const DJob *jobs, const int32_t *order, int njobs, const DGr
 void launch_rounds(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                    int maxn, int list_len, cudaStream_t s);
 
-void launch_prep(const DGraph &g, const DPrep &pr, bool first, cudaStream_t s) {
-  if (first) {
-    int nb = (g.V + 255) / 256;
-    if (nb > 0) k_prep_nodes<<<nb < 1184 ? nb : 1184, 256, 0, s>>>(g);
+void launch_prep_all(const DGraph *graphs_dev, const DPrep *preps_dev, int nprep, int max_ev, cudaStream_t s) {
+  if (nprep <= 0 || max_ev <= 0) return;
+  int x = (max_ev + 255) / 256;
+  const int cap = nprep >= 1184 ? 1 : 1184 / nprep;
+  if (x > cap) x = cap;
+  for (int b = 0; b < nprep; b += 65535) {
+    const int ny = nprep - b < 65535 ? nprep - b : 65535;
+    k_prep_all<<<dim3(x, ny), 256, 0, s>>>(graphs_dev, preps_dev + b);
   }
-  int eb = (g.E + 255) / 256;
-  if (eb > 0) k_prep_edges<<<eb < 1184 ? eb : 1184, 256, 0, s>>>(g, pr, first ? 1 : 0);
+}
+
+void launch_fill(const FillChunk *table, int n, cudaStream_t s) {
+  if (n > 0) k_fill<<<n < 148 * 8 ? n : 148 * 8, 256, 0, s>>>(table, n);
 }
 
 void launch_kahn(DGraph *graphs_dev, int32_t *const *queues_dev, int ngraphs, cudaStream_t s) {
   k_kahn<<<ngraphs, 512, 0, s>>>(graphs_dev, queues_dev);
 }
 
-// need_order: node indices by ascending (need, index); the radix sort is
-// stable, so equal needs keep ascending index order.
-cudaError_t sort_needs(void *tmp, size_t &tmp_bytes, const DGraph &g, int end_bit, cudaStream_t s) {
-  return cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, g.need, g.need_keys, g.iota, g.need_order, g.V, 0, end_bit,
-                                         s);
+// need_order: node indices by ascending (need, index), every graph of the
+// plan in one segmented sort over the concatenated need arrays (stable, so
+// equal needs keep ascending index order).
+cudaError_t sort_needs_all(void *tmp, size_t &tmp_bytes, const int64_t *need, int64_t *keys_out, const int32_t *iota,
+                           int32_t *order_out, int total, int nseg, const int32_t *seg_off, cudaStream_t s) {
+  return cub::DeviceSegmentedSort::StableSortPairs(tmp, tmp_bytes, need, keys_out, iota, order_out, total, nseg,
+                                                   seg_off, seg_off + 1, s);
 }
 
 void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_etf, int n_bpar, int n_bseq,

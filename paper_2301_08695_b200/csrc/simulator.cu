@@ -117,6 +117,21 @@ __device__ void try_start(SimCtx &c, int dev, int64_t now) {
   __syncwarp();
 }
 
+// Sim::trace (simulator.cpp:60-64): one record per event in processing
+// order; event 0 start, 1 finish, 2 xfer_begin, 3 xfer_end. Lane 0 only.
+__device__ __forceinline__ void trace_ev(const DSim &s, int64_t t, int dev, int ev, int meta) {
+  if (!s.trace) return;
+  const unsigned long long i = *s.trace_n;
+  if (static_cast<int64_t>(i) < s.trace_cap) {
+    int64_t *r = s.trace + 4 * i;
+    r[0] = t;
+    r[1] = dev;
+    r[2] = ev;
+    r[3] = meta;
+  }
+  *s.trace_n = i + 1;
+}
+
 // charge (simulator.cpp:66-76); returns false on a violation (error set).
 __device__ bool charge(SimCtx &c, int dev, int64_t delta, int64_t t, int meta) {
   int64_t m = c.s.mem[dev] + delta;
@@ -267,6 +282,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
         c.s.busy[dev] = 1;
         c.s.start[a] = t;
         ok = charge(c, dev, c.g.temp[a] + c.g.outb[a], t, a);
+        if (ok) trace_ev(c.s, t, dev, 0, a);
         if (ok) c.h.push(t + c.g.k[a], pack_ev(0, a, 0));
       }
       ok = __shfl_sync(kFullS, ok, 0);
@@ -280,6 +296,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
       ++finished_count;
       makespan = smax(makespan, t);
       if (lane == 0) {
+        trace_ev(c.s, t, dev, 1, j);
         c.s.busy[dev] = 0;
         c.s.qpos[dev]++;
         c.s.finished[j] = 1;
@@ -334,6 +351,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
           }
           ++xcount;
           xbytes += bytes;
+          trace_ev(c.s, begin, dev, 2, j);
           c.h.push(begin + cc, pack_ev(1, j, cdev));
         }
       }
@@ -345,7 +363,10 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
       try_start(c, dev, t);
     } else {
       // run_xfer_done (:186-190)
-      if (lane == 0) c.s.resident[static_cast<int64_t>(a) * n + b] = 1;
+      if (lane == 0) {
+        c.s.resident[static_cast<int64_t>(a) * n + b] = 1;
+        trace_ev(c.s, t, b, 3, a);
+      }
       __syncwarp();
       inputs_landed(c, a, b);
       try_start(c, b, t);
@@ -453,6 +474,7 @@ __global__ void k_sim_prep_a(const DSim *sims, const DGraph *graphs, int base) {
     s.rcnt[j] = 0;
     zero |= g.k[j] == 0;
   }
+  zero |= s.trace != nullptr;  // record_trace: the event loop records processing order
   if (__syncthreads_or(zero) && threadIdx.x == 0) atomicOr(&s.flow8[0], 1ull);
   BX_SIM_STRIDE(e, g.E) {
     const int i = g.esrc[e], dc = s.device_of[g.edst[e]], di = s.device_of[i];

@@ -73,6 +73,10 @@ def test_no_cpu_fallback_without_gpu():
         bx.round_and_extract(2, [0], [1], [0.0])
     with pytest.raises(bx.DeviceError):
         bx.Plan([g], [bx.Job(0, "m-etf", np.array([100, 100]), bx.CommModel())])
+    with pytest.raises(bx.DeviceError):
+        bx.critical_path_us(g)
+    with pytest.raises(bx.DeviceError):
+        bx.schedulable_time(bx.PlacerState(g.V, 2, bx.PARALLEL), 3, 0, g, bx.CommModel(0.0, 0.0, bx.PARALLEL))
 
 
 def test_product_never_imports_oracle():
