@@ -3,13 +3,17 @@ configs[4]), plus the reference CPU placer timed on this box's host cores.
 
 python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
 
-One process per GPU (torchrun for N > 1). Every rank places its own
-4096-problem sweep shard (64 graphs x {2,4,8,16} devices x 16 memory caps,
-graph seeds offset by rank), so per-GPU work is fixed as N grows ("weak").
-A "step" is one pass of the placement engine over the whole shard.
+One process per GPU (torchrun for N > 1). Every rank holds the SAME global
+sweep (64 graphs x {2,4,8,16} devices x 16 memory caps = 4096 problems) and
+places its longest-processing-time share (cost V*n), so the
+total work is fixed as N grows ("strong"). A "step" is one pass of the
+placement engine over the whole sweep; the job time is the slowest rank's.
 `value` is device-resident (inputs already in HBM); `e2e` re-uploads every
-input from pinned host memory and downloads every placement each step
-through the C ABI (bx_plan_upload / bx_plan_place / bx_plan_download).
+input from pinned host memory, places, and brings every placement to the
+host through the C ABI (bx_plan_upload / bx_plan_place / bx_plan_download),
+with the NCCL gather of all ranks' placements to rank 0 inside the step for
+N > 1. After timing, rank 0 compares all 4096 placements (device_of,
+start_us, exec_order, exec_off, stats, status) with the reference's.
 """
 from __future__ import annotations
 
@@ -35,6 +39,16 @@ NCU_SUMMARY = os.path.join(HERE, "profiles", "ncu_placer_summary.json")
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -86,29 +100,55 @@ def algorithmic_bytes(graphs, jobs):
     return sum(40 * graphs[g]["V"] + 16 * len(graphs[g]["esrc"]) for g, _, _ in jobs)
 
 
-def cpu_reference(graphs, jobs, sample_idx, threads, steps=1):
-    """The reference placer (oracle/_ref, the unmodified reference sources)
-    over `sample_idx` with the reference's own OpenMP sweep pattern
-    (proj/src/bench.cpp:121). Returns (placements/s per step list, statuses,
-    checksums, kind)."""
+def stratified(P, stride, offset=0):
+    """Every stride-th problem with a rotating offset: jobs are ordered
+    (graph, devices, cap) with the 16 caps innermost, so a plain stride would
+    always pick the same cap factor; this one cycles through all of them."""
+    return [i for i in range(P) if i % stride == (i // stride + offset) % stride]
+
+
+def cpu_reference(graphs, jobs, idx, threads, full=False):
+    """The reference placer (oracle/_ref = the unmodified reference sources)
+    over problems `idx` with the reference's own sweep pattern, OpenMP over
+    problems (proj/src/bench.cpp:121). Returns (placements/s, statuses,
+    placements or None)."""
     from oracle import Ref
     from paper_2301_08695_b200 import workloads as W
     if not Ref.available():
         raise RuntimeError("oracle/_ref/libdagsched_ref.so missing (build with make -C oracle)")
-    used = sorted({jobs[i][0] for i in sample_idx})
+    used = sorted({jobs[i][0] for i in idx})
     rg = {g: Ref.graph(W.as_ref_base(graphs[g]), -1) for g in used}
-    maxn = max(jobs[i][1] for i in sample_idx)
-    caps = np.zeros((len(sample_idx), maxn), np.int64)
-    for r, i in enumerate(sample_idx):
+    maxn = max(jobs[i][1] for i in idx)
+    caps = np.zeros((len(idx), maxn), np.int64)
+    for r, i in enumerate(idx):
         caps[r, :jobs[i][1]] = jobs[i][2]
-    gl = [rg[jobs[i][0]] for i in sample_idx]
-    algos = np.ones(len(sample_idx), np.int32)
-    ns = np.array([jobs[i][1] for i in sample_idx], np.int32)
-    rates, st, chk = [], None, None
-    for _ in range(steps):
-        st, chk, wall_ns = Ref.place_batch(gl, algos, ns, caps, W.COMM_TEST, threads)
-        rates.append(len(sample_idx) / (wall_ns / 1e9))
-    return rates, st, chk
+    gl = [rg[jobs[i][0]] for i in idx]
+    algos = np.ones(len(idx), np.int32)
+    ns = np.array([jobs[i][1] for i in idx], np.int32)
+    if full:
+        st, pls, wall_ns = Ref.place_batch_full(gl, algos, ns, caps, W.COMM_TEST, threads)
+    else:
+        st, _, wall_ns = Ref.place_batch(gl, algos, ns, caps, W.COMM_TEST, threads)
+        pls = None
+    return len(idx) / (wall_ns / 1e9), st, pls
+
+
+def compare_all(results, ref_status, ref_pls, idx):
+    """Full-placement parity of every problem in idx against the reference."""
+    mism = []
+    for r, i in enumerate(idx):
+        got = results[i]
+        if int(ref_status[r]) != got["status"]:
+            mism.append(i)
+            continue
+        if ref_status[r] != 0:
+            continue
+        o = ref_pls[r]
+        if not (np.array_equal(o.device_of, got["device_of"]) and np.array_equal(o.start_us, got["start_us"])
+                and np.array_equal(o.exec_order, got["exec_order"]) and np.array_equal(o.exec_off, got["exec_off"])
+                and np.array_equal(np.asarray(o.stats), got["stats"])):
+            mism.append(i)
+    return mism
 
 
 def per_graph(bx, W, cpu=True):
@@ -168,11 +208,6 @@ def per_graph(bx, W, cpu=True):
     return out
 
 
-def sample_indices(jobs, count):
-    stride = max(1, len(jobs) // count)
-    return list(range(0, len(jobs), stride))[:count]
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -180,41 +215,47 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--graphs", type=int, default=64)
-    ap.add_argument("--cpu-sample", type=int, default=256)
+    ap.add_argument("--ref-stride", type=int, default=8, help="reference arm: every k-th problem per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-per-graph", action="store_true")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2301_08695_b200 import sweep
     from paper_2301_08695_b200 import workloads as W
 
+    graphs, jobs = sweep.global_sweep(args.graphs)
+    P = len(jobs)
     config = {"workload": "C5 batched sweep: 64 graphs (layered/grid/branchy/wide, V 1k-20k) x "
                           "{2,4,8,16} devices x 16 caps (1.05+k*0.0633), m-ETF, comm_model_test.json "
                           "(12.5us + 0.002us/B, parallel)",
-              "problems_per_gpu": None, "algo": "m-etf",
+              "problems": P, "partition": "LPT by V*n over ranks (same problems at every N)", "algo": "m-etf",
               "l2": "inputs+workspace larger than L2 (GBs, rewritten every step)"}
 
     if args.impl == "reference":
+        # the reference's own sweep (oracle/_ref, unmodified sources): OpenMP
+        # over problems on every host thread, one stratified sample per step
         if rank != 0:
             return
-        graphs = W.sweep_graphs(0, args.graphs)
-        jobs = W.sweep_jobs(graphs)
-        idx = sample_indices(jobs, args.cpu_sample)
         threads = os.cpu_count() or 1
-        for _ in range(args.warmup):
-            cpu_reference(graphs, jobs, idx[: max(8, len(idx) // 8)], threads)
-        rates, _, _ = cpu_reference(graphs, jobs, idx, threads, steps=args.steps)
+        stride = max(1, args.ref_stride)
+        for w in range(args.warmup):
+            cpu_reference(graphs, jobs, stratified(P, stride * 4, w), threads)
+        rates = [cpu_reference(graphs, jobs, stratified(P, stride, k), threads)[0] for k in range(args.steps)]
         v = statistics.median(rates)
-        config["problems_per_gpu"] = len(jobs)
+        n_step = len(stratified(P, stride, 0))
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": len(idx) / v * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": P / v * 1e3,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
                 "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                                 "sample": f"{len(idx)} of the {len(jobs)} sweep problems (every "
-                                           f"{len(jobs) // len(idx)}th), OpenMP over problems"},
+                                 "cpu_model": cpu_model(),
+                                 "sample": f"{n_step} of the {P} sweep problems per step (every {stride}th, "
+                                           f"offset rotating through the cap factors), reference place_metf, "
+                                           f"OpenMP over problems"},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -222,18 +263,16 @@ def main():
     import torch
     import paper_2301_08695_b200 as bx
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
 
-    from paper_2301_08695_b200 import sweep
-    graphs, jobs = sweep.rank_sweep(rank, args.graphs)
-    config["problems_per_gpu"] = len(jobs)
-    P = len(jobs)
-    # pinned host copies of every input (the e2e path copies from these)
+    ids, sgraphs, sjobs = sweep.rank_shard(rank, world, graphs, jobs)
+    PR = len(ids)
     keep = []
 
     def pinned(a):
@@ -242,21 +281,22 @@ def main():
         return t.numpy()
 
     mgs = []
-    for g in graphs:
+    for g in sgraphs:
         mgs.append(bx.MetaGraph(pinned(g["k"]), pinned(g["temp"]), pinned(g["perm"]), pinned(g["out"]),
                                 pinned(g["esrc"]), pinned(g["edst"]), pinned(g["ebytes"])))
     for m in mgs:  # adjacency arrays pinned too
         m.in_off, m.in_edge, m.out_off = pinned(m.in_off), pinned(m.in_edge), pinned(m.out_off)
     cm = bx.CommModel(*W.COMM_TEST)
-    bjobs = [bx.Job(gi, "m-etf", pinned(np.full(n, cap, np.int64)), cm) for gi, n, cap in jobs]
+    bjobs = [bx.Job(gi, "m-etf", pinned(np.full(n, cap, np.int64)), cm) for gi, n, cap in sjobs]
     t0 = time.time()
     plan = bx.Plan(mgs, bjobs, device=local)
-    log(f"[rank {rank}] plan: {P} problems, {sum(g['V'] for g in graphs)} graph nodes, "
-        f"created in {time.time() - t0:.2f}s")
+    log(f"[rank {rank}] plan: {PR} of {P} problems (LPT cost {sum(sgraphs[g]['V'] * n for g, n, _ in sjobs)}), "
+        f"{sum(g['V'] for g in sgraphs)} graph nodes, created in {time.time() - t0:.2f}s")
     h2d = sum(m.k.nbytes + m.temp.nbytes + m.perm.nbytes + m.out.nbytes + m.esrc.nbytes + m.edst.nbytes
               + m.ebytes.nbytes + m.in_off.nbytes + m.in_edge.nbytes + m.out_off.nbytes for m in mgs)
-    h2d += sum(8 * n for _, n, _ in jobs)
-    d2h = sum(graphs[g]["V"] * (4 + 8 + 4) + 4 * (n + 1) + 24 + 8 for g, n, _ in jobs)
+    h2d += sum(8 * n for _, n, _ in sjobs)
+    d2h = plan.output_region()[1]
+    table = sweep.offsets_table(plan, ids)
 
     def barrier():
         torch.cuda.synchronize()
@@ -265,23 +305,22 @@ def main():
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return sweep.max_over_ranks(x, dist, dev)
+
+    def gather():
+        """Every rank's device-resident placements to rank 0 over NCCL."""
+        return sweep.gather_to_root(sweep.region_tensor(plan, dev), table, dist, dev)
 
     plan.upload(sp)
     for _ in range(args.warmup):
         plan.upload(sp)
         plan.place(sp)
         plan.download(sp)
-    fails = [i for i in range(P) if plan.status(i)[0] not in (0, 3)]
+    fails = [i for i in range(PR) if plan.status(i)[0] not in (0, 3)]
     if fails:
         raise RuntimeError(f"problems failed: {[plan.status(i) for i in fails[:3]]}")
 
     # ---- device-resident timed region -----------------------------------
-    kernel_ms = []
     barrier()
     with Clocks(local) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -289,15 +328,21 @@ def main():
         ev0.record(stream)
         for _ in range(args.steps):
             plan.place(sp)
-            kernel_ms.append(plan.kernel_ms())
         ev1.record(stream)
         ev1.synchronize()
         dev_ms = ev0.elapsed_time(ev1)
+    kernel_ms = plan.kernel_times(args.steps)  # placer-kernel events of the same steps
     barrier()
-    dev_ms = max_over_ranks(dev_ms)
+    rank_ms = dev_ms / args.steps
+    busy = [rank_ms]
+    if dist is not None:
+        t = torch.tensor([rank_ms], dtype=torch.float64, device=dev)
+        parts = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        busy = [float(x.item()) for x in parts]
+    ms_step = max(busy)
     launches = plan.launch_count() * args.steps
-    ms_step = dev_ms / args.steps
-    value = world * P / (ms_step / 1e3)
+    value = P / (ms_step / 1e3)
 
     # ---- end to end through the C ABI with host buffers --------------------
     barrier()
@@ -305,29 +350,40 @@ def main():
     for _ in range(args.steps):
         plan.upload(sp)
         plan.place(sp)
-        plan.download(sp)
+        if dist is not None:
+            got = gather()
+            if rank == 0:
+                plan.download(sp)
+        else:
+            plan.download(sp)
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3
     barrier()
     e2e_ms = max_over_ranks(e2e_ms)
-    e2e_value = world * P / (e2e_ms / args.steps / 1e3)
+    e2e_value = P / (e2e_ms / args.steps / 1e3)
 
-    # ---- final gather of per-problem summaries over NCCL --------------------
-    sts = [plan.status(i)[0] for i in range(P)]
-    summ = sweep.summarize(sts, [plan.result(i, copy=False) if sts[i] == 0 else None for i in range(P)],
-                           lambda i: graphs[jobs[i][0]]["k"], base_id=rank * P)
+    # ---- the final gather on its own (full placements to rank 0) ----------
+    barrier()
     gather_ms = None
+    g0 = time.perf_counter()
     if dist is not None:
-        torch.cuda.synchronize()
-        g0 = time.perf_counter()
-        sweep.gather_summaries(summ, dist, device=torch.device("cuda", local))
+        gathered = gather()
         torch.cuda.synchronize()
         gather_ms = (time.perf_counter() - g0) * 1e3
-    infeasible = int((summ[:, 0] == 3).sum())
+    else:
+        torch.cuda.synchronize()
+        region = sweep.region_tensor(plan, dev).cpu().numpy()
+        gathered = [(region, table)]
+    results = None
+    if rank == 0:
+        sizes = lambda i: (graphs[jobs[i][0]]["V"], jobs[i][1])  # noqa: E731
+        results = sweep.collect(gathered, sizes)
+        assert sorted(results) == list(range(P)), "gather lost problems"
+    infeasible = None if results is None else sum(1 for r in results.values() if r["status"] == 3)
 
     # ---- roofline of the dominant kernel (the placer) ------------------------
     kmean = statistics.mean(kernel_ms)
-    abytes = algorithmic_bytes(graphs, jobs)
+    abytes = algorithmic_bytes(sgraphs, sjobs)
     achieved = abytes / (kmean / 1e3) / 1e9
     peak = None
     peak_src = "fallback 6650 GB/s (B200_PROFILING.md)"
@@ -342,23 +398,27 @@ def main():
     except Exception:
         pass
 
-    # ---- CPU reference baseline (rank 0, N=1) + parity spot check ------------
+    # ---- parity of EVERY problem vs the reference; CPU baselines ---------------
     cpu = None
     parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_parity:
         try:
-            idx = sample_indices(jobs, args.cpu_sample)
             threads = os.cpu_count() or 1
-            rates, st, chk = cpu_reference(graphs, jobs, idx, threads)
-            cpu = {"value": rates[0], "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"{len(idx)} of the {P} sweep problems (every {P // len(idx)}th), reference "
-                             f"place_metf, OpenMP over problems"}
-            mism = sum(1 for r, i in enumerate(idx)
-                       if int(st[r]) != int(summ[i, 0]) or (st[r] == 0 and int(chk[r]) != int(summ[i, 1])))
-            parity = {"checked": len(idx), "mismatches": mism}
+            rate, st, pls = cpu_reference(graphs, jobs, list(range(P)), threads, full=True)
+            mism = compare_all(results, st, pls, list(range(P)))
+            parity = {"checked": P, "fields": "status, device_of, start_us, exec_order, exec_off, stats",
+                      "mismatches": len(mism), "first_mismatches": mism[:5]}
+            if world == 1 and not args.no_cpu_baseline:
+                one_idx = stratified(P, 64)
+                rate1, _, _ = cpu_reference(graphs, jobs, one_idx, 1)
+                cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "cpu_model": cpu_model(),
+                       "sample": f"all {P} sweep problems, reference place_metf, OpenMP over problems "
+                                 f"(the run parity is checked on)",
+                       "single_thread_value": rate1,
+                       "single_thread_sample": f"{len(one_idx)} problems (every 64th, rotating cap factor), 1 thread"}
         except Exception as e:  # the baseline is reported, never the target
-            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"unavailable: {e}"}
+            parity = {"error": str(e)}
 
     pg = None
     if rank == 0 and world == 1 and not args.no_per_graph:
@@ -367,31 +427,35 @@ def main():
         except Exception as e:
             pg = {"error": str(e)}
         # BASELINE configs C1-C3 (single model-shaped graphs): GPU placer
-        # kernels (device-resident, best of 3) next to the reference placer on
-        # one core, same meta graph, bit-exact flag
+        # kernels (device-resident) and the one-shot bx_place call, next to the
+        # reference placer on one core (median of 10), bit-exact flag
         try:
             sys.path.insert(0, os.path.join(HERE, "tools"))
             from latency_table import run_config
             pg["configs"] = [
-                {k: r.get(k) for k in ("case", "algo", "meta_V", "n", "gpu_kernel_ms", "cpu_ref_ms", "bit_exact",
-                                       "speedup")}
+                {k: r.get(k) for k in ("case", "algo", "meta_V", "n", "kernel", "gpu_kernel_ms", "gpu_oneshot_ms",
+                                       "cpu_ref_ms", "bit_exact", "speedup", "speedup_oneshot")}
                 for name in W.CONFIGS for r in run_config(name, cpu=not args.no_cpu_baseline)]
         except Exception as e:
             pg["configs"] = {"error": str(e)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": config,
-                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                        "note": "rank 0's numbers; each rank uploads its shard, rank 0 downloads all"
+                                if world > 1 else "upload + place + download per step"},
                 "gpu_launches": launches,
+                "ranks": {"busy_ms_per_step": busy, "imbalance": max(busy) / (sum(busy) / len(busy)),
+                          "gather_ms": gather_ms},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
                              "kernel": "k_place_list", "kernel_ms": kmean,
                              "algorithmic_bytes_per_launch": abytes, "peak_source": peak_src,
                              "note": "latency-bound dependent scheduling chain; bytes = 40V+16E per problem"},
                 "cpu_baseline": cpu, "parity_vs_reference": parity, "infeasible_problems": infeasible,
-                "gather_ms": gather_ms, "clocks": clk.summary(), "per_graph": pg}
+                "clocks": clk.summary(), "per_graph": pg}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

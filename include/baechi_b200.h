@@ -234,6 +234,18 @@ int bx_plan_job_kernel(bx_plan *plan, int32_t job);
 /* Device time (ms) of the placer kernel(s) of the last bx_plan_place,
  * measured with CUDA events on the plan's stream; waits for it. */
 float bx_plan_kernel_ms(bx_plan *plan);
+/* The same for each of the last `count` bx_plan_place calls (at most 64 are
+ * kept), oldest first, without synchronising between them: a timed loop of
+ * places reads its per-step kernel times afterwards. Returns how many. */
+int bx_plan_kernel_times(bx_plan *plan, int32_t count, float *ms);
+
+/* The device-resident output region of the plan (every job's placement and
+ * status, the bytes bx_plan_download copies) and, per job, the byte offsets
+ * inside it of device_of, start_us, exec_order, exec_off, stats[3] and the
+ * status record (int32 status, int32 code, 4 x int64 detail). A sweep
+ * gathers these regions from every rank over NCCL. */
+int bx_plan_output_region(const bx_plan *plan, void **dev, int64_t *bytes);
+int bx_plan_job_outputs(const bx_plan *plan, int32_t job, int64_t *offs6);
 
 /* Per-step latency breakdown of job `job` (plans created with
  * bx_plan_options.profile = 1 run a clock64-instrumented placer):

@@ -150,8 +150,42 @@ class Ref:
                                                 vp, C.c_int64, i64p]
             L.ref_placement_from_json.argtypes = [vp, cp, C.c_int64, C.c_int32, cp, ip, _i32p, _i64p, _i32p,
                                                   _i32p, cp, ip]
+            L.ref_place_batch_full.argtypes = [C.c_int32, C.POINTER(C.c_void_p), _i32p, _i32p, _i64p, C.c_int32,
+                                               C.c_double, C.c_double, C.c_int32, C.c_int32, _i64p, _i64p, _i32p,
+                                               _i64p, _i32p, _i32p, _i64p, _i32p, C.POINTER(C.c_int64)]
             cls._lib = L
         return cls._lib
+
+    @classmethod
+    def place_batch_full(cls, graphs, algos, ns, caps2d, cm, threads=0):
+        """ref_place_batch_full: every problem's full placement. Returns
+        (status [P], list of Placement | None, wall_ns)."""
+        count = len(graphs)
+        arr = (C.c_void_p * count)(*[g.h for g in graphs])
+        Vs = np.array([g.sizes()[2] for g in graphs], np.int64)
+        ns = _a(ns, np.int32)
+        voff = np.zeros(count, np.int64)
+        voff[1:] = np.cumsum(Vs)[:-1]
+        eoff = np.zeros(count, np.int64)
+        eoff[1:] = np.cumsum(ns.astype(np.int64) + 1)[:-1]
+        tv = int(Vs.sum())
+        dev, st, eo = np.zeros(max(tv, 1), np.int32), np.zeros(max(tv, 1), np.int64), np.zeros(max(tv, 1), np.int32)
+        off = np.zeros(int((ns.astype(np.int64) + 1).sum()), np.int32)
+        stats = np.zeros(3 * count, np.int64)
+        status = np.zeros(count, np.int32)
+        wall = C.c_int64()
+        caps2d = _a(caps2d, np.int64)
+        cls.lib().ref_place_batch_full(count, arr, _a(algos, np.int32), ns, caps2d, caps2d.shape[1], cm[0], cm[1],
+                                       cm[2], threads, voff, eoff, dev, st, eo, off, stats, status, C.byref(wall))
+        out = []
+        for i in range(count):
+            if status[i]:
+                out.append(None)
+                continue
+            a, b = voff[i], voff[i] + Vs[i]
+            out.append(Placement(dev[a:b], st[a:b], eo[a:b], off[eoff[i]:eoff[i] + ns[i] + 1],
+                                 stats[3 * i:3 * i + 3]))
+        return status, out, wall.value
 
     @staticmethod
     def _text(call):

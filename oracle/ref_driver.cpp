@@ -586,4 +586,37 @@ int ref_placement_from_json(void* h, const char* text, int64_t len, int32_t n, c
   });
 }
 
+// ref_place_batch with the full placements exported: problem i writes its
+// device_of / start_us / exec_order at element offset voff[i] of the flat
+// arrays, exec_off at eoff[i], stats at 3*i (the bench compares every one of
+// the sweep's problems with the GPU, not a checksum).
+int ref_place_batch_full(int32_t count, void* const* graphs, const int32_t* algo, const int32_t* n,
+                         const int64_t* caps, int32_t maxn, double intercept, double per_byte, int32_t mode,
+                         int32_t threads, const int64_t* voff, const int64_t* eoff, int32_t* device_of,
+                         int64_t* start, int32_t* exec_order, int32_t* exec_off, int64_t* stats3, int32_t* status,
+                         int64_t* wall_ns) {
+  if (threads > 0) omp_set_num_threads(threads);
+  auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(dynamic)
+  for (int i = 0; i < count; ++i) {
+    auto* rg = static_cast<RefGraph*>(graphs[i]);
+    try {
+      DeviceRoster roster = make_roster(n[i], caps + static_cast<size_t>(i) * maxn);
+      CommModel cm = make_cm(intercept, per_byte, mode);
+      PlacerStats st;
+      Placement p = algo[i] == 0 ? place_mtopo(rg->gg, roster, cm) : place_metf(rg->gg, roster, cm, &st);
+      export_placement(p, device_of + voff[i], start + voff[i], exec_order + voff[i], exec_off + eoff[i]);
+      stats3[3 * i + 0] = st.discarded_pairs;
+      stats3[3 * i + 1] = st.excluded_devices;
+      stats3[3 * i + 2] = st.awake_reservations;
+      status[i] = 0;
+    } catch (const Error& e) {
+      status[i] = kind_code(e);
+    }
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  *wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+  return 0;
+}
+
 }  // extern "C"

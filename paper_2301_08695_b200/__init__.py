@@ -196,6 +196,9 @@ def lib():
                                      C.POINTER(_PlanOptions), C.POINTER(_SimReport)]
         L.bx_plan_kernel_ms.argtypes = [_vp]
         L.bx_plan_kernel_ms.restype = C.c_float
+        L.bx_plan_kernel_times.argtypes = [_vp, i32, _vp]
+        L.bx_plan_output_region.argtypes = [_vp, C.POINTER(_vp), C.POINTER(i64)]
+        L.bx_plan_job_outputs.argtypes = [_vp, i32, _vp]
         L.bx_plan_profile.argtypes = [_vp, i32, _vp]
         L.bx_plan_simulate.argtypes = [_vp, i32, _vp]
         L.bx_plan_sim_download.argtypes = [_vp, _vp, C.POINTER(_SimReport)]
@@ -241,7 +244,8 @@ def lib():
 EXPORTED = ["bx_version", "bx_last_error", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
             "bx_plan_create_ex", "bx_plan_job_kernel", "bx_simulate_ex",
             "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download", "bx_plan_result_view",
-            "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_profile", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
+            "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_kernel_times",
+            "bx_plan_output_region", "bx_plan_job_outputs", "bx_plan_profile", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
             "bx_simulate", "bx_round_extract", "bx_grouped_create", "bx_grouped_view", "bx_grouped_destroy", "bx_lp_solve",
             "bx_schedulable_time", "bx_critical_path_us", "bx_simulate_trace", "bx_plan_sim_trace", "bx_trace_to_csv",
             "bx_comm_model_parse", "bx_comm_model_load", "bx_comm_model_to_json", "bx_graph_parse", "bx_graph_load",
@@ -436,6 +440,28 @@ class Plan:
     def kernel_ms(self) -> float:
         """CUDA-event time of the placer kernel(s) of the last place()."""
         return float(lib().bx_plan_kernel_ms(self.h))
+
+    def kernel_times(self, count: int) -> list:
+        """Placer-kernel CUDA-event times of the last `count` place() calls
+        (<= 64 kept), oldest first; no host sync between the places."""
+        out = np.zeros(max(count, 1), np.float32)
+        got = lib().bx_plan_kernel_times(self.h, count, _ptr(out))
+        if got < 0:
+            raise DeviceError("bx_plan_kernel_times failed")
+        return out[:got].astype(float).tolist()
+
+    def output_region(self) -> tuple[int, int]:
+        """(device pointer, bytes) of every job's device-resident outputs."""
+        p, n = _vp(), C.c_int64()
+        lib().bx_plan_output_region(self.h, C.byref(p), C.byref(n))
+        return int(p.value or 0), n.value
+
+    def job_outputs(self, i: int) -> list:
+        """Byte offsets of job i's device_of, start_us, exec_order, exec_off,
+        stats and status record inside output_region()."""
+        o = np.zeros(6, np.int64)
+        lib().bx_plan_job_outputs(self.h, i, _ptr(o))
+        return o.tolist()
 
     def download(self, stream=None):
         """One device->pinned-host copy of every job's placement."""

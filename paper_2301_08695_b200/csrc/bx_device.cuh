@@ -45,6 +45,7 @@ enum ErrCode : int32_t {
   E_SIM_STALL = 8,   // "deadlock: simulation stalled"
   E_SIM_EXEC = 9,    // "exec_order disagrees with assignments"   simulator.cpp:87-89
   E_SIM_ONCE = 10,   // "placement must assign every node exactly once" :92-95
+  E_HOST = 11,       // host-side validation failed (message kept by the plan)
 };
 
 struct DErr {
@@ -115,11 +116,12 @@ struct DJob {
   int32_t maxin;  // largest in-degree of the graph (K2s list sizing)
 };
 
-// One chunk of a per-step workspace fill (k_fill); at most kFillChunk bytes.
+// One chunk of a per-step workspace fill (k_fill); at most kFillChunk bytes,
+// 4-byte aligned; byte i = byte (i mod 4) of the little-endian `word`.
 struct FillChunk {
   void *ptr;
   uint32_t bytes;
-  uint32_t value;
+  uint32_t word;
 };
 constexpr size_t kFillChunk = 64 * 1024;
 

@@ -61,9 +61,9 @@ std::string fmt(const char *f, ...) {
     }                                                                                 \
   } while (0)
 
-struct Fill {  // one memset
+struct Fill {  // one k_fill range: byte i = byte (i mod 4) of the little-endian word
   void *ptr;
-  int value;
+  uint32_t word;
   size_t bytes;
 };
 
@@ -131,7 +131,12 @@ struct bx_plan {
   int64_t max_vn = 0;               // largest V*n over list-placer jobs
   bool any_topo = false, any_list = false;
   int launches = 0;
-  cudaEvent_t ev[2] = {nullptr, nullptr};  // brackets the placer kernel(s)
+  cudaEvent_t ev[2] = {nullptr, nullptr};  // brackets the placer kernel(s) (ring slot 0)
+  // per-step placer-kernel event pairs of the last kRing bx_plan_place calls
+  // (owned plans; a borrowed one-shot plan keeps the single pair above)
+  static constexpr int kRing = 64;
+  std::vector<cudaEvent_t> ring0, ring1;
+  int64_t places = 0;
   int64_t *prof = nullptr;                 // per-job latency breakdown (BX_PROFILE=1)
   // simulator
   void *sim_pool = nullptr;
@@ -234,6 +239,10 @@ void bx_plan_destroy(bx_plan *plan) {
   if (plan->sim_fill_dev) cudaFree(plan->sim_fill_dev);
   if (plan->ev[0]) cudaEventDestroy(plan->ev[0]);
   if (plan->ev[1]) cudaEventDestroy(plan->ev[1]);
+  for (size_t i = 1; i < plan->ring0.size(); ++i) {
+    cudaEventDestroy(plan->ring0[i]);
+    cudaEventDestroy(plan->ring1[i]);
+  }
   if (plan->fork) cudaEventDestroy(plan->fork);
   if (plan->join) cudaEventDestroy(plan->join);
   if (plan->s2) cudaStreamDestroy(plan->s2);
@@ -256,7 +265,7 @@ int upload_fills(const std::vector<Fill> &fills, Arena *A, int slot, FillChunk *
   for (const Fill &f : fills) {
     for (size_t o = 0; o < f.bytes; o += kFillChunk) {
       const size_t b = std::min(kFillChunk, f.bytes - o);
-      t.push_back({static_cast<char *>(f.ptr) + o, static_cast<uint32_t>(b), static_cast<uint32_t>(f.value & 0xff)});
+      t.push_back({static_cast<char *>(f.ptr) + o, static_cast<uint32_t>(b), f.word});
     }
   }
   *n = static_cast<int>(t.size());
@@ -636,7 +645,7 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     // a job that is never placed (host validation) or fails in the placer
     // leaves device_of = -1 and empty exec lists, so a later simulate of it
     // fails validation instead of walking stale lists
-    P->fills.push_back({d.device_of, 0xff, 4 * size_t(V)});
+    P->fills.push_back({d.device_of, 0xffffffffu, 4 * size_t(V)});
     P->fills.push_back({d.exec_off, 0, 4 * size_t(n + 1)});
     P->in_off.push_back({o.cap, o.fav});
     d.prof = P->prof ? P->prof + static_cast<size_t>(kProfSlots) * i : nullptr;
@@ -676,10 +685,16 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
         P->max_vn = std::max(P->max_vn, int64_t(G.V) * J.n);
       }
     }
-    P->fills.push_back({d.cache, 0xff, 8 * size_t(V * n)});
+    P->fills.push_back({d.cache, 0xffffffffu, 8 * size_t(V * n)});
     P->fills.push_back({d.dead, 0, size_t(V * n)});
     P->fills.push_back({d.sc_gen, 0, 4 * size_t(256 * n)});
-    P->fills.push_back({d.err, 0, sizeof(DErr)});
+    if (d.skip) {  // the status record carries the host verdict (message kept host-side)
+      P->fills.push_back({d.err, static_cast<uint32_t>(st), 4});
+      P->fills.push_back({reinterpret_cast<char *>(d.err) + 4, static_cast<uint32_t>(E_HOST), 4});
+      P->fills.push_back({reinterpret_cast<char *>(d.err) + 8, 0, sizeof(DErr) - 8});
+    } else {
+      P->fills.push_back({d.err, 0, sizeof(DErr)});
+    }
     // K2s: parallel-comm list jobs of single-graph-sized plans whose per-node
     // state fits one SM's shared memory; the kernel re-checks the value
     // bounds on the device and leaves the job to the general kernels if any
@@ -782,6 +797,17 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     BX_CUDA(cudaEventCreate(&P->ev[0]), msg, msglen);
     BX_CUDA(cudaEventCreate(&P->ev[1]), msg, msglen);
   }
+  P->ring0.assign(1, P->ev[0]);
+  P->ring1.assign(1, P->ev[1]);
+  if (!A) {
+    for (int i = 1; i < bx_plan::kRing; ++i) {
+      cudaEvent_t a = nullptr, b = nullptr;
+      BX_CUDA(cudaEventCreate(&a), msg, msglen);
+      BX_CUDA(cudaEventCreate(&b), msg, msglen);
+      P->ring0.push_back(a);
+      P->ring1.push_back(b);
+    }
+  }
   {
     int rc = upload_fills(P->fills, A, 4, &P->fill_dev, &P->nfill, msg, msglen);
     if (rc) return rc;
@@ -841,7 +867,8 @@ int bx_plan_place(bx_plan *P, void *stream) {
   }
   launch_kahn(P->dg_dev, P->queues_dev, P->ngraphs, s);
   P->launches += 1;
-  cudaEventRecord(P->ev[0], s);
+  const size_t slot = static_cast<size_t>(P->places % static_cast<int64_t>(P->ring0.size()));
+  cudaEventRecord(P->ring0[slot], s);
   if (P->n_sf_etf + P->n_sf_sct > 0) {
     launch_small_frontier(P->dj_dev, P->sf_order_dev, P->n_sf_etf, P->n_sf_sct, P->dg_dev, P->dp_dev, P->sf_smem,
                           P->prof != nullptr, s);
@@ -860,7 +887,8 @@ int bx_plan_place(bx_plan *P, void *stream) {
     cudaEventRecord(P->join, P->s2);
     cudaStreamWaitEvent(s, P->join, 0);
   }
-  cudaEventRecord(P->ev[1], s);
+  cudaEventRecord(P->ring1[slot], s);
+  P->places++;
   P->launches += (P->any_topo ? 1 : 0) + (P->n_etf > 0) + (P->n_small > P->n_etf) + (P->n_bpar > 0) + (P->n_bseq > 0);
   return launch_status();
 }
@@ -888,11 +916,39 @@ int bx_plan_profile(bx_plan *P, int32_t job, int64_t *out16) {
 }
 
 float bx_plan_kernel_ms(bx_plan *P) {
-  cudaSetDevice(P->device);
-  if (cudaEventSynchronize(P->ev[1]) != cudaSuccess) return -1.0f;
   float ms = -1.0f;
-  if (cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]) != cudaSuccess) return -1.0f;
-  return ms;
+  return bx_plan_kernel_times(P, 1, &ms) == 1 ? ms : -1.0f;
+}
+
+int bx_plan_kernel_times(bx_plan *P, int32_t count, float *ms) {
+  cudaSetDevice(P->device);
+  const int64_t ring = static_cast<int64_t>(P->ring0.size());
+  const int64_t have = std::min<int64_t>({static_cast<int64_t>(count), P->places, ring});
+  for (int64_t i = 0; i < have; ++i) {
+    const int64_t step = P->places - have + i;
+    const size_t slot = static_cast<size_t>(step % ring);
+    if (cudaEventSynchronize(P->ring1[slot]) != cudaSuccess) return -1;
+    if (cudaEventElapsedTime(&ms[i], P->ring0[slot], P->ring1[slot]) != cudaSuccess) return -1;
+  }
+  return static_cast<int>(have);
+}
+
+int bx_plan_output_region(const bx_plan *P, void **dev, int64_t *bytes) {
+  *dev = P->dev_out;
+  *bytes = static_cast<int64_t>(P->out_bytes);
+  return BX_OK;
+}
+
+int bx_plan_job_outputs(const bx_plan *P, int32_t job, int64_t *offs6) {
+  if (job < 0 || job >= P->njobs) return BX_VALIDATION;
+  const auto &o = P->out_off[job];
+  offs6[0] = static_cast<int64_t>(o.dev);
+  offs6[1] = static_cast<int64_t>(o.start);
+  offs6[2] = static_cast<int64_t>(o.eo);
+  offs6[3] = static_cast<int64_t>(o.eoff);
+  offs6[4] = static_cast<int64_t>(o.stats);
+  offs6[5] = static_cast<int64_t>(o.err);
+  return BX_OK;
 }
 
 static std::string cycle_message(const bx_plan *P, int g, cudaStream_t s) {

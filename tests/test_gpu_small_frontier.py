@@ -164,4 +164,4 @@ def test_small_frontier_can_be_disabled(bx):
     a = _plan_one(bx, gg, "m-etf", caps, bx.CommModel(*W.COMM_TEST))
     b = _plan_one(bx, gg, "m-etf", caps, bx.CommModel(*W.COMM_TEST), options={"no_small_frontier": 1})
     assert a[3] == "small-frontier" and b[3] == "rounds"
-    _same(a[2], b[2])
+    assert a[2] == b[2] and a[2].stats == b[2].stats
