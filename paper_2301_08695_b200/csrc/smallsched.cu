@@ -38,13 +38,20 @@
 // edge whose consumer first landed on q, so for a producer whose out-edges
 // all carry the same comm time the cache never changes a term: only the
 // remaining ("non-uniform") producers get cache rows (nu index x n, shared
-// memory).
+// memory), each entry the 16-bit comm time of the edge that brought the
+// tensor (its arrival is the producer's finish plus that).
 //
 // Times are int32 here: the kernel first checks sum(k) + (V + 2) * c_max
 // < 2^31 (every start is at most the previous largest finish + c_max, also
-// for the m-SCT floor) and 0 <= c < 2^30. Any check that fails — or a
-// frontier beyond 256 pairs at any point — leaves sdone = 0 and the general
-// kernels (listsched.cu), launched behind this one, place the job instead.
+// for the m-SCT floor), 0 <= c < 2^16 - 1 and in-degrees below 2^16 - 1
+// (16-bit pending counters). Any check that fails — or a frontier beyond
+// 256 pairs at any point — leaves sdone = 0 and the general kernels
+// (listsched.cu), launched behind this one, place the job instead.
+//
+// Per-node state is 12 bytes of shared memory (finish/device, pending,
+// ready slot), so graphs up to ~12k meta nodes fit; the rest of the SM's
+// 256 KB goes to L1, which three helper warps fill with the graph arrays
+// before the scheduling warp needs them.
 #include "sched_common.cuh"
 
 namespace bx {
@@ -70,8 +77,10 @@ struct SSm {
   int32_t *F, *awf, *awu, *excl;  // [32] per device
   int64_t *res, *cap;             // [32]
   uint64_t *info;                 // [V] finish << 32 | device (0xffffffff: unplaced)
-  int32_t *pending, *rpos;        // [V]
-  int32_t *nuc;                   // [nucap * n] cache arrival per non-uniform producer, -1 absent
+  uint16_t *pending;              // [V] parents not yet placed (decremented as 32-bit words)
+  int16_t *rpos;                  // [V] ready slot of a node, -1 none
+  uint16_t *nuc;                  // [nucap * n] per non-uniform producer and device: comm time of the
+                                  // edge that first brought its tensor there (arrival = finish + it), 0xffff absent
   // ready slots
   int32_t *node, *kk, *inb, *ine, *outb, *oute, *alive, *urg;  // [kSPairs]
   int64_t *need;                                               // [kSPairs]
@@ -87,8 +96,8 @@ __host__ __device__ inline size_t small_smem_bytes(int V, int n, int nucap, int 
   (void)n;
   size_t b = 0;
   b += 4 * 32 * 4 + 2 * 32 * 8;
-  b += size_t(V) * 8 + size_t(V) * 8;
-  b += (size_t(nucap) * n * 4 + 7) & ~size_t(7);
+  b += size_t(V) * 8 + 2 * ((size_t(V) * 2 + 3) & ~size_t(3));
+  b += (size_t(nucap) * n * 2 + 7) & ~size_t(7);
   b += kSPairs * (8 * 4 + 8 + 4);
   b += 7 * (kSCommits + 1) * 4 + 4;
   b += 2 * size_t(nccap) * 4 + kSPairs * 4 + 32 * 4;
@@ -108,11 +117,12 @@ __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, i
   m.awu = p32 + 64;
   m.excl = p32 + 96;
   p32 += 128;
-  m.pending = p32;
-  m.rpos = p32 + V;
-  p32 += 2 * V;
-  m.nuc = p32;
-  p32 += nucap * n;
+  const int vw = (V + 1) / 2;  // int32 words of a [V] 16-bit array
+  m.pending = reinterpret_cast<uint16_t *>(p32);
+  m.rpos = reinterpret_cast<int16_t *>(p32 + vw);
+  p32 += 2 * vw;
+  m.nuc = reinterpret_cast<uint16_t *>(p32);
+  p32 += (nucap * n + 1) / 2;
   m.node = p32;
   m.kk = p32 + kSPairs;
   m.inb = p32 + 2 * kSPairs;
@@ -164,14 +174,14 @@ __device__ __forceinline__ int32_t small_dr(const SSm &m, const SGraph &G, int n
     if (sm_dev(a0) == q) {
       t0 = f0;
     } else {
-      const int32_t z = u0 >= 0 ? m.nuc[u0 * n + q] : -1;
-      t0 = z >= 0 ? max(f0, z) : f0 + c0;
+      const unsigned z = u0 >= 0 ? m.nuc[u0 * n + q] : 0xffffu;
+      t0 = f0 + (z != 0xffffu ? static_cast<int32_t>(z) : c0);
     }
     if (sm_dev(a1) == q) {
       t1 = f1;
     } else {
-      const int32_t z = u1 >= 0 ? m.nuc[u1 * n + q] : -1;
-      t1 = z >= 0 ? max(f1, z) : f1 + c1;
+      const unsigned z = u1 >= 0 ? m.nuc[u1 * n + q] : 0xffffu;
+      t1 = f1 + (z != 0xffffu ? static_cast<int32_t>(z) : c1);
     }
     t = max(t, max(t0, t1));
     if (kUrg) u = max(u, max(f0 + c0, f1 + c1));
@@ -186,8 +196,8 @@ __device__ __forceinline__ int32_t small_dr(const SSm &m, const SGraph &G, int n
     if (sm_dev(a0) == q) {
       t0 = f0;
     } else {
-      const int32_t z = u0 >= 0 ? m.nuc[u0 * n + q] : -1;
-      t0 = z >= 0 ? max(f0, z) : f0 + c0;
+      const unsigned z = u0 >= 0 ? m.nuc[u0 * n + q] : 0xffffu;
+      t0 = f0 + (z != 0xffffu ? static_cast<int32_t>(z) : c0);
     }
     t = max(t, t0);
     if (kUrg) u = max(u, f0 + c0);
@@ -409,16 +419,48 @@ __device__ __forceinline__ int small_select(const SSm &m, const SGraph &G, const
   return nc;
 }
 
+// Brings [p, p + bytes) into this SM's L1 (one 16-byte load per 32-byte
+// sector, results folded into a value the caller keeps alive).
+__device__ __forceinline__ unsigned warm_l1(const void *p, size_t bytes, int tid, int nthreads) {
+  const char *b = static_cast<const char *>(p);
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(b) & ~uintptr_t(31);
+  const uintptr_t a1 = reinterpret_cast<uintptr_t>(b + bytes);
+  unsigned acc = 0;
+  for (uintptr_t a = a0 + 32 * static_cast<uintptr_t>(tid); a < a1; a += 32 * static_cast<uintptr_t>(nthreads)) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(a));
+    acc ^= v.x;
+  }
+  return acc;
+}
+
+// One CTA per job: warp 0 schedules; warps 1..kSWarm-1 first pull the
+// graph arrays the scheduler reads into the SM's L1 (every one of them is
+// read through __ldg, and each scheduling round is a chain of dependent
+// loads, so L1 instead of L2 latency on each level), then exit.
+constexpr int kSWarm = 4;
+
 template <bool kSct, bool kProf>
-__global__ void __launch_bounds__(32, 1)
+__global__ void __launch_bounds__(32 * kSWarm, 1)
     k_place_small(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   if (blockIdx.x >= njobs) return;
   const DJob jb = jobs[order[blockIdx.x]];
   if (jb.skip || jb.sdone == nullptr) return;
   const DGraph g = graphs[jb.graph];
   const DPrep pr = preps[jb.prep];
+  if (threadIdx.x >= 32) {
+    const int tid = threadIdx.x - 32, nt = 32 * (kSWarm - 1);
+    const size_t V = static_cast<size_t>(g.V), E = static_cast<size_t>(g.E);
+    unsigned acc = warm_l1(g.in_off, 4 * (V + 1), tid, nt) ^ warm_l1(g.out_off, 4 * (V + 1), tid, nt);
+    acc ^= warm_l1(g.in_src, 4 * E, tid, nt) ^ warm_l1(pr.in_c32, 4 * E, tid, nt);
+    acc ^= warm_l1(pr.nu, 4 * V, tid, nt) ^ warm_l1(g.edst, 4 * E, tid, nt);
+    acc ^= warm_l1(g.k, 8 * V, tid, nt) ^ warm_l1(g.need, 8 * V, tid, nt);
+    acc ^= warm_l1(g.need_order, 4 * V, tid, nt);
+    if (kSct && jb.fav) acc ^= warm_l1(jb.fav, 4 * V, tid, nt);
+    asm volatile("" ::"r"(acc));  // keeps the loads
+    return;
+  }
   if (g.flags[0] != g.V || g.flags[1]) {  // the reference's validation order: cycle, then bytes
     if (lane == 0) {
       set_err(jb.err, kValidation, g.flags[0] != g.V ? E_CYCLE : E_NEG_BYTES, 0, 0);
@@ -431,7 +473,7 @@ __global__ void __launch_bounds__(32, 1)
   const int nccap = jb.maxin > 1024 ? jb.maxin : 1024;
   // dynamic eligibility (see the header); otherwise the general kernel runs it
   if (*pr.cbad || g.flags[2] || *g.ksum < 0 || *pr.nu_count > jb.nucap || n > 32 || V >= (1 << 26) ||
-      cmax64 >= (int64_t(1) << 30) || *g.ksum + (int64_t(V) + 2) * cmax64 >= int64_t(INT32_MAX))
+      cmax64 >= 0xffff || jb.maxin >= 0xffff || *g.ksum + (int64_t(V) + 2) * cmax64 >= int64_t(INT32_MAX))
     return;
   const int32_t cmax = static_cast<int32_t>(cmax64);
   const SSm m = small_layout(smem, V, n, jb.nucap, nccap);
@@ -455,7 +497,7 @@ __global__ void __launch_bounds__(32, 1)
     m.excl[lane] = 0;
     m.res[lane] = 0;
     m.cap[lane] = lane < n ? jb.cap[lane] : 0;
-    for (int x = lane; x < jb.nucap * n; x += 32) m.nuc[x] = -1;
+    for (int x = lane; x < jb.nucap * n; x += 32) m.nuc[x] = 0xffffu;
   }
   int R = 0;
   bool overflow = false;
@@ -576,9 +618,10 @@ __global__ void __launch_bounds__(32, 1)
         if (sm_dev(a) != pr_) {
           const int u = __ldg(G.nu + i);
           if (u >= 0) {
-            int32_t *slot = m.nuc + u * n + pr_;
-            if (*slot < 0) {
-              *slot = sm_fin(a) + __ldg(G.c32 + x);
+            // one commit per device per round, so no two lanes share a slot
+            uint16_t *slot = m.nuc + u * n + pr_;
+            if (*slot == 0xffffu) {
+              *slot = static_cast<uint16_t>(__ldg(G.c32 + x));
               fresh = true;
             }
           }
@@ -602,7 +645,11 @@ __global__ void __launch_bounds__(32, 1)
         while (r + 1 < nc && m.pout[r + 1] <= idx) ++r;
         const int y = m.outb[m.cs[r]] + idx - m.pout[r];
         child = __ldg(G.out_dst + y);
-        fresh = atomicSub(&m.pending[child], 1) == 1;
+        // 16-bit counters decremented through their 32-bit word (a counter
+        // is >= 1 when decremented, so no borrow crosses halves)
+        unsigned *word = reinterpret_cast<unsigned *>(m.pending) + (child >> 1);
+        const int sh = 16 * (child & 1);
+        fresh = ((atomicSub(word, 1u << sh) >> sh) & 0xffffu) == 1;
       }
       const unsigned b = __ballot_sync(kFull, fresh);
       if (fresh) {
@@ -779,7 +826,11 @@ static void launch_sf(const DJob *jobs, const int32_t *order, int nj, const DGra
   if (nj <= 0) return;
   cudaFuncSetAttribute(k_place_small<kSct, kProf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
-  k_place_small<kSct, kProf><<<nj, 32, smem, s>>>(jobs, order, nj, graphs, preps);
+  // the smallest shared-memory carveout that holds the job state: the rest
+  // of the unified 256 KB is L1 for the warmed graph arrays
+  const int pct = static_cast<int>((smem * 100 + 228 * 1024 - 1) / (228 * 1024));
+  cudaFuncSetAttribute(k_place_small<kSct, kProf>, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 1 ? 1 : pct);
+  k_place_small<kSct, kProf><<<nj, 32 * kSWarm, smem, s>>>(jobs, order, nj, graphs, preps);
 }
 
 void launch_small_frontier(const DJob *jobs, const int32_t *order, int n_etf, int n_sct, const DGraph *graphs,

@@ -354,3 +354,43 @@ def test_model_configs_end_to_end(bx, name):
                               W.COMM_TEST, fv)
             assert pe is None
             _assert_same(p, o, stats=algo != "m-topo")
+
+
+@pytest.mark.parametrize("kernel", ["warp", "rounds", "cta-seq"])
+def test_composite_key_clip_falls_back_exactly(bx, kernel):
+    """Keys more than 2^32 - 2 us above a column's dev_free saturate the
+    composite (key - F[q]) << 32 | node scan (csrc/listsched.cu), which must
+    then rescan with the exact 96-bit comparison (warp_topk_exact). Compute
+    times around 2^33 us (the reference accepts any int64) drive every
+    kernel through that fallback; results stay bit-exact."""
+    opts = {"warp": {"wide_min_vn": (1 << 31) - 1, "no_small_frontier": 1},
+            "rounds": {"wide_min_vn": 0, "no_small_frontier": 1},
+            "cta-seq": {"wide_min_vn": 0, "no_small_frontier": 1}}[kernel]
+    cms = [(5.0, 0.001, 0)] if kernel == "cta-seq" else [(12.5, 0.002, 1), (0.0, 0.0, 1)]
+    rng = np.random.default_rng(33)
+    used = 0
+    for g in (W.layered_dag(6, 10, 1), W.branchy(4, 2), W.wide_random(80, 3), W.grid_chain(12, 4, 4)):
+        m = W.as_meta_dict(g)
+        m["k"] = rng.integers(1 << 32, 1 << 34, m["V"]).astype(np.int64)
+        m["k"][rng.random(m["V"]) < 0.3] = rng.integers(1, 100, 1)[0]  # mix tiny and huge durations
+        gg = _meta(bx, m)
+        for n in (2, 3, 5):
+            caps = [W.bench_capacity(g, n, 1.4)] * n
+            for cm in cms:
+                for algo in (1, 2):
+                    fv = golden_cases.fav_first(m) if algo == 2 else None
+                    o = Restate.place(m, algo, caps, cm, fv)
+                    plan = bx.Plan([gg], [bx.Job(0, ALGO[algo], np.array(caps, np.int64), bx.CommModel(*cm), fv)],
+                                   options=opts)
+                    plan.upload()
+                    plan.place()
+                    plan.download()
+                    kern = plan.job_kernel(0)
+                    p = plan.result(0)
+                    plan.close()
+                    _assert_same(p, o)
+                    used += kern == kernel
+    assert used > 0, f"the {kernel} kernel never ran"
+    # the scenario provably saturates: a device idle at t = 0 next to a ready
+    # node whose parent finishes beyond 2^32 us
+    assert (m["k"] >= (1 << 32)).any()

@@ -23,12 +23,37 @@ CASES = {
     "wide100k_x16": (lambda: W.wide_random(100000, 5), 16, "m-etf", 1.2),
     "layered100k_x4_sct": (lambda: W.layered_dag_fast(100, 1000, 3), 4, "m-sct", 1.2),
     "c4_layered1M_x64": (lambda: W.layered_dag_fast(1000, 1000, 1), 64, "m-etf", 1.5),
+    "c4_layered1M_x64_tight": (lambda: W.layered_dag_fast(1000, 1000, 1), 64, "m-etf", 1.05),
+    "c4_layered1M_x64_sct": (lambda: W.layered_dag_fast(1000, 1000, 1), 64, "m-sct", 1.5),
+    # the reference's own layered-chain family (generate_graph, 4 stacked chains,
+    # seed 55; SURVEY Appendix A / BASELINE.md §2): a 4-wide frontier
+    "refchain100k_x4": (lambda: _refchain(100000), 4, "m-etf", 1.5),
+    "refchain100k_x8": (lambda: _refchain(100000), 8, "m-etf", 1.5),
+    "seq_refchain100k_x4": (lambda: _refchain(100000), 4, "m-etf", 1.5),
+    "seq_refchain100k_x8": (lambda: _refchain(100000), 8, "m-etf", 1.5),
     # sequential comm mode (queues on both endpoints), the survey probe's model {5 us, 0.001 us/B}
     "seq_layered100k_x4": (lambda: W.layered_dag_fast(100, 1000, 3), 4, "m-etf", 1.2),
     "seq_layered100k_x8": (lambda: W.layered_dag_fast(100, 1000, 3), 8, "m-etf", 1.2),
     "seq_wide100k_x16": (lambda: W.wide_random(100000, 5), 16, "m-etf", 1.2),
 }
 COMM_SEQ = (5.0, 0.001, 0)
+
+
+def _refchain(V, layers=4, seed=55):
+    """generate_graph(layered-chain) from the compiled reference (input
+    generation only), as a singleton meta-graph dict."""
+    from oracle import Ref
+    base = Ref.generate("layered-chain", V, seed, layers=layers)
+    ids = base["id"]
+    order = np.argsort(ids, kind="stable")
+    idx = np.empty_like(order)
+    idx[order] = np.arange(len(ids))
+    src = idx[order[np.searchsorted(ids[order], base["src"])]]  # node id -> make_graph index
+    dst = idx[order[np.searchsorted(ids[order], base["dst"])]]
+    e = np.lexsort((dst, src))
+    return dict(V=len(ids), k=base["k"][order], temp=base["temp"][order], perm=base["perm"][order],
+                out=base["out"][order], esrc=src[e].astype(np.int32), edst=dst[e].astype(np.int32),
+                ebytes=base["bytes"][e], name="refchain")
 
 
 def run_config(name, cpu=True, reps=10):
