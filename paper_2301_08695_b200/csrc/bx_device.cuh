@@ -82,7 +82,9 @@ struct DPrep {
   int32_t *in_c32;    // [E] in_c as int32 (valid when *cbad == 0)
   int32_t *nu;        // [V] index of a producer whose out-edges carry different comm times, else -1
   int32_t *nu_count;  // number of such producers
-  int32_t *cbad;      // some comm time outside [0, 2^30)
+  int32_t *cbad;      // some comm time outside [0, 2^16 - 1)
+  int4 *node_pack;    // [V] in_b, out_b, in_cnt | out_cnt << 16, k (int32)
+  uint2 *in_pack;     // [E] per in-CSR slot: parent, (nu(parent) + 1) << 16 | comm time
 };
 
 struct DJob {

@@ -61,6 +61,9 @@ std::string fmt(const char *f, ...) {
     }                                                                                 \
   } while (0)
 
+constexpr int kMaxRosterList = 96;   // m-ETF / m-SCT
+constexpr int kMaxRosterTopo = 1000; // m-TOPO
+
 struct Fill {  // one k_fill range: byte i = byte (i mod 4) of the little-endian word
   void *ptr;
   uint32_t word;
@@ -127,7 +130,8 @@ struct bx_plan {
   std::vector<int32_t> res_status;   // decoded by the last download
   std::vector<std::string> res_msg;
   std::vector<Fill> fills;
-  int maxn = 1;
+  int maxn = 1;      // largest roster among jobs that reach a placer kernel
+  int maxn_all = 1;  // largest roster of any job (the simulator takes external placements)
   int64_t max_vn = 0;               // largest V*n over list-placer jobs
   bool any_topo = false, any_list = false;
   int launches = 0;
@@ -334,7 +338,7 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     auto it = prep_of.find(key);
     if (it == prep_of.end()) it = prep_of.emplace(key, static_cast<int>(prep_of.size())).first;
     job_prep[i] = it->second;
-    P->maxn = std::max(P->maxn, J.n);
+    P->maxn_all = std::max(P->maxn_all, J.n);
   }
   P->nprep = static_cast<int>(prep_of.size());
 
@@ -374,7 +378,7 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
   const size_t seg_at = L.take<int32_t>(size_t(ngraphs) + 1);
   std::vector<std::pair<size_t, size_t>> po(P->nprep);  // in_c, cmax
   struct POff {
-    size_t c32, nu, cnt;
+    size_t c32, nu, cnt, npk, ipk;
   };
   std::vector<POff> pso(P->nprep);
   std::vector<int> prep_graph(P->nprep);
@@ -389,6 +393,10 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     pso[pi].c32 = L.take<int32_t>(graphs[g].E);
     pso[pi].nu = L.take<int32_t>(graphs[g].V);
     pso[pi].cnt = L.take<int32_t>(2);
+    // K2s runs only in plans of at most 148 list jobs (`few` below)
+    const bool few_jobs = std::count_if(jobs, jobs + njobs, [](const bx_job &J) { return J.algo != BX_ALGO_MTOPO; }) <= 148;
+    pso[pi].npk = L.take<int4>(few_jobs ? graphs[g].V : 1);
+    pso[pi].ipk = L.take<uint2>(few_jobs ? graphs[g].E : 1);
   }
   struct JOff {
     size_t cap, fav, K, cache, dead, pending, alive, ready, rpos, cseq, nc, finish, urgent, scv, scg, pdev, pfin, K2, urgent2, ready2, alive2, ncw, newl, device_of,
@@ -501,6 +509,9 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
   void *pool = P->pool;
   P->dev_in = at<char>(pool, in_at);
   P->dev_out = at<char>(pool, out_at);
+  // alignment gaps of the output region are copied by every download: give
+  // them a defined value once
+  BX_CUDA(cudaMemset(P->dev_out, 0, std::max<size_t>(P->out_bytes, 1)), msg, msglen);
 
   P->need_all = at<int64_t>(pool, need_at);
   P->need_keys_all = at<int64_t>(pool, need_keys_at);
@@ -571,6 +582,8 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     d.nu = at<int32_t>(pool, pso[pi].nu);
     d.nu_count = at<int32_t>(pool, pso[pi].cnt);
     d.cbad = d.nu_count + 1;
+    d.node_pack = at<int4>(pool, pso[pi].npk);
+    d.in_pack = at<uint2>(pool, pso[pi].ipk);
     d.first = 0;
     if (!graph_seen[d.graph]) {
       graph_seen[d.graph] = 1;
@@ -669,6 +682,14 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
       st = BX_VALIDATION;
       why = "unknown placement algorithm";
     }
+    // per-device scheduling state lives in shared memory (the round kernel's
+    // 32-entry column lists: ~1.8 KB per device); larger rosters are refused
+    // per job instead of failing every launch of the plan
+    const int lim = J.algo == BX_ALGO_MTOPO ? kMaxRosterTopo : kMaxRosterList;
+    if (st == 0 && J.n > lim) {
+      st = BX_RUNTIME;
+      why = fmt("a roster of %d devices exceeds this engine's limit of %d per problem", J.n, lim);
+    }
     P->host_status[i] = st;
     P->host_msg[i] = why;
     d.skip = st != 0;
@@ -704,7 +725,7 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     d.maxin = g_maxin[J.graph];
     if (!d.skip && few && J.algo != BX_ALGO_MTOPO && J.cm.mode == BX_COMM_PARALLEL && J.n <= 32 && G.V > 0 &&
         G.V < (1 << 26) && !P->opt.no_small_frontier && P->opt.wide_min_vn < 0) {
-      const size_t sm = small_smem_bytes_host(G.V, J.n, d.nucap, std::max(1024, d.maxin));
+      const size_t sm = small_smem_bytes_host(G.V, J.n, d.nucap, J.n * std::max(1, d.maxin));
       if (sm <= 200 * 1024) {
         d.sdone = at<int32_t>(pool, o.sdone);
         P->fills.push_back({d.sdone, 0, 4});
@@ -713,6 +734,11 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
       }
     }
   }
+  // shared-memory slices are sized by the largest roster among jobs that
+  // reach a kernel: a rejected job's roster never costs the others a launch
+  P->maxn = 1;
+  for (int i = 0; i < njobs; ++i)
+    if (!P->dj[i].skip) P->maxn = std::max(P->maxn, jobs[i].n);
   P->dg_dev = at<DGraph>(pool, tables);
   P->dp_dev = at<DPrep>(pool, ptables);
   P->dj_dev = at<DJob>(pool, jtables);
@@ -1210,7 +1236,7 @@ int bx_plan_simulate(bx_plan *P, int32_t mem_mode, void *stream) {
     P->sim_mem_mode = mem_mode;
   }
   launch_fill(P->sim_fill_dev, P->nsim_fill, s);
-  launch_simulate(P->ds_dev, P->njobs, P->dg_dev, std::max(P->maxn, 1), P->opt.sim_heap_cap, s);
+  launch_simulate(P->ds_dev, P->njobs, P->dg_dev, std::max(P->maxn_all, 1), P->opt.sim_heap_cap, s);
   return launch_status();
 }
 

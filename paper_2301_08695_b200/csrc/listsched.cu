@@ -503,12 +503,16 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
   Tops T;
   int64_t *stg_t = nullptr;
   int32_t *stg_j = nullptr, *stg_s = nullptr, *stg_live = nullptr;
-  int32_t *s_R, *s_done, *s_rq;
+  // group control words, double-buffered by iteration parity: every warp
+  // reads buffer it & 1 after the loop-top barrier, the leader writes the
+  // next iteration's values into the other buffer, which nobody can still
+  // be reading (they all passed this iteration's barrier)
+  int32_t *ctl, *s_R, *s_done, *s_rq;
   int64_t *nk;   // [KT*st] sequential mode: re-keyed list entries
   int32_t *vst;  // [st] sequential mode: commit count + 1 at which the column's list was re-keyed
   int32_t *xr;   // [st] sequential mode: the column's stored keys proved stale -> exact rescan
   {
-    const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 16;
+    const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 32;  // + control words (2 x 3)
     unsigned char *base = smem + static_cast<size_t>(pslot) * per;
     c.F = reinterpret_cast<int64_t *>(base);
     c.tail = c.F + maxn;
@@ -539,9 +543,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
       stg_live = stg_s + maxn * kW * KT;
       p32 = stg_live + maxn * kW;
     }
-    s_R = p32;
-    s_done = p32 + 1;
-    s_rq = p32 + 2;  // the one column the group rescans next (-1: none)
+    ctl = p32;  // [2][3]: R, done, the one column the group rescans next (-1: none)
   }
   const int V = c.V, n = c.n;
   const int64_t Vs = V;
@@ -583,11 +585,12 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
     for (int q = 0; q < n; ++q)
       for (int s = lane; s < R; s += 32) c.Kc[q * Vs + s] = 0;
     if (lane == 0) {
-      *s_R = R;
-      *s_done = V == 0;
-      *s_rq = -1;
+      ctl[0] = R;
+      ctl[1] = V == 0;
+      ctl[2] = -1;
     }
   }
+  int it = 0;
 
   int32_t gen = 0;
   int placed = 0, nexcl = 0;
@@ -598,11 +601,21 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
 
   while (true) {
     group_sync<kW>();
-    if (*s_done) break;
-    int R = *s_R;
+    const int32_t *cur = ctl + 3 * (it & 1);
+    s_R = ctl + 3 * ((it + 1) & 1);
+    s_done = s_R + 1;
+    s_rq = s_R + 2;
+    ++it;
+    if (cur[1]) break;
+    int R = cur[0];
+    if (leader && lane == 0) {  // carried into the next iteration unless the leader changes them
+      s_R[0] = cur[0];
+      s_R[1] = cur[1];
+      s_R[2] = cur[2];
+    }
     if (kProf) ++prof[P_STEPS];
     // ---- rescan the column the leader asked for (every warp of the group) --
-    const int rq = *s_rq;
+    const int rq = cur[2];
     if (rq >= 0) {
       const int qq = rq;
       int64_t dt[KT];
@@ -1067,7 +1080,7 @@ template <int kW, bool kProf, bool kEtf = false>
 static void launch_w(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps,
                      int maxn, int seq_only, cudaStream_t s) {
   if (njobs <= 0) return;
-  const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 16;
+  const size_t per = static_cast<size_t>(maxn) * (kSmemPerDevice + stage_bytes_per_device(kW)) + 32;  // + control words (2 x 3)
   const int probs_per_cta = kW > 1 ? 1 : BX_PPC;
   const int threads = kW > 1 ? 32 * kW : 32 * BX_PPC;
   const int blocks = (njobs + probs_per_cta - 1) / probs_per_cta;

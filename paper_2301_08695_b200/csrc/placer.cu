@@ -201,6 +201,10 @@ __global__ void __launch_bounds__(32 * kWarps) k_place_topo(const DJob *jobs, in
     if (lane == 0) set_err(jb.err, kValidation, E_CYCLE, 0, 0);
     return;
   }
+  if (g.flags[1]) {  // a negative tensor size: comm_time throws (cost_model.cpp:31-33), as in the list placers
+    if (lane == 0) set_err(jb.err, kValidation, E_NEG_BYTES, 0, 0);
+    return;
+  }
 
   Ctx c;
   c.V = V;

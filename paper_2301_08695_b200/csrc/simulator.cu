@@ -322,8 +322,9 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
         if (cdev == dev) continue;
         ++remote;
         c.s.dest_cnt[cdev] = 1;
+        // the reference's per-destination slot starts at 0 (std::map value)
         atomicMax(reinterpret_cast<unsigned long long *>(&c.s.dest_bytes[cdev]),
-                  static_cast<unsigned long long>(c.g.ebytes[y]));
+                  static_cast<unsigned long long>(c.g.ebytes[y] > 0 ? c.g.ebytes[y] : 0));
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) remote += __shfl_xor_sync(kFullS, remote, o);
@@ -516,7 +517,8 @@ __global__ void k_sim_prep_b(const DSim *sims, const DGraph *graphs, int base) {
       auto *slot = reinterpret_cast<unsigned long long *>(s.mb + static_cast<int64_t>(i) * n + dc);
       f = atomicCAS(slot, ~0ull, ~0ull - 1) == ~0ull;
       cnt += f;
-      atomicMax(reinterpret_cast<long long *>(slot), static_cast<long long>(g.ebytes[e]));
+      // the reference's per-destination slot starts at 0 (simulator.cpp:160-162)
+      atomicMax(reinterpret_cast<long long *>(slot), static_cast<long long>(g.ebytes[e] > 0 ? g.ebytes[e] : 0));
     }
     s.first[e] = f;
   }

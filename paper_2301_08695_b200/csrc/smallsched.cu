@@ -5,18 +5,19 @@
 // (key(j,p), j, p) over the live pairs and commits or discards it.
 //
 // Model-shaped training graphs keep a tiny ready frontier under list
-// scheduling (Inception/GNMT/Transformer meta graphs and the reference's
-// layered-chain family: 3-6 ready nodes on average), so a placement is a
-// chain of V dependent steps over a few dozen pairs. This kernel is built
-// for that chain: ONE warp per problem, no CTA barriers, every mutable
-// per-node value in shared memory, and every live pair held in a register
-// of some lane (R*n <= 256, at most 8 pairs per lane).
+// scheduling (Inception/GNMT/Transformer meta graphs: 3-12 ready nodes on
+// average), so a placement is a chain of V dependent steps over a few dozen
+// pairs, and its speed is the latency of one scheduling round. This kernel
+// is built for that chain: ONE warp per problem, no CTA barriers, every
+// mutable per-node value in shared memory, every live pair in a register of
+// some lane (R * n <= 512, at most 16 pairs per lane), and the static graph
+// read through packed records (one load per node, one per in-edge).
 //
 // A round:
 //   1. keys: each lane forms key = max(dev_free[q], DR[s][q]) (+ the m-SCT
-//      awake floor, placers.cpp:147-156) for its pairs from shared memory,
-//      as one 64-bit word (key << 32 | node << 5 | q) — (key, node, device)
-//      order in a single unsigned compare;
+//      awake floor, placers.cpp:147-156) for its pairs, as one 64-bit word
+//      (key << 32 | node << 5 | q): (key, node, device) order in a single
+//      unsigned compare; the memory check (placers.cpp:203-205) is a bit;
 //   2. selection: a two-REDUX warp minimum gives the global argmin; a pair
 //      that does not fit is discarded on the spot (placers.cpp:203-219);
 //      a pair that fits commits. After committing (j, p) at t every key that
@@ -24,13 +25,20 @@
 //      dev_free[p]; a newly cached parent only touches column p; a newly
 //      ready child has j as a parent), so the next minimum among the
 //      untouched pairs commits in the same round while its key is below the
-//      least such finish time T. m-SCT: a lifted reservation may lower the
-//      keys of its column, which then drops out of the round and lowers T to
-//      its dev_free (every key of a column is >= its dev_free);
-//   3. one batched update for all of the round's commits: cache arrivals
-//      (commit_schedulable_time, :95-101), readiness (:256-268), new
-//      data-ready rows and the re-keys of consumers whose parent tensor just
-//      landed (:271-279).
+//      least such finish time T — at most one commit per device per round.
+//      m-SCT: a lifted reservation may lower the keys of its column, which
+//      then drops out of the round and lowers T to its dev_free (every key of
+//      a column is >= its dev_free). A commit only updates registers here;
+//   3. lane r applies commit r (dev_free, memory slack, finish, outputs);
+//   4. one pass over the committed nodes' in- and out-edges: cache arrivals
+//      of remote parents (commit_schedulable_time, placers.cpp:95-101) and
+//      readiness (:256-268);
+//   5. committed slots leave, the last live slots move into the holes (one
+//      parallel step);
+//   6. new slots: static fields and data-ready rows DR[s][q], one (slot,
+//      device) item per lane;
+//   7. re-keys of ready consumers whose parent tensor just landed on a
+//      device (:271-279).
 //
 // Data-ready time DR[s][q] = max over parents i of: finish_i (same device),
 // max(finish_i, cache[i][q]) (tensor already on q), finish_i + c_e otherwise
@@ -43,23 +51,24 @@
 //
 // Times are int32 here: the kernel first checks sum(k) + (V + 2) * c_max
 // < 2^31 (every start is at most the previous largest finish + c_max, also
-// for the m-SCT floor), 0 <= c < 2^16 - 1 and in-degrees below 2^16 - 1
-// (16-bit pending counters). Any check that fails — or a frontier beyond
-// 256 pairs at any point — leaves sdone = 0 and the general kernels
-// (listsched.cu), launched behind this one, place the job instead.
+// for the m-SCT floor), 0 <= c < 2^16 - 1, in-degrees below 2^16 - 1 and
+// V < 2^16 - 1 (16-bit counters and packed indices). Any check that fails —
+// or a frontier beyond 512 pairs at any point — leaves sdone = 0 and the
+// general kernels (listsched.cu), launched behind this one, place the job
+// instead.
 //
 // Per-node state is 12 bytes of shared memory (finish/device, pending,
 // ready slot), so graphs up to ~12k meta nodes fit; the rest of the SM's
-// 256 KB goes to L1, which three helper warps fill with the graph arrays
-// before the scheduling warp needs them.
+// 256 KB is L1, which three helper warps fill with the packed graph before
+// the scheduling warp needs it.
 #include "sched_common.cuh"
 
 namespace bx {
 
-constexpr int kSP = 8;                  // pairs per lane
-constexpr int kSPairs = 32 * kSP;       // R * n <= 256
-constexpr int kSCommits = 32;           // commits per round
-constexpr int32_t kSDead = 0x7fffffff;  // DR of a discarded / excluded pair
+constexpr int kSP = 16;                  // pairs per lane
+constexpr int kSPairs = 32 * kSP;        // R * n <= 512
+constexpr int kSSlots = kSPairs;         // ready slots (n = 1)
+constexpr int32_t kSDead = 0x7fffffff;   // DR of a discarded / excluded pair
 constexpr uint64_t kSNone = ~0ull;
 
 __device__ __forceinline__ uint64_t sm_min_u64(uint64_t v) {
@@ -75,43 +84,41 @@ __device__ __forceinline__ int32_t sm_fin(uint64_t info) { return static_cast<in
 // Shared-memory layout of one problem (host: small_smem_bytes).
 struct SSm {
   int32_t *F, *awf, *awu, *excl;  // [32] per device
-  int64_t *res, *cap;             // [32]
+  int64_t *slack;                 // [32] capacity - reserved
   uint64_t *info;                 // [V] finish << 32 | device (0xffffffff: unplaced)
   uint16_t *pending;              // [V] parents not yet placed (decremented as 32-bit words)
   int16_t *rpos;                  // [V] ready slot of a node, -1 none
   uint16_t *nuc;                  // [nucap * n] per non-uniform producer and device: comm time of the
                                   // edge that first brought its tensor there (arrival = finish + it), 0xffff absent
   // ready slots
-  int32_t *node, *kk, *inb, *ine, *outb, *oute, *alive, *urg;  // [kSPairs]
-  int64_t *need;                                               // [kSPairs]
-  int32_t *dr;                                                 // [kSPairs]  DR[s * n + q]
+  int32_t *node, *kk, *inb, *outb, *cnt, *alive, *urg;  // [kSSlots]; cnt = in_cnt | out_cnt << 16
+  int64_t *need;                                        // [kSSlots]
+  int32_t *dr;                                          // [kSPairs] DR[s * n + q]
   // per round
-  int32_t *cj, *cp, *cfin, *cs, *pin, *pout, *ord;  // [kSCommits + 1]
-  int32_t *nci, *ncp;                               // [nccap] newly cached (producer, device)
-  int32_t *newn;                                    // [kSPairs] newly ready nodes
-  int32_t *scal;                                    // [32] exec-order counters
+  int32_t *pin, *pout;  // [32] per commit: first in- / out-edge item
+  int32_t *cpd, *csl;   // [32] per commit: device, slot
+  int32_t *nci, *ncp;   // [nccap] newly cached (producer, device)
+  int32_t *newn;        // [kSSlots] newly ready nodes
+  int32_t *scal;        // [32] exec-order counters
 };
 
 __host__ __device__ inline size_t small_smem_bytes(int V, int n, int nucap, int nccap) {
-  (void)n;
   size_t b = 0;
-  b += 4 * 32 * 4 + 2 * 32 * 8;
-  b += size_t(V) * 8 + 2 * ((size_t(V) * 2 + 3) & ~size_t(3));
-  b += (size_t(nucap) * n * 2 + 7) & ~size_t(7);
-  b += kSPairs * (8 * 4 + 8 + 4);
-  b += 7 * (kSCommits + 1) * 4 + 4;
-  b += 2 * size_t(nccap) * 4 + kSPairs * 4 + 32 * 4;
+  b += 32 * 8 + 4 * 32 * 4;                                    // slack, F/awf/awu/excl
+  b += size_t(V) * 8 + 2 * ((size_t(V) * 2 + 3) & ~size_t(3)); // info, pending, rpos
+  b += (size_t(nucap) * n * 2 + 7) & ~size_t(7);               // nuc
+  b += size_t(kSSlots) * (7 * 4 + 8) + size_t(kSPairs) * 4;    // slots, dr
+  b += 4 * 32 * 4 + 2 * size_t(nccap) * 4 + size_t(kSSlots) * 4 + 32 * 4;
   return b + 64;
 }
 
 __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, int nucap, int nccap) {
   SSm m;
   int64_t *p64 = reinterpret_cast<int64_t *>(base);
-  m.res = p64;
-  m.cap = p64 + 32;
-  m.info = reinterpret_cast<uint64_t *>(p64 + 64);
+  m.slack = p64;
+  m.info = reinterpret_cast<uint64_t *>(p64 + 32);
   m.need = reinterpret_cast<int64_t *>(m.info + V);
-  int32_t *p32 = reinterpret_cast<int32_t *>(m.need + kSPairs);
+  int32_t *p32 = reinterpret_cast<int32_t *>(m.need + kSSlots);
   m.F = p32;
   m.awf = p32 + 32;
   m.awu = p32 + 64;
@@ -124,104 +131,72 @@ __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, i
   m.nuc = reinterpret_cast<uint16_t *>(p32);
   p32 += (nucap * n + 1) / 2;
   m.node = p32;
-  m.kk = p32 + kSPairs;
-  m.inb = p32 + 2 * kSPairs;
-  m.ine = p32 + 3 * kSPairs;
-  m.outb = p32 + 4 * kSPairs;
-  m.oute = p32 + 5 * kSPairs;
-  m.alive = p32 + 6 * kSPairs;
-  m.urg = p32 + 7 * kSPairs;
-  m.dr = p32 + 8 * kSPairs;
-  p32 += 9 * kSPairs;
-  constexpr int C1 = kSCommits + 1;
-  m.cj = p32;
-  m.cp = p32 + C1;
-  m.cfin = p32 + 2 * C1;
-  m.cs = p32 + 3 * C1;
-  m.pin = p32 + 4 * C1;
-  m.pout = p32 + 5 * C1;
-  m.ord = p32 + 6 * C1;
-  p32 += 7 * C1;
+  m.kk = p32 + kSSlots;
+  m.inb = p32 + 2 * kSSlots;
+  m.outb = p32 + 3 * kSSlots;
+  m.cnt = p32 + 4 * kSSlots;
+  m.alive = p32 + 5 * kSSlots;
+  m.urg = p32 + 6 * kSSlots;
+  p32 += 7 * kSSlots;
+  m.dr = p32;
+  p32 += kSPairs;
+  m.pin = p32;
+  m.pout = p32 + 32;
+  m.cpd = p32 + 64;
+  m.csl = p32 + 96;
+  p32 += 128;
   m.nci = p32;
   m.ncp = p32 + nccap;
   m.newn = p32 + 2 * nccap;
-  m.scal = m.newn + kSPairs;
+  m.scal = m.newn + kSSlots;
   return m;
 }
 
-// Read-only graph view (global memory, read through the non-coherent path).
+// Read-only packed graph (global memory, read through the non-coherent path).
 struct SGraph {
-  const int32_t *__restrict__ in_off, *__restrict__ in_src, *__restrict__ out_off, *__restrict__ out_dst;
-  const int32_t *__restrict__ c32, *__restrict__ nu, *__restrict__ fav;
-  const int64_t *__restrict__ k, *__restrict__ need;
+  const int4 *__restrict__ node;    // [V] in_b, out_b, in_cnt | out_cnt << 16, k
+  const uint2 *__restrict__ inp;    // [E] per in-CSR slot: parent, (nu(parent) + 1) << 16 | c
+  const int32_t *__restrict__ out_dst;
+  const int32_t *__restrict__ fav;
+  const int64_t *__restrict__ need;
   const int32_t *__restrict__ need_order;
 };
 
-// DR of node c on device q (and, for m-SCT, its urgency: max over parents of
-// finish + c_e ignoring caches, placers.cpp:259-266).
+// DR of a node with in-CSR range [lo, lo + cnt) on device q (and, for
+// m-SCT, its urgency: max over parents of finish + c_e ignoring caches,
+// placers.cpp:259-266).
 template <bool kUrg>
-__device__ __forceinline__ int32_t small_dr(const SSm &m, const SGraph &G, int n, int lo, int hi, int q,
+__device__ __forceinline__ int32_t small_dr(const SSm &m, const SGraph &G, int n, int lo, int cnt, int q,
                                             int32_t &urg) {
   int32_t t = 0, u = 0;
   int x = lo;
+  const int hi = lo + cnt;
   for (; x + 1 < hi; x += 2) {
-    const int i0 = __ldg(G.in_src + x), i1 = __ldg(G.in_src + x + 1);
-    const int32_t c0 = __ldg(G.c32 + x), c1 = __ldg(G.c32 + x + 1);
-    const int u0 = __ldg(G.nu + i0), u1 = __ldg(G.nu + i1);
-    const uint64_t a0 = m.info[i0], a1 = m.info[i1];
-    const int32_t f0 = sm_fin(a0), f1 = sm_fin(a1);
-    int32_t t0, t1;
-    if (sm_dev(a0) == q) {
-      t0 = f0;
-    } else {
-      const unsigned z = u0 >= 0 ? m.nuc[u0 * n + q] : 0xffffu;
-      t0 = f0 + (z != 0xffffu ? static_cast<int32_t>(z) : c0);
-    }
-    if (sm_dev(a1) == q) {
-      t1 = f1;
-    } else {
-      const unsigned z = u1 >= 0 ? m.nuc[u1 * n + q] : 0xffffu;
-      t1 = f1 + (z != 0xffffu ? static_cast<int32_t>(z) : c1);
-    }
-    t = max(t, max(t0, t1));
-    if (kUrg) u = max(u, max(f0 + c0, f1 + c1));
+    const uint2 a = __ldg(G.inp + x), b = __ldg(G.inp + x + 1);
+    const uint64_t ia = m.info[a.x], ib = m.info[b.x];
+    const int32_t ca = static_cast<int32_t>(a.y & 0xffffu), cb = static_cast<int32_t>(b.y & 0xffffu);
+    const int ua = static_cast<int>(a.y >> 16) - 1, ub = static_cast<int>(b.y >> 16) - 1;
+    const int32_t fa = sm_fin(ia), fb = sm_fin(ib);
+    const unsigned za = ua >= 0 ? m.nuc[ua * n + q] : 0xffffu;
+    const unsigned zb = ub >= 0 ? m.nuc[ub * n + q] : 0xffffu;
+    const int32_t ta = sm_dev(ia) == q ? fa : fa + (za != 0xffffu ? static_cast<int32_t>(za) : ca);
+    const int32_t tb = sm_dev(ib) == q ? fb : fb + (zb != 0xffffu ? static_cast<int32_t>(zb) : cb);
+    t = max(t, max(ta, tb));
+    if (kUrg) u = max(u, max(fa + ca, fb + cb));
   }
   if (x < hi) {
-    const int i0 = __ldg(G.in_src + x);
-    const int32_t c0 = __ldg(G.c32 + x);
-    const int u0 = __ldg(G.nu + i0);
-    const uint64_t a0 = m.info[i0];
-    const int32_t f0 = sm_fin(a0);
-    int32_t t0;
-    if (sm_dev(a0) == q) {
-      t0 = f0;
-    } else {
-      const unsigned z = u0 >= 0 ? m.nuc[u0 * n + q] : 0xffffu;
-      t0 = f0 + (z != 0xffffu ? static_cast<int32_t>(z) : c0);
-    }
-    t = max(t, t0);
-    if (kUrg) u = max(u, f0 + c0);
+    const uint2 a = __ldg(G.inp + x);
+    const uint64_t ia = m.info[a.x];
+    const int32_t ca = static_cast<int32_t>(a.y & 0xffffu);
+    const int ua = static_cast<int>(a.y >> 16) - 1;
+    const int32_t fa = sm_fin(ia);
+    const unsigned za = ua >= 0 ? m.nuc[ua * n + q] : 0xffffu;
+    const int32_t ta = sm_dev(ia) == q ? fa : fa + (za != 0xffffu ? static_cast<int32_t>(za) : ca);
+    t = max(t, ta);
+    if (kUrg) u = max(u, fa + ca);
   }
   urg = u;
   return t;
-}
-
-// Fills slot fields for newly ready nodes in slots [R0, R0 + cnt) (node ids
-// already in m.node).
-__device__ __forceinline__ void small_fill_slots(const SSm &m, const SGraph &G, int R0, int cnt, int alive,
-                                                 int lane) {
-  for (int x = lane; x < cnt; x += 32) {
-    const int s = R0 + x, c = m.node[s];
-    m.rpos[c] = s;
-    m.need[s] = __ldg(G.need + c);
-    m.kk[s] = static_cast<int32_t>(__ldg(G.k + c));
-    m.inb[s] = __ldg(G.in_off + c);
-    m.ine[s] = __ldg(G.in_off + c + 1);
-    m.outb[s] = __ldg(G.out_off + c);
-    m.oute[s] = __ldg(G.out_off + c + 1);
-    m.alive[s] = alive;
-    m.urg[s] = 0;
-  }
 }
 
 // Per-problem loop state kept in registers (identical in every lane).
@@ -233,13 +208,27 @@ struct SRun {
   int V, n, d32, r32, s0, q0;
 };
 
+// One round's commits, lane r holding commit r.
+struct SCommit {
+  int nc;
+  int j, p, s;
+  int32_t t, fin;
+};
+
+// Node j committed earlier in this round (not yet applied to `info`): the
+// selection keeps the round's commits in the tail of m.newn (free until step
+// 4 refills it).
+__device__ __forceinline__ bool committed_now(const SSm &m, int nc, int j) {
+  bool done = false;
+  for (int r = 0; r < nc; ++r) done |= m.newn[kSSlots - 1 - r] == j;
+  return done;
+}
+
 // Steps 1-2 of a round with P pairs per lane (R * n <= 32 P): keys, then
-// exact commits / discards below the threshold. Commits land in m.cj/cp/
-// cfin/cs; returns their count (sin/sout: their total in/out-degree),
-// `progress` false when no live pair exists at all.
+// exact commits / discards below the threshold. Returns false when no live
+// pair exists at all.
 template <int P, bool kSct>
-__device__ __forceinline__ int small_select(const SSm &m, const SGraph &G, const DJob &jb, SRun &st, int nccap,
-                                            int lane, int &sin, int &sout, bool &progress) {
+__device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun &st, int lane, SCommit &cm) {
   const int n = st.n;
   const int np = st.R * n;
   uint64_t ck[P];
@@ -266,7 +255,7 @@ __device__ __forceinline__ int small_select(const SSm &m, const SGraph &G, const
           ck[u] = (static_cast<uint64_t>(static_cast<uint32_t>(key)) << 32) |
                   (static_cast<uint32_t>(node) << 5 | static_cast<uint32_t>(q));
           kq[u] = m.kk[s];
-          if (m.res[q] + m.need[s] <= m.cap[q]) fitm |= 1u << u;
+          if (m.need[s] <= m.slack[q]) fitm |= 1u << u;
         }
       }
       if (P > 1) {
@@ -280,9 +269,8 @@ __device__ __forceinline__ int small_select(const SSm &m, const SGraph &G, const
     }
   }
   uint32_t T = 0xffffffffu;
-  int nc = 0;
-  sin = sout = 0;
-  progress = false;
+  cm.nc = 0;
+  bool progress = false;
   while (true) {
     uint64_t best = ck[0];
 #pragma unroll
@@ -321,17 +309,20 @@ __device__ __forceinline__ int small_select(const SSm &m, const SGraph &G, const
         st.err_status = kInfeasible;
         st.err_code = E_FITS_NONE;
         st.err_node = j;
-        return nc;
+        return true;
       }
       ++st.discarded;
-      // smallest need among all unplaced nodes (the `remaining` multiset)
+      // smallest need among all unplaced nodes (the `remaining` multiset);
+      // column p has no commit this round, so its slack is current
       int64_t minrem = 0;
       if (lane == 0) {
-        while (sm_dev(m.info[__ldg(G.need_order + st.minptr)]) >= 0) ++st.minptr;
-        minrem = __ldg(G.need + __ldg(G.need_order + st.minptr));
+        int x;
+        while (x = __ldg(G.need_order + st.minptr), sm_dev(m.info[x]) >= 0 || committed_now(m, cm.nc, x))
+          ++st.minptr;
+        minrem = __ldg(G.need + x);
       }
       minrem = __shfl_sync(kFull, minrem, 0);
-      if (m.res[p] + minrem > m.cap[p]) {
+      if (minrem > m.slack[p]) {
         // exclusion: every unplaced (j2, p) dies (ascending j2 in the
         // reference; the first node left with no device is the smallest)
         ++st.excluded;
@@ -339,22 +330,22 @@ __device__ __forceinline__ int small_select(const SSm &m, const SGraph &G, const
         int first_dead = INT32_MAX;
         for (int s2 = lane; s2 < st.R; s2 += 32) {
           const int node2 = m.node[s2];
-          if (sm_dev(m.info[node2]) >= 0) continue;  // committed earlier this round
+          if (sm_dev(m.info[node2]) >= 0 || committed_now(m, cm.nc, node2)) continue;
           const int x2 = s2 * n + p;
           if (m.dr[x2] != kSDead) {
             m.dr[x2] = kSDead;
             if (--m.alive[s2] == 0) first_dead = min(first_dead, node2);
           }
         }
-        if (st.nexcl == n)
+        if (st.nexcl == n)  // no device left: the smallest unplaced node is the casualty
           for (int x = lane; x < st.V; x += 32)
-            if (sm_dev(m.info[x]) < 0) first_dead = min(first_dead, x);
+            if (sm_dev(m.info[x]) < 0 && !committed_now(m, cm.nc, x)) first_dead = min(first_dead, x);
         first_dead = static_cast<int>(__reduce_min_sync(kFull, static_cast<unsigned>(first_dead)));
         if (first_dead != INT32_MAX) {
           st.err_status = kInfeasible;
           st.err_code = E_FITS_NONE;
           st.err_node = first_dead;
-          return nc;
+          return true;
         }
         if (lane == 0) m.excl[p] = 1;
 #pragma unroll
@@ -364,22 +355,18 @@ __device__ __forceinline__ int small_select(const SSm &m, const SGraph &G, const
       __syncwarp();
       continue;
     }
-    // ---- commit (placers.cpp:221-233) ----
+    // ---- commit (placers.cpp:221-233): registers only; step 3 applies it ----
     const int32_t fin = t + mk;
-    if (lane == 0) {
-      m.cj[nc] = j;
-      m.cp[nc] = p;
-      m.cfin[nc] = fin;
-      m.cs[nc] = s;
-      m.F[p] = fin;
-      m.res[p] += m.need[s];
-      m.info[j] = (static_cast<uint64_t>(static_cast<uint32_t>(fin)) << 32) | static_cast<uint32_t>(p);
-      jb.device_of[j] = p;
-      jb.start[j] = t;
-      jb.cseq[st.placed] = j;
+    if (lane == cm.nc) {
+      cm.j = j;
+      cm.p = p;
+      cm.s = s;
+      cm.t = t;
+      cm.fin = fin;
     }
+    if (lane == 0) m.newn[kSSlots - 1 - cm.nc] = j;
+    ++cm.nc;
     ++st.placed;
-    ++nc;
     T = min(T, static_cast<uint32_t>(fin));
 #pragma unroll
     for (int u = 0; u < P; ++u)
@@ -387,7 +374,8 @@ __device__ __forceinline__ int small_select(const SSm &m, const SGraph &G, const
     if (kSct) {
       // awake reservations (placers.cpp:235-254): columns whose reservation
       // awaited j are lifted — their keys may drop, so they leave the round
-      // and bound it by their dev_free
+      // and bound it by their dev_free (the one before this round's commit
+      // on that column, if any: smaller, so only more conservative)
       const bool lifted = lane < n && lane != p && m.awf[lane] == j;
       const unsigned lm = __ballot_sync(kFull, lifted);
       uint32_t fq = 0xffffffffu;
@@ -403,20 +391,19 @@ __device__ __forceinline__ int small_select(const SSm &m, const SGraph &G, const
       if (lane == 0) {
         m.awf[p] = -1;
         const int h = __ldg(G.fav + j);
-        if (h >= 0 && sm_dev(m.info[h]) < 0) {
+        // h unplaced: not placed before this round and not committed in it
+        if (h >= 0 && sm_dev(m.info[h]) < 0 && !committed_now(m, cm.nc, h)) {
           m.awf[p] = h;
           m.awu[p] = fin + st.cmax;
           got = 1;
         }
       }
       st.awake += __shfl_sync(kFull, got, 0);
+      __syncwarp();
     }
-    sin += m.ine[s] - m.inb[s];
-    sout += m.oute[s] - m.outb[s];
-    __syncwarp();
-    if (nc == kSCommits || sin + jb.maxin > nccap || st.placed == st.V) break;
+    if (st.placed == st.V) break;
   }
-  return nc;
+  return progress;
 }
 
 // Brings [p, p + bytes) into this SM's L1 (one 16-byte load per 32-byte
@@ -434,9 +421,7 @@ __device__ __forceinline__ unsigned warm_l1(const void *p, size_t bytes, int tid
 }
 
 // One CTA per job: warp 0 schedules; warps 1..kSWarm-1 first pull the
-// graph arrays the scheduler reads into the SM's L1 (every one of them is
-// read through __ldg, and each scheduling round is a chain of dependent
-// loads, so L1 instead of L2 latency on each level), then exit.
+// packed graph the scheduler reads into the SM's L1, then exit.
 constexpr int kSWarm = 4;
 
 template <bool kSct, bool kProf>
@@ -452,10 +437,8 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
   if (threadIdx.x >= 32) {
     const int tid = threadIdx.x - 32, nt = 32 * (kSWarm - 1);
     const size_t V = static_cast<size_t>(g.V), E = static_cast<size_t>(g.E);
-    unsigned acc = warm_l1(g.in_off, 4 * (V + 1), tid, nt) ^ warm_l1(g.out_off, 4 * (V + 1), tid, nt);
-    acc ^= warm_l1(g.in_src, 4 * E, tid, nt) ^ warm_l1(pr.in_c32, 4 * E, tid, nt);
-    acc ^= warm_l1(pr.nu, 4 * V, tid, nt) ^ warm_l1(g.edst, 4 * E, tid, nt);
-    acc ^= warm_l1(g.k, 8 * V, tid, nt) ^ warm_l1(g.need, 8 * V, tid, nt);
+    unsigned acc = warm_l1(pr.node_pack, 16 * V, tid, nt) ^ warm_l1(pr.in_pack, 8 * E, tid, nt);
+    acc ^= warm_l1(g.edst, 4 * E, tid, nt) ^ warm_l1(g.need, 8 * V, tid, nt);
     acc ^= warm_l1(g.need_order, 4 * V, tid, nt);
     if (kSct && jb.fav) acc ^= warm_l1(jb.fav, 4 * V, tid, nt);
     asm volatile("" ::"r"(acc));  // keeps the loads
@@ -470,22 +453,18 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
   }
   const int V = g.V, n = jb.n;
   const int64_t cmax64 = *pr.cmax;
-  const int nccap = jb.maxin > 1024 ? jb.maxin : 1024;
+  const int nccap = n * (jb.maxin > 1 ? jb.maxin : 1);
   // dynamic eligibility (see the header); otherwise the general kernel runs it
-  if (*pr.cbad || g.flags[2] || *g.ksum < 0 || *pr.nu_count > jb.nucap || n > 32 || V >= (1 << 26) ||
+  if (*pr.cbad || g.flags[2] || *g.ksum < 0 || *pr.nu_count > jb.nucap || n > 32 || V >= 0xffff ||
       cmax64 >= 0xffff || jb.maxin >= 0xffff || *g.ksum + (int64_t(V) + 2) * cmax64 >= int64_t(INT32_MAX))
     return;
   const int32_t cmax = static_cast<int32_t>(cmax64);
   const SSm m = small_layout(smem, V, n, jb.nucap, nccap);
   SGraph G;
-  G.in_off = g.in_off;
-  G.in_src = g.in_src;
-  G.out_off = g.out_off;
+  G.node = pr.node_pack;
+  G.inp = pr.in_pack;
   G.out_dst = g.edst;
-  G.c32 = pr.in_c32;
-  G.nu = pr.nu;
   G.fav = jb.fav;
-  G.k = g.k;
   G.need = g.need;
   G.need_order = g.need_order;
 
@@ -495,38 +474,33 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     m.awf[lane] = -1;
     m.awu[lane] = 0;
     m.excl[lane] = 0;
-    m.res[lane] = 0;
-    m.cap[lane] = lane < n ? jb.cap[lane] : 0;
+    m.slack[lane] = lane < n ? jb.cap[lane] : 0;
     for (int x = lane; x < jb.nucap * n; x += 32) m.nuc[x] = 0xffffu;
   }
   int R = 0;
-  bool overflow = false;
   for (int base = 0; base < V; base += 32) {
     const int j = base + lane;
     bool src = false;
     if (j < V) {
-      const int indeg = __ldg(G.in_off + j + 1) - __ldg(G.in_off + j);
+      const int4 nd = __ldg(G.node + j);
+      const int indeg = nd.z & 0xffff;
       m.info[j] = 0xffffffffull;
-      m.pending[j] = indeg;
+      m.pending[j] = static_cast<uint16_t>(indeg);
       m.rpos[j] = -1;
       src = indeg == 0;
     }
     const unsigned b = __ballot_sync(kFull, src);
     if (src) {
       const int s = R + __popc(b & ((1u << lane) - 1u));
-      if (s < kSPairs) m.node[s] = j;
+      if (s < kSSlots) m.newn[s] = j;
     }
     R += __popc(b);
   }
   if (R * n > kSPairs) return;  // frontier too wide from the start
   __syncwarp();
-  small_fill_slots(m, G, 0, R, n, lane);
-  for (int x = lane; x < R * n; x += 32) m.dr[x] = 0;
-  __syncwarp();
 
-  // per-lane pair walk: x = lane + 32 u -> (slot, device)
   SRun st;
-  st.R = R;
+  st.R = 0;
   st.V = V;
   st.n = n;
   st.d32 = 32 / n;
@@ -554,15 +528,60 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     }                                 \
   } while (0)
 
-  while (st.placed < V) {
+  int nnew = R;  // the sources are the first "newly ready" nodes
+  bool overflow = false;
+  SCommit cm;
+  cm.nc = 0;
+  cm.j = cm.p = cm.s = 0;
+  cm.t = cm.fin = 0;
+  while (true) {
+    // ---- 6. new slots: static fields and data-ready rows -----------------------
+    {
+      const int R0 = st.R;
+      st.R += nnew;
+      if (st.R * n > kSPairs) {
+        overflow = true;
+        break;
+      }
+      const int alive0 = n - st.nexcl;
+      for (int idx = lane; idx < nnew * n; idx += 32) {
+        const int sl = idx / n, q = idx - sl * n, s = R0 + sl;
+        const int c = m.newn[sl];
+        const int4 nd = __ldg(G.node + c);
+        int32_t urg = 0;
+        int32_t d;
+        if (m.excl[q]) {
+          d = kSDead;
+          if (kSct) small_dr<true>(m, G, n, nd.x, nd.z & 0xffff, q, urg);
+        } else {
+          d = small_dr<kSct>(m, G, n, nd.x, nd.z & 0xffff, q, urg);
+        }
+        m.dr[s * n + q] = d;
+        if (q == 0) {
+          m.node[s] = c;
+          m.rpos[c] = static_cast<int16_t>(s);
+          m.kk[s] = nd.w;
+          m.inb[s] = nd.x;
+          m.outb[s] = nd.y;
+          m.cnt[s] = nd.z;
+          m.alive[s] = alive0;
+          m.urg[s] = urg;
+          m.need[s] = __ldg(G.need + c);
+        }
+      }
+      __syncwarp();
+    }
+    SMARK(P_ROWS);
+    if (st.placed == V) break;
+
     // ---- 1-2. keys and the round's exact commits ------------------------------
-    int sin = 0, sout = 0;
-    bool progress = false;
     const int np = st.R * n;
-    const int nc = np <= 32    ? small_select<1, kSct>(m, G, jb, st, nccap, lane, sin, sout, progress)
-                   : np <= 64  ? small_select<2, kSct>(m, G, jb, st, nccap, lane, sin, sout, progress)
-                   : np <= 128 ? small_select<4, kSct>(m, G, jb, st, nccap, lane, sin, sout, progress)
-                               : small_select<8, kSct>(m, G, jb, st, nccap, lane, sin, sout, progress);
+    const bool progress = np <= 32    ? small_select<1, kSct>(m, G, st, lane, cm)
+                          : np <= 64  ? small_select<2, kSct>(m, G, st, lane, cm)
+                          : np <= 128 ? small_select<4, kSct>(m, G, st, lane, cm)
+                          : np <= 256 ? small_select<8, kSct>(m, G, st, lane, cm)
+                                      : small_select<16, kSct>(m, G, st, lane, cm);
+    const int nc = cm.nc;
     if (kProf) {
       ++prof[P_STEPS];
       prof[P_COMMITS] += nc;
@@ -574,184 +593,159 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       st.err_code = E_NO_PAIR;
       break;
     }
+    nnew = 0;
     if (nc == 0) continue;
 
-    // ---- 3. batched update of the round's commits ------------------------------
-    // per-commit in/out-degree prefixes (a single commit needs none)
-    if (nc > 1) {
-      int din = 0, dout = 0;
-      if (lane < nc) {
-        const int s = m.cs[lane];
-        din = m.ine[s] - m.inb[s];
-        dout = m.oute[s] - m.outb[s];
-      }
-      int a = din, b = dout;
+    // ---- 3. apply the commits (one device each) -------------------------------
+    int cin = 0, cout = 0;
+    if (lane < nc) {
+      const int p = cm.p, s = cm.s, j = cm.j;
+      m.cpd[lane] = p;
+      m.csl[lane] = s;
+      m.F[p] = cm.fin;
+      m.slack[p] -= m.need[s];
+      m.info[j] = (static_cast<uint64_t>(static_cast<uint32_t>(cm.fin)) << 32) | static_cast<uint32_t>(p);
+      jb.device_of[j] = p;
+      jb.start[j] = cm.t;
+      jb.cseq[st.placed - nc + lane] = j;
+      const int c2 = m.cnt[s];
+      cin = c2 & 0xffff;
+      cout = c2 >> 16;
+    }
+    // per-commit first item (inclusive scans of the packed counts)
+    int incl = cin | (cout << 16);
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int a2 = __shfl_up_sync(kFull, a, o), b2 = __shfl_up_sync(kFull, b, o);
-        if (lane >= o) {
-          a += a2;
-          b += b2;
-        }
-      }
-      if (lane < nc) {
-        m.pin[lane] = a - din;
-        m.pout[lane] = b - dout;
-      }
-    } else if (lane == 0) {
-      m.pin[0] = m.pout[0] = 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int tot = __shfl_sync(kFull, incl, 31);
+    const int tin = tot & 0xffff, tout = tot >> 16;
+    if (lane < nc) {
+      m.pin[lane] = (incl & 0xffff) - cin;
+      m.pout[lane] = (incl >> 16) - cout;
     }
     __syncwarp();
-    // A: cache arrivals of remote non-uniform parents; B: readiness
+    SMARK(P_COMMIT);
+
+    // ---- 4. cache arrivals and readiness, one pass over the edges -------------
     int nnc = 0;
-    for (int base = 0; base < sin; base += 32) {
+    for (int base = 0; base < tin + tout; base += 32) {
       const int idx = base + lane;
-      bool fresh = false;
-      int i = 0, pr_ = 0;
-      if (idx < sin) {
+      bool fresh = false, ready = false;
+      int a = 0, b = 0;
+      if (idx < tin) {
         int r = 0;
         while (r + 1 < nc && m.pin[r + 1] <= idx) ++r;
-        const int x = m.inb[m.cs[r]] + idx - m.pin[r];
-        pr_ = m.cp[r];
-        i = __ldg(G.in_src + x);
-        const uint64_t a = m.info[i];
-        if (sm_dev(a) != pr_) {
-          const int u = __ldg(G.nu + i);
-          if (u >= 0) {
-            // one commit per device per round, so no two lanes share a slot
-            uint16_t *slot = m.nuc + u * n + pr_;
-            if (*slot == 0xffffu) {
-              *slot = static_cast<uint16_t>(__ldg(G.c32 + x));
-              fresh = true;
-            }
+        const int p = m.cpd[r], s = m.csl[r];
+        const uint2 e = __ldg(G.inp + m.inb[s] + idx - m.pin[r]);
+        const int u = static_cast<int>(e.y >> 16) - 1;
+        if (u >= 0 && sm_dev(m.info[e.x]) != p) {
+          // one commit per device per round, so no two lanes share a slot
+          uint16_t *slot = m.nuc + u * n + p;
+          if (*slot == 0xffffu) {
+            *slot = static_cast<uint16_t>(e.y & 0xffffu);
+            fresh = true;
+            a = static_cast<int>(e.x);
+            b = p;
           }
         }
-      }
-      const unsigned b = __ballot_sync(kFull, fresh);
-      if (fresh) {
-        const int at = nnc + __popc(b & ((1u << lane) - 1u));
-        m.nci[at] = i;
-        m.ncp[at] = pr_;
-      }
-      nnc += __popc(b);
-    }
-    int nnew = 0;
-    for (int base = 0; base < sout; base += 32) {
-      const int idx = base + lane;
-      bool fresh = false;
-      int child = 0;
-      if (idx < sout) {
+      } else if (idx < tin + tout) {
+        const int i2 = idx - tin;
         int r = 0;
-        while (r + 1 < nc && m.pout[r + 1] <= idx) ++r;
-        const int y = m.outb[m.cs[r]] + idx - m.pout[r];
-        child = __ldg(G.out_dst + y);
+        while (r + 1 < nc && m.pout[r + 1] <= i2) ++r;
+        const int s = m.csl[r];
+        const int child = __ldg(G.out_dst + m.outb[s] + i2 - m.pout[r]);
         // 16-bit counters decremented through their 32-bit word (a counter
         // is >= 1 when decremented, so no borrow crosses halves)
         unsigned *word = reinterpret_cast<unsigned *>(m.pending) + (child >> 1);
         const int sh = 16 * (child & 1);
-        fresh = ((atomicSub(word, 1u << sh) >> sh) & 0xffffu) == 1;
+        ready = ((atomicSub(word, 1u << sh) >> sh) & 0xffffu) == 1;
+        a = child;
       }
-      const unsigned b = __ballot_sync(kFull, fresh);
+      const unsigned bf = __ballot_sync(kFull, fresh), br = __ballot_sync(kFull, ready);
+      const unsigned lt = (1u << lane) - 1u;
       if (fresh) {
-        const int at = nnew + __popc(b & ((1u << lane) - 1u));
-        if (at < kSPairs) m.newn[at] = child;
+        const int at = nnc + __popc(bf & lt);
+        m.nci[at] = a;
+        m.ncp[at] = b;
       }
-      nnew += __popc(b);
+      if (ready) {
+        const int at = nnew + __popc(br & lt);
+        if (at < kSSlots) m.newn[at] = a;
+      }
+      nnc += __popc(bf);
+      nnew += __popc(br);
     }
-    SMARK(P_COMMIT);
-    // remove the committed slots, largest first (a moved-in last slot is never
-    // a committed one)
-    if (nc > 1) {
-      if (lane < nc) {
-        const int sr = m.cs[lane];
-        int rank = 0;
-        for (int r2 = 0; r2 < nc; ++r2) rank += m.cs[r2] > sr;
-        m.ord[rank] = sr;
+    SMARK(P_READY);
+
+    // ---- 5. remove the committed slots -----------------------------------------
+    // holes = committed slots below the new end R'; movers = live slots in
+    // [R', R); the i-th hole takes the i-th mover
+    {
+      const int Rn = st.R - nc;
+      const bool committed_lane = lane < nc;
+      const int cs = committed_lane ? cm.s : -1;
+      const bool hole = committed_lane && cs < Rn;
+      const unsigned tailmask = __reduce_or_sync(kFull, committed_lane && cs >= Rn ? 1u << (cs - Rn) : 0u);
+      const unsigned live_tail = ~tailmask & ((nc >= 32) ? 0xffffffffu : ((1u << nc) - 1u));
+      const unsigned hb = __ballot_sync(kFull, hole);
+      if (hole) {
+        const int rank = __popc(hb & ((1u << lane) - 1u));
+        const int src = Rn + static_cast<int>(__fns(live_tail, 0, rank + 1));
+        const int nd = m.node[src];
+        m.node[cs] = nd;
+        m.rpos[nd] = static_cast<int16_t>(cs);
+        m.need[cs] = m.need[src];
+        m.kk[cs] = m.kk[src];
+        m.inb[cs] = m.inb[src];
+        m.outb[cs] = m.outb[src];
+        m.cnt[cs] = m.cnt[src];
+        m.alive[cs] = m.alive[src];
+        m.urg[cs] = m.urg[src];
+        for (int q = 0; q < n; ++q) m.dr[cs * n + q] = m.dr[src * n + q];
       }
-    } else if (lane == 0) {
-      m.ord[0] = m.cs[0];
-    }
-    __syncwarp();
-    for (int r = 0; r < nc; ++r) {
-      const int sc = m.ord[r], last = st.R - 1;
-      if (sc != last) {
-        // lanes move one field each
-        if (lane < 10) {
-          if (lane == 0) {
-            const int nd = m.node[last];
-            m.node[sc] = nd;
-            m.rpos[nd] = sc;
-          } else if (lane == 1) {
-            m.need[sc] = m.need[last];
-          } else {
-            int32_t *f = lane == 2 ? m.kk : lane == 3 ? m.inb : lane == 4 ? m.ine : lane == 5 ? m.outb
-                       : lane == 6 ? m.oute : lane == 7 ? m.alive : m.urg;
-            if (lane < 9) f[sc] = f[last];
-          }
-        }
-        if (lane < n) m.dr[sc * n + lane] = m.dr[last * n + lane];
-      }
-      --st.R;
+      if (committed_lane) m.rpos[cm.j] = -1;
+      st.R = Rn;
       __syncwarp();
     }
     SMARK(P_REMOVE);
-    // new ready slots
-    const int R0 = st.R;
-    st.R += nnew;
-    if (st.R * n > kSPairs) {
+    if (nnew > kSSlots || (st.R + nnew) * n > kSPairs) {
       overflow = true;
       break;
     }
-    for (int x = lane; x < nnew; x += 32) m.node[R0 + x] = m.newn[x];
-    __syncwarp();
-    small_fill_slots(m, G, R0, nnew, n - st.nexcl, lane);
-    __syncwarp();
-    // D: data-ready rows of the new slots ...
-    for (int idx = lane; idx < nnew * n; idx += 32) {
-      const int sl = idx / n, q = idx - sl * n, s = R0 + sl;
-      int32_t urg = 0;
-      if (m.excl[q]) {
-        m.dr[s * n + q] = kSDead;
-        if (kSct) small_dr<true>(m, G, n, m.inb[s], m.ine[s], q, urg);
-      } else {
-        m.dr[s * n + q] = small_dr<kSct>(m, G, n, m.inb[s], m.ine[s], q, urg);
-      }
-      if (kSct && q == 0) m.urg[s] = urg;
-    }
-    SMARK(P_ROWS);
-    // ... and the consumers of each newly cached (producer, device) there
+
+    // ---- 7. consumers of each newly cached (producer, device) re-key there -----
     for (int e0 = 0; e0 < nnc; e0 += 32) {
       const int ne = min(32, nnc - e0);
-      int ob = 0, cnt = 0;
+      int ob = 0, oc = 0;
       if (lane < ne) {
-        const int i = m.nci[e0 + lane];
-        ob = __ldg(G.out_off + i);
-        cnt = __ldg(G.out_off + i + 1) - ob;
+        const int4 nd = __ldg(G.node + m.nci[e0 + lane]);
+        ob = nd.y;
+        oc = nd.z >> 16;
       }
-      int incl = cnt;
+      int inc2 = oc;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += v;
+        const int v = __shfl_up_sync(kFull, inc2, o);
+        if (lane >= o) inc2 += v;
       }
-      const int tot = __shfl_sync(kFull, incl, 31);
-      __syncwarp();
-      m.pin[lane] = incl - cnt;  // free after phase A
-      m.pout[lane] = ob;
-      __syncwarp();
-      for (int b0 = 0; b0 < tot; b0 += 32) {
+      const int tt = __shfl_sync(kFull, inc2, 31);
+      const int start = inc2 - oc;
+      for (int b0 = 0; b0 < tt; b0 += 32) {
         const int idx = b0 + lane;
-        if (idx < tot) {
-          int r = 0;
-          while (r + 1 < ne && m.pin[r + 1] <= idx) ++r;
+        // the producer r whose out-edges cover idx: last one with start <= idx
+        int r = 0;
+        for (int k = 1; k < ne; ++k) r = __shfl_sync(kFull, start, k) <= idx ? k : r;
+        const int obr = __shfl_sync(kFull, ob, r), str = __shfl_sync(kFull, start, r);
+        if (idx < tt) {
           const int p = m.ncp[e0 + r];
-          const int c = __ldg(G.out_dst + m.pout[r] + idx - m.pin[r]);
-          if (m.pending[c] == 0 && sm_dev(m.info[c]) < 0) {
-            const int s = m.rpos[c];
-            if (s >= 0 && m.dr[s * n + p] != kSDead) {
-              int32_t urg;
-              m.dr[s * n + p] = small_dr<false>(m, G, n, m.inb[s], m.ine[s], p, urg);
-            }
+          const int c = __ldg(G.out_dst + obr + idx - str);
+          const int s = m.rpos[c];
+          if (s >= 0 && m.dr[s * n + p] != kSDead) {
+            int32_t urg;
+            const int c2 = m.cnt[s];
+            m.dr[s * n + p] = small_dr<false>(m, G, n, m.inb[s], c2 & 0xffff, p, urg);
           }
         }
       }
@@ -792,13 +786,12 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
   }
 }
 
-// ---- prep: int32 comm times and the non-uniform producers of a (graph, comm)
+// ---- prep: the packed graph and the non-uniform producers of a (graph, comm)
 __global__ void k_prep_small(DGraph g, DPrep pr) {
   int bad = 0;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.E; x += gridDim.x * blockDim.x) {
     const int64_t c = pr.in_c[x];
-    if (c < 0 || c >= (int64_t(1) << 30)) bad = 1;
-    pr.in_c32[x] = static_cast<int32_t>(c);
+    if (c < 0 || c >= 0xffff) bad = 1;
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.V; i += gridDim.x * blockDim.x) {
     const int b = g.out_off[i], e = g.out_off[i + 1];
@@ -808,18 +801,35 @@ __global__ void k_prep_small(DGraph g, DPrep pr) {
       for (int y = b + 1; y < e && uni; ++y) uni = pr.in_c[g.inpos[y]] == c0;
     }
     pr.nu[i] = uni ? -1 : atomicAdd(pr.nu_count, 1);
+    const int ib = g.in_off[i], ie = g.in_off[i + 1];
+    const int64_t k = g.k[i];
+    pr.node_pack[i] = make_int4(ib, b, (ie - ib) | ((e - b) << 16), static_cast<int32_t>(k));
   }
   if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(pr.cbad, 1);
 }
 
+// in_pack needs every producer's nu index (the kernel above), so it is a
+// second pass
+__global__ void k_prep_small_in(DGraph g, DPrep pr) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.E; x += gridDim.x * blockDim.x) {
+    const int i = g.in_src[x];
+    const int64_t c = pr.in_c[x];
+    const unsigned nu1 = static_cast<unsigned>(pr.nu[i] + 1);
+    pr.in_pack[x] = make_uint2(static_cast<unsigned>(i), (nu1 << 16) | static_cast<unsigned>(c & 0xffff));
+  }
+}
+
 void launch_prep_small(const DGraph &g, const DPrep &pr, cudaStream_t s) {
   const int nb = ((g.V > g.E ? g.V : g.E) + 255) / 256;
-  if (nb > 0) k_prep_small<<<nb < 1184 ? nb : 1184, 256, 0, s>>>(g, pr);
+  if (nb > 0) {
+    k_prep_small<<<nb < 1184 ? nb : 1184, 256, 0, s>>>(g, pr);
+    k_prep_small_in<<<nb < 1184 ? nb : 1184, 256, 0, s>>>(g, pr);
+  }
 }
 
 size_t small_smem_bytes_host(int V, int n, int nucap, int nccap) { return small_smem_bytes(V, n, nucap, nccap); }
 
-// One CTA (one warp) per job; `order` lists the K2s jobs, m-ETF first.
+// One CTA per job; `order` lists the K2s jobs, m-ETF first.
 template <bool kSct, bool kProf>
 static void launch_sf(const DJob *jobs, const int32_t *order, int nj, const DGraph *graphs, const DPrep *preps,
                       size_t smem, cudaStream_t s) {
@@ -827,7 +837,7 @@ static void launch_sf(const DJob *jobs, const int32_t *order, int nj, const DGra
   cudaFuncSetAttribute(k_place_small<kSct, kProf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
   // the smallest shared-memory carveout that holds the job state: the rest
-  // of the unified 256 KB is L1 for the warmed graph arrays
+  // of the unified 256 KB is L1 for the warmed graph
   const int pct = static_cast<int>((smem * 100 + 228 * 1024 - 1) / (228 * 1024));
   cudaFuncSetAttribute(k_place_small<kSct, kProf>, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 1 ? 1 : pct);
   k_place_small<kSct, kProf><<<nj, 32 * kSWarm, smem, s>>>(jobs, order, nj, graphs, preps);
