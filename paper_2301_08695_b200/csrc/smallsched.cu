@@ -97,6 +97,7 @@ struct SSm {
   // per round
   int32_t *pin, *pout;  // [32] per commit: first in- / out-edge item
   int32_t *cpd, *csl;   // [32] per commit: device, slot
+  int32_t *ita, *itb;   // [32] per item of a 32-item chunk: CSR position, device
   int32_t *nci, *ncp;   // [nccap] newly cached (producer, device)
   int32_t *newn;        // [kSSlots] newly ready nodes
   int32_t *scal;        // [32] exec-order counters
@@ -108,7 +109,7 @@ __host__ __device__ inline size_t small_smem_bytes(int V, int n, int nucap, int 
   b += size_t(V) * 8 + 2 * ((size_t(V) * 2 + 3) & ~size_t(3)); // info, pending, rpos
   b += (size_t(nucap) * n * 2 + 7) & ~size_t(7);               // nuc
   b += size_t(kSSlots) * (7 * 4 + 8) + size_t(kSPairs) * 4;    // slots, dr
-  b += 4 * 32 * 4 + 2 * size_t(nccap) * 4 + size_t(kSSlots) * 4 + 32 * 4;
+  b += 6 * 32 * 4 + 2 * size_t(nccap) * 4 + size_t(kSSlots) * 4 + 32 * 4;
   return b + 64;
 }
 
@@ -144,7 +145,9 @@ __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, i
   m.pout = p32 + 32;
   m.cpd = p32 + 64;
   m.csl = p32 + 96;
-  p32 += 128;
+  m.ita = p32 + 128;
+  m.itb = p32 + 160;
+  p32 += 192;
   m.nci = p32;
   m.ncp = p32 + nccap;
   m.newn = p32 + 2 * nccap;
@@ -154,7 +157,7 @@ __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, i
 
 // Read-only packed graph (global memory, read through the non-coherent path).
 struct SGraph {
-  const int4 *__restrict__ node;    // [V] in_b, out_b, in_cnt | out_cnt << 16, k
+  const int4 *__restrict__ node;    // [2V] in_b, out_b, in_cnt | out_cnt << 16, k; need (int64), 0, 0
   const uint2 *__restrict__ inp;    // [E] per in-CSR slot: parent, (nu(parent) + 1) << 16 | c
   const int32_t *__restrict__ out_dst;
   const int32_t *__restrict__ fav;
@@ -437,8 +440,8 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
   if (threadIdx.x >= 32) {
     const int tid = threadIdx.x - 32, nt = 32 * (kSWarm - 1);
     const size_t V = static_cast<size_t>(g.V), E = static_cast<size_t>(g.E);
-    unsigned acc = warm_l1(pr.node_pack, 16 * V, tid, nt) ^ warm_l1(pr.in_pack, 8 * E, tid, nt);
-    acc ^= warm_l1(g.edst, 4 * E, tid, nt) ^ warm_l1(g.need, 8 * V, tid, nt);
+    unsigned acc = warm_l1(pr.node_pack, 32 * V, tid, nt) ^ warm_l1(pr.in_pack, 8 * E, tid, nt);
+    acc ^= warm_l1(g.edst, 4 * E, tid, nt);
     acc ^= warm_l1(g.need_order, 4 * V, tid, nt);
     if (kSct && jb.fav) acc ^= warm_l1(jb.fav, 4 * V, tid, nt);
     asm volatile("" ::"r"(acc));  // keeps the loads
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     const int j = base + lane;
     bool src = false;
     if (j < V) {
-      const int4 nd = __ldg(G.node + j);
+      const int4 nd = __ldg(G.node + 2 * j);
       const int indeg = nd.z & 0xffff;
       m.info[j] = 0xffffffffull;
       m.pending[j] = static_cast<uint16_t>(indeg);
@@ -544,10 +547,12 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
         break;
       }
       const int alive0 = n - st.nexcl;
+      int sl = st.s0, q = st.q0;  // item idx = lane + 32 k -> (slot sl, device q), no division
       for (int idx = lane; idx < nnew * n; idx += 32) {
-        const int sl = idx / n, q = idx - sl * n, s = R0 + sl;
+        const int s = R0 + sl;
         const int c = m.newn[sl];
-        const int4 nd = __ldg(G.node + c);
+        const int4 nd = __ldg(G.node + 2 * c);
+        const int4 nb = __ldg(G.node + 2 * c + 1);
         int32_t urg = 0;
         int32_t d;
         if (m.excl[q]) {
@@ -566,7 +571,13 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
           m.cnt[s] = nd.z;
           m.alive[s] = alive0;
           m.urg[s] = urg;
-          m.need[s] = __ldg(G.need + c);
+          m.need[s] = (static_cast<int64_t>(nb.y) << 32) | static_cast<uint32_t>(nb.x);
+        }
+        sl += st.d32;
+        q += st.r32;
+        if (q >= n) {
+          q -= n;
+          ++sl;
         }
       }
       __syncwarp();
@@ -597,11 +608,9 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     if (nc == 0) continue;
 
     // ---- 3. apply the commits (one device each) -------------------------------
-    int cin = 0, cout = 0;
+    int cin = 0, cout = 0, cib = 0, cob = 0;
     if (lane < nc) {
       const int p = cm.p, s = cm.s, j = cm.j;
-      m.cpd[lane] = p;
-      m.csl[lane] = s;
       m.F[p] = cm.fin;
       m.slack[p] -= m.need[s];
       m.info[j] = (static_cast<uint64_t>(static_cast<uint32_t>(cm.fin)) << 32) | static_cast<uint32_t>(p);
@@ -611,8 +620,10 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       const int c2 = m.cnt[s];
       cin = c2 & 0xffff;
       cout = c2 >> 16;
+      cib = m.inb[s];
+      cob = m.outb[s];
     }
-    // per-commit first item (inclusive scans of the packed counts)
+    // per-commit first item (inclusive scan of the packed counts)
     int incl = cin | (cout << 16);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -621,24 +632,27 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     }
     const int tot = __shfl_sync(kFull, incl, 31);
     const int tin = tot & 0xffff, tout = tot >> 16;
-    if (lane < nc) {
-      m.pin[lane] = (incl & 0xffff) - cin;
-      m.pout[lane] = (incl >> 16) - cout;
-    }
-    __syncwarp();
+    const int pin = (incl & 0xffff) - cin, pout = (incl >> 16) - cout;
     SMARK(P_COMMIT);
 
-    // ---- 4. cache arrivals and readiness, one pass over the edges -------------
+    // ---- 4a. cache arrivals: every in-edge of a committed node --------------------
+    // 32-item chunks; each commit lane writes its items' (CSR position,
+    // device) into the chunk table, then lane i takes item base + i
     int nnc = 0;
-    for (int base = 0; base < tin + tout; base += 32) {
-      const int idx = base + lane;
-      bool fresh = false, ready = false;
+    for (int base = 0; base < tin; base += 32) {
+      if (lane < nc) {
+        const int lo = max(pin, base), hi = min(pin + cin, base + 32);
+        for (int k = lo; k < hi; ++k) {
+          m.ita[k - base] = cib + k - pin;
+          m.itb[k - base] = cm.p;
+        }
+      }
+      __syncwarp();
+      bool fresh = false;
       int a = 0, b = 0;
-      if (idx < tin) {
-        int r = 0;
-        while (r + 1 < nc && m.pin[r + 1] <= idx) ++r;
-        const int p = m.cpd[r], s = m.csl[r];
-        const uint2 e = __ldg(G.inp + m.inb[s] + idx - m.pin[r]);
+      if (base + lane < tin) {
+        const int x = m.ita[lane], p = m.itb[lane];
+        const uint2 e = __ldg(G.inp + x);
         const int u = static_cast<int>(e.y >> 16) - 1;
         if (u >= 0 && sm_dev(m.info[e.x]) != p) {
           // one commit per device per round, so no two lanes share a slot
@@ -650,32 +664,40 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
             b = p;
           }
         }
-      } else if (idx < tin + tout) {
-        const int i2 = idx - tin;
-        int r = 0;
-        while (r + 1 < nc && m.pout[r + 1] <= i2) ++r;
-        const int s = m.csl[r];
-        const int child = __ldg(G.out_dst + m.outb[s] + i2 - m.pout[r]);
+      }
+      const unsigned bf = __ballot_sync(kFull, fresh);
+      if (fresh) {
+        const int at = nnc + __popc(bf & ((1u << lane) - 1u));
+        m.nci[at] = a;
+        m.ncp[at] = b;
+      }
+      nnc += __popc(bf);
+      __syncwarp();
+    }
+    // ---- 4b. readiness: every out-edge of a committed node ----------------------
+    for (int base = 0; base < tout; base += 32) {
+      if (lane < nc) {
+        const int lo = max(pout, base), hi = min(pout + cout, base + 32);
+        for (int k = lo; k < hi; ++k) m.ita[k - base] = cob + k - pout;
+      }
+      __syncwarp();
+      bool ready = false;
+      int child = 0;
+      if (base + lane < tout) {
+        child = __ldg(G.out_dst + m.ita[lane]);
         // 16-bit counters decremented through their 32-bit word (a counter
         // is >= 1 when decremented, so no borrow crosses halves)
         unsigned *word = reinterpret_cast<unsigned *>(m.pending) + (child >> 1);
         const int sh = 16 * (child & 1);
         ready = ((atomicSub(word, 1u << sh) >> sh) & 0xffffu) == 1;
-        a = child;
       }
-      const unsigned bf = __ballot_sync(kFull, fresh), br = __ballot_sync(kFull, ready);
-      const unsigned lt = (1u << lane) - 1u;
-      if (fresh) {
-        const int at = nnc + __popc(bf & lt);
-        m.nci[at] = a;
-        m.ncp[at] = b;
-      }
+      const unsigned br = __ballot_sync(kFull, ready);
       if (ready) {
-        const int at = nnew + __popc(br & lt);
-        if (at < kSSlots) m.newn[at] = a;
+        const int at = nnew + __popc(br & ((1u << lane) - 1u));
+        if (at < kSSlots) m.newn[at] = child;
       }
-      nnc += __popc(bf);
       nnew += __popc(br);
+      __syncwarp();
     }
     SMARK(P_READY);
 
@@ -718,11 +740,12 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     // ---- 7. consumers of each newly cached (producer, device) re-key there -----
     for (int e0 = 0; e0 < nnc; e0 += 32) {
       const int ne = min(32, nnc - e0);
-      int ob = 0, oc = 0;
+      int ob = 0, oc = 0, pp = 0;
       if (lane < ne) {
-        const int4 nd = __ldg(G.node + m.nci[e0 + lane]);
+        const int4 nd = __ldg(G.node + 2 * m.nci[e0 + lane]);
         ob = nd.y;
         oc = nd.z >> 16;
+        pp = m.ncp[e0 + lane];
       }
       int inc2 = oc;
 #pragma unroll
@@ -733,25 +756,26 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       const int tt = __shfl_sync(kFull, inc2, 31);
       const int start = inc2 - oc;
       for (int b0 = 0; b0 < tt; b0 += 32) {
-        const int idx = b0 + lane;
-        // the producer r whose out-edges cover idx: last one with start <= idx
-        int r = 0;
-        for (int k = 1; k < ne; ++k) r = __shfl_sync(kFull, start, k) <= idx ? k : r;
-        const int obr = __shfl_sync(kFull, ob, r), str = __shfl_sync(kFull, start, r);
-        if (idx < tt) {
-          const int p = m.ncp[e0 + r];
-          const int c = __ldg(G.out_dst + obr + idx - str);
+        if (lane < ne) {
+          const int lo = max(start, b0), hi = min(start + oc, b0 + 32);
+          for (int k = lo; k < hi; ++k) {
+            m.ita[k - b0] = ob + k - start;
+            m.itb[k - b0] = pp;
+          }
+        }
+        __syncwarp();
+        if (b0 + lane < tt) {
+          const int p = m.itb[lane];
+          const int c = __ldg(G.out_dst + m.ita[lane]);
           const int s = m.rpos[c];
           if (s >= 0 && m.dr[s * n + p] != kSDead) {
             int32_t urg;
-            const int c2 = m.cnt[s];
-            m.dr[s * n + p] = small_dr<false>(m, G, n, m.inb[s], c2 & 0xffff, p, urg);
+            m.dr[s * n + p] = small_dr<false>(m, G, n, m.inb[s], m.cnt[s] & 0xffff, p, urg);
           }
         }
+        __syncwarp();
       }
-      __syncwarp();
     }
-    __syncwarp();
     SMARK(P_CACHE);
   }
 #undef SMARK
@@ -803,7 +827,9 @@ __global__ void k_prep_small(DGraph g, DPrep pr) {
     pr.nu[i] = uni ? -1 : atomicAdd(pr.nu_count, 1);
     const int ib = g.in_off[i], ie = g.in_off[i + 1];
     const int64_t k = g.k[i];
-    pr.node_pack[i] = make_int4(ib, b, (ie - ib) | ((e - b) << 16), static_cast<int32_t>(k));
+    const int64_t need = g.need[i];
+    pr.node_pack[2 * i] = make_int4(ib, b, (ie - ib) | ((e - b) << 16), static_cast<int32_t>(k));
+    pr.node_pack[2 * i + 1] = make_int4(static_cast<int32_t>(need), static_cast<int32_t>(need >> 32), 0, 0);
   }
   if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(pr.cbad, 1);
 }
