@@ -67,7 +67,11 @@ namespace bx {
 
 constexpr int kSP = 16;                  // pairs per lane
 constexpr int kSPairs = 32 * kSP;        // R * n <= 512
-constexpr int kSSlots = kSPairs;         // ready slots (n = 1)
+constexpr int kSSlots = kSPairs;         // newly-ready list capacity
+constexpr int kKI = 8;                   // parents cached per ready slot (in_pack records)
+constexpr int kKO = 8;                   // children cached per ready slot
+// ready-slot capacity for n devices (R * n <= kSPairs)
+__host__ __device__ inline int small_slots(int n) { return kSPairs / (n > 0 ? n : 1); }
 constexpr int32_t kSDead = 0x7fffffff;   // DR of a discarded / excluded pair
 constexpr uint64_t kSNone = ~0ull;
 
@@ -90,10 +94,13 @@ struct SSm {
   int16_t *rpos;                  // [V] ready slot of a node, -1 none
   uint16_t *nuc;                  // [nucap * n] per non-uniform producer and device: comm time of the
                                   // edge that first brought its tensor there (arrival = finish + it), 0xffff absent
-  // ready slots
-  int32_t *node, *kk, *inb, *outb, *cnt, *alive, *urg;  // [kSSlots]; cnt = in_cnt | out_cnt << 16
-  int64_t *need;                                        // [kSSlots]
+  // ready slots (ns = small_slots(n))
+  int32_t *node, *kk, *inb, *outb, *cnt, *alive, *urg;  // [ns]; cnt = in_cnt | out_cnt << 16
+  int64_t *need;                                        // [ns]
+  uint2 *sip;                                           // [ns * kKI] the slot's first parents (in_pack records)
+  int32_t *sco;                                         // [ns * kKO] the slot's first children
   int32_t *dr;                                          // [kSPairs] DR[s * n + q]
+  int32_t *cjs;                                         // [32] the round's commits so far (lane 0)
   // per round
   int32_t *pin, *pout;  // [32] per commit: first in- / out-edge item
   int32_t *cpd, *csl;   // [32] per commit: device, slot
@@ -108,7 +115,8 @@ __host__ __device__ inline size_t small_smem_bytes(int V, int n, int nucap, int 
   b += 32 * 8 + 4 * 32 * 4;                                    // slack, F/awf/awu/excl
   b += size_t(V) * 8 + 2 * ((size_t(V) * 2 + 3) & ~size_t(3)); // info, pending, rpos
   b += (size_t(nucap) * n * 2 + 7) & ~size_t(7);               // nuc
-  b += size_t(kSSlots) * (7 * 4 + 8) + size_t(kSPairs) * 4;    // slots, dr
+  const size_t ns = static_cast<size_t>(small_slots(n));
+  b += ns * (7 * 4 + 8 + 8 * kKI + 4 * kKO) + size_t(kSPairs) * 4 + 32 * 4;  // slots, caches, dr, cjs
   b += 6 * 32 * 4 + 2 * size_t(nccap) * 4 + size_t(kSSlots) * 4 + 32 * 4;
   return b + 64;
 }
@@ -118,8 +126,10 @@ __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, i
   int64_t *p64 = reinterpret_cast<int64_t *>(base);
   m.slack = p64;
   m.info = reinterpret_cast<uint64_t *>(p64 + 32);
+  const int ns = small_slots(n);
   m.need = reinterpret_cast<int64_t *>(m.info + V);
-  int32_t *p32 = reinterpret_cast<int32_t *>(m.need + kSSlots);
+  m.sip = reinterpret_cast<uint2 *>(m.need + ns);
+  int32_t *p32 = reinterpret_cast<int32_t *>(m.sip + ns * kKI);
   m.F = p32;
   m.awf = p32 + 32;
   m.awu = p32 + 64;
@@ -132,15 +142,19 @@ __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, i
   m.nuc = reinterpret_cast<uint16_t *>(p32);
   p32 += (nucap * n + 1) / 2;
   m.node = p32;
-  m.kk = p32 + kSSlots;
-  m.inb = p32 + 2 * kSSlots;
-  m.outb = p32 + 3 * kSSlots;
-  m.cnt = p32 + 4 * kSSlots;
-  m.alive = p32 + 5 * kSSlots;
-  m.urg = p32 + 6 * kSSlots;
-  p32 += 7 * kSSlots;
+  m.kk = p32 + ns;
+  m.inb = p32 + 2 * ns;
+  m.outb = p32 + 3 * ns;
+  m.cnt = p32 + 4 * ns;
+  m.alive = p32 + 5 * ns;
+  m.urg = p32 + 6 * ns;
+  p32 += 7 * ns;
+  m.sco = p32;
+  p32 += ns * kKO;
   m.dr = p32;
   p32 += kSPairs;
+  m.cjs = p32;
+  p32 += 32;
   m.pin = p32;
   m.pout = p32 + 32;
   m.cpd = p32 + 64;
@@ -165,38 +179,37 @@ struct SGraph {
   const int32_t *__restrict__ need_order;
 };
 
-// DR of a node with in-CSR range [lo, lo + cnt) on device q (and, for
-// m-SCT, its urgency: max over parents of finish + c_e ignoring caches,
-// placers.cpp:259-266).
+// Parent k of ready slot s (its in_pack record): the slot cache for the
+// first kKI, the packed graph beyond.
+__device__ __forceinline__ uint2 slot_parent(const SSm &m, const SGraph &G, int s, int k) {
+  return k < kKI ? m.sip[s * kKI + k] : __ldg(G.inp + m.inb[s] + k);
+}
+
+__device__ __forceinline__ int slot_child(const SSm &m, const SGraph &G, int s, int k) {
+  return k < kKO ? m.sco[s * kKO + k] : __ldg(G.out_dst + m.outb[s] + k);
+}
+
+// One parent's term of DR on device q (placers.cpp:55-61), and its
+// urgency term.
+__device__ __forceinline__ int32_t parent_term(const SSm &m, int n, uint2 a, int q, int32_t &urg_term) {
+  const uint64_t ia = m.info[a.x];
+  const int32_t ca = static_cast<int32_t>(a.y & 0xffffu);
+  const int ua = static_cast<int>(a.y >> 16) - 1;
+  const int32_t fa = sm_fin(ia);
+  const unsigned za = ua >= 0 ? m.nuc[ua * n + q] : 0xffffu;
+  urg_term = fa + ca;
+  return sm_dev(ia) == q ? fa : fa + (za != 0xffffu ? static_cast<int32_t>(za) : ca);
+}
+
+// DR of ready slot s on device q from its cached parents (and urgency).
 template <bool kUrg>
-__device__ __forceinline__ int32_t small_dr(const SSm &m, const SGraph &G, int n, int lo, int cnt, int q,
-                                            int32_t &urg) {
+__device__ __forceinline__ int32_t slot_dr(const SSm &m, const SGraph &G, int n, int s, int indeg, int q,
+                                           int32_t &urg) {
   int32_t t = 0, u = 0;
-  int x = lo;
-  const int hi = lo + cnt;
-  for (; x + 1 < hi; x += 2) {
-    const uint2 a = __ldg(G.inp + x), b = __ldg(G.inp + x + 1);
-    const uint64_t ia = m.info[a.x], ib = m.info[b.x];
-    const int32_t ca = static_cast<int32_t>(a.y & 0xffffu), cb = static_cast<int32_t>(b.y & 0xffffu);
-    const int ua = static_cast<int>(a.y >> 16) - 1, ub = static_cast<int>(b.y >> 16) - 1;
-    const int32_t fa = sm_fin(ia), fb = sm_fin(ib);
-    const unsigned za = ua >= 0 ? m.nuc[ua * n + q] : 0xffffu;
-    const unsigned zb = ub >= 0 ? m.nuc[ub * n + q] : 0xffffu;
-    const int32_t ta = sm_dev(ia) == q ? fa : fa + (za != 0xffffu ? static_cast<int32_t>(za) : ca);
-    const int32_t tb = sm_dev(ib) == q ? fb : fb + (zb != 0xffffu ? static_cast<int32_t>(zb) : cb);
-    t = max(t, max(ta, tb));
-    if (kUrg) u = max(u, max(fa + ca, fb + cb));
-  }
-  if (x < hi) {
-    const uint2 a = __ldg(G.inp + x);
-    const uint64_t ia = m.info[a.x];
-    const int32_t ca = static_cast<int32_t>(a.y & 0xffffu);
-    const int ua = static_cast<int>(a.y >> 16) - 1;
-    const int32_t fa = sm_fin(ia);
-    const unsigned za = ua >= 0 ? m.nuc[ua * n + q] : 0xffffu;
-    const int32_t ta = sm_dev(ia) == q ? fa : fa + (za != 0xffffu ? static_cast<int32_t>(za) : ca);
-    t = max(t, ta);
-    if (kUrg) u = max(u, fa + ca);
+  for (int k = 0; k < indeg; ++k) {
+    int32_t ut;
+    t = max(t, parent_term(m, n, slot_parent(m, G, s, k), q, ut));
+    if (kUrg) u = max(u, ut);
   }
   urg = u;
   return t;
@@ -218,12 +231,11 @@ struct SCommit {
   int32_t t, fin;
 };
 
-// Node j committed earlier in this round (not yet applied to `info`): the
-// selection keeps the round's commits in the tail of m.newn (free until step
-// 4 refills it).
+// Node j committed earlier in this round (not yet applied to `info`; the
+// selection lists the round's commits in m.cjs).
 __device__ __forceinline__ bool committed_now(const SSm &m, int nc, int j) {
   bool done = false;
-  for (int r = 0; r < nc; ++r) done |= m.newn[kSSlots - 1 - r] == j;
+  for (int r = 0; r < nc; ++r) done |= m.cjs[r] == j;
   return done;
 }
 
@@ -367,7 +379,7 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
       cm.t = t;
       cm.fin = fin;
     }
-    if (lane == 0) m.newn[kSSlots - 1 - cm.nc] = j;
+    if (lane == 0) m.cjs[cm.nc] = j;
     ++cm.nc;
     ++st.placed;
     T = min(T, static_cast<uint32_t>(fin));
@@ -538,7 +550,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
   cm.j = cm.p = cm.s = 0;
   cm.t = cm.fin = 0;
   while (true) {
-    // ---- 6. new slots: static fields and data-ready rows -----------------------
+    // ---- 6. new slots: statics, parent / child caches, data-ready rows ---------
     {
       const int R0 = st.R;
       st.R += nnew;
@@ -547,32 +559,57 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
         break;
       }
       const int alive0 = n - st.nexcl;
-      int sl = st.s0, q = st.q0;  // item idx = lane + 32 k -> (slot sl, device q), no division
-      for (int idx = lane; idx < nnew * n; idx += 32) {
+      // 6a. one lane per new slot: the packed node record, then its first
+      // kKI parents and kKO children (independent loads, issued together);
+      // the children's records are prefetched for when they become ready
+      for (int sl = lane; sl < nnew; sl += 32) {
         const int s = R0 + sl;
         const int c = m.newn[sl];
         const int4 nd = __ldg(G.node + 2 * c);
         const int4 nb = __ldg(G.node + 2 * c + 1);
+        const int ci = nd.z & 0xffff, co = nd.z >> 16;
+        uint2 pa[kKI];
+        int ch[kKO];
+#pragma unroll
+        for (int k = 0; k < kKI; ++k)
+          if (k < ci) pa[k] = __ldg(G.inp + nd.x + k);
+#pragma unroll
+        for (int k = 0; k < kKO; ++k)
+          if (k < co) ch[k] = __ldg(G.out_dst + nd.y + k);
+        m.node[s] = c;
+        m.rpos[c] = static_cast<int16_t>(s);
+        m.kk[s] = nd.w;
+        m.inb[s] = nd.x;
+        m.outb[s] = nd.y;
+        m.cnt[s] = nd.z;
+        m.alive[s] = alive0;
+        m.need[s] = (static_cast<int64_t>(nb.y) << 32) | static_cast<uint32_t>(nb.x);
+#pragma unroll
+        for (int k = 0; k < kKI; ++k)
+          if (k < ci) m.sip[s * kKI + k] = pa[k];
+#pragma unroll
+        for (int k = 0; k < kKO; ++k)
+          if (k < co) {
+            m.sco[s * kKO + k] = ch[k];
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(G.node + 2 * ch[k]));
+          }
+      }
+      __syncwarp();
+      // 6b. data-ready rows: item idx = lane + 32 k -> (slot sl, device q)
+      int sl = st.s0, q = st.q0;
+      for (int idx = lane; idx < nnew * n; idx += 32) {
+        const int s = R0 + sl;
+        const int ci = m.cnt[s] & 0xffff;
         int32_t urg = 0;
         int32_t d;
         if (m.excl[q]) {
           d = kSDead;
-          if (kSct) small_dr<true>(m, G, n, nd.x, nd.z & 0xffff, q, urg);
+          if (kSct) slot_dr<true>(m, G, n, s, ci, q, urg);
         } else {
-          d = small_dr<kSct>(m, G, n, nd.x, nd.z & 0xffff, q, urg);
+          d = slot_dr<kSct>(m, G, n, s, ci, q, urg);
         }
         m.dr[s * n + q] = d;
-        if (q == 0) {
-          m.node[s] = c;
-          m.rpos[c] = static_cast<int16_t>(s);
-          m.kk[s] = nd.w;
-          m.inb[s] = nd.x;
-          m.outb[s] = nd.y;
-          m.cnt[s] = nd.z;
-          m.alive[s] = alive0;
-          m.urg[s] = urg;
-          m.need[s] = (static_cast<int64_t>(nb.y) << 32) | static_cast<uint32_t>(nb.x);
-        }
+        if (q == 0) m.urg[s] = urg;
         sl += st.d32;
         q += st.r32;
         if (q >= n) {
@@ -608,7 +645,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     if (nc == 0) continue;
 
     // ---- 3. apply the commits (one device each) -------------------------------
-    int cin = 0, cout = 0, cib = 0, cob = 0;
+    int cin = 0, cout = 0;
     if (lane < nc) {
       const int p = cm.p, s = cm.s, j = cm.j;
       m.F[p] = cm.fin;
@@ -620,8 +657,6 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       const int c2 = m.cnt[s];
       cin = c2 & 0xffff;
       cout = c2 >> 16;
-      cib = m.inb[s];
-      cob = m.outb[s];
     }
     // per-commit first item (inclusive scan of the packed counts)
     int incl = cin | (cout << 16);
@@ -636,14 +671,14 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     SMARK(P_COMMIT);
 
     // ---- 4a. cache arrivals: every in-edge of a committed node --------------------
-    // 32-item chunks; each commit lane writes its items' (CSR position,
+    // 32-item chunks; each commit lane writes its items' (slot << 16 | k,
     // device) into the chunk table, then lane i takes item base + i
     int nnc = 0;
     for (int base = 0; base < tin; base += 32) {
       if (lane < nc) {
         const int lo = max(pin, base), hi = min(pin + cin, base + 32);
         for (int k = lo; k < hi; ++k) {
-          m.ita[k - base] = cib + k - pin;
+          m.ita[k - base] = cm.s << 16 | (k - pin);
           m.itb[k - base] = cm.p;
         }
       }
@@ -651,8 +686,8 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       bool fresh = false;
       int a = 0, b = 0;
       if (base + lane < tin) {
-        const int x = m.ita[lane], p = m.itb[lane];
-        const uint2 e = __ldg(G.inp + x);
+        const int it = m.ita[lane], p = m.itb[lane];
+        const uint2 e = slot_parent(m, G, it >> 16, it & 0xffff);
         const int u = static_cast<int>(e.y >> 16) - 1;
         if (u >= 0 && sm_dev(m.info[e.x]) != p) {
           // one commit per device per round, so no two lanes share a slot
@@ -678,13 +713,14 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     for (int base = 0; base < tout; base += 32) {
       if (lane < nc) {
         const int lo = max(pout, base), hi = min(pout + cout, base + 32);
-        for (int k = lo; k < hi; ++k) m.ita[k - base] = cob + k - pout;
+        for (int k = lo; k < hi; ++k) m.ita[k - base] = cm.s << 16 | (k - pout);
       }
       __syncwarp();
       bool ready = false;
       int child = 0;
       if (base + lane < tout) {
-        child = __ldg(G.out_dst + m.ita[lane]);
+        const int it = m.ita[lane];
+        child = slot_child(m, G, it >> 16, it & 0xffff);
         // 16-bit counters decremented through their 32-bit word (a counter
         // is >= 1 when decremented, so no borrow crosses halves)
         unsigned *word = reinterpret_cast<unsigned *>(m.pending) + (child >> 1);
@@ -712,9 +748,12 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       const unsigned tailmask = __reduce_or_sync(kFull, committed_lane && cs >= Rn ? 1u << (cs - Rn) : 0u);
       const unsigned live_tail = ~tailmask & ((nc >= 32) ? 0xffffffffu : ((1u << nc) - 1u));
       const unsigned hb = __ballot_sync(kFull, hole);
+      const int nholes = __popc(hb);
       if (hole) {
         const int rank = __popc(hb & ((1u << lane) - 1u));
         const int src = Rn + static_cast<int>(__fns(live_tail, 0, rank + 1));
+        m.pin[rank] = cs;  // hole / mover pairs for the cache copies below
+        m.pout[rank] = src;
         const int nd = m.node[src];
         m.node[cs] = nd;
         m.rpos[nd] = static_cast<int16_t>(cs);
@@ -730,6 +769,14 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       if (committed_lane) m.rpos[cm.j] = -1;
       st.R = Rn;
       __syncwarp();
+      // the movers' parent / child caches, kKI + kKO words per pair of slots
+      for (int it = lane; it < nholes * (kKI + kKO); it += 32) {
+        const int h = it / (kKI + kKO), k = it - h * (kKI + kKO);
+        const int dst = m.pin[h], src = m.pout[h];
+        if (k < kKI) m.sip[dst * kKI + k] = m.sip[src * kKI + k];
+        else m.sco[dst * kKO + k - kKI] = m.sco[src * kKO + k - kKI];
+      }
+      __syncwarp();
     }
     SMARK(P_REMOVE);
     if (nnew > kSSlots || (st.R + nnew) * n > kSPairs) {
@@ -737,44 +784,25 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       break;
     }
 
-    // ---- 7. consumers of each newly cached (producer, device) re-key there -----
-    for (int e0 = 0; e0 < nnc; e0 += 32) {
-      const int ne = min(32, nnc - e0);
-      int ob = 0, oc = 0, pp = 0;
-      if (lane < ne) {
-        const int4 nd = __ldg(G.node + 2 * m.nci[e0 + lane]);
-        ob = nd.y;
-        oc = nd.z >> 16;
-        pp = m.ncp[e0 + lane];
-      }
-      int inc2 = oc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(kFull, inc2, o);
-        if (lane >= o) inc2 += v;
-      }
-      const int tt = __shfl_sync(kFull, inc2, 31);
-      const int start = inc2 - oc;
-      for (int b0 = 0; b0 < tt; b0 += 32) {
-        if (lane < ne) {
-          const int lo = max(start, b0), hi = min(start + oc, b0 + 32);
-          for (int k = lo; k < hi; ++k) {
-            m.ita[k - b0] = ob + k - start;
-            m.itb[k - b0] = pp;
+    // ---- 7. ready consumers of each newly cached (producer, device) re-key ----
+    // one lane per ready slot scans its parents against the round's new
+    // (producer, device) arrivals (all in shared memory)
+    if (nnc > 0) {
+      for (int s = lane; s < st.R; s += 32) {
+        const int ci = m.cnt[s] & 0xffff;
+        for (int k = 0; k < ci; ++k) {
+          const int par = static_cast<int>(slot_parent(m, G, s, k).x);
+          for (int e = 0; e < nnc; ++e) {
+            if (m.nci[e] != par) continue;
+            const int p = m.ncp[e];
+            if (m.dr[s * n + p] != kSDead) {
+              int32_t urg;
+              m.dr[s * n + p] = slot_dr<false>(m, G, n, s, ci, p, urg);
+            }
           }
         }
-        __syncwarp();
-        if (b0 + lane < tt) {
-          const int p = m.itb[lane];
-          const int c = __ldg(G.out_dst + m.ita[lane]);
-          const int s = m.rpos[c];
-          if (s >= 0 && m.dr[s * n + p] != kSDead) {
-            int32_t urg;
-            m.dr[s * n + p] = small_dr<false>(m, G, n, m.inb[s], m.cnt[s] & 0xffff, p, urg);
-          }
-        }
-        __syncwarp();
       }
+      __syncwarp();
     }
     SMARK(P_CACHE);
   }
