@@ -107,6 +107,9 @@ typedef struct {
 const char *bx_version(void);
 /* Text of the last CUDA launch failure seen by this thread ("" if none). */
 const char *bx_last_error(void);
+/* Full reference error text of this thread's last bx_place call (msg[256]
+ * holds a prefix; a CycleError lists every residue group id). */
+const char *bx_last_message(void);
 /* Number of CUDA devices visible (0 on a CPU-only host). */
 int bx_device_count(void);
 
@@ -218,6 +221,9 @@ int bx_plan_download(bx_plan *plan, void *stream, bx_placement *out);
  * returns a zero-copy view of job `job` inside that mirror (valid until the
  * next download or destroy). */
 int bx_plan_result_view(bx_plan *plan, int32_t job, bx_placement *view);
+/* Full error text of a job after bx_plan_download (msg[256] holds a prefix):
+ * copies up to buflen-1 bytes + NUL, returns the full length (-1: no result). */
+int64_t bx_plan_message(const bx_plan *plan, int32_t job, char *buf, int64_t buflen);
 
 /* Number of kernel launches the last bx_plan_place issued. */
 int bx_plan_launch_count(const bx_plan *plan);

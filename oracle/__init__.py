@@ -27,6 +27,8 @@ import subprocess
 
 import numpy as np
 
+_ERRLEN = 1 << 20  # error-text buffers: a CycleError lists every residue group id
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libdagsched_ref.so")
 RESTATE_SO = os.path.join(HERE, "_build", "librestate.so")
@@ -202,11 +204,11 @@ class Ref:
     def simulate_trace_csv(cls, rg, caps, cm, mem_mode, device_of, exec_order, exec_off):
         """simulate(record_trace) + trace_to_csv -> (csv text, event count)."""
         caps = _a(caps, np.int64)
-        err = C.create_string_buffer(4096)
+        err = C.create_string_buffer(_ERRLEN)
         ev = C.c_int64()
         args = (_a(device_of, np.int32), _a(exec_order, np.int32), _a(exec_off, np.int32))
         rc, text = cls._text(lambda b, bl, nd: cls.lib().ref_simulate_trace_csv(
-            rg.h, len(caps), caps, cm[0], cm[1], cm[2], mem_mode, *args, b, bl, nd, C.byref(ev), err, 4096))
+            rg.h, len(caps), caps, cm[0], cm[1], cm[2], mem_mode, *args, b, bl, nd, C.byref(ev), err, _ERRLEN))
         if rc:
             raise OracleError(rc, err.value.decode())
         return text, ev.value
@@ -215,9 +217,9 @@ class Ref:
     def graph_json_roundtrip(cls, text: str) -> str:
         """parse_graph(text) -> graph_to_json."""
         raw = text.encode("utf-8")
-        err = C.create_string_buffer(4096)
+        err = C.create_string_buffer(_ERRLEN)
         rc, out = cls._text(lambda b, bl, nd: cls.lib().ref_graph_json_roundtrip(raw, len(raw), b, bl, nd, err,
-                                                                                 4096))
+                                                                                 _ERRLEN))
         if rc:
             raise OracleError(rc, err.value.decode())
         return out
@@ -230,10 +232,10 @@ class Ref:
     def comm_model_roundtrip(cls, text: str):
         """parse_comm_model(text) -> ((ic, pb, mode), save_comm_model text)."""
         raw = text.encode("utf-8")
-        err = C.create_string_buffer(4096)
+        err = C.create_string_buffer(_ERRLEN)
         ic, pb, md = C.c_double(), C.c_double(), C.c_int32()
         rc, out = cls._text(lambda b, bl, nd: cls.lib().ref_comm_model_roundtrip(
-            raw, len(raw), C.byref(ic), C.byref(pb), C.byref(md), b, bl, nd, err, 4096))
+            raw, len(raw), C.byref(ic), C.byref(pb), C.byref(md), b, bl, nd, err, _ERRLEN))
         if rc:
             raise OracleError(rc, err.value.decode())
         return (ic.value, pb.value, md.value), out
@@ -253,8 +255,8 @@ class Ref:
         algo = C.create_string_buffer(256)
         dev, st = np.zeros(max(V, 1), np.int32), np.zeros(max(V, 1), np.int64)
         eo, off = np.zeros(max(V, 1), np.int32), np.zeros(n + 1, np.int32)
-        err = C.create_string_buffer(4096)
-        rc = cls.lib().ref_placement_from_json(rg.h, raw, len(raw), n, algo, 256, dev, st, eo, off, err, 4096)
+        err = C.create_string_buffer(_ERRLEN)
+        rc = cls.lib().ref_placement_from_json(rg.h, raw, len(raw), n, algo, 256, dev, st, eo, off, err, _ERRLEN)
         if rc:
             raise OracleError(rc, err.value.decode())
         return algo.value.decode(), Placement(dev[:V], st[:V], eo[:V], off)
@@ -301,13 +303,13 @@ class Ref:
         n = len(g["id"])
         e = len(g["src"])
         h = C.c_void_p()
-        err = C.create_string_buffer(4096)
+        err = C.create_string_buffer(_ERRLEN)
         rc = L.ref_graph_new(n, _a(g["id"], np.int64), _a(g["k"], np.int64),
                              _a(g["temp"], np.int64), _a(g["perm"], np.int64),
                              _a(g["out"], np.int64), _a(g["coloc"], np.int32),
                              _a(g["has_pair"], np.uint8), _a(g["pair"], np.int64), e,
                              _a(g["src"], np.int64), _a(g["dst"], np.int64),
-                             _a(g["bytes"], np.int64), pipeline, C.byref(h), err, 4096)
+                             _a(g["bytes"], np.int64), pipeline, C.byref(h), err, _ERRLEN)
         if rc:
             raise OracleError(rc, err.value.decode())
         return cls.Graph(h)
@@ -316,8 +318,8 @@ class Ref:
     def topo_order(cls, rg):
         V = rg.sizes()[2]
         order = np.zeros(max(V, 1), np.int32)
-        err = C.create_string_buffer(4096)
-        rc = cls.lib().ref_meta_topo_order(rg.h, order, err, 4096)
+        err = C.create_string_buffer(_ERRLEN)
+        rc = cls.lib().ref_meta_topo_order(rg.h, order, err, _ERRLEN)
         if rc:
             raise OracleError(rc, err.value.decode())
         return order[:V]
@@ -351,13 +353,13 @@ class Ref:
         off = np.zeros(n + 1, np.int32)
         stats = np.zeros(3, np.int64)
         wall = C.c_int64()
-        err = C.create_string_buffer(4096)
+        err = C.create_string_buffer(_ERRLEN)
         favp = None
         if fav is not None:
             favp = _a(fav, np.int32)
         rc = cls.lib().ref_place(rg.h, algo, n, caps, cm[0], cm[1], cm[2],
                                  favp.ctypes.data if favp is not None else None, dev, st, eo,
-                                 off, stats, C.byref(wall), err, 4096)
+                                 off, stats, C.byref(wall), err, _ERRLEN)
         if rc:
             raise OracleError(rc, err.value.decode())
         return Placement(dev[:V], st[:V], eo[:V], off, stats, wall.value)
@@ -366,11 +368,11 @@ class Ref:
     def place_timed(cls, rg, algo, caps, cm, reps, fav=None):
         caps = _a(caps, np.int64)
         ns = np.zeros(reps, np.int64)
-        err = C.create_string_buffer(4096)
+        err = C.create_string_buffer(_ERRLEN)
         favp = _opt(fav, np.int32)
         rc = cls.lib().ref_place_timed(rg.h, algo, len(caps), caps, cm[0], cm[1], cm[2],
                                        favp.ctypes.data if favp is not None else None, reps, ns,
-                                       err, 4096)
+                                       err, _ERRLEN)
         if rc:
             raise OracleError(rc, err.value.decode())
         return ns
@@ -410,11 +412,11 @@ class Ref:
         dev3n = np.zeros(3 * n, np.int64)
         x4 = np.zeros(4, np.int64)
         wall = C.c_int64()
-        err = C.create_string_buffer(4096)
+        err = C.create_string_buffer(_ERRLEN)
         rc = cls.lib().ref_simulate(rg.h, n, caps, cm[0], cm[1], cm[2], mem_mode,
                                     _a(device_of, np.int32), _a(exec_order, np.int32),
                                     _a(exec_off, np.int32), C.byref(mk), st, dev3n, x4,
-                                    C.byref(wall), err, 4096)
+                                    C.byref(wall), err, _ERRLEN)
         if rc:
             raise OracleError(rc, err.value.decode())
         return SimResult(mk.value, st[:V], dev3n, x4, wall.value)
@@ -517,11 +519,11 @@ class Restate:
         eo = np.zeros(max(V, 1), np.int32)
         off = np.zeros(n + 1, np.int32)
         stats = np.zeros(3, np.int64)
-        err = C.create_string_buffer(4096)
+        err = C.create_string_buffer(_ERRLEN)
         favp = _opt(fav, np.int32)
         rc = cls.lib().rs_place(C.byref(g), algo, n, caps, cm[0], cm[1], cm[2],
                                 favp.ctypes.data if favp is not None else None, dev, st, eo, off,
-                                stats, err, 4096)
+                                stats, err, _ERRLEN)
         if rc:
             raise OracleError(rc, err.value.decode())
         return Placement(dev[:V], st[:V], eo[:V], off, stats)
@@ -536,10 +538,10 @@ class Restate:
         st = np.zeros(max(V, 1), np.int64)
         dev3n = np.zeros(3 * n, np.int64)
         x4 = np.zeros(4, np.int64)
-        err = C.create_string_buffer(4096)
+        err = C.create_string_buffer(_ERRLEN)
         rc = cls.lib().rs_simulate(C.byref(g), n, caps, cm[0], cm[1], cm[2], mem_mode,
                                    _a(device_of, np.int32), _a(exec_order, np.int32),
-                                   _a(exec_off, np.int32), C.byref(mk), st, dev3n, x4, err, 4096)
+                                   _a(exec_off, np.int32), C.byref(mk), st, dev3n, x4, err, _ERRLEN)
         if rc:
             raise OracleError(rc, err.value.decode())
         return SimResult(mk.value, st[:V], dev3n, x4)
@@ -561,8 +563,8 @@ class Restate:
     def topo_order(cls, m):
         g, keep = cls._g(m)
         order = np.zeros(max(g.V, 1), np.int32)
-        err = C.create_string_buffer(4096)
-        rc = cls.lib().rs_topo_order(C.byref(g), order, err, 4096)
+        err = C.create_string_buffer(_ERRLEN)
+        rc = cls.lib().rs_topo_order(C.byref(g), order, err, _ERRLEN)
         if rc:
             raise OracleError(rc, err.value.decode())
         return order[:g.V]

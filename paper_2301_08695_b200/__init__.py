@@ -177,6 +177,9 @@ def lib():
         i32, i64, cp = C.c_int32, C.c_int64, C.c_char_p
         L.bx_version.restype = C.c_char_p
         L.bx_last_error.restype = C.c_char_p
+        L.bx_last_message.restype = C.c_char_p
+        L.bx_plan_message.argtypes = [_vp, i32, C.c_char_p, i64]
+        L.bx_plan_message.restype = i64
         L.bx_device_count.restype = C.c_int
         L.bx_comm_time.argtypes = [C.POINTER(_Comm), i64, C.POINTER(i64)]
         L.bx_build_adjacency.argtypes = [i32, i32, _vp, _vp, _vp, _vp, _vp, cp, C.c_int]
@@ -241,7 +244,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["bx_version", "bx_last_error", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
+EXPORTED = ["bx_version", "bx_last_error", "bx_last_message", "bx_plan_message", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
             "bx_plan_create_ex", "bx_plan_job_kernel", "bx_simulate_ex",
             "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download", "bx_plan_result_view",
             "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_kernel_times",
@@ -488,7 +491,13 @@ class Plan:
                          view(o.exec_order, C.c_int32, V), view(o.exec_off, C.c_int32, n + 1), tuple(o.stats))
 
     def status(self, i: int) -> tuple[int, str]:
-        return self.out[i].status, self.out[i].msg.decode()
+        st = self.out[i].status
+        if not st:
+            return st, ""
+        full = lib().bx_plan_message(self.h, i, None, 0)  # msg[256] holds a prefix
+        buf = C.create_string_buffer(int(full) + 1)
+        lib().bx_plan_message(self.h, i, buf, full + 1)
+        return st, buf.value.decode()
 
     def simulate(self, mem_mode=TRAINING_PERSISTENT, stream=None):
         rc = lib().bx_plan_simulate(self.h, mem_mode, stream)
@@ -597,7 +606,8 @@ def _one(gg: MetaGraph, algo: str, capacity, cm: CommModel, fav=None, stats_out=
     out = _Placement(_ptr(bufs[0]), _ptr(bufs[1]), _ptr(bufs[2]), _ptr(bufs[3]))
     g = gg._c()
     lib().bx_place(C.byref(g), C.byref(job), C.byref(out))
-    _raise(out.status, out.msg.decode())
+    if out.status:
+        _raise(out.status, lib().bx_last_message().decode())  # the full text (msg[256] is a prefix)
     if stats_out is not None:
         stats_out[:] = list(out.stats)
     return Placement(algo, bufs[0][:V].copy(), bufs[1][:V].copy(), bufs[2][:V].copy(), bufs[3].copy(),

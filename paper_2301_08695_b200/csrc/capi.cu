@@ -26,13 +26,16 @@ cudaError_t sort_needs_all(void *tmp, size_t &tmp_bytes, const int64_t *need, in
                            int32_t *order_out, int total, int nseg, const int32_t *seg_off, cudaStream_t s);
 void launch_extract(const XCtx &c, cudaStream_t s);
 void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_etf, int n_bpar, int n_bseq,
-                    int njobs, const DGraph *graphs, const DPrep *preps, int maxn, bool any_topo, bool prof,
+                    int njobs, const DGraph *graphs, const DPrep *preps, int maxn, bool prof,
                     int list_len, cudaStream_t s_small, cudaStream_t s_big);
 void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn, int force_cap, cudaStream_t s);
 void launch_prep_small(const DGraph &g, const DPrep &pr, cudaStream_t s);
 void launch_small_frontier(const DJob *jobs, const int32_t *order, int n_etf, int n_sct, const DGraph *graphs,
                            const DPrep *preps, size_t smem, bool prof, cudaStream_t s);
 size_t small_smem_bytes_host(int V, int n, int nucap, int nccap);
+size_t topo_smem_bytes(int V, size_t limit);
+void launch_topo(const DJob *jobs, int njobs, const DGraph *graphs, const DPrep *preps, size_t smem_bytes,
+                 cudaStream_t s);
 }  // namespace bx
 
 using namespace bx;
@@ -101,6 +104,7 @@ struct bx_plan {
   int n_small = 0, n_etf = 0, n_bpar = 0, n_bseq = 0;  // n_etf: leading parallel m-ETF small jobs
   int n_sf_etf = 0, n_sf_sct = 0;   // small-frontier (K2s) jobs, launched first
   size_t sf_smem = 0;
+  size_t topo_smem = 0;  // m-TOPO CTA: bitsets (+ counters) of the largest m-TOPO graph
   int32_t *sf_order_dev = nullptr;
   std::vector<char> prep_small;     // prep index -> K2s extras needed
   std::vector<int> job_kernel;      // BX_KERNEL_* of the general kernel each job is queued on
@@ -184,6 +188,10 @@ extern "C" {
 const char *bx_version(void) { return "baechi-b200 0.1 (sm_100a)"; }
 
 const char *bx_last_error(void) { return g_last_error.c_str(); }
+
+// Full text of the last one-shot call's error (msg[256] keeps a prefix).
+static thread_local std::string g_last_message;
+const char *bx_last_message(void) { return g_last_message.c_str(); }
 
 int bx_device_count(void) {
   int n = 0;
@@ -701,6 +709,7 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
       }
       if (J.algo == BX_ALGO_MTOPO) {
         P->any_topo = true;
+        P->topo_smem = std::max(P->topo_smem, topo_smem_bytes(G.V, 200 * 1024));
       } else {
         P->any_list = true;
         P->max_vn = std::max(P->max_vn, int64_t(G.V) * J.n);
@@ -881,7 +890,7 @@ int bx_plan_place(bx_plan *P, void *stream) {
     launch_prep_small(g, P->dp[pi], s);
     P->launches += 2;
   }
-  if (P->total_V > 0) {
+  if (P->total_V > 0 && P->any_list) {  // need_order serves the list placers only
     size_t bytes = P->sort_tmp_bytes;
     cudaError_t e = sort_needs_all(P->sort_tmp, bytes, P->need_all, P->need_keys_all, P->iota_all, P->need_order_all,
                                    P->total_V, P->ngraphs, P->seg_off, s);
@@ -908,7 +917,8 @@ int bx_plan_place(bx_plan *P, void *stream) {
   }
   launch_placers(P->dj_dev, P->order_dev, P->n_small, P->n_etf, P->n_bpar, P->n_bseq, P->njobs, P->dg_dev,
                  P->dp_dev,
-                 P->maxn, P->any_topo, P->prof != nullptr, P->opt.list_len, s, sb);
+                 P->maxn, P->prof != nullptr, P->opt.list_len, s, sb);
+  if (P->any_topo) launch_topo(P->dj_dev, P->njobs, P->dg_dev, P->dp_dev, P->topo_smem, s);
   if (fork) {
     cudaEventRecord(P->join, P->s2);
     cudaStreamWaitEvent(s, P->join, 0);
@@ -1072,6 +1082,17 @@ int bx_plan_download(bx_plan *P, void *stream, bx_placement *out) {
 
 // Zero-copy view of job `job`'s placement inside the plan's pinned host
 // mirror (valid until the next bx_plan_download or bx_plan_destroy).
+int64_t bx_plan_message(const bx_plan *P, int32_t job, char *buf, int64_t buflen) {
+  if (job < 0 || job >= P->njobs || P->res_msg.empty()) return -1;
+  const std::string &m = P->res_msg[job];
+  if (buf && buflen > 0) {
+    const size_t k = std::min(m.size(), static_cast<size_t>(buflen - 1));
+    std::memcpy(buf, m.data(), k);
+    buf[k] = 0;
+  }
+  return static_cast<int64_t>(m.size());
+}
+
 int bx_plan_result_view(bx_plan *P, int32_t job, bx_placement *view) {
   if (job < 0 || job >= P->njobs || P->res_status.empty()) return BX_VALIDATION;
   const bx_plan::OOff &o = P->out_off[job];
@@ -1318,11 +1339,13 @@ int bx_place(const bx_graph *graph, const bx_job *job, bx_placement *out) {
   int rc = plan_create(1, graph, 1, &j, dev, nullptr, true, &P, out->msg, sizeof out->msg);
   if (rc) {
     out->status = rc;
+    g_last_message = out->msg;
     return rc;
   }
   rc = bx_plan_upload(P, nullptr);
   if (!rc) rc = bx_plan_place(P, nullptr);
   if (!rc) rc = bx_plan_download(P, nullptr, out);
+  g_last_message = !rc && !P->res_msg.empty() ? P->res_msg[0] : std::string(out->msg);
   if (rc) {
     out->status = rc;
     put_msg(out->msg, sizeof out->msg, std::string("CUDA error: ") + cudaGetErrorString(cudaGetLastError()));

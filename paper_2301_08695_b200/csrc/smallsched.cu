@@ -85,6 +85,21 @@ __device__ __forceinline__ uint64_t sm_min_u64(uint64_t v) {
 __device__ __forceinline__ int sm_dev(uint64_t info) { return static_cast<int>(static_cast<uint32_t>(info)); }
 __device__ __forceinline__ int32_t sm_fin(uint64_t info) { return static_cast<int32_t>(info >> 32); }
 
+// New-arrival bitset over (non-uniform producer, device): words, one spare
+// so a producer's n bits can always be read as a 64-bit window.
+__host__ __device__ inline int small_ncm_words(int nucap, int n) { return (nucap * n + 31) / 32 + 1; }
+__device__ __forceinline__ uint32_t ncm_bits(const uint32_t *w, int u, int n) {
+  const int b = u * n;
+  const uint64_t v = (static_cast<uint64_t>(w[(b >> 5) + 1]) << 32 | w[b >> 5]) >> (b & 31);
+  return static_cast<uint32_t>(v) & (n >= 32 ? ~0u : (1u << n) - 1u);
+}
+__device__ __forceinline__ void ncm_clear(uint32_t *w, int u, int n) {
+  const int b = u * n;
+  const uint64_t m = (n >= 32 ? 0xffffffffull : (1ull << n) - 1ull) << (b & 31);
+  atomicAnd(w + (b >> 5), ~static_cast<uint32_t>(m));
+  if (m >> 32) atomicAnd(w + (b >> 5) + 1, ~static_cast<uint32_t>(m >> 32));
+}
+
 // Shared-memory layout of one problem (host: small_smem_bytes).
 struct SSm {
   int32_t *F, *awf, *awu, *excl;  // [32] per device
@@ -105,7 +120,8 @@ struct SSm {
   int32_t *pin, *pout;  // [32] per commit: first in- / out-edge item
   int32_t *cpd, *csl;   // [32] per commit: device, slot
   int32_t *ita, *itb;   // [32] per item of a 32-item chunk: CSR position, device
-  int32_t *nci, *ncp;   // [nccap] newly cached (producer, device)
+  int32_t *nci;         // [nccap] non-uniform producers newly cached this round (nu index)
+  uint32_t *ncm;        // bit u * n + p: non-uniform producer u newly reached device p this round
   int32_t *newn;        // [kSSlots] newly ready nodes
   int32_t *scal;        // [32] exec-order counters
 };
@@ -117,7 +133,7 @@ __host__ __device__ inline size_t small_smem_bytes(int V, int n, int nucap, int 
   b += (size_t(nucap) * n * 2 + 7) & ~size_t(7);               // nuc
   const size_t ns = static_cast<size_t>(small_slots(n));
   b += ns * (7 * 4 + 8 + 8 * kKI + 4 * kKO) + size_t(kSPairs) * 4 + 32 * 4;  // slots, caches, dr, cjs
-  b += 6 * 32 * 4 + 2 * size_t(nccap) * 4 + size_t(kSSlots) * 4 + 32 * 4;
+  b += 6 * 32 * 4 + size_t(nccap) * 4 + small_ncm_words(nucap, n) * 4 + size_t(kSSlots) * 4 + 32 * 4;
   return b + 64;
 }
 
@@ -163,8 +179,8 @@ __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, i
   m.itb = p32 + 160;
   p32 += 192;
   m.nci = p32;
-  m.ncp = p32 + nccap;
-  m.newn = p32 + 2 * nccap;
+  m.ncm = reinterpret_cast<uint32_t *>(p32 + nccap);
+  m.newn = p32 + nccap + small_ncm_words(nucap, n);
   m.scal = m.newn + kSSlots;
   return m;
 }
@@ -491,6 +507,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     m.excl[lane] = 0;
     m.slack[lane] = lane < n ? jb.cap[lane] : 0;
     for (int x = lane; x < jb.nucap * n; x += 32) m.nuc[x] = 0xffffu;
+    for (int x = lane; x < small_ncm_words(jb.nucap, n); x += 32) m.ncm[x] = 0;
   }
   int R = 0;
   for (int base = 0; base < V; base += 32) {
@@ -684,7 +701,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       }
       __syncwarp();
       bool fresh = false;
-      int a = 0, b = 0;
+      int a = 0;
       if (base + lane < tin) {
         const int it = m.ita[lane], p = m.itb[lane];
         const uint2 e = slot_parent(m, G, it >> 16, it & 0xffff);
@@ -694,18 +711,15 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
           uint16_t *slot = m.nuc + u * n + p;
           if (*slot == 0xffffu) {
             *slot = static_cast<uint16_t>(e.y & 0xffffu);
-            fresh = true;
-            a = static_cast<int>(e.x);
-            b = p;
+            const int bit = u * n + p;
+            atomicOr(m.ncm + (bit >> 5), 1u << (bit & 31));
+            fresh = true;  // u may be listed twice (two commits of the round share it)
+            a = u;
           }
         }
       }
       const unsigned bf = __ballot_sync(kFull, fresh);
-      if (fresh) {
-        const int at = nnc + __popc(bf & ((1u << lane) - 1u));
-        m.nci[at] = a;
-        m.ncp[at] = b;
-      }
+      if (fresh) m.nci[nnc + __popc(bf & ((1u << lane) - 1u))] = a;
       nnc += __popc(bf);
       __syncwarp();
     }
@@ -785,23 +799,27 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     }
 
     // ---- 7. ready consumers of each newly cached (producer, device) re-key ----
-    // one lane per ready slot scans its parents against the round's new
-    // (producer, device) arrivals (all in shared memory)
+    // one lane per ready slot ORs its non-uniform parents' new-arrival device
+    // masks (step 4a) and re-keys those columns; the masks are then cleared
     if (nnc > 0) {
       for (int s = lane; s < st.R; s += 32) {
         const int ci = m.cnt[s] & 0xffff;
+        uint32_t rk = 0;
         for (int k = 0; k < ci; ++k) {
-          const int par = static_cast<int>(slot_parent(m, G, s, k).x);
-          for (int e = 0; e < nnc; ++e) {
-            if (m.nci[e] != par) continue;
-            const int p = m.ncp[e];
-            if (m.dr[s * n + p] != kSDead) {
-              int32_t urg;
-              m.dr[s * n + p] = slot_dr<false>(m, G, n, s, ci, p, urg);
-            }
+          const int u = static_cast<int>(slot_parent(m, G, s, k).y >> 16) - 1;
+          if (u >= 0) rk |= ncm_bits(m.ncm, u, n);
+        }
+        while (rk) {
+          const int p = __ffs(rk) - 1;
+          rk &= rk - 1;
+          if (m.dr[s * n + p] != kSDead) {
+            int32_t urg;
+            m.dr[s * n + p] = slot_dr<false>(m, G, n, s, ci, p, urg);
           }
         }
       }
+      __syncwarp();
+      for (int e = lane; e < nnc; e += 32) ncm_clear(m.ncm, m.nci[e], n);
       __syncwarp();
     }
     SMARK(P_CACHE);

@@ -394,3 +394,119 @@ def test_composite_key_clip_falls_back_exactly(bx, kernel):
     # the scenario provably saturates: a device idle at t = 0 next to a ready
     # node whose parent finishes beyond 2^32 us
     assert (m["k"] >= (1 << 32)).any()
+
+
+
+def _renumber(g, perm):
+    """The same DAG with node i renamed perm[i] (edges re-sorted by (src, dst))."""
+    out = dict(V=g["V"])
+    for f in ("k", "temp", "perm", "out"):
+        a = np.empty_like(g[f])
+        a[perm] = g[f]
+        out[f] = a
+    s, d = perm[g["esrc"]], perm[g["edst"]]
+    o = np.lexsort((d, s))
+    out["esrc"], out["edst"] = s[o].astype(np.int32), d[o].astype(np.int32)
+    out["ebytes"] = np.asarray(g["ebytes"])[o]
+    out["E"] = len(o)
+    return out
+
+
+def _tiny(V, seed):
+    rng = np.random.default_rng(seed)
+    e = np.array([[0, 1]] if V == 2 else np.zeros((0, 2)), np.int32).reshape(-1, 2)
+    return dict(V=V, E=len(e), k=rng.integers(50, 151, V), temp=rng.integers(0, 100, V),
+                perm=rng.integers(1, 100, V), out=rng.integers(1, 100, V), esrc=e[:, 0].copy(),
+                edst=e[:, 1].copy(), ebytes=np.full(len(e), 4096, np.int64))
+
+
+@pytest.mark.parametrize("shape", ["relabeled", "partial", "forward"])
+def test_mtopo_kahn_bursts_vs_restatement(bx, shape):
+    """m-TOPO's burst Kahn against the C restatement: graphs numbered
+    topologically (one burst), fully renumbered at random (mostly single
+    pops) and with a few swapped id pairs (bursts broken by local backward
+    edges); 1, 3 and 7 devices, both comm modes; the 30k graph is past the
+    shared-memory counter limit (counters in HBM)."""
+    rng = np.random.default_rng(11)
+    for i, V in enumerate([1, 2, 300, 2500, 30000]):
+        g = _tiny(V, i) if V < 50 else dict(W.as_meta_dict(W.layered_dag(V // 50, 50, seed=100 + i)))
+        if shape == "relabeled":
+            g = _renumber(g, rng.permutation(g["V"]))
+        elif shape == "partial":
+            perm = np.arange(g["V"])
+            for _ in range(max(1, g["V"] // 200)):
+                a, b = rng.integers(0, g["V"], 2)
+                perm[a], perm[b] = perm[b], perm[a]
+            g = _renumber(g, perm)
+        gg = _meta(bx, g)
+        need = g["perm"] + g["out"] + g["temp"]
+        for n in (1, 3, 7):
+            cap = int(need.sum() // n + need.max() + 10)
+            for cm in ((12.5, 0.002, 1), (5.0, 0.001, 0)):
+                p = bx._one(gg, "m-topo", [cap] * n, bx.CommModel(*cm), None)
+                o = Restate.place(g, 0, [cap] * n, cm)
+                _assert_same(p, o, stats=False)
+
+
+@pytest.mark.parametrize("renumber", [False, True])
+def test_acyclicity_residue_vs_restatement(bx, renumber):
+    """The burst/level acyclicity peel: cyclic meta graphs (back edges added
+    to layered DAGs, optionally renumbered) raise CycleError with the same
+    residue as the restatement's Kahn, for every algorithm; the acyclic
+    originals place normally."""
+    rng = np.random.default_rng(5)
+    for i, V in enumerate([200, 3000, 40000]):
+        g = dict(W.as_meta_dict(W.layered_dag(V // 20, 20, seed=200 + i)))
+        if renumber:
+            g = _renumber(g, rng.permutation(V))
+        for extra in (0, 1, 3):
+            h = dict(g)
+            if extra:
+                s, d = list(h["esrc"]), list(h["edst"])
+                # a back edge from a late node to an earlier one on a path: a cycle
+                order = np.argsort(W_levels(h))
+                for _ in range(extra):
+                    a = int(order[rng.integers(V // 2, V)])
+                    b = int(order[rng.integers(0, V // 4)])
+                    s.append(a)
+                    d.append(b)
+                key = np.unique(np.array(s, np.int64) * V + np.array(d, np.int64))
+                s, d = key // V, key % V
+                h["esrc"], h["edst"] = s.astype(np.int32), d.astype(np.int32)
+                h["ebytes"] = np.full(len(s), 4096, np.int64)
+                h["E"] = len(s)
+            gg = _meta(bx, h)
+            for algo in (0, 1):
+                try:
+                    o = Restate.place(h, algo, [10 ** 15] * 3, (12.5, 0.002, 1))
+                    oe = None
+                except OracleError as e:
+                    oe = (e.kind, str(e))
+                try:
+                    p = bx._one(gg, ALGO[algo], [10 ** 15] * 3, bx.CommModel(12.5, 0.002, 1), None)
+                    pe = None
+                except bx.Error as e:
+                    pe = (e.kind, e.msg)
+                assert pe == oe, (V, extra, algo)
+                if oe is None:
+                    _assert_same(p, o, stats=algo != 0)
+
+
+def W_levels(h):
+    """Longest-path level of every node (numpy, edges in any numbering)."""
+    V = h["V"]
+    s, d = np.asarray(h["esrc"]), np.asarray(h["edst"])
+    indeg = np.bincount(d, minlength=V)
+    lvl = np.zeros(V, np.int64)
+    out = [[] for _ in range(V)]
+    for a, b in zip(s.tolist(), d.tolist()):
+        out[a].append(b)
+    stack = [v for v in range(V) if indeg[v] == 0]
+    while stack:
+        v = stack.pop()
+        for c in out[v]:
+            lvl[c] = max(lvl[c], lvl[v] + 1)
+            indeg[c] -= 1
+            if indeg[c] == 0:
+                stack.append(c)
+    return lvl
