@@ -438,6 +438,16 @@ def main():
                 for name in W.CONFIGS for r in run_config(name, cpu=not args.no_cpu_baseline)]
         except Exception as e:
             pg["configs"] = {"error": str(e)}
+        # other 100k-op families next to the reference on one core: the
+        # reference's own layered-chain (4-wide frontier), 16 chains, a wide
+        # random DAG, 64 devices, and sequential comm mode
+        try:
+            from latency_table import run as run_case
+            pg["families"] = [run_case(nm, cpu=not args.no_cpu_baseline)
+                              for nm in ("refchain100k_x4", "grid100k_x8", "wide100k_x16", "layered100k_x64",
+                                         "seq_layered100k_x4", "seq_wide100k_x16", "seq_refchain100k_x4")]
+        except Exception as e:
+            pg["families"] = {"error": str(e)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

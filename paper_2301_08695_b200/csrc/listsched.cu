@@ -1496,6 +1496,7 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
     int indeg = g.in_off[j + 1] - g.in_off[j];
     c.pending[j] = indeg;
     c.device_of[j] = -1;
+    c.rpos[j] = -1;  // read speculatively beside pending / device_of (the cached-consumer re-keys)
     if (indeg == 0) {
       int s = atomicAdd(&S->R, 1);
       c.node_s[s] = j;

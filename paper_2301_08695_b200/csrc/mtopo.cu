@@ -498,6 +498,7 @@ __global__ void __launch_bounds__(kTopoThreads) k_acyclic(DGraph *graphs, int32_
           if (T2 == T) break;
           T = T2;
         }
+        __syncwarp();  // every lane has read done[c] and its parents' words
         if (lane == 0 && T) done[c] = dw | T;
         __syncwarp();
         got += __popc(T);

@@ -119,7 +119,8 @@ struct SSm {
   // per round
   int32_t *pin, *pout;  // [32] per commit: first in- / out-edge item
   int32_t *cpd, *csl;   // [32] per commit: device, slot
-  int32_t *ita, *itb;   // [32] per item of a 32-item chunk: CSR position, device
+  int32_t *ita, *itb;   // [32] per in-item of a 32-item chunk: slot << 16 | k, device
+  int32_t *ito;         // [32] per out-item: slot << 16 | k
   int32_t *nci;         // [nccap] non-uniform producers newly cached this round (nu index)
   uint32_t *ncm;        // bit u * n + p: non-uniform producer u newly reached device p this round
   int32_t *newn;        // [kSSlots] newly ready nodes
@@ -133,7 +134,7 @@ __host__ __device__ inline size_t small_smem_bytes(int V, int n, int nucap, int 
   b += (size_t(nucap) * n * 2 + 7) & ~size_t(7);               // nuc
   const size_t ns = static_cast<size_t>(small_slots(n));
   b += ns * (7 * 4 + 8 + 8 * kKI + 4 * kKO) + size_t(kSPairs) * 4 + 32 * 4;  // slots, caches, dr, cjs
-  b += 6 * 32 * 4 + size_t(nccap) * 4 + small_ncm_words(nucap, n) * 4 + size_t(kSSlots) * 4 + 32 * 4;
+  b += 7 * 32 * 4 + size_t(nccap) * 4 + small_ncm_words(nucap, n) * 4 + size_t(kSSlots) * 4 + 32 * 4;
   return b + 64;
 }
 
@@ -177,7 +178,8 @@ __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, i
   m.csl = p32 + 96;
   m.ita = p32 + 128;
   m.itb = p32 + 160;
-  p32 += 192;
+  m.ito = p32 + 192;
+  p32 += 224;
   m.nci = p32;
   m.ncm = reinterpret_cast<uint32_t *>(p32 + nccap);
   m.newn = p32 + nccap + small_ncm_words(nucap, n);
@@ -299,6 +301,7 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
       }
     }
   }
+  __syncwarp();  // every lane's key reads precede the selection's shared-memory writes
   uint32_t T = 0xffffffffu;
   cm.nc = 0;
   bool progress = false;
@@ -434,6 +437,7 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
     }
     if (st.placed == st.V) break;
   }
+  __syncwarp();  // ... and the commits' writes (step 3) follow every lane's reads
   return progress;
 }
 
@@ -677,75 +681,67 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     }
     // per-commit first item (inclusive scan of the packed counts)
     int incl = cin | (cout << 16);
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+    for (int o = 1; o < nc; o <<= 1) {  // lanes >= nc hold 0 and are never read below
       const int v = __shfl_up_sync(kFull, incl, o);
       if (lane >= o) incl += v;
     }
-    const int tot = __shfl_sync(kFull, incl, 31);
+    const int tot = __shfl_sync(kFull, incl, nc - 1);
     const int tin = tot & 0xffff, tout = tot >> 16;
     const int pin = (incl & 0xffff) - cin, pout = (incl >> 16) - cout;
     SMARK(P_COMMIT);
 
-    // ---- 4a. cache arrivals: every in-edge of a committed node --------------------
-    // 32-item chunks; each commit lane writes its items' (slot << 16 | k,
-    // device) into the chunk table, then lane i takes item base + i
+    // ---- 4. cache arrivals (every in-edge of a committed node) and readiness
+    // (every out-edge), one pass: 32-item chunks of both lists side by side;
+    // each commit lane writes its items into the chunk tables, then lane i
+    // takes in-item base + i and out-item base + i (two independent chains)
     int nnc = 0;
-    for (int base = 0; base < tin; base += 32) {
+    const int titems = max(tin, tout);
+    for (int base = 0; base < titems; base += 32) {
       if (lane < nc) {
-        const int lo = max(pin, base), hi = min(pin + cin, base + 32);
-        for (int k = lo; k < hi; ++k) {
+        const int ilo = max(pin, base), ihi = min(pin + cin, base + 32);
+        const int olo = max(pout, base), ohi = min(pout + cout, base + 32);
+        for (int k = ilo; k < ihi; ++k) {
           m.ita[k - base] = cm.s << 16 | (k - pin);
           m.itb[k - base] = cm.p;
         }
+        for (int k = olo; k < ohi; ++k) m.ito[k - base] = cm.s << 16 | (k - pout);
       }
       __syncwarp();
-      bool fresh = false;
-      int a = 0;
-      if (base + lane < tin) {
-        const int it = m.ita[lane], p = m.itb[lane];
-        const uint2 e = slot_parent(m, G, it >> 16, it & 0xffff);
+      bool fresh = false, ready = false;
+      int a = 0, child = 0;
+      const bool hin = base + lane < tin, hout = base + lane < tout;
+      const int iti = m.ita[lane], itp = m.itb[lane], ito = m.ito[lane];
+      if (hout) {
+        child = slot_child(m, G, ito >> 16, ito & 0xffff);
+        // 16-bit counters decremented through their 32-bit word (a counter
+        // is >= 1 when decremented, so no borrow crosses halves)
+        unsigned *word = reinterpret_cast<unsigned *>(m.pending) + (child >> 1);
+        const int sh = 16 * (child & 1);
+        ready = ((atomicSub(word, 1u << sh) >> sh) & 0xffffu) == 1;
+        if (ready) asm volatile("prefetch.global.L1 [%0];" ::"l"(G.node + 2 * child));
+      }
+      if (hin) {
+        const uint2 e = slot_parent(m, G, iti >> 16, iti & 0xffff);
         const int u = static_cast<int>(e.y >> 16) - 1;
-        if (u >= 0 && sm_dev(m.info[e.x]) != p) {
+        if (u >= 0 && sm_dev(m.info[e.x]) != itp) {
           // one commit per device per round, so no two lanes share a slot
-          uint16_t *slot = m.nuc + u * n + p;
+          uint16_t *slot = m.nuc + u * n + itp;
           if (*slot == 0xffffu) {
             *slot = static_cast<uint16_t>(e.y & 0xffffu);
-            const int bit = u * n + p;
+            const int bit = u * n + itp;
             atomicOr(m.ncm + (bit >> 5), 1u << (bit & 31));
             fresh = true;  // u may be listed twice (two commits of the round share it)
             a = u;
           }
         }
       }
-      const unsigned bf = __ballot_sync(kFull, fresh);
+      const unsigned bf = __ballot_sync(kFull, fresh), br = __ballot_sync(kFull, ready);
       if (fresh) m.nci[nnc + __popc(bf & ((1u << lane) - 1u))] = a;
-      nnc += __popc(bf);
-      __syncwarp();
-    }
-    // ---- 4b. readiness: every out-edge of a committed node ----------------------
-    for (int base = 0; base < tout; base += 32) {
-      if (lane < nc) {
-        const int lo = max(pout, base), hi = min(pout + cout, base + 32);
-        for (int k = lo; k < hi; ++k) m.ita[k - base] = cm.s << 16 | (k - pout);
-      }
-      __syncwarp();
-      bool ready = false;
-      int child = 0;
-      if (base + lane < tout) {
-        const int it = m.ita[lane];
-        child = slot_child(m, G, it >> 16, it & 0xffff);
-        // 16-bit counters decremented through their 32-bit word (a counter
-        // is >= 1 when decremented, so no borrow crosses halves)
-        unsigned *word = reinterpret_cast<unsigned *>(m.pending) + (child >> 1);
-        const int sh = 16 * (child & 1);
-        ready = ((atomicSub(word, 1u << sh) >> sh) & 0xffffu) == 1;
-      }
-      const unsigned br = __ballot_sync(kFull, ready);
       if (ready) {
         const int at = nnew + __popc(br & ((1u << lane) - 1u));
         if (at < kSSlots) m.newn[at] = child;
       }
+      nnc += __popc(bf);
       nnew += __popc(br);
       __syncwarp();
     }

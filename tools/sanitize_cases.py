@@ -68,6 +68,40 @@ def main():
         st = bx.PlacerState(m["V"], 3, bx.PARALLEL)
         bx.schedulable_times(st, list(range(m["V"])), [0] * m["V"], gg, bx.CommModel(12.5, 0.002, 1))
         bx.critical_path_us(gg)
+    # m-TOPO single pops and the acyclicity check's level-peel fallback
+    # (a randomly renumbered DAG), and its cycle residue (one back edge)
+    g = W.as_meta_dict(W.layered_dag(30, 10, 4))
+    perm = np.random.default_rng(2).permutation(g["V"])
+    r = dict(V=g["V"])
+    for f in ("k", "temp", "perm", "out"):
+        a = np.empty_like(g[f])
+        a[perm] = g[f]
+        r[f] = a
+    sv, dv = perm[g["esrc"]], perm[g["edst"]]
+    o = np.lexsort((dv, sv))
+    r.update(esrc=sv[o].astype(np.int32), edst=dv[o].astype(np.int32), ebytes=np.asarray(g["ebytes"])[o], E=len(o))
+    gg = bx.MetaGraph.from_dict(r)
+    caps = [10 ** 12] * 3
+    for algo in (0, 1):
+        p = bx._one(gg, ALGO[algo], caps, bx.CommModel(12.5, 0.002, 1))
+        o = Restate.place(r, algo, caps, (12.5, 0.002, 1))
+        assert np.array_equal(p.device_of, o.device_of) and np.array_equal(p.start_us, o.start_us)
+    x = int(g["esrc"][0])  # follow first out-edges to a sink: a path, so sink -> start closes a cycle
+    start = x
+    while True:
+        nxt = g["edst"][g["esrc"] == x]
+        if len(nxt) == 0:
+            break
+        x = int(nxt[0])
+    last, first = int(perm[x]), int(perm[start])
+    cyc = dict(r, esrc=np.append(r["esrc"], last).astype(np.int32), edst=np.append(r["edst"], first).astype(np.int32),
+               ebytes=np.append(r["ebytes"], 4096), E=r["E"] + 1)
+    o = np.lexsort((cyc["edst"], cyc["esrc"]))
+    cyc.update(esrc=cyc["esrc"][o], edst=cyc["edst"][o], ebytes=cyc["ebytes"][o])
+    try:
+        bx._one(bx.MetaGraph.from_dict(cyc), "m-etf", caps, bx.CommModel(12.5, 0.002, 1))
+    except bx.CycleError:
+        ran["cycle"] = ran.get("cycle", 0) + 1
     # a batch: the many-job dispatch (warp kernel lists, the side stream)
     graphs = [W.branchy(3, s) for s in range(4)]
     mgs = [bx.MetaGraph.from_dict(W.as_meta_dict(g)) for g in graphs]
