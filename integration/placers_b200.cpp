@@ -1,25 +1,3 @@
-# INTEGRATION — dropping the B200 engine into `dagsched`
-
-The engine is `paper_2301_08695_b200/libbaechi_b200.so` (built for sm_100a by
-`make -C paper_2301_08695_b200/csrc`), with the C ABI in
-`include/baechi_b200.h`. The reference is C++ (`namespace dagsched`), so the
-binding a maintainer adds is a thin C++ shim that keeps the reference
-signatures (`proj/include/dagsched/placers.hpp:73-89`,
-`simulator.hpp:53-55`, `lp.hpp:88-90`) and forwards to the ABI.
-
-## C++ shim (reference side)
-
-The shim is `integration/placers_b200.cpp` (reproduced below). It is compiled
-against the reference's own headers and tested: `make -C oracle shim` builds
-`oracle/_ref/shim_driver`, which links the shim, the reference's other
-objects and `libbaechi_b200.so`, next to the unmodified reference placer
-compiled with its `place_*` renamed `ref_place_*`, and compares the two on
-864 reference-typed cases (three generator families, singleton and
-colocation groupings, 1/3/8 devices, feasible and infeasible capacities,
-both comm modes, all three algorithms): same `Placement` + `PlacerStats`, or
-the same exception kind and `what()` text (`tests/test_shim.py`).
-
-```cpp
 // proj/src/placers_b200.cpp — the reference-side shim: the
 // dagsched placer entry points (proj/include/dagsched/placers.hpp:73-89) with
 // their reference signatures, forwarded to the B200 engine's C ABI
@@ -114,44 +92,3 @@ Placement place_mtopo(const GroupedGraph& gg, const DeviceRoster& r, const CommM
   return run(gg, r, cm, BX_ALGO_MTOPO, nullptr, nullptr, "m-topo");
 }
 }  // namespace dagsched
-```
-
-Build change: add `placers_b200.cpp` instead of `placers.cpp` to
-`proj/src/CMakeLists.txt` and link `libbaechi_b200.so` (add its directory to
-the rpath). `simulate` / `verify_placement` forward the same way to
-`bx_simulate` (placement → `device_of` + flattened `exec_order`/offsets), and
-`round_and_extract` to `bx_round_extract` (`lp.edge_ends` → `esrc`/`edst`,
-`solution.x`), `build_lp` + `solve_relaxed` to `bx_lp_solve` (graph + comm
-model → `x`, `s`, `w`, iteration count; `SolverError` texts kept), and
-`build_grouped` / `make_graph` (`bench.hpp:29-44`, `graph.cpp:99-194`) to
-`bx_grouped_create` + `bx_grouped_view` (base nodes/edges in, the meta graph
-and the grouping out; the reference's `ValidationError` / `CycleError` texts).
-
-## Batched sweeps (`run_bench`)
-
-`run_bench` (`proj/src/bench.cpp:105-237`) fans cells over an OpenMP pool. The
-GPU replacement builds one `bx_plan` for all cells: `bx_plan_create` (graphs +
-jobs), `bx_plan_upload`, `bx_plan_place` (one pass of the placer kernels over every cell: the warp kernel for the sweep's parallel m-ETF cells, its generic instantiation and the CTA kernels for the rest, concurrently on two streams),
-`bx_plan_download`. Each job's `status`/`msg` carries the reference's
-per-cell error exactly as `run_placer` would throw it.
-
-## Python (ctypes) binding
-
-`paper_2301_08695_b200/__init__.py` is the ctypes binding used by the tests
-and `bench.py`; it mirrors the reference names and exceptions:
-
-```python
-import paper_2301_08695_b200 as bx
-gg = bx.MetaGraph(k, temp, perm, out, esrc, edst, tensor_bytes)   # a GroupedGraph
-p = bx.place_metf(gg, capacities, bx.CommModel(12.5, 0.002, bx.PARALLEL))
-rep = bx.simulate(gg, p, capacities, bx.CommModel(12.5, 0.002, bx.PARALLEL), bx.TRAINING_PERSISTENT)
-```
-
-## Error behaviour
-
-`status` is `ErrorKind` + 0 / 2 / 3 / 4 (the CLI exit codes,
-`tools/dagsched.cpp:350-368`), `msg` is the reference's `what()` text
-(e.g. `node 17 fits on no device`, `meta graph is cyclic; groups of base node
-ids {1, 2} remain`, `memory violation on device 0 at t=5us while holding node
-1: 120 > 100`). `5` (`BX_RUNTIME`) is a CUDA failure, including "no CUDA
-device: the B200 placement engine has no CPU fallback".
