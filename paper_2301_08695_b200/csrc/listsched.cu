@@ -744,6 +744,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
     const int p = static_cast<int>(bi % static_cast<unsigned>(n));
     const int64_t t = bt;
     const int sj = T.s[p];
+    __syncwarp();  // every lane has read the head before any owner edits the lists
     BX_MARK(P_ARGMIN);
 
     if (c.mode == 0 && vst[p] != placed + 1) {
