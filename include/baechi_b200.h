@@ -289,12 +289,18 @@ typedef struct {
   double rel_gap;
   double w;            /* unscaled objective after re-tightening the starts */
   int32_t num_rows, completion_rows, precedence_rows, child_rows, parent_rows, bound_rows;
+  /* K5 solver diagnostics: host build (rows, ordering, symbolic factor) and
+   * device IPM time, factor nonzeros, right-looking update pairs (0 = the
+   * factorization walks target columns instead of a precomputed map) */
+  double host_ms, device_ms;
+  int64_t factor_nnz, update_pairs;
 } bx_lp_info;
 
 /* bx_lp_solve == build_lp + solve_relaxed (lp.hpp:45-59, lp.cpp:14-278) on a
  * meta graph: the same Mehrotra IPM (scaling, start point, eta, stopping
- * rule, 200-iteration cap), normal equations factored on the GPU (cuSOLVER
- * sparse Cholesky). x [E] (clipped to [0,1]) and s [V] (nullable) are the
+ * rule, 200-iteration cap), the whole IPM loop on the GPU in one CTA with a
+ * hand-written sparse Cholesky of the normal equations (minimum-degree
+ * ordering, K5). x [E] (clipped to [0,1]) and s [V] (nullable) are the
  * unscaled solution. BX_SOLVER with the reference's text on failure. */
 int bx_lp_solve(const bx_graph *graph, const bx_comm *cm, double tolerance, double *x, double *s,
                 bx_lp_info *info, char *msg, int msglen);

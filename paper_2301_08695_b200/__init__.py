@@ -114,7 +114,9 @@ class _Grouping(C.Structure):
 class _LpInfo(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("rel_gap", C.c_double), ("w", C.c_double),
                 ("num_rows", C.c_int32), ("completion_rows", C.c_int32), ("precedence_rows", C.c_int32),
-                ("child_rows", C.c_int32), ("parent_rows", C.c_int32), ("bound_rows", C.c_int32)]
+                ("child_rows", C.c_int32), ("parent_rows", C.c_int32), ("bound_rows", C.c_int32),
+                ("host_ms", C.c_double), ("device_ms", C.c_double), ("factor_nnz", C.c_int64),
+                ("update_pairs", C.c_int64)]
 
 
 class _Comm(C.Structure):
@@ -710,7 +712,10 @@ def solve_relaxed(gg: MetaGraph, cm: CommModel, tolerance: float = 1e-6) -> LpSo
     _raise(rc, msg.value.decode())
     rows = dict(total=info.num_rows, completion=info.completion_rows, precedence=info.precedence_rows,
                 child=info.child_rows, parent=info.parent_rows, bound=info.bound_rows)
-    return LpSolution(x[:gg.E].copy(), s[:gg.V].copy(), info.w, info.iterations, info.rel_gap, rows)
+    sol = LpSolution(x[:gg.E].copy(), s[:gg.V].copy(), info.w, info.iterations, info.rel_gap, rows)
+    sol.solver = dict(host_ms=info.host_ms, device_ms=info.device_ms, factor_nnz=info.factor_nnz,
+                      update_pairs=info.update_pairs)
+    return sol
 
 
 def sct_favorites(gg: MetaGraph, cm: CommModel, threshold: float = 0.1, tolerance: float = 1e-6):
