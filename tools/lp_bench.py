@@ -32,4 +32,9 @@ for name, gg in cases:
     ms = (time.perf_counter() - t0) * 1e3
     print(json.dumps({"case": name, "V": gg.V, "E": gg.E, "lp_rows": sol.rows["total"], "iterations": sol.iterations,
                       "w": sol.w, "rel_gap": sol.rel_gap, "favorite_edges": int(st[0]), "repaired": int(st[1]),
-                      "sct_front_ms": round(ms, 1), "solver": sol.solver}), flush=True)
+                      "sct_front_ms": round(ms, 1), "solver": sol.solver,
+                      # favourite-map stability: relaxed x values near the 0.1 rounding threshold
+                      "x_within_1e-3_of_thr": int(np.sum(np.abs(sol.x - 0.1) < 1e-3)),
+                      "x_within_1e-6_of_thr": int(np.sum(np.abs(sol.x - 0.1) < 1e-6)),
+                      "min_abs_x_minus_thr": float(np.min(np.abs(sol.x - 0.1))) if len(sol.x) else None}),
+          flush=True)
