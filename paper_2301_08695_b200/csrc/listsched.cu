@@ -911,7 +911,10 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
             int64_t *slot = c.cache + static_cast<int64_t>(i) * n + p;
             if (*slot < 0) {
               *slot = c.pfin[x] + c.in_c[x];
-              fresh = true;
+              // a producer whose out-edges all carry the same bytes caches
+              // finish + the same c its other consumers already use: their
+              // keys cannot change, so no re-key (parallel mode only)
+              fresh = pr.nu[i] >= 0;
             }
           }
         }
@@ -1947,9 +1950,11 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
           int64_t *slot = c.cache + static_cast<int64_t>(par) * n + cm.q;
           if (*slot < 0) {  // commit_schedulable_time, parallel mode
             *slot = c.pfin[x] + c.in_c[x];
-            int a = atomicAdd(&S->nnc, 1);
-            c.nc[a] = par;
-            jb.ncw[a] = i;
+            if (pr.nu[par] >= 0) {  // uniform producers change no consumer key (see the warp kernel)
+              int a = atomicAdd(&S->nnc, 1);
+              c.nc[a] = par;
+              jb.ncw[a] = i;
+            }
           }
         }
       }

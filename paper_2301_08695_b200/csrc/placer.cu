@@ -63,6 +63,19 @@ __device__ __forceinline__ void prep_edges(const DGraph &g, const DPrep &pr, int
   }
 }
 
+// Per producer: -1 when every out-edge carries the same byte count (so the
+// same comm time: a cache arrival changes no consumer's parallel-mode key),
+// else 0. k_prep_small, which runs after this for small-frontier jobs,
+// refines it from the comm times and numbers the rest.
+__device__ __forceinline__ void prep_uniform(const DGraph &g, const DPrep &pr, int tid, int nthreads) {
+  for (int i = tid; i < g.V; i += nthreads) {
+    const int b = g.out_off[i], e = g.out_off[i + 1];
+    bool uni = true;
+    for (int y = b + 1; y < e && uni; ++y) uni = g.ebytes[y] == g.ebytes[b];
+    pr.nu[i] = uni ? -1 : 0;
+  }
+}
+
 // need[j] = perm + out + temp (reserve_bytes, placers.hpp:43-45); the sum of
 // compute times and a negative-time flag (the small-frontier kernel's bounds).
 __device__ __forceinline__ void prep_nodes(const DGraph &g, int tid, int nthreads) {
@@ -95,6 +108,7 @@ __global__ void k_prep_all(const DGraph *graphs, const DPrep *preps) {
   const DGraph g = graphs[pr.graph];
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
   prep_edges(g, pr, pr.first, tid, nth);
+  prep_uniform(g, pr, tid, nth);
   if (pr.first) prep_nodes(g, tid, nth);
 }
 
