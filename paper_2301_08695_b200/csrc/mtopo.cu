@@ -196,116 +196,128 @@ __global__ void __launch_bounds__(kTopoThreads) k_place_topo_cta(const DJob *job
   const bool neg_need = s_neg != 0;
 
   // ---- 1. min-index Kahn in bursts --------------------------------------------
-  const int nw = (V + 31) >> 5;
-  uint32_t *popped, *ready, *blocked;
-  int *pend, *pbwd;
-  {
-    // bitsets (and, when they fit too, the counters) in shared memory;
-    // otherwise in the job's byte scratch (V * n >= 3 V / 8 bytes) and its
-    // int32 arrays
-    const bool bits_sm = 3 * nw <= smem_words;
-    const bool cnt_sm = bits_sm && 3 * nw + 2 * V <= smem_words;
-    uint32_t *bb = bits_sm ? tsm : reinterpret_cast<uint32_t *>(jb.dead);
-    popped = bb;
-    ready = bb + nw;
-    blocked = bb + 2 * nw;
-    pend = cnt_sm ? reinterpret_cast<int *>(tsm + 3 * nw) : jb.pending;
-    pbwd = cnt_sm ? reinterpret_cast<int *>(tsm + 3 * nw + V) : jb.alive;
-  }
-  for (int w = tid; w < nw; w += kTopoThreads) {
-    popped[w] = 0;
-    ready[w] = 0;
-    blocked[w] = 0;
-  }
-  __syncthreads();
-  for (int y = tid; y < V; y += kTopoThreads) {
-    const int b = g.in_off[y], e = g.in_off[y + 1];
-    int bw = 0;
-    for (int x = e - 1; x >= b && g.in_src[x] > y; --x) ++bw;  // in_src ascending
-    pend[y] = e - b;
-    pbwd[y] = bw;
-    if (e == b) atomicOr(ready + (y >> 5), 1u << (y & 31));
-    if (bw) atomicOr(blocked + (y >> 5), 1u << (y & 31));
-  }
-  __syncthreads();
   int32_t *order = jb.exec_order;  // the topo order doubles as the exec lists
-  int cnt = 0, U = 0;
-  while (cnt < V) {
-    // U = first unpopped: scan the complement of `popped` word by word
-    {
-      int w0 = U >> 5;
-      int found = V;
-      for (; w0 < nw; w0 += kTopoThreads) {
-        const int w = w0 + tid;
-        int cand = INT32_MAX;
-        if (w < nw) {
-          uint32_t word = ~popped[w];
-          if (w == (U >> 5)) word &= ~0u << (U & 31);
-          if (word) cand = 32 * w + __ffs(word) - 1;
-        }
-        const int r = block_min(S, par, cand);
-        if (r != INT32_MAX) {
-          found = r < V ? r : V;
-          break;
-        }
-      }
-      U = found;
-    }
-    if (U >= V) break;
-    const int B = block_ffs(S, par, blocked, U, V);
-    if (B > U) {
-      // burst: the unpopped nodes of [U, B) in ascending order; one word per thread
-      const int wb = U >> 5, we = (B - 1) >> 5;
-      const int cnt0 = cnt;
-      for (int w0 = wb; w0 <= we; w0 += kTopoThreads) {
-        const int w = w0 + tid;
-        uint32_t take = 0;
-        if (w <= we) {
-          uint32_t m = ~popped[w];
-          if (w == wb) m &= ~0u << (U & 31);
-          if (w == we && ((B & 31) != 0)) m &= (1u << (B & 31)) - 1u;
-          take = m;
-        }
-        long long tot;
-        const int pos = cnt + static_cast<int>(block_scan(S, par, __popc(take), tot));
-        if (take) {
-          uint32_t m = take;
-          int k = pos;
-          while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            const int y = 32 * w + b;
-            order[k++] = y;
-            pend[y] = -kTopoBig;
-          }
-          popped[w] |= take;
-          ready[w] &= ~take;
-        }
-        cnt += static_cast<int>(tot);
-      }
-      __syncthreads();
-      for (int x = cnt0 + tid; x < cnt; x += kTopoThreads) topo_release(g, order[x], pend, pbwd, ready, blocked);
-      __syncthreads();
-      U = B;
-    } else {
-      // U is blocked: the first ready node >= U pops alone
-      const int r = block_ffs(S, par, ready, U, V);
-      if (tid == 0) {
-        order[cnt] = r;
-        pend[r] = -kTopoBig;
-        popped[r >> 5] |= 1u << (r & 31);
-        ready[r >> 5] &= ~(1u << (r & 31));
-      }
-      ++cnt;
-      __syncthreads();
-      for (int e = g.out_off[r] + tid; e < g.out_off[r + 1]; e += kTopoThreads) {
-        const int c = g.edst[e];
-        if (atomicSub(pend + c, 1) == 1) atomicOr(ready + (c >> 5), 1u << (c & 31));
-        if (r > c && atomicSub(pbwd + c, 1) == 1) atomicAnd(blocked + (c >> 5), ~(1u << (c & 31)));
-      }
-      __syncthreads();
-    }
+  int any_bwd = 0;
+  for (int y = tid; y < V; y += kTopoThreads) {
+    const int e = g.in_off[y + 1];
+    any_bwd |= e > g.in_off[y] && g.in_src[e - 1] > y;  // in_src ascending: the last parent is the largest
   }
+  if (!__syncthreads_or(any_bwd)) {
+    // numbered topologically: one burst over [0, V), the identity
+    for (int x = tid; x < V; x += kTopoThreads) order[x] = x;
+  } else {
+    const int nw = (V + 31) >> 5;
+    uint32_t *popped, *ready, *blocked;
+    int *pend, *pbwd;
+    {
+      // bitsets (and, when they fit too, the counters) in shared memory;
+      // otherwise in the job's byte scratch (V * n >= 3 V / 8 bytes) and its
+      // int32 arrays
+      const bool bits_sm = 3 * nw <= smem_words;
+      const bool cnt_sm = bits_sm && 3 * nw + 2 * V <= smem_words;
+      uint32_t *bb = bits_sm ? tsm : reinterpret_cast<uint32_t *>(jb.dead);
+      popped = bb;
+      ready = bb + nw;
+      blocked = bb + 2 * nw;
+      pend = cnt_sm ? reinterpret_cast<int *>(tsm + 3 * nw) : jb.pending;
+      pbwd = cnt_sm ? reinterpret_cast<int *>(tsm + 3 * nw + V) : jb.alive;
+    }
+    for (int w = tid; w < nw; w += kTopoThreads) {
+      popped[w] = 0;
+      ready[w] = 0;
+      blocked[w] = 0;
+    }
+    __syncthreads();
+    for (int y = tid; y < V; y += kTopoThreads) {
+      const int b = g.in_off[y], e = g.in_off[y + 1];
+      int bw = 0;
+      for (int x = e - 1; x >= b && g.in_src[x] > y; --x) ++bw;  // in_src ascending
+      pend[y] = e - b;
+      pbwd[y] = bw;
+      if (e == b) atomicOr(ready + (y >> 5), 1u << (y & 31));
+      if (bw) atomicOr(blocked + (y >> 5), 1u << (y & 31));
+    }
+    __syncthreads();
+    int cnt = 0, U = 0;
+    while (cnt < V) {
+      // U = first unpopped: scan the complement of `popped` word by word
+      {
+        int w0 = U >> 5;
+        int found = V;
+        for (; w0 < nw; w0 += kTopoThreads) {
+          const int w = w0 + tid;
+          int cand = INT32_MAX;
+          if (w < nw) {
+            uint32_t word = ~popped[w];
+            if (w == (U >> 5)) word &= ~0u << (U & 31);
+            if (word) cand = 32 * w + __ffs(word) - 1;
+          }
+          const int r = block_min(S, par, cand);
+          if (r != INT32_MAX) {
+            found = r < V ? r : V;
+            break;
+          }
+        }
+        U = found;
+      }
+      if (U >= V) break;
+      const int B = block_ffs(S, par, blocked, U, V);
+      if (B > U) {
+        // burst: the unpopped nodes of [U, B) in ascending order; one word per thread
+        const int wb = U >> 5, we = (B - 1) >> 5;
+        const int cnt0 = cnt;
+        for (int w0 = wb; w0 <= we; w0 += kTopoThreads) {
+          const int w = w0 + tid;
+          uint32_t take = 0;
+          if (w <= we) {
+            uint32_t m = ~popped[w];
+            if (w == wb) m &= ~0u << (U & 31);
+            if (w == we && ((B & 31) != 0)) m &= (1u << (B & 31)) - 1u;
+            take = m;
+          }
+          long long tot;
+          const int pos = cnt + static_cast<int>(block_scan(S, par, __popc(take), tot));
+          if (take) {
+            uint32_t m = take;
+            int k = pos;
+            while (m) {
+              const int b = __ffs(m) - 1;
+              m &= m - 1;
+              const int y = 32 * w + b;
+              order[k++] = y;
+              pend[y] = -kTopoBig;
+            }
+            popped[w] |= take;
+            ready[w] &= ~take;
+          }
+          cnt += static_cast<int>(tot);
+        }
+        __syncthreads();
+        for (int x = cnt0 + tid; x < cnt; x += kTopoThreads) topo_release(g, order[x], pend, pbwd, ready, blocked);
+        __syncthreads();
+        U = B;
+      } else {
+        // U is blocked: the first ready node >= U pops alone
+        const int r = block_ffs(S, par, ready, U, V);
+        if (tid == 0) {
+          order[cnt] = r;
+          pend[r] = -kTopoBig;
+          popped[r >> 5] |= 1u << (r & 31);
+          ready[r >> 5] &= ~(1u << (r & 31));
+        }
+        ++cnt;
+        __syncthreads();
+        for (int e = g.out_off[r] + tid; e < g.out_off[r + 1]; e += kTopoThreads) {
+          const int c = g.edst[e];
+          if (atomicSub(pend + c, 1) == 1) atomicOr(ready + (c >> 5), 1u << (c & 31));
+          if (r > c && atomicSub(pbwd + c, 1) == 1) atomicAnd(blocked + (c >> 5), ~(1u << (c & 31)));
+        }
+        __syncthreads();
+      }
+    }
+
+  }  // bursts
+  __syncthreads();
 
   // ---- 2. balanced fill; the last device absorbs the rest --------------------------
   int64_t *S_need = jb.urgent;  // inclusive prefix sums of needs in topo order
@@ -322,25 +334,40 @@ __global__ void __launch_bounds__(kTopoThreads) k_place_topo_cta(const DJob *job
   }
   __syncthreads();
   int32_t *off = jb.exec_off;
-  if (tid == 0) {
-    off[0] = 0;
+  if (tid < 32) {
+    const int lane = tid;
     int d = 0;
     if (!neg_need) {
       // boundary d+1 = first x > s_d (x >= 0 for d = 0) with S[x] - S[s_d - 1] > cap
+      // (S non-decreasing): a 32-way search per device, 32 probes per step
       int s = 0;
       for (; d + 1 < n; ++d) {
         const long long base = s > 0 ? S_need[s - 1] : 0;
-        int lo = d == 0 ? 0 : s + 1, hi = V;  // answer in [lo, hi], V = none
+        int lo = d == 0 ? 0 : s + 1, hi = V;  // first true in [lo, hi); hi = V: none
         while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (S_need[mid] - base > cap) hi = mid;
-          else lo = mid + 1;
+          const int step = (hi - lo + 31) / 32;
+          const int x = lo + lane * step;
+          const bool pr = x < hi && S_need[x] - base > cap;
+          const unsigned m = __ballot_sync(kFull, pr);
+          if (step == 1) {
+            lo = hi = m ? lo + __ffs(m) - 1 : hi;
+          } else if (!m) {
+            lo += ((hi - 1 - lo) / step) * step + 1;  // past the last probe below hi
+          } else {
+            const int f = __ffs(m) - 1;
+            if (f == 0) {
+              hi = lo;  // x_0 = lo is the first
+            } else {
+              hi = lo + f * step + 1;  // the answer is in (x_{f-1}, x_f]
+              lo = lo + (f - 1) * step + 1;
+            }
+          }
         }
         if (lo >= V) break;
-        off[d + 1] = lo;
+        if (lane == 0) off[d + 1] = lo;
         s = lo;
       }
-    } else {
+    } else if (lane == 0) {
       long long used = 0;
       for (int x = 0; x < V; ++x) {
         const long long b = g.need[order[x]];
@@ -351,7 +378,11 @@ __global__ void __launch_bounds__(kTopoThreads) k_place_topo_cta(const DJob *job
         used += b;
       }
     }
-    for (int e = d + 1; e <= n; ++e) off[e] = V;
+    d = __shfl_sync(kFull, d, 0);
+    if (lane == 0) {
+      off[0] = 0;
+      for (int e = d + 1; e <= n; ++e) off[e] = V;
+    }
   }
   __syncthreads();
   int32_t *tpos = jb.rpos;
@@ -470,6 +501,19 @@ __global__ void __launch_bounds__(kTopoThreads) k_acyclic(DGraph *graphs, int32_
   const int tid = threadIdx.x, lane = tid & 31, V = g.V;
   const int nw = (V + 31) >> 5;
   uint32_t *done = nw <= kAcycSmemWords ? bsm : reinterpret_cast<uint32_t *>(g.iota);
+  // no edge from a larger to a smaller index: the numbering is a topological
+  // order, nothing to peel (every model-shaped graph here); the pass also
+  // pulls the in-CSR into L1 for warp 0's sweeps otherwise
+  int bwd = 0;
+  for (int y = tid; y < V; y += kTopoThreads) {
+    const int e = g.in_off[y + 1];
+    bwd |= e > g.in_off[y] && g.in_src[e - 1] > y;  // in_src ascending: the last parent is the largest
+  }
+  if (!__syncthreads_or(bwd)) {
+    for (int y = tid; y < V; y += kTopoThreads) g.indeg_left[y] = 0;
+    if (tid == 0) g.flags[0] = V;
+    return;
+  }
   for (int w = tid; w < nw; w += kTopoThreads) done[w] = 0;
   __syncthreads();
   if (tid < 32) {
