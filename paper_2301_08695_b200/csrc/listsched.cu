@@ -375,18 +375,31 @@ __device__ void warp_topk(const Ctx &c, int q, int s0, int step, int R, int lane
 
 // ---- lane-owned list edits (lane q % 32 owns column q) -------------------------
 __device__ __forceinline__ void list_remove(const Tops &T, int q, int j) {
-  int c = T.cnt[q];
-  int at = -1;
-  for (int k = 0; k < c; ++k)
-    if (T.j[(k) * T.st + q] == j) at = k;
-  if (at < 0) return;
-  for (int k = at; k + 1 < c; ++k) {
-    T.t[(k) * T.st + q] = T.t[(k + 1) * T.st + q];
-    T.j[(k) * T.st + q] = T.j[(k + 1) * T.st + q];
-    T.s[(k) * T.st + q] = T.s[(k + 1) * T.st + q];
+  // every entry loaded up front (independent shared-memory loads), then the
+  // tail shifted down one place from the removed entry
+  const int c = T.cnt[q];
+  int64_t lt[KT];
+  int lj[KT], ls[KT];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) {
+    lt[k] = T.t[k * T.st + q];
+    lj[k] = T.j[k * T.st + q];
+    ls[k] = T.s[k * T.st + q];
   }
-  T.cnt[q] = --c;
-  if (c == 0 && !(T.flg[q] & kComplete)) T.flg[q] |= kDirty;
+  int at = -1;
+#pragma unroll
+  for (int k = 0; k < KT; ++k)
+    if (k < c && lj[k] == j) at = k;
+  if (at < 0) return;
+#pragma unroll
+  for (int k = 0; k + 1 < KT; ++k)
+    if (k >= at && k + 1 < c) {
+      T.t[k * T.st + q] = lt[k + 1];
+      T.j[k * T.st + q] = lj[k + 1];
+      T.s[k * T.st + q] = ls[k + 1];
+    }
+  T.cnt[q] = c - 1;
+  if (c == 1 && !(T.flg[q] & kComplete)) T.flg[q] |= kDirty;
 }
 
 __device__ __forceinline__ void list_insert(const Tops &T, int q, int64_t t, int j, int s) {
@@ -960,10 +973,12 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
         c.alive_s[sj] = mv_alive;
         c.rpos[mv] = sj;
       }
-      for (int e = lane; e < n * KT; e += 32) {
-        const int x = (e / n) * T.st + e % n;
-        if (T.j[x] == mv) T.s[x] = sj;
-      }
+#pragma unroll
+      for (int k = 0; k < KT; ++k)
+        for (int q = lane; q < n; q += 32) {
+          const int x = k * T.st + q;
+          if (T.j[x] == mv) T.s[x] = sj;
+        }
     }
     --R;
     __syncwarp();

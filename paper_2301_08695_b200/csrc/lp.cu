@@ -235,6 +235,12 @@ struct LpDev {
   // dense Cholesky, copied back into L
   int tail_t, tail_d;
   double *Dm;
+  // entries (L positions) of each level's sparse columns whose update list
+  // is short (one thread sums it) or long (one warp sums it); the tail's
+  // long-list entries (L position, Dm index)
+  const int *lev_sptr, *lev_sent, *lev_lptr, *lev_lent;
+  int tail_nlong;
+  const int *tail_long_p, *tail_long_x;
   double *z, *lam, *slack, *rd, *W, *rc, *tmp, *rhs, *dza, *dz, *dsa, *dla, *ds, *dl, *y, *L;
   int *status;     // 0 ok, 1 lost feasibility, 2 no convergence, 3 factorization failed
   int *iters;
@@ -292,6 +298,19 @@ __device__ void gt_times(const LpDev &D, const double *u, double *out, const dou
   }
 }
 
+constexpr int kLongList = 16;  // update lists longer than this are summed by a warp
+
+// sum of an entry's update products, lanes over the list, fixed-order tree
+// reduction (every lane returns it)
+__device__ __forceinline__ double list_sum(const LpDev &D, int p, int lane) {
+  double acc = 0.0;
+  for (long long q = D.upd_ptr[p] + lane; q < D.upd_ptr[p + 1]; q += 32) {
+    const int2 xy = D.upd[q];
+    acc += D.L[xy.x] * D.L[xy.y];
+  }
+  return warp_red<R_SUM>(acc);
+}
+
 // The dense tail (see LpDev): each entry starts from A minus its own list of
 // sparse-column products (fixed order), then a right-looking dense Cholesky
 // (one column per step, trailing update by warps over columns), copy back.
@@ -302,12 +321,18 @@ __device__ void dense_tail(const LpDev &D, int *s_fail) {
     const int i = static_cast<int>(x % d), j = static_cast<int>(x / d);
     if (i < j) continue;
     const int p = D.colptr[t + j] + (i - j);
+    const long long q0 = D.upd_ptr[p], q1 = D.upd_ptr[p + 1];
+    if (q1 - q0 > kLongList) continue;  // summed by a warp below
     double v = D.L[p];
-    for (long long q = D.upd_ptr[p]; q < D.upd_ptr[p + 1]; ++q) {
+    for (long long q = q0; q < q1; ++q) {
       const int2 xy = D.upd[q];
       v -= D.L[xy.x] * D.L[xy.y];
     }
     D.Dm[x] = v;
+  }
+  for (int e = warp; e < D.tail_nlong; e += kLpWarps) {
+    const int p = D.tail_long_p[e];
+    D.Dm[D.tail_long_x[e]] = D.L[p] - list_sum(D, p, lane);
   }
   __syncthreads();
   for (int j = 0; j < d; ++j) {
@@ -357,28 +382,37 @@ __device__ bool factor(const LpDev &D, double reg, int *s_fail) {
   __syncthreads();
   if (D.upd_ptr) {
     for (int lv = 0; lv < D.nlev; ++lv) {
+      // every entry of the level's sparse columns minus its update products
+      // (short lists: one thread each; long lists: one warp each) ...
+      for (int i = D.lev_sptr[lv] + tid; i < D.lev_sptr[lv + 1]; i += kLpThreads) {
+        const int p = D.lev_sent[i];
+        double v = D.L[p];
+        for (long long q = D.upd_ptr[p]; q < D.upd_ptr[p + 1]; ++q) {
+          const int2 xy = D.upd[q];
+          v -= D.L[xy.x] * D.L[xy.y];
+        }
+        D.L[p] = v;
+      }
+      for (int i = D.lev_lptr[lv] + warp; i < D.lev_lptr[lv + 1]; i += kLpWarps) {
+        const int p = D.lev_lent[i];
+        const double sum = list_sum(D, p, lane);
+        if (lane == 0) D.L[p] -= sum;
+      }
+      __syncthreads();
+      // ... then each column's pivot and scaling, one warp per column
       for (int c = D.lev_ptr[lv] + warp; c < D.lev_ptr[lv + 1]; c += kLpWarps) {
         const int k = D.lev_col[c];
         if (k >= D.tail_t) continue;  // the dense tail comes after every sparse column
         const int b = D.colptr[k], e = D.colptr[k + 1];
-        for (int p = b + lane; p < e; p += 32) {
-          double v = D.L[p];
-          for (long long q = D.upd_ptr[p]; q < D.upd_ptr[p + 1]; ++q) {
-            const int2 xy = D.upd[q];
-            v -= D.L[xy.x] * D.L[xy.y];
-          }
-          D.L[p] = v;
-        }
-        __syncwarp();
         double d = D.L[b];
         if (!(d > 0.0)) {
           if (lane == 0) *s_fail = 1;
           d = 1.0;
         }
         const double sd = sqrt(d), inv = 1.0 / sd;
+        __syncwarp();
         for (int p = b + 1 + lane; p < e; p += 32) D.L[p] *= inv;
         if (lane == 0) D.L[b] = sd;
-        __syncwarp();
       }
       __syncthreads();
     }
@@ -779,6 +813,30 @@ extern "C" int bx_lp_solve(const bx_graph *graph, const bx_comm *cm, double tole
           for (int p2 = p1; p2 < e; ++p2) upd[at[tpos[x++]]++] = make_int2(p1, p2);
       }
     }
+    // per level: the sparse columns' entries split by update-list length;
+    // the tail's long-list entries
+    std::vector<int> lev_sptr{0}, lev_sent, lev_lptr{0}, lev_lent, tail_long_p, tail_long_x;
+    if (!upd_ptr.empty()) {
+      constexpr long long kLong = 16;  // == kLongList
+      for (int l = 0; l < nlev; ++l) {
+        for (int c = lev_ptr[l]; c < lev_ptr[l + 1]; ++c) {
+          const int k = lev_col[c];
+          if (k >= tail_t) continue;
+          for (int p = S.colptr[k]; p < S.colptr[k + 1]; ++p)
+            (upd_ptr[p + 1] - upd_ptr[p] > kLong ? lev_lent : lev_sent).push_back(p);
+        }
+        lev_sptr.push_back(static_cast<int>(lev_sent.size()));
+        lev_lptr.push_back(static_cast<int>(lev_lent.size()));
+      }
+      for (int j = 0; j < tail_d; ++j)
+        for (int i = j; i < tail_d; ++i) {
+          const int p = S.colptr[tail_t + j] + (i - j);
+          if (upd_ptr[p + 1] - upd_ptr[p] > kLong) {
+            tail_long_p.push_back(p);
+            tail_long_x.push_back(j * tail_d + i);
+          }
+        }
+    }
     // device side
     DevBufs B;
     LpDev D{};
@@ -816,6 +874,13 @@ extern "C" int bx_lp_solve(const bx_graph *graph, const bx_comm *cm, double tole
     D.tail_t = upd_ptr.empty() ? nv : tail_t;
     D.tail_d = upd_ptr.empty() ? 0 : tail_d;
     D.Dm = B.zeros<double>(static_cast<size_t>(D.tail_d) * static_cast<size_t>(D.tail_d));
+    D.lev_sptr = B.put(lev_sptr);
+    D.lev_sent = B.put(lev_sent);
+    D.lev_lptr = B.put(lev_lptr);
+    D.lev_lent = B.put(lev_lent);
+    D.tail_nlong = static_cast<int>(tail_long_p.size());
+    D.tail_long_p = B.put(tail_long_p);
+    D.tail_long_x = B.put(tail_long_x);
     D.z = B.put(z);
     D.lam = B.put(std::vector<double>(nr, 1.0));
     D.slack = B.zeros<double>(nr);

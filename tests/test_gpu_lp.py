@@ -183,3 +183,61 @@ def test_c3_transformer_lp_end_to_end(bx):
                   bounds=[(0, None)] * V + [(0, 1)] * E + [(0, None)], method="highs")
     assert ref.status == 0
     assert sol.w == pytest.approx(ref.fun, rel=1e-4)
+
+
+def _highs_objective(mg, cm):
+    """build_lp's rows (lp.cpp:14-79, unscaled) solved by HiGHS."""
+    from scipy.optimize import linprog
+    import scipy.sparse as sp
+    V, E = mg.V, mg.E
+    c = np.array([bx_comm(cm, b) for b in mg.ebytes], float)
+    rows, cols, vals, b = [], [], [], []
+    r = 0
+    for i in range(V):
+        rows += [r, r]
+        cols += [i, V + E]
+        vals += [1, -1]
+        b.append(-mg.k[i])
+        r += 1
+    for e in range(E):
+        rows += [r, r, r]
+        cols += [mg.esrc[e], mg.edst[e], V + e]
+        vals += [1, -1, c[e]]
+        b.append(-mg.k[mg.esrc[e]])
+        r += 1
+    for off, ids in ((mg.out_off, None), (mg.in_off, mg.in_edge)):
+        for i in range(V):
+            lo, hi = off[i], off[i + 1]
+            if hi > lo:
+                for x in range(lo, hi):
+                    rows.append(r)
+                    cols.append(V + (x if ids is None else ids[x]))
+                    vals.append(-1)
+                b.append(1 - (hi - lo))
+                r += 1
+    A = sp.csr_matrix((vals, (rows, cols)), shape=(r, V + E + 1))
+    obj = np.zeros(V + E + 1)
+    obj[-1] = 1
+    ref = linprog(obj, A_ub=A, b_ub=np.array(b, float), bounds=[(0, None)] * V + [(0, 1)] * E + [(0, None)],
+                  method="highs")
+    assert ref.status == 0
+    return ref.fun
+
+
+def bx_comm(cm, b):
+    import paper_2301_08695_b200 as bx
+    return bx.comm_time(cm, b)
+
+
+@pytest.mark.parametrize("name", ["C1_inception_mtopo_metf", "C2_gnmt_metf_coplace"])
+def test_model_config_lps_match_highs(bx, name):
+    """The device IPM (K5) on the C1 and C2 meta graphs (10.8k / 26.5k LP
+    variables): level-scheduled left-looking factor with warp-summed long
+    update lists, and on C2 the dense tail block (the ordering's final 507
+    columns); objective = HiGHS on the same rows."""
+    gen, n, _, kw, f = W.CONFIGS[name]
+    mg, _ = bx.build_grouped(gen(), **kw)
+    cm = bx.CommModel(*W.COMM_TEST)
+    sol = bx.solve_relaxed(mg, cm)
+    assert sol.iterations < 200 and sol.solver["update_pairs"] > 0
+    assert sol.w == pytest.approx(_highs_objective(mg, cm), rel=1e-4)
