@@ -27,6 +27,8 @@
 //    data-ready time A_l, then a block max-plus scan
 //    f_l = max(f_{l-1} + k_l, A_l + k_l). Sequential comm keeps the
 //    reference fold (queue tails) on one thread.
+#include <algorithm>
+
 #include "sched_common.cuh"
 
 namespace bx {
@@ -153,6 +155,38 @@ __global__ void __launch_bounds__(kTopoThreads) k_place_topo_cta(const DJob *job
   const DPrep pr = preps[jb.prep];
   const int V = g.V, n = jb.n;
   int par = 0;
+  long long t_mark = clock64();
+  // profile builds (plan option profile): SM cycles per phase into jb.prof
+  // (0 warm + cap, 1 order, 2 fill, 3 devices, 4 estimate)
+#define TMARK(k)                                   \
+  do {                                             \
+    if (jb.prof && tid == 0) {                     \
+      const long long now_ = clock64();            \
+      jb.prof[k] = now_ - t_mark;                  \
+      t_mark = now_;                               \
+    }                                              \
+  } while (0)
+  // pull the graph arrays the dependent chains below walk (in-CSR, out-CSR,
+  // comm times, needs, compute times) into this SM's L1 first: independent
+  // 16-byte loads, one per 32-byte sector
+  if (static_cast<size_t>(V) * 64 + static_cast<size_t>(g.E) * 20 <= 160 * 1024) {
+    unsigned acc = 0;
+    auto warm = [&](const void *ptr, size_t bytes) {
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(ptr) & ~uintptr_t(31);
+      const uintptr_t a1 = reinterpret_cast<uintptr_t>(ptr) + bytes;
+      for (uintptr_t q = a0 + 32 * static_cast<uintptr_t>(tid); q < a1; q += 32 * kTopoThreads)
+        acc ^= __ldg(reinterpret_cast<const unsigned *>(q));
+    };
+    warm(g.in_off, 4 * size_t(V + 1));
+    warm(g.in_src, 4 * size_t(g.E));
+    warm(g.out_off, 4 * size_t(V + 1));
+    warm(g.edst, 4 * size_t(g.E));
+    warm(g.inpos, 4 * size_t(g.E));
+    warm(pr.in_c, 8 * size_t(g.E));
+    warm(g.need, 8 * size_t(V));
+    warm(g.k, 8 * size_t(V));
+    asm volatile("" ::"r"(acc));
+  }
   // cap = ceil(total / n) + largest (largest starts at 0); infeasible comes
   // before the acyclicity check
   if (tid == 0) s_cap = 0;
@@ -195,6 +229,7 @@ __global__ void __launch_bounds__(kTopoThreads) k_place_topo_cta(const DJob *job
   const int64_t cap = s_cap;
   const bool neg_need = s_neg != 0;
 
+  TMARK(0);
   // ---- 1. min-index Kahn in bursts --------------------------------------------
   int32_t *order = jb.exec_order;  // the topo order doubles as the exec lists
   int any_bwd = 0;
@@ -202,7 +237,8 @@ __global__ void __launch_bounds__(kTopoThreads) k_place_topo_cta(const DJob *job
     const int e = g.in_off[y + 1];
     any_bwd |= e > g.in_off[y] && g.in_src[e - 1] > y;  // in_src ascending: the last parent is the largest
   }
-  if (!__syncthreads_or(any_bwd)) {
+  const bool ident = !__syncthreads_or(any_bwd);
+  if (ident) {
     // numbered topologically: one burst over [0, V), the identity
     for (int x = tid; x < V; x += kTopoThreads) order[x] = x;
   } else {
@@ -319,6 +355,7 @@ __global__ void __launch_bounds__(kTopoThreads) k_place_topo_cta(const DJob *job
   }  // bursts
   __syncthreads();
 
+  TMARK(1);
   // ---- 2. balanced fill; the last device absorbs the rest --------------------------
   int64_t *S_need = jb.urgent;  // inclusive prefix sums of needs in topo order
   {
@@ -385,16 +422,73 @@ __global__ void __launch_bounds__(kTopoThreads) k_place_topo_cta(const DJob *job
     }
   }
   __syncthreads();
+  TMARK(2);
   int32_t *tpos = jb.rpos;
+  // identity order, parallel comm, small graph: finish times and devices in
+  // shared memory for the estimate (the bitsets are not needed)
+  const bool fast = ident && jb.mode == 1 && static_cast<size_t>(V) * 18 + 16 <= static_cast<size_t>(smem_words) * 4;
+  long long *fin_s = reinterpret_cast<long long *>(tsm);
+  long long *A_s = fin_s + V;
+  uint16_t *dev_s = reinterpret_cast<uint16_t *>(A_s + V);
   for (int x = tid; x < V; x += kTopoThreads) {
     int d = 0;
     while (off[d + 1] <= x) ++d;  // n is small; the rosters' largest chunk count
     const int j = order[x];
     jb.device_of[j] = d;
     tpos[j] = x;
+    if (fast) dev_s[j] = static_cast<uint16_t>(d);
   }
   __syncthreads();
 
+  TMARK(3);
+  if (fast) {
+    // ---- 3. schedule estimate, parallel comm, identity order: node index =
+    // topo position, so a remote parent's first consumer on device d is its
+    // first out-edge (ascending dst) at or past off[d]. Per device: the
+    // arrival terms edge-parallel over the device's in-edges (its nodes are
+    // contiguous, so are their in-CSR slots) into A_s, then the block scans.
+    for (int x = tid; x < V; x += kTopoThreads) A_s[x] = 0;
+    __syncthreads();
+    for (int d = 0; d < n; ++d) {
+      const int o = off[d], len = off[d + 1] - o;
+      const int xb = g.in_off[o], xe = g.in_off[o + len];
+      for (int x = xb + tid; x < xe; x += kTopoThreads) {
+        const int i = g.in_src[x];
+        if (dev_s[i] == d) continue;  // earlier on this device: covered by the chain
+        int lo = g.out_off[i], hi = g.out_off[i + 1];  // first out-edge with dst >= o
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (g.edst[mid] < o) lo = mid + 1;
+          else hi = mid;
+        }
+        // the consumer: the in-CSR slot's node (binary search on in_off is
+        // avoided: x's node is the one whose in-CSR range holds x)
+        atomicMax(reinterpret_cast<long long *>(A_s) + g.edst[g.in_edge[x]], fin_s[i] + pr.in_c[g.inpos[lo]]);
+      }
+      __syncthreads();
+      long long prev = 0;
+      for (int b0 = 0; b0 < len; b0 += kTopoThreads) {
+        const int idx = b0 + tid;
+        const int j = o + idx;
+        const long long kk = idx < len ? g.k[j] : 0, A = idx < len ? A_s[j] : 0;
+        long long a = kk, bb = A + kk, ta, tb;
+        block_maxplus(S, par, a, bb, ta, tb);
+        const long long f = max64(prev + a, bb);
+        if (idx < len) {
+          jb.start[j] = f - kk;
+          fin_s[j] = f;
+        }
+        prev = max64(prev + ta, tb);
+      }
+      __syncthreads();  // device d's finishes before device d + 1 reads them
+    }
+    TMARK(4);
+    if (tid == 0) {
+      jb.stats[0] = jb.stats[1] = jb.stats[2] = 0;
+      set_err(jb.err, kOk, E_NONE, 0, 0);
+    }
+    return;
+  }
   if (jb.mode == 1) {
     // ---- 3. schedule estimate, parallel comm --------------------------------------
     for (int y = tid; y < g.E; y += kTopoThreads) {  // y = edge id = out-CSR slot
@@ -613,8 +707,9 @@ void launch_topo(const DJob *jobs, int njobs, const DGraph *graphs, const DPrep 
 // under `limit` bytes, else bitsets only (counters in HBM), else none.
 size_t topo_smem_bytes(int V, size_t limit) {
   const size_t nw = (static_cast<size_t>(V) + 31) / 32;
-  const size_t full = 4 * (3 * nw + 2 * static_cast<size_t>(V));
-  if (full <= limit) return full;
+  // bitsets + counters, or (identity order) finish times + devices
+  const size_t full = std::max(4 * (3 * nw + 2 * static_cast<size_t>(V)), 18 * static_cast<size_t>(V) + 16);
+  if (full <= limit) return (full + 15) & ~size_t(15);
   return 12 * nw <= limit ? 12 * nw : 0;
 }
 
