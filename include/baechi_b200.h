@@ -305,6 +305,15 @@ typedef struct {
 int bx_lp_solve(const bx_graph *graph, const bx_comm *cm, double tolerance, double *x, double *s,
                 bx_lp_info *info, char *msg, int msglen);
 
+/* oracle_makespan (oracle.hpp:29-34, oracle.cpp:17-212): the exact minimum
+ * makespan over every canonical device assignment and every DAG-consistent
+ * per-device execution order, each scored by the GPU simulator in batches.
+ * capacity < 0: none (OracleLimits / prepare() limits and error texts;
+ * BX_INFEASIBLE when nothing fits or the instance is too large). */
+int bx_oracle_makespan(const bx_graph *graph, int32_t n, const bx_comm *cm, int64_t capacity, int32_t mem_mode,
+                       int32_t max_nodes, int32_t max_devices, int64_t max_extensions, int64_t *out_us,
+                       char *msg, int msglen);
+
 /* bx_round_extract == round_and_extract (lp.hpp:88-90, lp.cpp:280-326) on
  * the device (K3): x[E] per meta edge, threshold in (0, 0.5).
  * stats2 = {favorite_edges, repaired_nodes}. */

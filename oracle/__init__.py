@@ -155,6 +155,8 @@ class Ref:
             L.ref_place_batch_full.argtypes = [C.c_int32, C.POINTER(C.c_void_p), _i32p, _i32p, _i64p, C.c_int32,
                                                C.c_double, C.c_double, C.c_int32, C.c_int32, _i64p, _i64p, _i32p,
                                                _i64p, _i32p, _i32p, _i64p, _i32p, C.POINTER(C.c_int64)]
+            L.ref_oracle_makespan.argtypes = [vp, C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_int64, C.c_int32,
+                                              C.c_int32, C.c_int32, C.c_int64, i64p, cp, ip]
             cls._lib = L
         return cls._lib
 
@@ -336,6 +338,19 @@ class Ref:
     @classmethod
     def bench_capacity(cls, rg, n, factor):
         return cls.lib().ref_bench_capacity(rg.h, n, factor)
+
+    @classmethod
+    def oracle_makespan(cls, rg, n, cm, capacity=None, mem_mode=1, max_nodes=12, max_devices=3,
+                        max_extensions=200000):
+        """oracle_makespan (oracle.cpp:185-212)."""
+        out = C.c_int64()
+        err = C.create_string_buffer(_ERRLEN)
+        rc = cls.lib().ref_oracle_makespan(rg.h, n, cm[0], cm[1], cm[2], -1 if capacity is None else capacity,
+                                           mem_mode, max_nodes, max_devices, max_extensions, C.byref(out), err,
+                                           _ERRLEN)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return out.value
 
     @classmethod
     def critical_path(cls, rg):

@@ -38,6 +38,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -46,6 +47,7 @@
 #include "dagsched/generator.hpp"
 #include "dagsched/graph.hpp"
 #include "dagsched/lp.hpp"
+#include "dagsched/oracle.hpp"
 #include "dagsched/placers.hpp"
 #include "dagsched/simulator.hpp"
 #include "dagsched/transforms.hpp"
@@ -617,6 +619,23 @@ int ref_place_batch_full(int32_t count, void* const* graphs, const int32_t* algo
   auto t1 = std::chrono::steady_clock::now();
   *wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
   return 0;
+}
+
+// oracle_makespan (proj/src/oracle.cpp:185-212). capacity < 0: none.
+int ref_oracle_makespan(void* h, int32_t n, double intercept, double per_byte, int32_t mode,
+                        int64_t capacity, int32_t mem_mode, int32_t max_nodes, int32_t max_devices,
+                        int64_t max_extensions, int64_t* out, char* err, int errlen) {
+  auto* rg = static_cast<RefGraph*>(h);
+  return guarded(err, errlen, [&] {
+    OracleLimits lim;
+    lim.max_nodes = max_nodes;
+    lim.max_devices = max_devices;
+    lim.max_extensions = max_extensions;
+    std::optional<bytes_t> cap;
+    if (capacity >= 0) cap = capacity;
+    *out = oracle_makespan(rg->gg, n, make_cm(intercept, per_byte, mode), cap,
+                           mem_mode == 1 ? MemoryMode::TrainingPersistent : MemoryMode::GraphStatic, lim);
+  });
 }
 
 }  // extern "C"

@@ -180,6 +180,8 @@ def lib():
         L.bx_version.restype = C.c_char_p
         L.bx_last_error.restype = C.c_char_p
         L.bx_last_message.restype = C.c_char_p
+        L.bx_oracle_makespan.argtypes = [C.POINTER(_Graph), i32, C.POINTER(_Comm), i64, i32, i32, i32, i64,
+                                         C.POINTER(i64), cp, C.c_int]
         L.bx_plan_message.argtypes = [_vp, i32, C.c_char_p, i64]
         L.bx_plan_message.restype = i64
         L.bx_device_count.restype = C.c_int
@@ -246,7 +248,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["bx_version", "bx_last_error", "bx_last_message", "bx_plan_message", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
+EXPORTED = ["bx_version", "bx_last_error", "bx_last_message", "bx_plan_message", "bx_oracle_makespan", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
             "bx_plan_create_ex", "bx_plan_job_kernel", "bx_simulate_ex",
             "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download", "bx_plan_result_view",
             "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_kernel_times",
@@ -796,6 +798,24 @@ def critical_path_us(gg: MetaGraph) -> int:
     msg = C.create_string_buffer(4096)
     g = gg._c()
     rc = lib().bx_critical_path_us(C.byref(g), C.byref(out), msg, 4096)
+    _raise(rc, msg.value.decode())
+    return out.value
+
+
+def oracle_makespan(gg: MetaGraph, device_count: int, cm: CommModel, capacity=None,
+                    mode: int = TRAINING_PERSISTENT, max_nodes: int = 12, max_devices: int = 3,
+                    max_extensions: int = 200000) -> int:
+    """oracle_makespan (oracle.hpp:29-34): exact minimum makespan over every
+    canonical device assignment and DAG-consistent execution order, each
+    scored by the GPU simulator. Raises InfeasibleError like the reference
+    (too large, nothing fits)."""
+    out = C.c_int64()
+    msg = C.create_string_buffer(4096)
+    g = gg._c()
+    cmc = cm._c()
+    rc = lib().bx_oracle_makespan(C.byref(g), int(device_count), C.byref(cmc), -1 if capacity is None else int(capacity),
+                                  int(mode), int(max_nodes), int(max_devices), int(max_extensions), C.byref(out),
+                                  msg, 4096)
     _raise(rc, msg.value.decode())
     return out.value
 

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <new>
 #include <string>
@@ -1543,3 +1544,201 @@ int bx_round_extract(int32_t V, int32_t E, const int32_t *esrc, const int32_t *e
 }
 
 }  // extern "C"
+
+// ---- exhaustive oracle (oracle.hpp:29-34, oracle.cpp:17-212) ---------------------
+// The exact minimum makespan over every canonical device assignment and every
+// DAG-consistent global order (restricted per device), each pair scored by
+// the GPU simulator (K4 / K4f) in batches of one plan: the placements are
+// written into the plan's output region, simulated, and a reduction kernel
+// keeps the batch minimum. Pruning as the reference (static memory, the
+// assignment's load floor, the global lower bound) only skips pairs that
+// cannot change the minimum.
+namespace bx {
+__global__ void k_oracle_min(const DSim *sims, int count, unsigned long long *best, unsigned int *bad) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    const DSim &d = sims[i];
+    const int st = d.err->status;
+    if (st == kOk) atomicMin(best, static_cast<unsigned long long>(*d.makespan));
+    else if (!(st == kInfeasible && d.err->code == E_SIM_MEMORY)) atomicAdd(bad, 1u);  // memory: skipped
+  }
+}
+}  // namespace bx
+
+extern "C" int bx_oracle_makespan(const bx_graph *graph, int32_t n, const bx_comm *cm, int64_t capacity,
+                                  int32_t mem_mode, int32_t max_nodes, int32_t max_devices, int64_t max_extensions,
+                                  int64_t *out_us, char *msg, int msglen) {
+  *out_us = 0;
+  const int V = graph->V;
+  if (V > max_nodes) {
+    put_msg(msg, msglen, "instance too large: " + std::to_string(V) + " nodes > " + std::to_string(max_nodes));
+    return BX_INFEASIBLE;
+  }
+  if (n < 1 || n > max_devices) {
+    put_msg(msg, msglen, "instance too large: " + std::to_string(n) + " devices > " + std::to_string(max_devices));
+    return BX_INFEASIBLE;
+  }
+  const bool limited = capacity >= 0;
+  const int64_t cap = limited ? capacity : INT64_MAX / 4;
+  // every DAG-consistent global order (enumerate_extensions, oracle.cpp:23-54)
+  std::vector<std::vector<int>> ext;
+  {
+    std::vector<int> pending(V, 0), prefix;
+    for (int e = 0; e < graph->E; ++e) pending[graph->edst[e]]++;
+    bool too_many = false;
+    std::function<void()> rec = [&]() {
+      if (too_many) return;
+      if (static_cast<int>(prefix.size()) == V) {
+        if (static_cast<int64_t>(ext.size()) >= max_extensions) {
+          too_many = true;
+          return;
+        }
+        ext.push_back(prefix);
+        return;
+      }
+      for (int j = 0; j < V && !too_many; ++j) {
+        if (pending[j] != 0) continue;
+        pending[j] = -1;
+        for (int e = graph->out_off[j]; e < graph->out_off[j + 1]; ++e) pending[graph->edst[e]]--;
+        prefix.push_back(j);
+        rec();
+        prefix.pop_back();
+        for (int e = graph->out_off[j]; e < graph->out_off[j + 1]; ++e) pending[graph->edst[e]]++;
+        pending[j] = 0;
+      }
+    };
+    rec();
+    if (too_many) {
+      put_msg(msg, msglen,
+              "instance too large: more than " + std::to_string(max_extensions) + " execution orders to enumerate");
+      return BX_INFEASIBLE;
+    }
+  }
+  // canonical assignments: labels in first-use order (oracle.cpp:58-73)
+  std::vector<std::vector<int>> asg;
+  {
+    std::vector<int> a(V, 0);
+    std::function<void(int, int)> rec = [&](int i, int used) {
+      if (i == V) {
+        asg.push_back(a);
+        return;
+      }
+      const int limit = std::min(n, used + 1);
+      for (int d = 0; d < limit; ++d) {
+        a[i] = d;
+        rec(i + 1, std::max(used, d + 1));
+      }
+    };
+    rec(0, 0);
+  }
+  // lower bound: critical path and the work bound (oracle.cpp:103-105)
+  int64_t cp = 0;
+  {
+    const int rc = bx_critical_path_us(graph, &cp, msg, msglen);
+    if (rc) return rc;
+  }
+  int64_t total = 0;
+  for (int j = 0; j < V; ++j) total += graph->compute_us[j];
+  const int64_t lower = std::max(cp, (total + n - 1) / n);
+  constexpr uint64_t kNone = ~0ull;
+  uint64_t best = kNone;
+  if (ext.empty()) {  // V == 0: one (empty) schedule
+    put_msg(msg, msglen, "");
+    *out_us = 0;
+    return BX_OK;
+  }
+  // one plan, B identical jobs; placements go into its output region
+  const int64_t pairs_total = static_cast<int64_t>(asg.size()) * static_cast<int64_t>(ext.size());
+  const int B = static_cast<int>(std::min<int64_t>(pairs_total, 8192));
+  std::vector<int64_t> caps(n, cap);
+  bx_job j = {};
+  j.graph = 0;
+  j.algo = BX_ALGO_METF;
+  j.n = n;
+  j.capacity = caps.data();
+  j.cm = *cm;
+  std::vector<bx_job> jobs(B, j);
+  bx_plan *P = nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int rc = plan_create(1, graph, B, jobs.data(), dev, nullptr, false, &P, msg, msglen);
+  if (rc) return rc;
+  unsigned long long *dbest = nullptr;
+  unsigned int *dbad = nullptr;
+  char *dscratch = nullptr;
+  if (cudaMalloc(&dscratch, 16) != cudaSuccess) {
+    bx_plan_destroy(P);
+    put_msg(msg, msglen, "CUDA failure in the oracle");
+    return BX_RUNTIME;
+  }
+  dbest = reinterpret_cast<unsigned long long *>(dscratch);
+  dbad = reinterpret_cast<unsigned int *>(dscratch + 8);
+  char *H = static_cast<char *>(P->host_out);
+  int filled = 0;
+  bool failed = false, done = false;
+  auto run_batch = [&]() {
+    if (filled == 0 || failed) return;
+    for (int i = filled; i < B; ++i)  // unused slots repeat the first pair of the batch
+      std::memcpy(H + P->out_off[i].dev, H + P->out_off[0].dev, 4 * size_t(V)),
+          std::memcpy(H + P->out_off[i].eo, H + P->out_off[0].eo, 4 * size_t(V)),
+          std::memcpy(H + P->out_off[i].eoff, H + P->out_off[0].eoff, 4 * size_t(n + 1));
+    unsigned long long init[2] = {kNone, 0};
+    if (cudaMemcpy(P->dev_out, H, P->out_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(dscratch, init, 16, cudaMemcpyHostToDevice) != cudaSuccess ||
+        bx_plan_simulate(P, mem_mode, nullptr) != BX_OK) {
+      failed = true;
+      return;
+    }
+    bx::k_oracle_min<<<(B + 255) / 256, 256>>>(P->ds_dev, B, dbest, dbad);
+    unsigned long long res[2];
+    if (cudaMemcpy(res, dscratch, 16, cudaMemcpyDeviceToHost) != cudaSuccess || (res[1] & 0xffffffffull)) {
+      failed = true;
+      return;
+    }
+    best = std::min<uint64_t>(best, res[0]);
+    filled = 0;
+    if (best != kNone && static_cast<int64_t>(best) <= lower) done = true;
+  };
+  std::vector<int64_t> need(n), load(n);
+  for (size_t a = 0; a < asg.size() && !done && !failed; ++a) {
+    const std::vector<int> &as = asg[a];
+    if (limited) {  // static memory (perm) before anything runs (oracle.cpp:118-128)
+      std::fill(need.begin(), need.end(), 0);
+      for (int v = 0; v < V; ++v) need[as[v]] += graph->perm_bytes[v];
+      bool over = false;
+      for (int d = 0; d < n; ++d) over |= need[d] > cap;
+      if (over) continue;
+    }
+    std::fill(load.begin(), load.end(), 0);
+    for (int v = 0; v < V; ++v) load[as[v]] += graph->compute_us[v];
+    const int64_t floor_a = std::max(lower, *std::max_element(load.begin(), load.end()));
+    if (best != kNone && floor_a >= static_cast<int64_t>(best)) continue;  // cannot beat the incumbent
+    for (size_t x = 0; x < ext.size() && !done && !failed; ++x) {
+      const bx_plan::OOff &o = P->out_off[filled];
+      int32_t *dv = reinterpret_cast<int32_t *>(H + o.dev), *eo = reinterpret_cast<int32_t *>(H + o.eo),
+              *eoff = reinterpret_cast<int32_t *>(H + o.eoff);
+      std::fill(eoff, eoff + n + 1, 0);
+      for (int v = 0; v < V; ++v) {
+        dv[v] = as[v];
+        eoff[as[v] + 1]++;
+      }
+      for (int d = 0; d < n; ++d) eoff[d + 1] += eoff[d];
+      std::vector<int> at(eoff, eoff + n);
+      for (int v : ext[x]) eo[at[as[v]]++] = v;
+      if (++filled == B) run_batch();
+    }
+  }
+  run_batch();
+  cudaFree(dscratch);
+  bx_plan_destroy(P);
+  if (failed) {
+    put_msg(msg, msglen, "CUDA failure or unexpected simulator error in the oracle");
+    return BX_RUNTIME;
+  }
+  if (best == kNone) {
+    put_msg(msg, msglen, "no device assignment fits the memory capacities");
+    return BX_INFEASIBLE;
+  }
+  *out_us = static_cast<int64_t>(best);
+  put_msg(msg, msglen, "");
+  return BX_OK;
+}

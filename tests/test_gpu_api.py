@@ -212,3 +212,60 @@ def test_plan_simulate_skips_jobs_without_placement(bx):
         for i in (1, 2, 3):
             assert reps[i] == (2, "placement must assign every node exactly once")
     plan.close()
+
+
+def _tiny_dag(rng, V, p=0.35):
+    src, dst = [], []
+    for a in range(V):
+        for b in range(a + 1, V):
+            if rng.random() < p:
+                src.append(a)
+                dst.append(b)
+    o = np.lexsort((dst, src))
+    src, dst = np.array(src, np.int32)[o], np.array(dst, np.int32)[o]
+    tensor = rng.integers(1, 4000, V)
+    return dict(V=V, E=len(src), k=rng.integers(10, 121, V), temp=rng.integers(0, 50, V),
+                perm=rng.integers(1, 100, V), out=rng.integers(1, 100, V), esrc=src, edst=dst,
+                ebytes=tensor[src].astype(np.int64) if len(src) else np.zeros(0, np.int64))
+
+
+@needs_ref
+def test_oracle_makespan_vs_reference(bx):
+    """The exhaustive oracle (oracle.cpp:185-212) on the GPU simulator vs the
+    reference's own oracle_makespan: tiny DAGs, 1-3 devices, both comm
+    modes, both memory modes, no / loose / tight capacities (memory-skipped
+    assignments, and nothing fitting), error texts included."""
+    rng = np.random.default_rng(21)
+    cases = 0
+    for t in range(14):
+        V = int(rng.integers(1, 9))
+        g = _tiny_dag(rng, V)
+        gg = bx.MetaGraph.from_dict(g)
+        rg = Ref.graph(W.as_ref_base(g), pipeline=-1)
+        need = g["perm"] + g["out"] + g["temp"]
+        for n in (1, 2, 3):
+            for cm in ((3.0, 0.01, 1), (2.0, 0.02, 0)):
+                for cap in (None, int(need.sum()), int(need.max() + need.min())):
+                    mm = int(rng.integers(0, 2))
+                    try:
+                        o = Ref.oracle_makespan(rg, n, cm, cap, mm)
+                        oe = None
+                    except OracleError as e:
+                        o, oe = None, (e.kind, str(e))
+                    try:
+                        p = bx.oracle_makespan(gg, n, bx.CommModel(*cm), cap, mm)
+                        pe = None
+                    except bx.Error as e:
+                        p, pe = None, (e.kind, e.msg)
+                    assert (p, pe) == (o, oe), (t, n, cm, cap, mm)
+                    cases += 1
+    assert cases == 14 * 3 * 2 * 3
+    g = _tiny_dag(rng, 13)
+    with pytest.raises(bx.InfeasibleError, match="instance too large: 13 nodes > 12"):
+        bx.oracle_makespan(bx.MetaGraph.from_dict(g), 2, bx.CommModel(1.0, 0.0, 1))
+    g = _tiny_dag(rng, 6)
+    with pytest.raises(bx.InfeasibleError, match="instance too large: 4 devices > 3"):
+        bx.oracle_makespan(bx.MetaGraph.from_dict(g), 4, bx.CommModel(1.0, 0.0, 1))
+    g = _tiny_dag(rng, 8, p=0.05)
+    with pytest.raises(bx.InfeasibleError, match="more than 10 execution orders"):
+        bx.oracle_makespan(bx.MetaGraph.from_dict(g), 2, bx.CommModel(1.0, 0.0, 1), max_extensions=10)
