@@ -1662,6 +1662,11 @@ extern "C" int bx_oracle_makespan(const bx_graph *graph, int32_t n, const bx_com
   cudaGetDevice(&dev);
   int rc = plan_create(1, graph, B, jobs.data(), dev, nullptr, false, &P, msg, msglen);
   if (rc) return rc;
+  if (bx_plan_upload(P, nullptr) != BX_OK) {  // the graph and the capacities
+    bx_plan_destroy(P);
+    put_msg(msg, msglen, "CUDA failure in the oracle");
+    return BX_RUNTIME;
+  }
   unsigned long long *dbest = nullptr;
   unsigned int *dbad = nullptr;
   char *dscratch = nullptr;
