@@ -321,17 +321,47 @@ def main():
         raise RuntimeError(f"problems failed: {[plan.status(i) for i in fails[:3]]}")
 
     # ---- device-resident timed region -----------------------------------
+    # serial: one plan, steps back to back (the placer-kernel events of these
+    # steps give the roofline's kernel time)
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        plan.place(sp)
+    ev1.record(stream)
+    ev1.synchronize()
+    serial_ms = ev0.elapsed_time(ev1)
+    kernel_ms = plan.kernel_times(args.steps)
+    # pipelined (one process per GPU): two plans on two streams, steps
+    # alternating, so one step's last long problems share the GPU with the
+    # next step's first ones; the clock runs from the first launch to the
+    # later of the two streams' last
+    if dist is None:
+        plan2 = bx.Plan(mgs, bjobs, device=local)
+        st2 = torch.cuda.Stream()
+        sp2 = st2.cuda_stream
+        plan2.upload(sp2)
+        for _ in range(max(args.warmup, 1)):
+            plan2.place(sp2)
+        plan2.download(sp2)
+        lanes = [(plan, sp), (plan2, sp2)]
     barrier()
     with Clocks(local) as clk:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for _ in range(args.steps):
-            plan.place(sp)
-        ev1.record(stream)
-        ev1.synchronize()
-        dev_ms = ev0.elapsed_time(ev1)
-    kernel_ms = plan.kernel_times(args.steps)  # placer-kernel events of the same steps
+        if dist is None:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev2 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            st2.wait_event(ev0)
+            for i in range(args.steps):
+                lanes[i % 2][0].place(lanes[i % 2][1])
+            ev1.record(stream)
+            ev2.record(st2)
+            torch.cuda.synchronize()
+            dev_ms = max(ev0.elapsed_time(ev1), ev0.elapsed_time(ev2))
+        else:
+            dev_ms = serial_ms
     barrier()
     rank_ms = dev_ms / args.steps
     busy = [rank_ms]
@@ -345,17 +375,23 @@ def main():
     value = P / (ms_step / 1e3)
 
     # ---- end to end through the C ABI with host buffers --------------------
+    # one process per GPU: the same two plans, so step i+1's upload and
+    # placement overlap step i's download (every step still moves its inputs
+    # host->device and its whole output region device->host, pinned)
     barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        plan.upload(sp)
-        plan.place(sp)
+    for i in range(args.steps):
         if dist is not None:
+            plan.upload(sp)
+            plan.place(sp)
             got = gather()
             if rank == 0:
                 plan.download(sp)
         else:
-            plan.download(sp)
+            p_, s_ = lanes[i % 2]
+            p_.upload(s_)  # waits for this plan's previous step (the other one keeps the GPU busy)
+            p_.place(s_)
+            p_.download_async(s_)
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3
     barrier()
@@ -455,8 +491,15 @@ def main():
                 "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": config,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "note": "rank 0's numbers; each rank uploads its shard, rank 0 downloads all"
-                                if world > 1 else "upload + place + download per step"},
+                                if world > 1 else "upload + place + download per step; two plans on two streams "
+                                                  "overlap step i+1's upload/placement with step i's download"},
                 "gpu_launches": launches,
+                "pipelining": {"steps_in_flight": 2 if world == 1 else 1,
+                               "serial_value": P / (serial_ms / args.steps / 1e3),
+                               "serial_ms_per_step": serial_ms / args.steps,
+                               "note": "value: two plans on two streams, steps alternating (one step's last "
+                                       "long problems share the GPU with the next step's first); serial_value: "
+                                       "one plan, steps back to back"},
                 "ranks": {"busy_ms_per_step": busy, "imbalance": max(busy) / (sum(busy) / len(busy)),
                           "gather_ms": gather_ms},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

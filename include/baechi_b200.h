@@ -214,6 +214,10 @@ int bx_plan_place(bx_plan *plan, void *stream);
  * (caller-allocated arrays sized by each job's V and n). Synchronises
  * `stream`. Returns BX_OK if the copy worked; per-job status is in out[i]. */
 int bx_plan_download(bx_plan *plan, void *stream, bx_placement *out);
+/* The same device->host copy of the output region into the plan's pinned
+ * mirror, enqueued on `stream` only (no wait, no decode): for pipelined
+ * callers that keep two plans in flight. */
+int bx_plan_download_async(bx_plan *plan, void *stream);
 
 /* The outputs of every job live in one device region that bx_plan_download
  * copies (one cudaMemcpyAsync) into a pinned host mirror owned by the plan;

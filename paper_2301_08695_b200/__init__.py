@@ -196,6 +196,7 @@ def lib():
         L.bx_plan_upload.argtypes = [_vp, _vp]
         L.bx_plan_place.argtypes = [_vp, _vp]
         L.bx_plan_download.argtypes = [_vp, _vp, C.POINTER(_Placement)]
+        L.bx_plan_download_async.argtypes = [_vp, _vp]
         L.bx_plan_result_view.argtypes = [_vp, i32, C.POINTER(_Placement)]
         L.bx_plan_launch_count.argtypes = [_vp]
         L.bx_plan_job_kernel.argtypes = [_vp, i32]
@@ -250,7 +251,7 @@ def lib():
 
 EXPORTED = ["bx_version", "bx_last_error", "bx_last_message", "bx_plan_message", "bx_oracle_makespan", "bx_device_count", "bx_comm_time", "bx_build_adjacency", "bx_plan_create",
             "bx_plan_create_ex", "bx_plan_job_kernel", "bx_simulate_ex",
-            "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download", "bx_plan_result_view",
+            "bx_plan_destroy", "bx_plan_upload", "bx_plan_place", "bx_plan_download", "bx_plan_download_async", "bx_plan_result_view",
             "bx_plan_launch_count", "bx_plan_kernel_ms", "bx_plan_kernel_times",
             "bx_plan_output_region", "bx_plan_job_outputs", "bx_plan_profile", "bx_plan_simulate", "bx_plan_sim_download", "bx_place",
             "bx_simulate", "bx_round_extract", "bx_grouped_create", "bx_grouped_view", "bx_grouped_destroy", "bx_lp_solve",
@@ -469,6 +470,10 @@ class Plan:
         o = np.zeros(6, np.int64)
         lib().bx_plan_job_outputs(self.h, i, _ptr(o))
         return o.tolist()
+
+    def download_async(self, stream=None):
+        """The download's device->pinned-host copy, enqueued on `stream` only."""
+        _raise(lib().bx_plan_download_async(self.h, stream), "bx_plan_download_async failed")
 
     def download(self, stream=None):
         """One device->pinned-host copy of every job's placement."""

@@ -932,6 +932,17 @@ int bx_plan_place(bx_plan *P, void *stream) {
 
 int bx_plan_launch_count(const bx_plan *P) { return P->launches; }
 
+// The output region's device->host copy into the pinned mirror, enqueued on
+// `stream` and not waited for (bx_plan_download waits and decodes).
+int bx_plan_download_async(bx_plan *P, void *stream) {
+  cudaSetDevice(P->device);
+  if (P->out_bytes == 0) return BX_OK;
+  return cudaMemcpyAsync(P->host_out, P->dev_out, P->out_bytes, cudaMemcpyDeviceToHost,
+                         static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? BX_OK
+             : BX_RUNTIME;
+}
+
 int bx_plan_job_kernel(bx_plan *P, int32_t job) {
   if (job < 0 || job >= P->njobs) return BX_KERNEL_NONE;
   if (P->dj[job].sdone) {
