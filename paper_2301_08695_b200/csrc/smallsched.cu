@@ -110,7 +110,7 @@ struct SSm {
   uint16_t *nuc;                  // [nucap * n] per non-uniform producer and device: comm time of the
                                   // edge that first brought its tensor there (arrival = finish + it), 0xffff absent
   // ready slots (ns = small_slots(n))
-  int32_t *node, *kk, *inb, *outb, *cnt, *alive, *urg;  // [ns]; cnt = in_cnt | out_cnt << 16
+  int32_t *node, *kk, *inb, *outb, *cnt, *alive, *urg, *favs;  // [ns]; cnt = in_cnt | out_cnt << 16; favs: m-SCT favourite
   int64_t *need;                                        // [ns]
   uint2 *sip;                                           // [ns * kKI] the slot's first parents (in_pack records)
   int32_t *sco;                                         // [ns * kKO] the slot's first children
@@ -133,7 +133,7 @@ __host__ __device__ inline size_t small_smem_bytes(int V, int n, int nucap, int 
   b += size_t(V) * 8 + 2 * ((size_t(V) * 2 + 3) & ~size_t(3)); // info, pending, rpos
   b += (size_t(nucap) * n * 2 + 7) & ~size_t(7);               // nuc
   const size_t ns = static_cast<size_t>(small_slots(n));
-  b += ns * (7 * 4 + 8 + 8 * kKI + 4 * kKO) + size_t(kSPairs) * 4 + 32 * 4;  // slots, caches, dr, cjs
+  b += ns * (8 * 4 + 8 + 8 * kKI + 4 * kKO) + size_t(kSPairs) * 4 + 32 * 4;  // slots, caches, dr, cjs
   b += 7 * 32 * 4 + size_t(nccap) * 4 + small_ncm_words(nucap, n) * 4 + size_t(kSSlots) * 4 + 32 * 4;
   return b + 64;
 }
@@ -165,7 +165,8 @@ __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, i
   m.cnt = p32 + 4 * ns;
   m.alive = p32 + 5 * ns;
   m.urg = p32 + 6 * ns;
-  p32 += 7 * ns;
+  m.favs = p32 + 7 * ns;
+  p32 += 8 * ns;
   m.sco = p32;
   p32 += ns * kKO;
   m.dr = p32;
@@ -281,9 +282,10 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
         if (d != kSDead && !m.excl[q]) {
           const int node = m.node[s];
           int32_t key = max(m.F[q], d);
-          if (kSct) {
+          if (kSct) {  // the three loads issue together
             const int a = m.awf[q];
-            if (a >= 0 && a != node) key = max(key, min(m.awu[q], m.urg[s]));
+            const int32_t fl = min(m.awu[q], m.urg[s]);
+            if (a >= 0 && a != node) key = max(key, fl);
           }
           ck[u] = (static_cast<uint64_t>(static_cast<uint32_t>(key)) << 32) |
                   (static_cast<uint32_t>(node) << 5 | static_cast<uint32_t>(q));
@@ -424,7 +426,7 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
       int got = 0;
       if (lane == 0) {
         m.awf[p] = -1;
-        const int h = __ldg(G.fav + j);
+        const int h = m.favs[s];  // the committed slot's favourite (loaded with the slot)
         // h unplaced: not placed before this round and not committed in it
         if (h >= 0 && sm_dev(m.info[h]) < 0 && !committed_now(m, cm.nc, h)) {
           m.awf[p] = h;
@@ -604,6 +606,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
         m.outb[s] = nd.y;
         m.cnt[s] = nd.z;
         m.alive[s] = alive0;
+        if (kSct) m.favs[s] = __ldg(G.fav + c);
         m.need[s] = (static_cast<int64_t>(nb.y) << 32) | static_cast<uint32_t>(nb.x);
 #pragma unroll
         for (int k = 0; k < kKI; ++k)
@@ -774,6 +777,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
         m.cnt[cs] = m.cnt[src];
         m.alive[cs] = m.alive[src];
         m.urg[cs] = m.urg[src];
+        if (kSct) m.favs[cs] = m.favs[src];
         for (int q = 0; q < n; ++q) m.dr[cs * n + q] = m.dr[src * n + q];
       }
       if (committed_lane) m.rpos[cm.j] = -1;
