@@ -480,7 +480,9 @@ def main():
         try:
             from latency_table import run as run_case
             pg["families"] = [run_case(nm, cpu=not args.no_cpu_baseline)
-                              for nm in ("refchain100k_x4", "grid100k_x8", "wide100k_x16", "layered100k_x64",
+                              for nm in ("refchain100k_x4", "refchain100k_x4_sct", "refchain100k_x8_sct", "grid100k_x8",
+                                         "wide100k_x16",
+                                         "layered100k_x64",
                                          "seq_layered100k_x4", "seq_wide100k_x16", "seq_refchain100k_x4")]
         except Exception as e:
             pg["families"] = {"error": str(e)}

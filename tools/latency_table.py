@@ -32,6 +32,9 @@ CASES = {
     "seq_refchain100k_x4": (lambda: _refchain(100000), 4, "m-etf", 1.5),
     "seq_refchain100k_x8": (lambda: _refchain(100000), 8, "m-etf", 1.5),
     "refchain1M_x64": (lambda: _refchain(1000000), 64, "m-etf", 1.5),
+    "refchain100k_x8_sct": (lambda: _refchain(100000), 8, "m-sct", 1.5),
+    "refchain100k_x4_sct": (lambda: _refchain(100000), 4, "m-sct", 1.5),
+    "seq_refchain100k_x4_sct": (lambda: _refchain(100000), 4, "m-sct", 1.5),
     # sequential comm mode (queues on both endpoints), the survey probe's model {5 us, 0.001 us/B}
     "seq_layered100k_x4": (lambda: W.layered_dag_fast(100, 1000, 3), 4, "m-etf", 1.2),
     "seq_layered100k_x8": (lambda: W.layered_dag_fast(100, 1000, 3), 8, "m-etf", 1.2),
