@@ -1693,10 +1693,11 @@ extern "C" int bx_oracle_makespan(const bx_graph *graph, int32_t n, const bx_com
   bool failed = false, done = false;
   auto run_batch = [&]() {
     if (filled == 0 || failed) return;
-    for (int i = filled; i < B; ++i)  // unused slots repeat the first pair of the batch
-      std::memcpy(H + P->out_off[i].dev, H + P->out_off[0].dev, 4 * size_t(V)),
-          std::memcpy(H + P->out_off[i].eo, H + P->out_off[0].eo, 4 * size_t(V)),
-          std::memcpy(H + P->out_off[i].eoff, H + P->out_off[0].eoff, 4 * size_t(n + 1));
+    for (int i = filled; i < B; ++i) {  // unused slots repeat the first pair of the batch
+      std::memcpy(H + P->out_off[i].dev, H + P->out_off[0].dev, 4 * size_t(V));
+      std::memcpy(H + P->out_off[i].eo, H + P->out_off[0].eo, 4 * size_t(V));
+      std::memcpy(H + P->out_off[i].eoff, H + P->out_off[0].eoff, 4 * size_t(n + 1));
+    }
     unsigned long long init[2] = {kNone, 0};
     if (cudaMemcpy(P->dev_out, H, P->out_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(dscratch, init, 16, cudaMemcpyHostToDevice) != cudaSuccess ||
