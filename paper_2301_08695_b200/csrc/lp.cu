@@ -138,13 +138,23 @@ struct Symbolic {
   std::vector<int> colptr, rowidx;  // L in CSC, permuted indices, diagonal first, rows ascending
 };
 
-Symbolic min_degree_symbolic(const std::vector<std::vector<int>> &adj0) {
+// `last`: a vertex adjacent to nearly everything (the makespan variable w,
+// in every completion row) is kept out of the elimination graph — merging
+// its adjacency at every elimination would cost O(V) each — ordered last,
+// and added to every column's structure (a superset: the extra entries stay
+// zero in the factor).
+Symbolic min_degree_symbolic(const std::vector<std::vector<int>> &adj0, int last) {
   Symbolic S;
   const int m = static_cast<int>(adj0.size());
   S.m = m;
   std::vector<std::vector<int>> adj(adj0), lst(m);
+  if (last >= 0) {
+    for (auto &l : adj) l.erase(std::remove(l.begin(), l.end(), last), l.end());
+    adj[last].clear();
+  }
   std::set<std::pair<int, int>> q;
-  for (int v = 0; v < m; ++v) q.insert({static_cast<int>(adj[v].size()), v});
+  for (int v = 0; v < m; ++v)
+    if (v != last) q.insert({static_cast<int>(adj[v].size()), v});
   std::vector<char> gone(m, 0);
   std::vector<int> merged;
   S.perm.reserve(m);
@@ -179,6 +189,7 @@ Symbolic min_degree_symbolic(const std::vector<std::vector<int>> &adj0) {
       q.insert({static_cast<int>(adj[u].size()), u});
     }
   }
+  if (last >= 0) S.perm.push_back(last);
   S.iperm.assign(m, 0);
   for (int k = 0; k < m; ++k) S.iperm[S.perm[k]] = k;
   S.colptr.assign(m + 1, 0);
@@ -187,6 +198,7 @@ Symbolic min_degree_symbolic(const std::vector<std::vector<int>> &adj0) {
     std::vector<int> rows;
     rows.reserve(lst[v].size());
     for (int u : lst[v]) rows.push_back(S.iperm[u]);
+    if (last >= 0 && v != last) rows.push_back(m - 1);
     std::sort(rows.begin(), rows.end());
     S.rowidx.push_back(k);
     S.rowidx.insert(S.rowidx.end(), rows.begin(), rows.end());
@@ -632,6 +644,17 @@ extern "C" int bx_lp_solve(const bx_graph *graph, const bx_comm *cm, double tole
         put("comm_time: negative byte count");
         return BX_VALIDATION;
       }
+    {
+      // keep freed LP buffers in the stream-ordered pool (repeated solves
+      // then allocate without going back to the driver)
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    }
     const auto t_host0 = std::chrono::steady_clock::now();
     const Lp lp = build_lp(*graph, *cm);
     const int nv = lp.nvars(), nr = static_cast<int>(lp.rows.size());
@@ -701,7 +724,7 @@ extern "C" int bx_lp_solve(const bx_graph *graph, const bx_comm *cm, double tole
       std::sort(l.begin(), l.end());
       l.erase(std::unique(l.begin(), l.end()), l.end());
     }
-    const Symbolic S = min_degree_symbolic(adj);
+    const Symbolic S = min_degree_symbolic(adj, lp.w_var());
     adj.clear();
     adj.shrink_to_fit();
     // normal-matrix entries (lower triangle, permuted) -> L positions, each
