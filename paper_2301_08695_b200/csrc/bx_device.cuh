@@ -115,6 +115,7 @@ struct DJob {
   // its error); the general kernels then skip it. Null: not a K2s job.
   int32_t *sdone;
   int32_t nucap;  // K2s shared-memory slots reserved for non-uniform producers
+  int32_t nocache;  // parallel comm, every producer uniform in bytes: no cache (Ctx::nocache)
   int32_t maxin;  // largest in-degree of the graph (K2s list sizing)
 };
 

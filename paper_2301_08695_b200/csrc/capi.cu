@@ -716,7 +716,10 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
         P->max_vn = std::max(P->max_vn, int64_t(G.V) * J.n);
       }
     }
-    P->fills.push_back({d.cache, 0xffffffffu, 8 * size_t(V * n)});
+    // parallel comm, every producer sends the same bytes on all its
+    // out-edges: the list placers never touch the cache (DJob::nocache)
+    d.nocache = J.algo != BX_ALGO_MTOPO && J.cm.mode == BX_COMM_PARALLEL && g_nu[J.graph] == 0;
+    if (!d.nocache) P->fills.push_back({d.cache, 0xffffffffu, 8 * size_t(V * n)});
     P->fills.push_back({d.dead, 0, size_t(V * n)});
     P->fills.push_back({d.sc_gen, 0, 4 * size_t(256 * n)});
     if (d.skip) {  // the status record carries the host verdict (message kept host-side)

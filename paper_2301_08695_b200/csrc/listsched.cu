@@ -76,6 +76,14 @@ constexpr int kDirty = 1, kComplete = 2;
 __device__ __forceinline__ int64_t key_of(const Ctx &c, int j, int q, int32_t &gen) {
   const int b = c.in_off[j], e = c.in_off[j + 1];
   const int n = c.n;
+  if (c.mode == 1 && c.nocache) {
+    int64_t t = 0;
+    for (int x = b; x < e; ++x) {
+      const int64_t f = c.pfin[x];
+      t = max64(t, c.pdev[x] == q ? f : f + c.in_c[x]);
+    }
+    return t;
+  }
   if (c.mode == 1) {
     int64_t t = 0;
     int x = b;
@@ -497,6 +505,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
   c.cmax = *pr.cmax;
   c.Kc = jb.K;
   c.cache = jb.cache;
+  c.nocache = jb.nocache != 0;
   c.finish = jb.finish;
   c.urg_s = jb.urgent;
   c.start = jb.start;
@@ -911,7 +920,9 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
     // ---- commit (placers.cpp:221-233) ------------------------------------
     const int64_t fin = t + kj;
     int ncount = 0;
-    if (c.mode == 1) {
+    if (c.mode == 1 && c.nocache) {
+      // no cache: nothing to record, no consumer to re-key
+    } else if (c.mode == 1) {
       // commit_schedulable_time, parallel mode: every remote uncached parent
       // tensor lands on p at finish + c_e; order-free, so lanes split parents
       for (int x0 = ib; x0 < ie; x0 += 32) {
@@ -1424,6 +1435,7 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
   c.cmax = *pr.cmax;
   c.Kc = jb.K;
   c.cache = jb.cache;
+  c.nocache = jb.nocache != 0;
   c.finish = jb.finish;
   c.urg_s = jb.urgent;
   c.start = jb.start;
@@ -1960,7 +1972,7 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
         while (inoff[i + 1] <= w) ++i;
         const RCommit &cm = CM[i];
         const int x = cm.inb + (w - inoff[i]);
-        if (c.pdev[x] != cm.q) {
+        if (!c.nocache && c.pdev[x] != cm.q) {
           const int par = c.in_src[x];
           int64_t *slot = c.cache + static_cast<int64_t>(par) * n + cm.q;
           if (*slot < 0) {  // commit_schedulable_time, parallel mode

@@ -12,6 +12,10 @@ constexpr int64_t kInf = INT64_MAX;
 // ---------------------------------------------------------------- K2 ----
 struct Ctx {
   int V, n, mode, sct;
+  // parallel comm on a graph whose every producer sends the same bytes on
+  // all its out-edges: a cache arrival (finish + the same c) never changes a
+  // term, so the cache is neither read nor written
+  bool nocache = false;
   const int64_t *k, *need, *in_c, *cap;
   const int32_t *in_off, *in_src, *out_off, *out_dst, *fav;
   int64_t cmax;
