@@ -331,37 +331,33 @@ def main():
         plan.place(sp)
     ev1.record(stream)
     ev1.synchronize()
-    serial_ms = ev0.elapsed_time(ev1)
+    serial_ms = max_over_ranks(ev0.elapsed_time(ev1))
     kernel_ms = plan.kernel_times(args.steps)
-    # pipelined (one process per GPU): two plans on two streams, steps
-    # alternating, so one step's last long problems share the GPU with the
-    # next step's first ones; the clock runs from the first launch to the
-    # later of the two streams' last
-    if dist is None:
-        plan2 = bx.Plan(mgs, bjobs, device=local)
-        st2 = torch.cuda.Stream()
-        sp2 = st2.cuda_stream
-        plan2.upload(sp2)
-        for _ in range(max(args.warmup, 1)):
-            plan2.place(sp2)
-        plan2.download(sp2)
-        lanes = [(plan, sp), (plan2, sp2)]
+    # pipelined: two plans on two streams (every rank), steps alternating, so
+    # one step's last long problems share the GPU with the next step's first
+    # ones; the clock runs from the first launch to the later of the two
+    # streams' last
+    plan2 = bx.Plan(mgs, bjobs, device=local)
+    st2 = torch.cuda.Stream()
+    sp2 = st2.cuda_stream
+    plan2.upload(sp2)
+    for _ in range(max(args.warmup, 1)):
+        plan2.place(sp2)
+    plan2.download(sp2)
+    lanes = [(plan, sp), (plan2, sp2)]
     barrier()
     with Clocks(local) as clk:
-        if dist is None:
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            ev2 = torch.cuda.Event(enable_timing=True)
-            ev0.record(stream)
-            st2.wait_event(ev0)
-            for i in range(args.steps):
-                lanes[i % 2][0].place(lanes[i % 2][1])
-            ev1.record(stream)
-            ev2.record(st2)
-            torch.cuda.synchronize()
-            dev_ms = max(ev0.elapsed_time(ev1), ev0.elapsed_time(ev2))
-        else:
-            dev_ms = serial_ms
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev2 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        st2.wait_event(ev0)
+        for i in range(args.steps):
+            lanes[i % 2][0].place(lanes[i % 2][1])
+        ev1.record(stream)
+        ev2.record(st2)
+        torch.cuda.synchronize()
+        dev_ms = max(ev0.elapsed_time(ev1), ev0.elapsed_time(ev2))
     barrier()
     rank_ms = dev_ms / args.steps
     busy = [rank_ms]
@@ -496,7 +492,7 @@ def main():
                                 if world > 1 else "upload + place + download per step; two plans on two streams "
                                                   "overlap step i+1's upload/placement with step i's download"},
                 "gpu_launches": launches,
-                "pipelining": {"steps_in_flight": 2 if world == 1 else 1,
+                "pipelining": {"steps_in_flight": 2,
                                "serial_value": P / (serial_ms / args.steps / 1e3),
                                "serial_ms_per_step": serial_ms / args.steps,
                                "note": "value: two plans on two streams, steps alternating (one step's last "
