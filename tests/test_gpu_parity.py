@@ -510,3 +510,37 @@ def W_levels(h):
             if indeg[c] == 0:
                 stack.append(c)
     return lvl
+
+
+@pytest.mark.parametrize("kernel", ["warp", "rounds"])
+@pytest.mark.parametrize("mix", ["all", "some"])
+def test_transfer_cache_paths_vs_oracle(bx, kernel, mix):
+    """Parallel comm with producers whose out-edges carry DIFFERENT byte
+    counts: the warp and round kernels keep the transfer cache, record
+    arrivals and re-key consumers (only for those producers: uniform ones are
+    skipped), against the C restatement. `all`: every edge random; `some`:
+    a quarter of the producers mixed, the rest uniform."""
+    opts = {"warp": {"wide_min_vn": (1 << 31) - 1, "no_small_frontier": 1},
+            "rounds": {"wide_min_vn": 0, "no_small_frontier": 1}}[kernel]
+    rng = np.random.default_rng(3 if mix == "all" else 4)
+    for gi, g in enumerate((W.layered_dag(8, 12, 1), W.branchy(6, 2), W.wide_random(150, 3), W.grid_chain(20, 6, 4))):
+        m = dict(W.as_meta_dict(g))
+        if mix == "all":
+            m["ebytes"] = rng.integers(1, 200_000, len(m["esrc"])).astype(np.int64)
+        else:
+            eb = np.asarray(m["ebytes"]).copy()
+            mixed = rng.random(m["V"]) < 0.25
+            sel = mixed[np.asarray(m["esrc"])]
+            eb[sel] = rng.integers(1, 200_000, int(sel.sum()))
+            m["ebytes"] = eb
+        gg = _meta(bx, m)
+        fav = golden_cases.fav_first(m)
+        for n in (2, 5, 12):
+            cap = int(np.ceil(((m["perm"] + m["out"] + m["temp"]).sum() / n
+                               + (m["perm"] + m["out"] + m["temp"]).max()) * 1.3))
+            for cm in ((12.5, 0.002, 1), (40.0, 0.01, 1)):
+                for algo in (1, 2):
+                    fv = fav if algo == 2 else None
+                    o = Restate.place(m, algo, [cap] * n, cm, fv)
+                    p = bx._one(gg, ALGO[algo], [cap] * n, bx.CommModel(*cm), fv, options=opts)
+                    _assert_same(p, o)
