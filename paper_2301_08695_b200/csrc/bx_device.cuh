@@ -83,7 +83,7 @@ struct DPrep {
   int32_t *nu;        // [V] index of a producer whose out-edges carry different comm times, else -1
   int32_t *nu_count;  // number of such producers
   int32_t *cbad;      // some comm time outside [0, 2^16 - 1)
-  int4 *node_pack;    // [2V] in_b, out_b, in_cnt | out_cnt << 16, k (int32); need (int64), 0, 0
+  int4 *node_pack;    // [V] in_b, out_b, in_cnt | out_cnt << 16, k (int32) (needs from the graph's need[])
   uint2 *in_pack;     // [E] per in-CSR slot: parent, (nu(parent) + 1) << 16 | comm time
 };
 

@@ -404,7 +404,7 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     pso[pi].cnt = L.take<int32_t>(2);
     // K2s runs only in plans of at most 148 list jobs (`few` below)
     const bool few_jobs = std::count_if(jobs, jobs + njobs, [](const bx_job &J) { return J.algo != BX_ALGO_MTOPO; }) <= 148;
-    pso[pi].npk = L.take<int4>(few_jobs ? 2 * size_t(graphs[g].V) : 1);
+    pso[pi].npk = L.take<int4>(few_jobs ? size_t(graphs[g].V) : 1);
     pso[pi].ipk = L.take<uint2>(few_jobs ? graphs[g].E : 1);
   }
   struct JOff {

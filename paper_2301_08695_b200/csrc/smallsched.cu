@@ -474,9 +474,10 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
   if (threadIdx.x >= 32) {
     const int tid = threadIdx.x - 32, nt = 32 * (kSWarm - 1);
     const size_t V = static_cast<size_t>(g.V), E = static_cast<size_t>(g.E);
-    unsigned acc = warm_l1(pr.node_pack, 32 * V, tid, nt) ^ warm_l1(pr.in_pack, 8 * E, tid, nt);
+    unsigned acc = warm_l1(pr.node_pack, 16 * V, tid, nt) ^ warm_l1(pr.in_pack, 8 * E, tid, nt);
+    acc ^= warm_l1(g.need, 8 * V, tid, nt);
     acc ^= warm_l1(g.edst, 4 * E, tid, nt);
-    acc ^= warm_l1(g.need_order, 4 * V, tid, nt);
+    // (need_order is read only when a pair is discarded: not warmed)
     if (kSct && jb.fav) acc ^= warm_l1(jb.fav, 4 * V, tid, nt);
     asm volatile("" ::"r"(acc));  // keeps the loads
     return;
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     const int j = base + lane;
     bool src = false;
     if (j < V) {
-      const int4 nd = __ldg(G.node + 2 * j);
+      const int4 nd = __ldg(G.node + j);
       const int indeg = nd.z & 0xffff;
       m.info[j] = 0xffffffffull;
       m.pending[j] = static_cast<uint16_t>(indeg);
@@ -588,8 +589,8 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       for (int sl = lane; sl < nnew; sl += 32) {
         const int s = R0 + sl;
         const int c = m.newn[sl];
-        const int4 nd = __ldg(G.node + 2 * c);
-        const int4 nb = __ldg(G.node + 2 * c + 1);
+        const int4 nd = __ldg(G.node + c);
+        const int64_t nneed = __ldg(G.need + c);
         const int ci = nd.z & 0xffff, co = nd.z >> 16;
         uint2 pa[kKI];
         int ch[kKO];
@@ -607,7 +608,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
         m.cnt[s] = nd.z;
         m.alive[s] = alive0;
         if (kSct) m.favs[s] = __ldg(G.fav + c);
-        m.need[s] = (static_cast<int64_t>(nb.y) << 32) | static_cast<uint32_t>(nb.x);
+        m.need[s] = nneed;
 #pragma unroll
         for (int k = 0; k < kKI; ++k)
           if (k < ci) m.sip[s * kKI + k] = pa[k];
@@ -615,7 +616,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
         for (int k = 0; k < kKO; ++k)
           if (k < co) {
             m.sco[s * kKO + k] = ch[k];
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(G.node + 2 * ch[k]));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(G.node + ch[k]));
           }
       }
       __syncwarp();
@@ -721,7 +722,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
         unsigned *word = reinterpret_cast<unsigned *>(m.pending) + (child >> 1);
         const int sh = 16 * (child & 1);
         ready = ((atomicSub(word, 1u << sh) >> sh) & 0xffffu) == 1;
-        if (ready) asm volatile("prefetch.global.L1 [%0];" ::"l"(G.node + 2 * child));
+        if (ready) asm volatile("prefetch.global.L1 [%0];" ::"l"(G.node + child));
       }
       if (hin) {
         const uint2 e = slot_parent(m, G, iti >> 16, iti & 0xffff);
@@ -873,9 +874,7 @@ __global__ void k_prep_small(DGraph g, DPrep pr) {
     pr.nu[i] = uni ? -1 : atomicAdd(pr.nu_count, 1);
     const int ib = g.in_off[i], ie = g.in_off[i + 1];
     const int64_t k = g.k[i];
-    const int64_t need = g.need[i];
-    pr.node_pack[2 * i] = make_int4(ib, b, (ie - ib) | ((e - b) << 16), static_cast<int32_t>(k));
-    pr.node_pack[2 * i + 1] = make_int4(static_cast<int32_t>(need), static_cast<int32_t>(need >> 32), 0, 0);
+    pr.node_pack[i] = make_int4(ib, b, (ie - ib) | ((e - b) << 16), static_cast<int32_t>(k));
   }
   if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(pr.cbad, 1);
 }
