@@ -31,8 +31,8 @@ void launch_placers(const DJob *jobs, const int32_t *order, int n_small, int n_e
                     int list_len, cudaStream_t s_small, cudaStream_t s_big);
 void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn, int force_cap, cudaStream_t s);
 void launch_prep_small(const DGraph &g, const DPrep &pr, cudaStream_t s);
-void launch_small_frontier(const DJob *jobs, const int32_t *order, int n_etf, int n_sct, const DGraph *graphs,
-                           const DPrep *preps, size_t smem, bool prof, cudaStream_t s);
+void launch_small_frontier(const DJob *jobs, const int32_t *order, const int *cnt, const DGraph *graphs,
+                           const DPrep *preps, const size_t *smem, bool prof, cudaStream_t s);
 size_t small_smem_bytes_host(int V, int n, int nucap, int nccap);
 size_t topo_smem_bytes(int V, size_t limit);
 void launch_topo(const DJob *jobs, int njobs, const DGraph *graphs, const DPrep *preps, size_t smem_bytes,
@@ -103,8 +103,10 @@ struct bx_plan {
   DJob *dj_dev = nullptr;
   int32_t *order_dev = nullptr;     // launch lists: small | big parallel | big sequential
   int n_small = 0, n_etf = 0, n_bpar = 0, n_bseq = 0;  // n_etf: leading parallel m-ETF small jobs
-  int n_sf_etf = 0, n_sf_sct = 0;   // small-frontier (K2s) jobs, launched first
-  size_t sf_smem = 0;
+  int n_sf[4] = {0, 0, 0, 0};       // small-frontier (K2s) jobs, launched first: m-ETF, m-SCT with
+                                    // shared-memory node state, then both with global node state
+  size_t sf_smem[2] = {0, 0};
+  std::vector<char> sf_global;      // job -> K2s with global node state
   size_t topo_smem = 0;  // m-TOPO CTA: bitsets (+ counters) of the largest m-TOPO graph
   int32_t *sf_order_dev = nullptr;
   std::vector<char> prep_small;     // prep index -> K2s extras needed
@@ -617,6 +619,7 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     }
   }
   P->prep_small.assign(P->nprep, 0);
+  P->sf_global.assign(njobs, 0);
   P->dj.resize(njobs);
   if (P->opt.profile == 1) {
     BX_CUDA(cudaMalloc(&P->prof, sizeof(int64_t) * kProfSlots * size_t(njobs)), msg, msglen);
@@ -738,11 +741,15 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     d.maxin = g_maxin[J.graph];
     if (!d.skip && few && J.algo != BX_ALGO_MTOPO && J.cm.mode == BX_COMM_PARALLEL && J.n <= 32 && G.V > 0 &&
         G.V < (1 << 26) && !P->opt.no_small_frontier && P->opt.wide_min_vn < 0) {
-      const size_t sm = small_smem_bytes_host(G.V, J.n, d.nucap, J.n * std::max(1, d.maxin));
-      if (sm <= 200 * 1024) {
+      const int nccap = J.n * std::max(1, d.maxin);
+      const size_t sm = small_smem_bytes_host(G.V, J.n, d.nucap, nccap);
+      const size_t smg = small_smem_bytes_host(0, J.n, d.nucap, nccap);  // node state in HBM
+      const bool glob = sm > 200 * 1024;
+      if (!glob || smg <= 200 * 1024) {
         d.sdone = at<int32_t>(pool, o.sdone);
         P->fills.push_back({d.sdone, 0, 4});
-        P->sf_smem = std::max(P->sf_smem, sm);
+        P->sf_smem[glob] = std::max(P->sf_smem[glob], glob ? smg : sm);
+        P->sf_global[i] = glob;
         P->prep_small[job_prep[i]] = 1;
       }
     }
@@ -759,16 +766,17 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
   P->order_dev = at<int32_t>(pool, otable);
   P->sf_order_dev = at<int32_t>(pool, sftable);
   {
-    std::vector<int32_t> sfe, sfs;
+    std::vector<int32_t> lists[4], all;
     for (int i = 0; i < njobs; ++i) {
       if (!P->dj[i].sdone) continue;
-      (P->dj[i].algo == BX_ALGO_MSCT && P->dj[i].fav ? sfs : sfe).push_back(i);
+      lists[2 * P->sf_global[i] + (P->dj[i].algo == BX_ALGO_MSCT && P->dj[i].fav ? 1 : 0)].push_back(i);
     }
-    P->n_sf_etf = static_cast<int>(sfe.size());
-    P->n_sf_sct = static_cast<int>(sfs.size());
-    sfe.insert(sfe.end(), sfs.begin(), sfs.end());
-    if (!sfe.empty())
-      BX_CUDA(cudaMemcpy(P->sf_order_dev, sfe.data(), 4 * sfe.size(), cudaMemcpyHostToDevice), msg, msglen);
+    for (int k = 0; k < 4; ++k) {
+      P->n_sf[k] = static_cast<int>(lists[k].size());
+      all.insert(all.end(), lists[k].begin(), lists[k].end());
+    }
+    if (!all.empty())
+      BX_CUDA(cudaMemcpy(P->sf_order_dev, all.data(), 4 * all.size(), cudaMemcpyHostToDevice), msg, msglen);
   }
   {
     // three launch lists, each longest-first: small (one warp per job),
@@ -908,10 +916,10 @@ int bx_plan_place(bx_plan *P, void *stream) {
   P->launches += 1;
   const size_t slot = static_cast<size_t>(P->places % static_cast<int64_t>(P->ring0.size()));
   cudaEventRecord(P->ring0[slot], s);
-  if (P->n_sf_etf + P->n_sf_sct > 0) {
-    launch_small_frontier(P->dj_dev, P->sf_order_dev, P->n_sf_etf, P->n_sf_sct, P->dg_dev, P->dp_dev, P->sf_smem,
+  if (P->n_sf[0] + P->n_sf[1] + P->n_sf[2] + P->n_sf[3] > 0) {
+    launch_small_frontier(P->dj_dev, P->sf_order_dev, P->n_sf, P->dg_dev, P->dp_dev, P->sf_smem,
                           P->prof != nullptr, s);
-    P->launches += (P->n_sf_etf > 0) + (P->n_sf_sct > 0);
+    for (int k = 0; k < 4; ++k) P->launches += P->n_sf[k] > 0;
   }
   const bool fork = (P->n_small > 0 && (P->n_bpar + P->n_bseq) > 0) || (P->n_etf > 0 && P->n_small > P->n_etf);
   cudaStream_t sb = fork ? P->s2 : s;

@@ -461,7 +461,12 @@ __device__ __forceinline__ unsigned warm_l1(const void *p, size_t bytes, int tid
 // packed graph the scheduler reads into the SM's L1, then exit.
 constexpr int kSWarm = 4;
 
-template <bool kSct, bool kProf>
+// kGlobal: graphs whose per-node state does not fit one SM's shared memory
+// (the reference's layered-chain at 100k nodes, 16 chains, ...): finish /
+// device, pending counts and ready slots live in the job's HBM scratch
+// (L1/L2-resident), the ready slots, column caches and key rows stay in
+// shared memory, and the graph is not pre-warmed.
+template <bool kSct, bool kProf, bool kGlobal>
 __global__ void __launch_bounds__(32 * kSWarm, 1)
     k_place_small(const DJob *jobs, const int32_t *order, int njobs, const DGraph *graphs, const DPrep *preps) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -472,6 +477,7 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
   const DGraph g = graphs[jb.graph];
   const DPrep pr = preps[jb.prep];
   if (threadIdx.x >= 32) {
+    if (kGlobal) return;
     const int tid = threadIdx.x - 32, nt = 32 * (kSWarm - 1);
     const size_t V = static_cast<size_t>(g.V), E = static_cast<size_t>(g.E);
     unsigned acc = warm_l1(pr.node_pack, 16 * V, tid, nt) ^ warm_l1(pr.in_pack, 8 * E, tid, nt);
@@ -493,11 +499,16 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
   const int64_t cmax64 = *pr.cmax;
   const int nccap = n * (jb.maxin > 1 ? jb.maxin : 1);
   // dynamic eligibility (see the header); otherwise the general kernel runs it
-  if (*pr.cbad || g.flags[2] || *g.ksum < 0 || *pr.nu_count > jb.nucap || n > 32 || V >= 0xffff ||
+  if (*pr.cbad || g.flags[2] || *g.ksum < 0 || *pr.nu_count > jb.nucap || n > 32 || V >= (kGlobal ? (1 << 26) : 0xffff) ||
       cmax64 >= 0xffff || jb.maxin >= 0xffff || *g.ksum + (int64_t(V) + 2) * cmax64 >= int64_t(INT32_MAX))
     return;
   const int32_t cmax = static_cast<int32_t>(cmax64);
-  const SSm m = small_layout(smem, V, n, jb.nucap, nccap);
+  SSm m = small_layout(smem, kGlobal ? 0 : V, n, jb.nucap, nccap);
+  if (kGlobal) {
+    m.info = reinterpret_cast<uint64_t *>(jb.finish);    // [V] int64
+    m.pending = reinterpret_cast<uint16_t *>(jb.pending);  // [V] int32 words hold 2V halves
+    m.rpos = reinterpret_cast<int16_t *>(jb.rpos);
+  }
   SGraph G;
   G.node = pr.node_pack;
   G.inp = pr.in_pack;
@@ -901,27 +912,35 @@ void launch_prep_small(const DGraph &g, const DPrep &pr, cudaStream_t s) {
 size_t small_smem_bytes_host(int V, int n, int nucap, int nccap) { return small_smem_bytes(V, n, nucap, nccap); }
 
 // One CTA per job; `order` lists the K2s jobs, m-ETF first.
-template <bool kSct, bool kProf>
+template <bool kSct, bool kProf, bool kGlobal>
 static void launch_sf(const DJob *jobs, const int32_t *order, int nj, const DGraph *graphs, const DPrep *preps,
                       size_t smem, cudaStream_t s) {
   if (nj <= 0) return;
-  cudaFuncSetAttribute(k_place_small<kSct, kProf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(smem));
+  auto kern = k_place_small<kSct, kProf, kGlobal>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   // the smallest shared-memory carveout that holds the job state: the rest
   // of the unified 256 KB is L1 for the warmed graph
   const int pct = static_cast<int>((smem * 100 + 228 * 1024 - 1) / (228 * 1024));
-  cudaFuncSetAttribute(k_place_small<kSct, kProf>, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 1 ? 1 : pct);
-  k_place_small<kSct, kProf><<<nj, 32 * kSWarm, smem, s>>>(jobs, order, nj, graphs, preps);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 1 ? 1 : pct);
+  kern<<<nj, 32 * kSWarm, smem, s>>>(jobs, order, nj, graphs, preps);
 }
 
-void launch_small_frontier(const DJob *jobs, const int32_t *order, int n_etf, int n_sct, const DGraph *graphs,
-                           const DPrep *preps, size_t smem, bool prof, cudaStream_t s) {
+// `order` lists the K2s jobs in four runs: m-ETF and m-SCT with shared-memory
+// node state, then m-ETF and m-SCT with global node state (counts cnt[4],
+// shared-memory bytes smem[2]: per-node-state and global variants).
+void launch_small_frontier(const DJob *jobs, const int32_t *order, const int *cnt, const DGraph *graphs,
+                           const DPrep *preps, const size_t *smem, bool prof, cudaStream_t s) {
+  const int32_t *o1 = order + cnt[0], *o2 = o1 + cnt[1], *o3 = o2 + cnt[2];
   if (prof) {
-    launch_sf<false, true>(jobs, order, n_etf, graphs, preps, smem, s);
-    launch_sf<true, true>(jobs, order + n_etf, n_sct, graphs, preps, smem, s);
+    launch_sf<false, true, false>(jobs, order, cnt[0], graphs, preps, smem[0], s);
+    launch_sf<true, true, false>(jobs, o1, cnt[1], graphs, preps, smem[0], s);
+    launch_sf<false, true, true>(jobs, o2, cnt[2], graphs, preps, smem[1], s);
+    launch_sf<true, true, true>(jobs, o3, cnt[3], graphs, preps, smem[1], s);
   } else {
-    launch_sf<false, false>(jobs, order, n_etf, graphs, preps, smem, s);
-    launch_sf<true, false>(jobs, order + n_etf, n_sct, graphs, preps, smem, s);
+    launch_sf<false, false, false>(jobs, order, cnt[0], graphs, preps, smem[0], s);
+    launch_sf<true, false, false>(jobs, o1, cnt[1], graphs, preps, smem[0], s);
+    launch_sf<false, false, true>(jobs, o2, cnt[2], graphs, preps, smem[1], s);
+    launch_sf<true, false, true>(jobs, o3, cnt[3], graphs, preps, smem[1], s);
   }
 }
 
