@@ -739,7 +739,9 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     d.sdone = nullptr;
     d.nucap = g_nu[J.graph];
     d.maxin = g_maxin[J.graph];
-    if (!d.skip && few && J.algo != BX_ALGO_MTOPO && J.cm.mode == BX_COMM_PARALLEL && J.n <= 32 && G.V > 0 &&
+    // (64 devices for m-ETF; the kernel takes more than 32 only without cache rows)
+    if (!d.skip && few && J.algo != BX_ALGO_MTOPO && J.cm.mode == BX_COMM_PARALLEL &&
+        J.n <= (J.algo == BX_ALGO_MSCT ? 32 : 64) && G.V > 0 &&
         G.V < (1 << 26) && !P->opt.no_small_frontier && P->opt.wide_min_vn < 0) {
       const int nccap = J.n * std::max(1, d.maxin);
       const size_t sm = small_smem_bytes_host(G.V, J.n, d.nucap, nccap);

@@ -67,6 +67,9 @@ namespace bx {
 
 constexpr int kSP = 16;                  // pairs per lane
 constexpr int kSPairs = 32 * kSP;        // R * n <= 512
+constexpr int kSDev = 64;                // devices (m-ETF on graphs without cache rows; m-SCT and
+                                         // graphs with non-uniform producers: 32)
+constexpr int kSDevBits = 6;             // device field of a packed pair
 constexpr int kSSlots = kSPairs;         // newly-ready list capacity
 constexpr int kKI = 8;                   // parents cached per ready slot (in_pack records)
 constexpr int kKO = 8;                   // children cached per ready slot
@@ -102,8 +105,8 @@ __device__ __forceinline__ void ncm_clear(uint32_t *w, int u, int n) {
 
 // Shared-memory layout of one problem (host: small_smem_bytes).
 struct SSm {
-  int32_t *F, *awf, *awu, *excl;  // [32] per device
-  int64_t *slack;                 // [32] capacity - reserved
+  int32_t *F, *awf, *awu, *excl;  // [kSDev] per device
+  int64_t *slack;                 // [kSDev] capacity - reserved
   uint64_t *info;                 // [V] finish << 32 | device (0xffffffff: unplaced)
   uint16_t *pending;              // [V] parents not yet placed (decremented as 32-bit words)
   int16_t *rpos;                  // [V] ready slot of a node, -1 none
@@ -124,17 +127,17 @@ struct SSm {
   int32_t *nci;         // [nccap] non-uniform producers newly cached this round (nu index)
   uint32_t *ncm;        // bit u * n + p: non-uniform producer u newly reached device p this round
   int32_t *newn;        // [kSSlots] newly ready nodes
-  int32_t *scal;        // [32] exec-order counters
+  int32_t *scal;        // [kSDev] exec-order counters
 };
 
 __host__ __device__ inline size_t small_smem_bytes(int V, int n, int nucap, int nccap) {
   size_t b = 0;
-  b += 32 * 8 + 4 * 32 * 4;                                    // slack, F/awf/awu/excl
+  b += kSDev * 8 + 4 * kSDev * 4;                              // slack, F/awf/awu/excl
   b += size_t(V) * 8 + 2 * ((size_t(V) * 2 + 3) & ~size_t(3)); // info, pending, rpos
   b += (size_t(nucap) * n * 2 + 7) & ~size_t(7);               // nuc
   const size_t ns = static_cast<size_t>(small_slots(n));
   b += ns * (8 * 4 + 8 + 8 * kKI + 4 * kKO) + size_t(kSPairs) * 4 + 32 * 4;  // slots, caches, dr, cjs
-  b += 7 * 32 * 4 + size_t(nccap) * 4 + small_ncm_words(nucap, n) * 4 + size_t(kSSlots) * 4 + 32 * 4;
+  b += 7 * 32 * 4 + size_t(nccap) * 4 + small_ncm_words(nucap, n) * 4 + size_t(kSSlots) * 4 + kSDev * 4;
   return b + 64;
 }
 
@@ -142,16 +145,16 @@ __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, i
   SSm m;
   int64_t *p64 = reinterpret_cast<int64_t *>(base);
   m.slack = p64;
-  m.info = reinterpret_cast<uint64_t *>(p64 + 32);
+  m.info = reinterpret_cast<uint64_t *>(p64 + kSDev);
   const int ns = small_slots(n);
   m.need = reinterpret_cast<int64_t *>(m.info + V);
   m.sip = reinterpret_cast<uint2 *>(m.need + ns);
   int32_t *p32 = reinterpret_cast<int32_t *>(m.sip + ns * kKI);
   m.F = p32;
-  m.awf = p32 + 32;
-  m.awu = p32 + 64;
-  m.excl = p32 + 96;
-  p32 += 128;
+  m.awf = p32 + kSDev;
+  m.awu = p32 + 2 * kSDev;
+  m.excl = p32 + 3 * kSDev;
+  p32 += 4 * kSDev;
   const int vw = (V + 1) / 2;  // int32 words of a [V] 16-bit array
   m.pending = reinterpret_cast<uint16_t *>(p32);
   m.rpos = reinterpret_cast<int16_t *>(p32 + vw);
@@ -267,7 +270,7 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
   const int np = st.R * n;
   uint64_t ck[P];
   int32_t kq[P];  // k of the pair's node
-  int32_t sq[P];  // slot << 5 | device
+  int32_t sq[P];  // slot << kSDevBits | device
   unsigned fitm = 0;
   {
     int s = st.s0, q = st.q0;
@@ -276,7 +279,7 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
       const int x = lane + 32 * u;
       ck[u] = kSNone;
       kq[u] = 0;
-      sq[u] = s << 5 | q;
+      sq[u] = s << kSDevBits | q;
       if (x < np) {
         const int32_t d = m.dr[x];
         if (d != kSDead && !m.excl[q]) {
@@ -288,7 +291,7 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
             if (a >= 0 && a != node) key = max(key, fl);
           }
           ck[u] = (static_cast<uint64_t>(static_cast<uint32_t>(key)) << 32) |
-                  (static_cast<uint32_t>(node) << 5 | static_cast<uint32_t>(q));
+                  (static_cast<uint32_t>(node) << kSDevBits | static_cast<uint32_t>(q));
           kq[u] = m.kk[s];
           if (m.need[s] <= m.slack[q]) fitm |= 1u << u;
         }
@@ -328,9 +331,9 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
     msq = __shfl_sync(kFull, msq, ol);
     mk = __shfl_sync(kFull, mk, ol);
     const int32_t t = static_cast<int32_t>(w >> 32);
-    const int j = static_cast<int>((static_cast<uint32_t>(w)) >> 5);
-    const int p = static_cast<int>(w & 31u);
-    const int s = (msq >> 5) & 0x1ffffff;
+    const int j = static_cast<int>((static_cast<uint32_t>(w)) >> kSDevBits);
+    const int p = static_cast<int>(w & (kSDev - 1u));
+    const int s = (msq >> kSDevBits) & 0xffffff;
     progress = true;
     if (!(msq >> 30)) {
       // ---- discard (placers.cpp:203-219) ----
@@ -386,7 +389,7 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
         if (lane == 0) m.excl[p] = 1;
 #pragma unroll
         for (int u = 0; u < P; ++u)
-          if ((sq[u] & 31) == p) ck[u] = kSNone;
+          if ((sq[u] & (kSDev - 1)) == p) ck[u] = kSNone;
       }
       __syncwarp();
       continue;
@@ -406,7 +409,8 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
     T = min(T, static_cast<uint32_t>(fin));
 #pragma unroll
     for (int u = 0; u < P; ++u)
-      if ((sq[u] & 31) == p || (static_cast<uint32_t>(ck[u]) >> 5) == static_cast<uint32_t>(j)) ck[u] = kSNone;
+      if ((sq[u] & (kSDev - 1)) == p || (static_cast<uint32_t>(ck[u]) >> kSDevBits) == static_cast<uint32_t>(j))
+        ck[u] = kSNone;
     if (kSct) {
       // awake reservations (placers.cpp:235-254): columns whose reservation
       // awaited j are lifted — their keys may drop, so they leave the round
@@ -422,7 +426,7 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
       T = min(T, __reduce_min_sync(kFull, fq));
 #pragma unroll
       for (int u = 0; u < P; ++u)
-        if ((lm >> (sq[u] & 31)) & 1) ck[u] = kSNone;
+        if ((lm >> (sq[u] & (kSDev - 1))) & 1) ck[u] = kSNone;  // m-SCT: n <= 32
       int got = 0;
       if (lane == 0) {
         m.awf[p] = -1;
@@ -437,7 +441,7 @@ __device__ __forceinline__ bool small_select(const SSm &m, const SGraph &G, SRun
       st.awake += __shfl_sync(kFull, got, 0);
       __syncwarp();
     }
-    if (st.placed == st.V) break;
+    if (st.placed == st.V || cm.nc == 32) break;  // lane r holds commit r (n may reach 64)
   }
   __syncwarp();  // ... and the commits' writes (step 3) follow every lane's reads
   return progress;
@@ -499,7 +503,8 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
   const int64_t cmax64 = *pr.cmax;
   const int nccap = n * (jb.maxin > 1 ? jb.maxin : 1);
   // dynamic eligibility (see the header); otherwise the general kernel runs it
-  if (*pr.cbad || g.flags[2] || *g.ksum < 0 || *pr.nu_count > jb.nucap || n > 32 || V >= (kGlobal ? (1 << 26) : 0xffff) ||
+  if (*pr.cbad || g.flags[2] || *g.ksum < 0 || *pr.nu_count > jb.nucap || n > kSDev ||
+      (n > 32 && (kSct || *pr.nu_count > 0)) || V >= (kGlobal ? (1 << 26) : 0xffff) ||
       cmax64 >= 0xffff || jb.maxin >= 0xffff || *g.ksum + (int64_t(V) + 2) * cmax64 >= int64_t(INT32_MAX))
     return;
   const int32_t cmax = static_cast<int32_t>(cmax64);
@@ -519,11 +524,13 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
 
   // ---- init ------------------------------------------------------------------
   {
-    m.F[lane] = 0;
-    m.awf[lane] = -1;
-    m.awu[lane] = 0;
-    m.excl[lane] = 0;
-    m.slack[lane] = lane < n ? jb.cap[lane] : 0;
+    for (int d = lane; d < kSDev; d += 32) {
+      m.F[d] = 0;
+      m.awf[d] = -1;
+      m.awu[d] = 0;
+      m.excl[d] = 0;
+      m.slack[d] = d < n ? jb.cap[d] : 0;
+    }
     for (int x = lane; x < jb.nucap * n; x += 32) m.nuc[x] = 0xffffu;
     for (int x = lane; x < small_ncm_words(jb.nucap, n); x += 32) m.ncm[x] = 0;
   }

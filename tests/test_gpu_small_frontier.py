@@ -165,3 +165,42 @@ def test_small_frontier_can_be_disabled(bx):
     b = _plan_one(bx, gg, "m-etf", caps, bx.CommModel(*W.COMM_TEST), options={"no_small_frontier": 1})
     assert a[3] == "small-frontier" and b[3] == "rounds"
     assert a[2] == b[2] and a[2].stats == b[2].stats
+
+
+@pytest.mark.parametrize("which", ["smem", "global"])
+def test_small_frontier_up_to_64_devices(bx, which):
+    """K2s takes 33-64 devices for m-ETF when no producer needs cache rows
+    (pairs pack the device in 6 bits, at most 32 commits per round), with its
+    node state in shared memory or (graphs past it) in HBM; graphs with mixed
+    byte counts and m-SCT stay at 32 and hand off. Against the restatement,
+    tight capacities (discards, exclusions) included."""
+    if which == "smem":
+        graphs = [W.as_meta_dict(W.grid_chain(40, 3, 1)), W.as_meta_dict(W.branchy(6, 2))]
+    else:  # node state past shared memory: 16k+ nodes
+        graphs = [W.as_meta_dict(W.grid_chain(5000, 4, 3))]
+    rng = np.random.default_rng(9)
+    took = 0
+    for m in graphs:
+        gg = bx.MetaGraph.from_dict(m)
+        need = m["perm"] + m["out"] + m["temp"]
+        for n in (33, 40, 64):
+            for f in (0.95, 1.05, 1.6):
+                cap = int(np.ceil((need.sum() / n + need.max()) * f))
+                caps = [int(cap * rng.uniform(0.8, 1.1)) for _ in range(n)]
+                cmv = (12.5, 0.002, 1)
+                o, oe = _oracle(m, 1, caps, cmv, None)
+                st, msg, p, kern = _plan_one(bx, gg, "m-etf", caps, bx.CommModel(*cmv))
+                assert (None if st == 0 else (st, msg)) == oe, (n, f)
+                if oe is None:
+                    _same(p, o)
+                took += kern == "small-frontier"
+    assert took > 0
+    # mixed bytes at 40 devices: cache rows needed, so the general kernels place it
+    m = _mixed_bytes(W.grid_chain(30, 3, 5), 5)
+    gg = bx.MetaGraph.from_dict(m)
+    need = m["perm"] + m["out"] + m["temp"]
+    caps = [int(np.ceil((need.sum() / 40 + need.max()) * 1.3))] * 40
+    o, _ = _oracle(m, 1, caps, (12.5, 0.002, 1), None)
+    st, msg, p, kern = _plan_one(bx, gg, "m-etf", caps, bx.CommModel(12.5, 0.002, 1))
+    assert st == 0 and kern != "small-frontier"
+    _same(p, o)
