@@ -476,7 +476,8 @@ def main():
         try:
             from latency_table import run as run_case
             pg["families"] = [run_case(nm, cpu=not args.no_cpu_baseline)
-                              for nm in ("refchain100k_x4", "refchain100k_x4_sct", "refchain100k_x8_sct", "grid100k_x8",
+                              for nm in ("refchain100k_x4", "refchain100k_x8", "refchain1M_x64", "refchain100k_x4_sct",
+                                         "refchain100k_x8_sct", "grid100k_x8",
                                          "wide100k_x16",
                                          "layered100k_x64",
                                          "seq_layered100k_x4", "seq_wide100k_x16", "seq_refchain100k_x4")]
