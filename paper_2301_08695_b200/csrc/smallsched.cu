@@ -925,11 +925,14 @@ static void launch_sf(const DJob *jobs, const int32_t *order, int nj, const DGra
   if (nj <= 0) return;
   auto kern = k_place_small<kSct, kProf, kGlobal>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  // the smallest shared-memory carveout that holds the job state: the rest
-  // of the unified 256 KB is L1 for the warmed graph
-  const int pct = static_cast<int>((smem * 100 + 228 * 1024 - 1) / (228 * 1024));
-  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 1 ? 1 : pct);
-  kern<<<nj, 32 * kSWarm, smem, s>>>(jobs, order, nj, graphs, preps);
+  // shared memory: the smallest carveout that holds the job state (the rest
+  // of the unified 256 KB is L1 for the warmed graph); node state in HBM:
+  // no warm-up warps, one warp per CTA, room for up to 8 CTAs per SM (the
+  // register budget's limit)
+  const size_t per_sm = kGlobal ? 8 * smem : smem;
+  const int pct = static_cast<int>((per_sm * 100 + 228 * 1024 - 1) / (228 * 1024));
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 1 ? 1 : (pct > 100 ? 100 : pct));
+  kern<<<nj, kGlobal ? 32 : 32 * kSWarm, smem, s>>>(jobs, order, nj, graphs, preps);
 }
 
 // `order` lists the K2s jobs in four runs: m-ETF and m-SCT with shared-memory
