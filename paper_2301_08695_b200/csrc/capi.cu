@@ -1586,6 +1586,62 @@ __global__ void k_oracle_min(const DSim *sims, int count, unsigned long long *be
     else if (!(st == kInfeasible && d.err->code == E_SIM_MEMORY)) atomicAdd(bad, 1u);  // memory: skipped
   }
 }
+
+// Fast path (parallel comm, no capacity, every node k > 0): a node's start is
+// max(its device predecessor's finish, max over remote parents of finish +
+// c(parent, device)), c = comm_time of the largest tensor the parent sends to
+// that device (K4f's recurrence, simulator.cpp:156-181), so walking a
+// DAG-consistent global order gives the simulator's schedule for the
+// per-device orders it induces. One warp per canonical assignment (its
+// transfer-time table built once), lanes over the global orders, a
+// warp-minimum then one atomicMin per warp. Every (assignment, order) pair
+// is scored, so no pruning is needed.
+constexpr int kOrMaxV = 16, kOrMaxN = 8;
+__device__ __forceinline__ int64_t omax(int64_t a, int64_t b) { return a > b ? a : b; }
+__global__ void k_oracle_fast(int V, int n, int64_t A, int64_t X, const uint8_t *asg, const uint8_t *ext,
+                              const int32_t *in_off, const int32_t *in_src, const int32_t *out_off,
+                              const int32_t *edst, const int64_t *bytes, const int64_t *k, double ic, double pb,
+                              unsigned long long *best) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t a = warp; a < A; a += nwarps) {
+    int dev[kOrMaxV];
+    int64_t ct[kOrMaxV][kOrMaxN];
+    for (int i = 0; i < V; ++i) dev[i] = asg[a * V + i];
+    for (int i = 0; i < V; ++i) {
+      int64_t mb[kOrMaxN];
+      for (int d = 0; d < n; ++d) mb[d] = 0;  // the reference's per-destination slot starts at 0
+      for (int e = out_off[i]; e < out_off[i + 1]; ++e) {
+        const int dc = dev[edst[e]];
+        if (dc != dev[i]) mb[dc] = omax(mb[dc], bytes[e]);
+      }
+      for (int d = 0; d < n; ++d) ct[i][d] = comm_time_exact(ic, pb, mb[d]);
+    }
+    unsigned long long mine = ~0ull;
+    for (int64_t x = lane; x < X; x += 32) {
+      int64_t fin[kOrMaxV], dfree[kOrMaxN];
+      for (int d = 0; d < n; ++d) dfree[d] = 0;
+      int64_t mk = 0;
+      for (int r = 0; r < V; ++r) {
+        const int j = ext[x * V + r], dj = dev[j];
+        int64_t t = dfree[dj];
+        for (int y = in_off[j]; y < in_off[j + 1]; ++y) {
+          const int i = in_src[y];
+          t = omax(t, dev[i] == dj ? fin[i] : fin[i] + ct[i][dj]);
+        }
+        fin[j] = t + k[j];
+        dfree[dj] = fin[j];
+        mk = omax(mk, fin[j]);
+      }
+      mine = min(mine, static_cast<unsigned long long>(mk));
+    }
+    const unsigned hi = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(mine >> 32));
+    const unsigned lo = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(mine >> 32) == hi
+                                                           ? static_cast<unsigned>(mine) : 0xffffffffu);
+    if (lane == 0) atomicMin(best, (static_cast<unsigned long long>(hi) << 32) | lo);
+  }
+}
 }  // namespace bx
 
 extern "C" int bx_oracle_makespan(const bx_graph *graph, int32_t n, const bx_comm *cm, int64_t capacity,
@@ -1669,6 +1725,65 @@ extern "C" int bx_oracle_makespan(const bx_graph *graph, int32_t n, const bx_com
     put_msg(msg, msglen, "");
     *out_us = 0;
     return BX_OK;
+  }
+  // fast path: parallel comm, no capacity, every node k > 0, small enough
+  {
+    bool ok = cm->mode == BX_COMM_PARALLEL && !limited && V <= bx::kOrMaxV && n <= bx::kOrMaxN;
+    for (int v = 0; v < V && ok; ++v) ok = graph->compute_us[v] > 0;
+    for (int e = 0; e < graph->E && ok; ++e) ok = graph->tensor_bytes[e] >= 0;
+    if (ok) {
+      const int64_t A = static_cast<int64_t>(asg.size()), X = static_cast<int64_t>(ext.size());
+      std::vector<uint8_t> ha(A * V), hx(X * V);
+      for (int64_t a = 0; a < A; ++a)
+        for (int v = 0; v < V; ++v) ha[a * V + v] = static_cast<uint8_t>(asg[a][v]);
+      for (int64_t x = 0; x < X; ++x)
+        for (int v = 0; v < V; ++v) hx[x * V + v] = static_cast<uint8_t>(ext[x][v]);
+      std::vector<int32_t> in_src(std::max(graph->E, 1));
+      for (int x = 0; x < graph->E; ++x) in_src[x] = graph->esrc[graph->in_edge[x]];
+      char *d = nullptr;
+      const size_t bA = ha.size(), bX = hx.size(), bV1 = 4 * size_t(V + 1), bE = std::max(graph->E, 1);
+      const size_t total = 256 + bA + bX + 2 * bV1 + 4 * bE * 2 + 8 * bE + 8 * size_t(V) + 64 * 8;
+      if (cudaMalloc(&d, total) != cudaSuccess) {
+        put_msg(msg, msglen, "CUDA failure in the oracle");
+        return BX_RUNTIME;
+      }
+      size_t o = 0;
+      auto take = [&](size_t b) {
+        char *p = d + o;
+        o += (b + 15) & ~size_t(15);
+        return p;
+      };
+      unsigned long long *dbest = reinterpret_cast<unsigned long long *>(take(8));
+      uint8_t *da = reinterpret_cast<uint8_t *>(take(bA)), *dx = reinterpret_cast<uint8_t *>(take(bX));
+      int32_t *dio = reinterpret_cast<int32_t *>(take(bV1)), *doo = reinterpret_cast<int32_t *>(take(bV1));
+      int32_t *dis = reinterpret_cast<int32_t *>(take(4 * bE)), *ded = reinterpret_cast<int32_t *>(take(4 * bE));
+      int64_t *dby = reinterpret_cast<int64_t *>(take(8 * bE)), *dk = reinterpret_cast<int64_t *>(take(8 * size_t(V)));
+      const unsigned long long init = ~0ull;
+      bool good = cudaMemcpy(dbest, &init, 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(da, ha.data(), bA, cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(dx, hx.data(), bX, cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(dio, graph->in_off, bV1, cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(doo, graph->out_off, bV1, cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(dis, in_src.data(), 4 * size_t(graph->E), cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(ded, graph->edst, 4 * size_t(graph->E), cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(dby, graph->tensor_bytes, 8 * size_t(graph->E), cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(dk, graph->compute_us, 8 * size_t(V), cudaMemcpyHostToDevice) == cudaSuccess;
+      unsigned long long res = ~0ull;
+      if (good) {
+        const int64_t warps = std::min<int64_t>(A, 148 * 64);
+        bx::k_oracle_fast<<<static_cast<int>((warps * 32 + 255) / 256), 256>>>(
+            V, n, A, X, da, dx, dio, dis, doo, ded, dby, dk, cm->intercept_us, cm->us_per_byte, dbest);
+        good = cudaMemcpy(&res, dbest, 8, cudaMemcpyDeviceToHost) == cudaSuccess;
+      }
+      cudaFree(d);
+      if (!good) {
+        put_msg(msg, msglen, "CUDA failure in the oracle");
+        return BX_RUNTIME;
+      }
+      *out_us = static_cast<int64_t>(res);
+      put_msg(msg, msglen, "");
+      return BX_OK;
+    }
   }
   // one plan, B identical jobs; placements go into its output region
   const int64_t pairs_total = static_cast<int64_t>(asg.size()) * static_cast<int64_t>(ext.size());
