@@ -568,6 +568,8 @@ __global__ void __launch_bounds__(kTopoThreads) k_place_topo_cta(const DJob *job
   }
 }
 
+#undef TMARK
+
 // Acyclicity (meta_topo_order's CycleError, transforms.cpp:446-479): the set
 // of nodes Kahn's algorithm cannot peel does not depend on the pop order, so
 // any peel order finds the same residue. One CTA per graph.

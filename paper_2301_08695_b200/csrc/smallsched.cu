@@ -11,12 +11,13 @@
 // is built for that chain: ONE warp per problem, no CTA barriers, every
 // mutable per-node value in shared memory, every live pair in a register of
 // some lane (R * n <= 512, at most 16 pairs per lane), and the static graph
-// read through packed records (one load per node, one per in-edge).
+// read through packed records (one load per node, one per in-edge). Up to
+// 32 devices (64 for m-ETF on graphs that need no cache rows).
 //
 // A round:
 //   1. keys: each lane forms key = max(dev_free[q], DR[s][q]) (+ the m-SCT
 //      awake floor, placers.cpp:147-156) for its pairs, as one 64-bit word
-//      (key << 32 | node << 5 | q): (key, node, device) order in a single
+//      (key << 32 | node << 6 | q): (key, node, device) order in a single
 //      unsigned compare; the memory check (placers.cpp:203-205) is a bit;
 //   2. selection: a two-REDUX warp minimum gives the global argmin; a pair
 //      that does not fit is discarded on the spot (placers.cpp:203-219);
