@@ -765,7 +765,9 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
     const int j = static_cast<int>(bi / static_cast<unsigned>(n));
     const int p = static_cast<int>(bi % static_cast<unsigned>(n));
     const int64_t t = bt;
-    const int sj = T.s[p];
+    // the winner's ready slot: parallel m-ETF reads it from rpos, so the
+    // lists' slot fields need no relabelling when a slot moves
+    const int sj = kEtf ? c.rpos[j] : T.s[p];
     __syncwarp();  // every lane has read the head before any owner edits the lists
     BX_MARK(P_ARGMIN);
 
@@ -984,12 +986,14 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
         c.alive_s[sj] = mv_alive;
         c.rpos[mv] = sj;
       }
+      if (!kEtf) {
 #pragma unroll
-      for (int k = 0; k < KT; ++k)
-        for (int q = lane; q < n; q += 32) {
-          const int x = k * T.st + q;
-          if (T.j[x] == mv) T.s[x] = sj;
-        }
+        for (int k = 0; k < KT; ++k)
+          for (int q = lane; q < n; q += 32) {
+            const int x = k * T.st + q;
+            if (T.j[x] == mv) T.s[x] = sj;
+          }
+      }
     }
     --R;
     __syncwarp();
