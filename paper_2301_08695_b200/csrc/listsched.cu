@@ -593,8 +593,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
       if (j < V) {
         int indeg = g.in_off[j + 1] - g.in_off[j];
         c.pending[j] = indeg;
-        c.device_of[j] = -1;
-        c.finish[j] = 0;
+        c.device_of[j] = -1;  // (finish times reach the children through pfin: no per-node copy)
         src = indeg == 0;
       }
       R = ready_append(c, R, src, j, lane);
@@ -857,7 +856,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
     if (sj != last) {
       mv = c.node_s[last];
       if (lane == 0) {
-        mv_urg = c.urg_s[last];
+        if (!kEtf) mv_urg = c.urg_s[last];
         mv_alive = c.alive_s[last];
       }
       if (lane < n) mv_kc = c.Kc[lane * Vs + last];
@@ -968,7 +967,6 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
     if (lane == 0) {
       c.device_of[j] = p;
       c.start[j] = t;
-      c.finish[j] = fin;
       c.F[p] = fin;
       c.res[p] += needj;
       c.cseq[placed] = j;
@@ -982,7 +980,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
       for (int q = lane + 32; q < n; q += 32) c.Kc[q * Vs + sj] = c.Kc[q * Vs + last];
       if (lane == 0) {
         c.node_s[sj] = mv;
-        c.urg_s[sj] = mv_urg;
+        if (!kEtf) c.urg_s[sj] = mv_urg;
         c.alive_s[sj] = mv_alive;
         c.rpos[mv] = sj;
       }
@@ -1047,7 +1045,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
     if (nnew > 0) {
       for (int s = R0 + lane; s < R; s += 32) {
         c.alive_s[s] = n - nexcl;
-        c.urg_s[s] = c.sct ? urgency_e(c, c.node_s[s]) : 0;
+        if (!kEtf) c.urg_s[s] = c.sct ? urgency_e(c, c.node_s[s]) : 0;  // read only by m-SCT
       }
       for (int r = lane; r < nnew * n; r += 32) {
         int s = R0 + r / n;
