@@ -160,7 +160,8 @@ struct DSim {
   int64_t *fin;                     // [V] finish time, -1 until published
   int64_t *sx;                      // [V] start time per exec slot
   int64_t *bucket;                  // [V] output bytes freed before each exec slot's start
-  int64_t *mb;                      // [V*n] max bytes per (producer, consumer device)
+  int64_t *mb;                      // [V*n] max bytes per (producer, consumer device); sequencer:
+                                    //     transfer time, then -2 - arrival once sent
   uint8_t *first;                   // [E] edge opens its (producer, device) transfer
   unsigned long long *flow8;        // [8] zero-k, bad exec, bad once, transfers, bytes, remote edges
   int32_t *rcnt;                    // [V] remote parents per node (bit 30: never ready)
@@ -170,6 +171,7 @@ struct DSim {
   int64_t *kx;                      // [V] compute time by FIFO slot (-1: never ready)
   int64_t *dv;                      // [4n] per device: peak, violation t, node, memory
   int32_t *ninp;                    // [V] K4: inputs of a node not yet resident on its device
+                                    //     sequencer: remote destination mask
   // SimOptions::record_trace (simulator.hpp:37): K4 appends (t, device,
   // event, meta) per event in processing order; null = no trace
   int64_t *trace;

@@ -162,9 +162,10 @@ __global__ void __launch_bounds__(32 * kWarps) k_simulate(const DSim *sims, int 
   c.V = c.g.V;
   c.n = c.s.n;
   c.lane = lane;
-  // parallel comm mode without zero-duration nodes belongs to K4f (its first
-  // prep pass flags zero durations)
-  if (c.s.mode == 1 && !c.s.flow8[0]) return;
+  // without zero-duration nodes or a trace, parallel comm mode belongs to K4f
+  // and sequential comm mode on <= 32 devices to its sequencer (the first prep
+  // pass flags those)
+  if ((c.s.mode == 1 || (c.s.mode == 0 && c.n <= 32)) && !c.s.flow8[0]) return;
   {
     extern __shared__ int64_t sim_heap_smem[];
     const int64_t scap = static_cast<int64_t>(sim_heap_cap);
@@ -458,13 +459,17 @@ __device__ __forceinline__ void st_cta(int64_t *p, int64_t v) {
 #define BX_SIM_STRIDE(i, N) for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (N); i += gridDim.x * blockDim.x)
 constexpr int32_t kNever = 1 << 30;  // rcnt flag: a same-device parent comes later in the FIFO
 
+// K4f takes parallel comm mode; sequential comm with at most 32 devices goes
+// through the same passes with the sequencer below in place of the walkers
+__device__ __forceinline__ bool flow_ok(const DSim &s) { return s.mode == 1 || (s.mode == 0 && s.n <= 32); }
+
 __device__ __forceinline__ bool flow_skip(const DSim &s) {
-  return s.mode != 1 || s.flow8[0] || s.flow8[1] || s.flow8[2];
+  return !flow_ok(s) || s.flow8[0] || s.flow8[1] || s.flow8[2];
 }
 
 __global__ void k_sim_prep_a(const DSim *sims, const DGraph *graphs, int base) {
   const DSim s = sims[base + blockIdx.y];
-  if (s.mode != 1) return;
+  if (!flow_ok(s)) return;
   const DGraph g = graphs[s.graph];
   const int n = s.n;
   int zero = 0;
@@ -473,6 +478,7 @@ __global__ void k_sim_prep_a(const DSim *sims, const DGraph *graphs, int base) {
     s.fin[j] = -1;
     s.bucket[j] = 0;
     s.rcnt[j] = 0;
+    if (s.mode == 0) s.ninp[j] = 0;  // sequencer: remote destination mask
     zero |= g.k[j] == 0;
   }
   zero |= s.trace != nullptr;  // record_trace: the event loop records processing order
@@ -485,7 +491,7 @@ __global__ void k_sim_prep_a(const DSim *sims, const DGraph *graphs, int base) {
 
 __global__ void k_sim_prep_b(const DSim *sims, const DGraph *graphs, int base) {
   const DSim s = sims[base + blockIdx.y];
-  if (s.mode != 1) return;
+  if (!flow_ok(s)) return;
   const DGraph g = graphs[s.graph];
   const int V = g.V, n = s.n;
   // exec lists (simulator.cpp:84-90): range and device agreement, counts
@@ -517,6 +523,7 @@ __global__ void k_sim_prep_b(const DSim *sims, const DGraph *graphs, int base) {
       auto *slot = reinterpret_cast<unsigned long long *>(s.mb + static_cast<int64_t>(i) * n + dc);
       f = atomicCAS(slot, ~0ull, ~0ull - 1) == ~0ull;
       cnt += f;
+      if (f && s.mode == 0) atomicOr(reinterpret_cast<unsigned *>(s.ninp + i), 1u << dc);
       // the reference's per-destination slot starts at 0 (simulator.cpp:160-162)
       atomicMax(reinterpret_cast<long long *>(slot), static_cast<long long>(g.ebytes[e] > 0 ? g.ebytes[e] : 0));
     }
@@ -535,7 +542,7 @@ __global__ void k_sim_prep_b(const DSim *sims, const DGraph *graphs, int base) {
 
 __global__ void k_sim_prep_c(const DSim *sims, const DGraph *graphs, int base) {
   const DSim s = sims[base + blockIdx.y];
-  if (s.mode != 1) return;
+  if (!flow_ok(s)) return;
   const DGraph g = graphs[s.graph];
   const int V = g.V, n = s.n;
   int bad = 0;
@@ -624,6 +631,10 @@ __global__ void k_sim_prep_e(const DSim *sims, const DGraph *graphs, int base) {
     const int64_t cc = s.cx[x];
     if (cc < 0) continue;
     const int e = g.in_edge[x];
+    if (s.mode == 0 && s.first[e]) {  // the sequencer reads transfer times, not bytes
+      const int64_t y = static_cast<int64_t>(g.esrc[e]) * s.n + s.device_of[g.edst[e]];
+      s.mb[y] = comm_time_exact(s.ic, s.pb, s.mb[y]);
+    }
     const int i = g.esrc[e], c = g.edst[e];
     const int xs = s.exec_off[s.device_of[c]] + s.pos[c];
     const int slot = s.rp_off[xs] + atomicSub(&s.rcnt[c], 1) - 1;
@@ -632,31 +643,222 @@ __global__ void k_sim_prep_e(const DSim *sims, const DGraph *graphs, int base) {
   }
 }
 
+// ---- sequential comm mode: the transfer sequencer ---------------------------
+// In sequential mode a finish at t sends its output to each remote consumer
+// device in ascending order, each transfer starting at max(t, xfree[src],
+// xfree[dst]) and holding both queues (simulator.cpp:163-173), so arrivals
+// depend on the global order of finishes. With every k > 0 the heap pops a
+// device's start and a transfer's landing no later than anything they cause,
+// so the run reduces to a merge of the device FIFOs by (finish, node):
+//   * a FIFO head starts at max(finish of its FIFO predecessor, arrival of
+//     each remote input on its device) — the last try_start that finds it
+//     ready (:113-119); same-device parents finish before its predecessor;
+//   * the next finish processed is the minimum (t, node) over the running
+//     heads (one per device, lane = device): a head still waiting for an
+//     input waits for a finish not yet processed, so its own finish is later;
+//   * processing it folds its transfers into the queues (one destination: one
+//     max; several: a warp max-plus scan over the destination lanes,
+//     X_d = max(X_{d-1}, t, xfree[d]) + c_d), publishes each arrival A(i, d),
+//     and wakes a head waiting on exactly that input; the source lane moves
+//     to its next FIFO entry.
+// mb[i*n + d] holds the transfer time c(i, d) (precomputed in prep_e) until
+// i is sent, then -2 - A(i, d): column d is only ever touched by lane d. A
+// lane prefetches its next FIFO entry's row into L1.
+// Memory, the report and the deadlock verdict are K4f's passes (the starts
+// are the same events).
+constexpr int kSeqRun = 0, kSeqWait = 1, kSeqDone = 2, kSeqNever = 3;
+
+__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+__device__ __forceinline__ unsigned long long warp_min_u64s(unsigned long long v) {
+  const unsigned hi = static_cast<unsigned>(v >> 32), lo = static_cast<unsigned>(v);
+  const unsigned mhi = __reduce_min_sync(kFullS, hi);
+  const unsigned mlo = __reduce_min_sync(kFullS, hi == mhi ? lo : 0xffffffffu);
+  return (static_cast<unsigned long long>(mhi) << 32) | mlo;
+}
+
+__device__ __forceinline__ void seq_sequencer(const DSim &s) {
+  const int n = s.n, lane = threadIdx.x & 31;
+  // column `lane` of mb: the transfer time c(p, lane) >= 0 until p is sent,
+  // then -2 - A(p, lane) (only lane d ever touches column d)
+  int64_t *mc = s.mb + lane;
+  // arrival of p's output on this lane's device, -1 while not sent
+  auto arrival = [&](int p) -> int64_t {
+    const int64_t v = mc[static_cast<int64_t>(p) * n];
+    return v >= 0 ? -1 : -2 - v;
+  };
+
+  int o = 0, len = 0, pos = 0, st = kSeqDone, h = -1, r = 0, re = 0, cp = -1;
+  int64_t prev = 0, xf = 0, ft = 0, amax = 0, kk = 0, mk = 0;
+  unsigned hm = 0;
+  // FIFO entries pos+1 (n1*) and pos+2 (n2*), loaded ahead of use
+  int n1h = -1, n1r = 0, n1re = 0, n2h = -1, n2r = 0, n2re = 0;
+  int n1p[4] = {-1, -1, -1, -1};
+  unsigned n1m = 0;
+  int64_t n1k = 0, n2k = 0;
+  auto load2 = [&](int q) {
+    if (q < len) {
+      const int xs = o + q;
+      n2h = s.exec_order[xs];
+      n2k = s.kx[xs];
+      n2r = s.rp_off[xs];
+      n2re = s.rp_off[xs + 1];
+    }
+  };
+  auto shift = [&](int q) {  // entry q (loaded as n2) becomes n1; load q + 1 as n2
+    n1h = n2h;
+    n1k = n2k;
+    n1r = n2r;
+    n1re = n2re;
+    if (q < len) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) n1p[u] = n1r + u < n1re ? s.rp_src[n1r + u] : -1;
+      n1m = static_cast<unsigned>(s.ninp[n1h]);
+      prefetch_l1(s.mb + static_cast<int64_t>(n1h) * n);  // its transfer times, read when it finishes
+    }
+    load2(q + 1);
+  };
+  auto advance = [&](int c0, int c1, int c2, int c3) {  // c_u = rp_src[r + u] where r + u < re
+    while (r < re) {
+      const int lim = re - r;
+      const int64_t v0 = arrival(c0);
+      const int64_t v1 = lim > 1 ? arrival(c1) : 0;
+      const int64_t v2 = lim > 2 ? arrival(c2) : 0;
+      const int64_t v3 = lim > 3 ? arrival(c3) : 0;
+      // the first input of the four not sent yet (4: none)
+      const int f = v0 < 0 ? 0 : (lim > 1 && v1 < 0) ? 1 : (lim > 2 && v2 < 0) ? 2 : (lim > 3 && v3 < 0) ? 3 : 4;
+      const int take = min(f, lim);
+      if (take > 0) amax = smax(amax, v0);
+      if (take > 1) amax = smax(amax, v1);
+      if (take > 2) amax = smax(amax, v2);
+      if (take > 3) amax = smax(amax, v3);
+      r += take;
+      if (f < 4) {  // waits for this input (f < 4 only within the chunk)
+        cp = f == 0 ? c0 : f == 1 ? c1 : f == 2 ? c2 : c3;
+        return;
+      }
+      if (r >= re) break;
+      c0 = s.rp_src[r];
+      c1 = r + 1 < re ? s.rp_src[r + 1] : -1;
+      c2 = r + 2 < re ? s.rp_src[r + 2] : -1;
+      c3 = r + 3 < re ? s.rp_src[r + 3] : -1;
+    }
+    st = kSeqRun;
+    ft = amax + kk;
+    s.sx[o + pos] = amax;
+    s.start[h] = amax;
+  };
+  auto setup = [&]() {  // entry pos becomes the head
+    if (pos >= len) {
+      st = kSeqDone;
+      return;
+    }
+    h = n1h;
+    kk = n1k;
+    r = n1r;
+    re = n1re;
+    hm = n1m;
+    const int p0 = n1p[0], p1 = n1p[1], p2 = n1p[2], p3 = n1p[3];
+    amax = prev;
+    shift(pos + 1);
+    if (kk < 0) {  // a same-device parent comes later in the FIFO: never ready
+      st = kSeqNever;
+      return;
+    }
+    st = kSeqWait;
+    advance(p0, p1, p2, p3);
+  };
+  if (lane < n) {
+    o = s.exec_off[lane];
+    len = s.exec_off[lane + 1] - o;
+    load2(0);
+    shift(0);
+    setup();
+  }
+  while (true) {
+    const bool run = st == kSeqRun;
+    if (!__any_sync(kFullS, run)) break;
+    // the next finish: minimum (t, node) over the running heads
+    const unsigned long long mt = warp_min_u64s(run ? static_cast<unsigned long long>(ft) : ~0ull);
+    const bool tied = run && static_cast<unsigned long long>(ft) == mt;
+    const unsigned tie = __ballot_sync(kFullS, tied);
+    int w = __ffs(tie) - 1;
+    if (tie & (tie - 1)) {
+      const unsigned hn = __reduce_min_sync(kFullS, tied ? static_cast<unsigned>(h) : 0xffffffffu);
+      w = __ffs(__ballot_sync(kFullS, tied && static_cast<unsigned>(h) == hn)) - 1;
+    }
+    const int64_t t = static_cast<int64_t>(mt);
+    const int i = __shfl_sync(kFullS, h, w);
+    const unsigned M = __shfl_sync(kFullS, hm, w);
+    if (M) {
+      const int64_t x0 = __shfl_sync(kFullS, xf, w);
+      const bool dst = (M >> lane) & 1u;
+      int64_t X = 0;  // the queues' free time after this lane's transfer
+      int64_t xl;     // the source queue's afterwards
+      if (!(M & (M - 1))) {  // one destination
+        if (dst) X = smax(smax(x0, t), xf) + mc[static_cast<int64_t>(i) * n];
+        xl = __shfl_sync(kFullS, X, __ffs(M) - 1);
+      } else {
+        int64_t a = 0, b = INT64_MIN / 4;  // identity of f(X) = max(X + a, b)
+        if (dst) {
+          const int64_t c = mc[static_cast<int64_t>(i) * n];
+          a = c;
+          b = smax(t, xf) + c;
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int64_t a2 = __shfl_up_sync(kFullS, a, off), b2 = __shfl_up_sync(kFullS, b, off);
+          if (lane >= off) {
+            b = smax(b2 + a, b);
+            a = a2 + a;
+          }
+        }
+        X = smax(x0 + a, b);
+        xl = __shfl_sync(kFullS, X, 31);
+      }
+      if (dst) {
+        xf = X;
+        mc[static_cast<int64_t>(i) * n] = -2 - X;
+        if (st == kSeqWait && cp == i) {
+          amax = smax(amax, X);
+          ++r;
+          advance(r < re ? s.rp_src[r] : -1, r + 1 < re ? s.rp_src[r + 1] : -1, r + 2 < re ? s.rp_src[r + 2] : -1,
+                  r + 3 < re ? s.rp_src[r + 3] : -1);
+        }
+      }
+      if (lane == w) xf = xl;
+    }
+    if (lane == w) {
+      s.fin[i] = t;
+      prev = t;
+      mk = smax(mk, t);
+      ++pos;
+      setup();
+    }
+  }
+  if (lane < n) s.qpos[lane] = pos;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mk = smax(mk, __shfl_xor_sync(kFullS, mk, off));
+  if (lane == 0) *s.makespan = mk;
+}
+
 constexpr int kWalkSpin = 64;
 
-// K4f walkers: validation verdicts, permanent memory, then the FIFO walk.
-__global__ void __launch_bounds__(1024) k_sim_flow(const DSim *sims, int nsims, const DGraph *graphs) {
-  __shared__ long long sh_mk;
-  __shared__ int sh_bad;
-  const DSim s = sims[blockIdx.x];
-  if (s.mode != 1) return;
-  const DGraph g = graphs[s.graph];
+// validation verdicts and permanent memory, shared by the walkers and the
+// sequencer; false when the run already ended (error set)
+__device__ bool flow_preamble(const DSim &s, const DGraph &g, int *sh_bad) {
   const int n = s.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
   DErr *err = s.err;
-  if (s.flow8[0]) return;  // zero-duration nodes: event-loop kernel
   // validate_placement (simulator.cpp:78-97), decided by its first failing check
   if (s.flow8[1] || s.flow8[2]) {
     if (tid == 0) {
       err->status = kValidation;
       err->code = s.flow8[1] ? E_SIM_EXEC : E_SIM_ONCE;
     }
-    return;
+    return false;
   }
-  if (tid == 0) {
-    sh_mk = 0;
-    sh_bad = INT32_MAX;
-  }
+  if (tid == 0) *sh_bad = INT32_MAX;
   __syncthreads();
   // permanent memory up front, device by device in FIFO order (:209-214)
   for (int d = warp; d < n; d += NW) {
@@ -688,13 +890,13 @@ __global__ void __launch_bounds__(1024) k_sim_flow(const DSim *sims, int nsims, 
       s.xfree[d] = 0;
       s.dest_cnt[d] = vbad;  // first violating FIFO slot (perm)
       s.dest_bytes[d] = vmem;
-      if (vbad != INT32_MAX) atomicMin(&sh_bad, d);
+      if (vbad != INT32_MAX) atomicMin(sh_bad, d);
     }
   }
   __syncthreads();
-  if (sh_bad != INT32_MAX) {
+  if (*sh_bad != INT32_MAX) {
     if (tid == 0) {
-      const int d = sh_bad;
+      const int d = *sh_bad;
       err->status = kInfeasible;
       err->code = E_SIM_MEMORY;
       err->a = d;
@@ -702,8 +904,34 @@ __global__ void __launch_bounds__(1024) k_sim_flow(const DSim *sims, int nsims, 
       err->c = s.exec_order[s.exec_off[d] + s.dest_cnt[d]];
       err->d = s.dest_bytes[d];
     }
-    return;
+    return false;
   }
+  return true;
+}
+
+// sequential comm mode, <= 32 devices: warp 0 sequences, warp 1 warms L1
+// sequential comm mode, <= 32 devices: one warp per problem
+__global__ void __launch_bounds__(32, 1) k_sim_seq(const DSim *sims, int nsims, const DGraph *graphs) {
+  __shared__ int sh_bad;
+  const DSim s = sims[blockIdx.x];
+  if (s.mode != 0 || s.n > 32 || s.flow8[0]) return;  // zero-duration nodes, traces: event loop
+  const DGraph g = graphs[s.graph];
+  if (!flow_preamble(s, g, &sh_bad)) return;
+  seq_sequencer(s);
+}
+
+// K4f walkers: validation verdicts, permanent memory, then the FIFO walk.
+__global__ void __launch_bounds__(1024) k_sim_flow(const DSim *sims, int nsims, const DGraph *graphs) {
+  __shared__ long long sh_mk;
+  __shared__ int sh_bad;
+  const DSim s = sims[blockIdx.x];
+  if (s.mode != 1) return;
+  const DGraph g = graphs[s.graph];
+  const int n = s.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
+  if (s.flow8[0]) return;  // zero-duration nodes: event-loop kernel
+  if (tid == 0) sh_mk = 0;
+  if (!flow_preamble(s, g, &sh_bad)) return;
 
   // ---- walkers ----------------------------------------------------------------
   int64_t mk = 0;
@@ -995,6 +1223,7 @@ void launch_simulate(const DSim *sims, int nsims, const DGraph *graphs, int maxn
   k_sim_prep_d<<<nsims, cta, 0, s>>>(sims, graphs);
   grid(k_sim_prep_e, gx, 256);
   k_sim_flow<<<nsims, cta, 0, s>>>(sims, nsims, graphs);
+  k_sim_seq<<<nsims, 32, 0, s>>>(sims, nsims, graphs);
   grid(k_sim_free, gx, 256);
   grid(k_sim_mem, static_cast<unsigned>(maxn), cta);
   k_sim_report<<<(nsims + 127) / 128, 128, 0, s>>>(sims, nsims);

@@ -2,9 +2,10 @@
 assignments and FIFO orders (valid topological ones and deadlocking ones),
 ample / tight / permanent-memory-violating capacities, both memory modes and
 both comm modes, with and without zero-duration nodes. Parallel comm mode
-without zero-duration nodes runs the dataflow kernel (K4f), everything else
-the event-loop kernel (K4); both must match the C restatement of
-simulator.cpp bit for bit, error texts included."""
+without zero-duration nodes runs the dataflow kernel (K4f), sequential comm
+mode on <= 32 devices its transfer sequencer, everything else the event-loop
+kernel (K4); all must match the C restatement of simulator.cpp bit for bit,
+error texts included."""
 import heapq
 
 import numpy as np
@@ -108,13 +109,18 @@ def test_sim_random_placements(bx, gi):
     assert None in seen_err and len(seen_err) >= 2  # both successes and errors were exercised
 
 
-def test_sim_flow_full_size_vs_event_loop(bx):
-    """100k-op m-ETF placement: the dataflow kernel against the C restatement
-    in both memory modes (full-size, bit-exact)."""
+SEQ = (5.0, 0.001, 0)
+
+
+@pytest.mark.parametrize("cmt", [W.COMM_TEST, SEQ], ids=["parallel", "sequential"])
+def test_sim_flow_full_size_vs_event_loop(bx, cmt):
+    """100k-op m-ETF placement: the dataflow kernel (parallel comm) and the
+    transfer sequencer (sequential comm) against the C restatement in both
+    memory modes (full-size, bit-exact)."""
     g = W.layered_dag_fast(100, 1000, 3)
     m = W.as_meta_dict(g)
     gg = bx.MetaGraph.from_dict(m)
-    cm = bx.CommModel(*W.COMM_TEST)
+    cm = bx.CommModel(*cmt)
     caps = np.full(4, W.bench_capacity(g, 4, 1.2), np.int64)
     plan = bx.Plan([gg], [bx.Job(0, "m-etf", caps, cm)])
     plan.upload()
@@ -124,7 +130,7 @@ def test_sim_flow_full_size_vs_event_loop(bx):
     for mm in (0, 1):
         plan.simulate(mm)
         r = plan.sim_download()[0]
-        o = Restate.simulate(m, caps, W.COMM_TEST, mm, p.device_of, p.exec_order_flat, p.exec_off)
+        o = Restate.simulate(m, caps, cmt, mm, p.device_of, p.exec_order_flat, p.exec_off)
         assert r.makespan_us == o.makespan and np.array_equal(r.start_us, o.start_us)
         assert r.peak_bytes.tolist() == o.peak.tolist() and r.idle_us.tolist() == o.idle.tolist()
         assert [r.transfer_count, r.transfer_bytes, r.duplicate_transfers, r.cache_hits] == [
@@ -133,19 +139,22 @@ def test_sim_flow_full_size_vs_event_loop(bx):
 
 
 def test_sim_many_devices_and_tiny_graphs(bx):
-    """Walker warps owning several devices (n = 40 > 32 warps) and degenerate
-    graphs (one node, isolated nodes, empty device FIFOs)."""
+    """Walker warps owning several devices (n = 40 > 32 warps), the sequencer
+    at its 32-lane limit and the event loop past it (sequential comm, n = 32
+    and 40), and degenerate graphs (one node, isolated nodes, empty device
+    FIFOs)."""
     rng = np.random.default_rng(5)
     g = W.layered_dag(10, 30, 3)
     m = W.as_meta_dict(g)
     gg = bx.MetaGraph.from_dict(m)
     need = m["perm"] + m["out"] + m["temp"]
-    for trial in range(4):
-        pl = _placement(bx, m, 40, rng, deadlock=trial == 3)
-        tot_d = np.bincount(pl.device_of, weights=need, minlength=40).astype(np.int64)
-        for caps in (tot_d + 1, tot_d // 2 + 1):
-            for mm in (0, 1):
-                _check(bx, m, gg, pl, [int(c) for c in caps], (12.5, 0.002, 1), mm)
+    for n, cm in ((40, (12.5, 0.002, 1)), (32, SEQ), (40, SEQ), (32, (0.0, 0.0, 0))):
+        for trial in range(4):
+            pl = _placement(bx, m, n, rng, deadlock=trial == 3)
+            tot_d = np.bincount(pl.device_of, weights=need, minlength=n).astype(np.int64)
+            for caps in (tot_d + 1, tot_d // 2 + 1):
+                for mm in (0, 1):
+                    _check(bx, m, gg, pl, [int(c) for c in caps], cm, mm)
     one = dict(V=1, E=0, k=np.array([7], np.int64), temp=np.array([3], np.int64), perm=np.array([5], np.int64),
                out=np.array([2], np.int64), esrc=np.zeros(0, np.int32), edst=np.zeros(0, np.int32),
                ebytes=np.zeros(0, np.int64))
@@ -156,18 +165,19 @@ def test_sim_many_devices_and_tiny_graphs(bx):
         gm = bx.MetaGraph.from_dict(mg)
         pl = _placement(bx, mg, n, rng)
         for mm in (0, 1):
-            _check(bx, mg, gm, pl, [100] * n, (12.5, 0.002, 1), mm)
+            for cm in ((12.5, 0.002, 1), SEQ):
+                _check(bx, mg, gm, pl, [100] * n, cm, mm)
 
 
-def test_sim_batched_plan_vs_restatement(bx):
-    """A many-job plan (> 148 problems: 256-thread walker CTAs, several
-    devices per warp at n = 16) placed and simulated on the device, every
-    report against the C restatement."""
+@pytest.mark.parametrize("cmt", [W.COMM_TEST, SEQ], ids=["parallel", "sequential"])
+def test_sim_batched_plan_vs_restatement(bx, cmt):
+    """A many-job plan (> 148 problems: 256-thread walker / sequencer CTAs,
+    several devices per warp at n = 16) placed and simulated on the device,
+    every report against the C restatement."""
     graphs = W.sweep_graphs(3, 8, 800, 3000)
     jobs = [(gi, n, W.bench_capacity(graphs[gi], n, f)) for gi in range(len(graphs)) for n in (2, 5, 16)
             for f in (1.05, 1.3, 1.6, 2.0, 3.0, 4.0, 5.0)]
     assert len(jobs) > 148
-    cmt = W.COMM_TEST
     mgs = [bx.MetaGraph.from_dict(W.as_meta_dict(g)) for g in graphs]
     plan = bx.Plan(mgs, [bx.Job(gi, "m-etf", np.full(n, cap, np.int64), bx.CommModel(*cmt)) for gi, n, cap in jobs])
     plan.upload()
