@@ -239,6 +239,7 @@ int bx_plan_launch_count(const bx_plan *plan);
 #define BX_KERNEL_ROUNDS 2           /* k_place_rounds: CTA per problem, parallel comm */
 #define BX_KERNEL_CTA_SEQ 3          /* k_place_list<8>: CTA per problem, sequential comm */
 #define BX_KERNEL_SMALL_FRONTIER 4   /* k_place_small: one warp, shared-memory state (smallsched.cu) */
+#define BX_KERNEL_SEQ_SMALL 5        /* k_place_seq_small: one warp, sequential comm, small frontier (seqsmall.cu) */
 int bx_plan_job_kernel(bx_plan *plan, int32_t job);
 
 /* Device time (ms) of the placer kernel(s) of the last bx_plan_place,

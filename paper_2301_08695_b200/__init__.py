@@ -429,7 +429,7 @@ class Plan:
     def launch_count(self) -> int:
         return lib().bx_plan_launch_count(self.h)
 
-    KERNELS = {-1: "none", 0: "m-topo", 1: "warp", 2: "rounds", 3: "cta-seq", 4: "small-frontier"}
+    KERNELS = {-1: "none", 0: "m-topo", 1: "warp", 2: "rounds", 3: "cta-seq", 4: "small-frontier", 5: "seq-small"}
 
     def job_kernel(self, i: int) -> str:
         """Which kernel placed job i in the last place()."""

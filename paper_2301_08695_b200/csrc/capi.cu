@@ -34,6 +34,9 @@ void launch_prep_small(const DGraph &g, const DPrep &pr, cudaStream_t s);
 void launch_small_frontier(const DJob *jobs, const int32_t *order, const int *cnt, const DGraph *graphs,
                            const DPrep *preps, const size_t *smem, bool prof, cudaStream_t s);
 size_t small_smem_bytes_host(int V, int n, int nucap, int nccap);
+size_t seq_small_smem_bytes_host(int n);
+void launch_seq_small(const DJob *jobs, const int32_t *order, int nj, const DGraph *graphs, const DPrep *preps,
+                      size_t smem, bool prof, cudaStream_t s);
 size_t topo_smem_bytes(int V, size_t limit);
 void launch_topo(const DJob *jobs, int njobs, const DGraph *graphs, const DPrep *preps, size_t smem_bytes,
                  cudaStream_t s);
@@ -103,10 +106,13 @@ struct bx_plan {
   DJob *dj_dev = nullptr;
   int32_t *order_dev = nullptr;     // launch lists: small | big parallel | big sequential
   int n_small = 0, n_etf = 0, n_bpar = 0, n_bseq = 0;  // n_etf: leading parallel m-ETF small jobs
-  int n_sf[4] = {0, 0, 0, 0};       // small-frontier (K2s) jobs, launched first: m-ETF, m-SCT with
-                                    // shared-memory node state, then both with global node state
+  int n_sf[5] = {0, 0, 0, 0, 0};    // small-frontier (K2s) jobs, launched first: m-ETF, m-SCT with
+                                    // shared-memory node state, then both with global node state;
+                                    // [4]: sequential-comm m-ETF (K2q, seqsmall.cu)
+  size_t sq_smem = 0;               // K2q shared memory (largest slot table among its jobs)
   size_t sf_smem[2] = {0, 0};
   std::vector<char> sf_global;      // job -> K2s with global node state
+  std::vector<char> sf_seq;         // job -> K2q (sequential comm, small frontier)
   size_t topo_smem = 0;  // m-TOPO CTA: bitsets (+ counters) of the largest m-TOPO graph
   int32_t *sf_order_dev = nullptr;
   std::vector<char> prep_small;     // prep index -> K2s extras needed
@@ -620,6 +626,7 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
   }
   P->prep_small.assign(P->nprep, 0);
   P->sf_global.assign(njobs, 0);
+  P->sf_seq.assign(njobs, 0);
   P->dj.resize(njobs);
   if (P->opt.profile == 1) {
     BX_CUDA(cudaMalloc(&P->prof, sizeof(int64_t) * kProfSlots * size_t(njobs)), msg, msglen);
@@ -755,6 +762,16 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
         P->prep_small[job_prep[i]] = 1;
       }
     }
+    // K2q: sequential-comm m-ETF jobs of single-graph-sized plans (the kernel
+    // leaves the job to the general kernels once its frontier passes 512 pairs)
+    if (!d.skip && few && J.algo != BX_ALGO_MTOPO && J.cm.mode != BX_COMM_PARALLEL && d.fav == nullptr &&
+        J.n <= 32 && G.V > 0 && G.V < (1 << 26) && !P->opt.no_small_frontier && P->opt.wide_min_vn < 0) {
+      d.sdone = at<int32_t>(pool, o.sdone);
+      P->fills.push_back({d.sdone, 0, 4});
+      P->sq_smem = std::max(P->sq_smem, seq_small_smem_bytes_host(J.n));
+      P->sf_seq[i] = 1;
+      P->prep_small[job_prep[i]] = 1;
+    }
   }
   // shared-memory slices are sized by the largest roster among jobs that
   // reach a kernel: a rejected job's roster never costs the others a launch
@@ -768,12 +785,13 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
   P->order_dev = at<int32_t>(pool, otable);
   P->sf_order_dev = at<int32_t>(pool, sftable);
   {
-    std::vector<int32_t> lists[4], all;
+    std::vector<int32_t> lists[5], all;
     for (int i = 0; i < njobs; ++i) {
       if (!P->dj[i].sdone) continue;
-      lists[2 * P->sf_global[i] + (P->dj[i].algo == BX_ALGO_MSCT && P->dj[i].fav ? 1 : 0)].push_back(i);
+      if (P->sf_seq[i]) lists[4].push_back(i);
+      else lists[2 * P->sf_global[i] + (P->dj[i].algo == BX_ALGO_MSCT && P->dj[i].fav ? 1 : 0)].push_back(i);
     }
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 5; ++k) {
       P->n_sf[k] = static_cast<int>(lists[k].size());
       all.insert(all.end(), lists[k].begin(), lists[k].end());
     }
@@ -923,6 +941,11 @@ int bx_plan_place(bx_plan *P, void *stream) {
                           P->prof != nullptr, s);
     for (int k = 0; k < 4; ++k) P->launches += P->n_sf[k] > 0;
   }
+  if (P->n_sf[4] > 0) {
+    launch_seq_small(P->dj_dev, P->sf_order_dev + P->n_sf[0] + P->n_sf[1] + P->n_sf[2] + P->n_sf[3], P->n_sf[4],
+                     P->dg_dev, P->dp_dev, P->sq_smem, P->prof != nullptr, s);
+    P->launches += 1;
+  }
   const bool fork = (P->n_small > 0 && (P->n_bpar + P->n_bseq) > 0) || (P->n_etf > 0 && P->n_small > P->n_etf);
   cudaStream_t sb = fork ? P->s2 : s;
   if (fork) {
@@ -962,7 +985,7 @@ int bx_plan_job_kernel(bx_plan *P, int32_t job) {
     int32_t done = 0;
     cudaSetDevice(P->device);
     if (cudaMemcpy(&done, P->dj[job].sdone, 4, cudaMemcpyDeviceToHost) == cudaSuccess && done)
-      return BX_KERNEL_SMALL_FRONTIER;
+      return P->sf_seq[job] ? BX_KERNEL_SEQ_SMALL : BX_KERNEL_SMALL_FRONTIER;
   }
   return P->job_kernel[job];
 }
