@@ -44,6 +44,11 @@ def cases():
         g = mk()
         gg = bx.MetaGraph.from_dict(W.as_meta_dict(g))
         yield name, gg, bx.Job(0, "m-etf", np.full(n, W.bench_capacity(g, n, 1.2), np.int64), cms)
+    # the reference's own layered-chain graph (K2q in sequential comm)
+    from latency_table import _refchain
+    g = _refchain(100000)
+    gg = bx.MetaGraph.from_dict(W.as_meta_dict(g))
+    yield "seq_refchain100k_x4", gg, bx.Job(0, "m-etf", np.full(4, W.bench_capacity(g, 4, 1.5), np.int64), cms)
 
 
 def main():
