@@ -34,7 +34,7 @@ void launch_prep_small(const DGraph &g, const DPrep &pr, cudaStream_t s);
 void launch_small_frontier(const DJob *jobs, const int32_t *order, const int *cnt, const DGraph *graphs,
                            const DPrep *preps, const size_t *smem, bool prof, cudaStream_t s);
 size_t small_smem_bytes_host(int V, int n, int nucap, int nccap);
-size_t seq_small_smem_bytes_host(int n);
+size_t seq_small_smem_bytes_host(int n, int V, int maxin);
 void launch_seq_small(const DJob *jobs, const int32_t *order, int nj, const DGraph *graphs, const DPrep *preps,
                       size_t smem, bool prof, cudaStream_t s);
 size_t topo_smem_bytes(int V, size_t limit);
@@ -768,7 +768,7 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
         J.n <= 32 && G.V > 0 && G.V < (1 << 26) && !P->opt.no_small_frontier && P->opt.wide_min_vn < 0) {
       d.sdone = at<int32_t>(pool, o.sdone);
       P->fills.push_back({d.sdone, 0, 4});
-      P->sq_smem = std::max(P->sq_smem, seq_small_smem_bytes_host(J.n));
+      P->sq_smem = std::max(P->sq_smem, seq_small_smem_bytes_host(J.n, G.V, d.maxin));
       P->sf_seq[i] = 1;
       P->prep_small[job_prep[i]] = 1;
     }

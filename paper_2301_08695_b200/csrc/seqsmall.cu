@@ -54,6 +54,8 @@ constexpr int kQPairs = 512;  // live pairs per problem
 constexpr int kQKI = 8;       // parents recorded per ready slot (the rest read from the graph)
 constexpr int kQKO = 8;       // children recorded per ready slot
 constexpr int kQWarps = 8;    // CTA size for the init; warp 0 alone schedules
+constexpr int kQPendV = 160 * 1024;  // largest graph whose pending counts live in shared memory
+constexpr size_t kQSmemMax = 220 * 1024;  // dynamic shared memory per CTA
 
 __host__ __device__ inline int seq_small_slots(int n) { return kQPairs / (n > 0 ? n : 1); }
 
@@ -63,7 +65,12 @@ __host__ __device__ inline size_t seq_small_smem_bytes(int n) {
          + ns * (8 + 8)                              // k, need
          + ns * kQKI * (8 + 8)                       // parent finish, comm time
          + ns * kQKI * 4 + ns * kQKO * 4             // parent index << 5 | device; children
-         + ns * 4 * 9 + 64;                          // node, inb, deg, outb, odeg, mask, act, free, apos
+         + ns * 4 * 9 + 64 + 64;                     // node, inb, deg, outb, odeg, mask, act, free, apos
+}
+
+// with the pending counts in shared memory (one byte a node)
+__host__ __device__ inline size_t seq_small_smem_bytes_pend(int n, int V) {
+  return seq_small_smem_bytes(n) + ((static_cast<size_t>(V) + 15) & ~size_t(15));
 }
 
 struct QSm {
@@ -76,6 +83,8 @@ struct QSm {
   uint32_t *mask;                 // [ns] live devices of a slot
   int32_t *cnt;                   // [32] exec-order counters
   int32_t *ctl;                   // [4] init: source count
+  uint8_t *pend;                  // [V] parents not yet placed (graphs with in-degrees < 256 and
+                                  // V <= kQPendV), else null: the job's pending array in HBM
 };
 
 __device__ __forceinline__ QSm seq_small_layout(unsigned char *base, int n) {
@@ -110,6 +119,7 @@ __device__ __forceinline__ QSm seq_small_layout(unsigned char *base, int n) {
   p32 += 9 * ns;
   m.cnt = p32;
   m.ctl = p32 + 32;
+  m.pend = reinterpret_cast<uint8_t *>(p32 + 48);
   return m;
 }
 
@@ -204,9 +214,15 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
   }
   __syncthreads();
   const uint32_t full = n >= 32 ? 0xffffffffu : (1u << n) - 1u;
+  // pending counts: bytes in shared memory when every in-degree fits one and
+  // the slot tables plus V bytes fit the SM (the host sizes the launch alike)
+  const bool pend_s = jb.maxin < 256 && V <= kQPendV && seq_small_smem_bytes_pend(n, V) <= kQSmemMax;
   for (int j = tid; j < V; j += 32 * kQWarps) {
     const int ib = g.in_off[j], indeg = g.in_off[j + 1] - ib;
-    jb.pending[j] = indeg;
+    if (pend_s)
+      m.pend[j] = static_cast<uint8_t>(indeg);
+    else
+      jb.pending[j] = indeg;
     jb.device_of[j] = -1;
     if (indeg == 0) {
       const int s = atomicAdd(m.ctl, 1);
@@ -232,6 +248,8 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
   if (R * n > kQPairs) return;  // frontier too wide from the start
   for (int s = R + lane; s < ns; s += 32) m.freel[s - R] = s;  // free slots, popped from the end
   int nfree = ns - R;
+  // pair x = lane + 32 t <-> (active position a, device q): stepped, no division
+  const int a0 = lane / n, q0 = lane - (lane / n) * n, da = 32 / n, dq = 32 - (32 / n) * n;
   __syncwarp();
 
   int placed = 0, nexcl = 0, minptr = 0;
@@ -248,8 +266,11 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
     int64_t bt = kInf;
     unsigned bi = 0xffffffffu;
     int bs = -1;
-    for (int x = lane; x < np; x += 32) {
-      const int a = x / n, q = x - a * n;
+    for (int x = lane, a = a0, q = q0; x < np; x += 32, a += da, q += dq) {
+      if (q >= n) {
+        q -= n;
+        ++a;
+      }
       const int s = m.act[a];
       if (!((m.mask[s] >> q) & 1u)) continue;
       const int64_t key = seq_key(m, jb, g, pr, cache, n, s, q);
@@ -334,7 +355,7 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
     const int od = m.odeg[s];
     int child = -1;
     bool ready = false;
-    if (lane < od && lane < kQKO) {
+    if (!pend_s && lane < od && lane < kQKO) {
       child = m.sco[s * kQKO + lane];
       ready = atomicSub(jb.pending + child, 1) == 1;
     }
@@ -373,16 +394,27 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
 
     // ---- readiness of the children (placers.cpp:256-268) -----------------------
     for (int y0 = 0; y0 < od; y0 += 32) {
-      if (y0 > 0) {  // children past the first 32 (the first kQKO came from the slot)
-        const int y = y0 + lane;
+      // (HBM counts: the slot's first kQKO children were decremented above)
+      const int y = y0 + lane;
+      const bool fresh = pend_s || y0 > 0 || lane >= kQKO;
+      if (fresh) {
         child = -1;
         ready = false;
-        if (y < od) {
-          child = __ldg(g.edst + m.outb[s] + y);
-          ready = atomicSub(jb.pending + child, 1) == 1;
+        if (y < od) child = y < kQKO ? m.sco[s * kQKO + y] : __ldg(g.edst + m.outb[s] + y);
+      }
+      if (pend_s) {
+        // one warp owns the counts: lanes holding the same child (a repeated
+        // edge) fold into one decrement by the group's first lane
+        const unsigned has = __ballot_sync(kFull, child >= 0);
+        if (child >= 0) {
+          const unsigned grp = __match_any_sync(has, child);
+          if (lane == __ffs(grp) - 1) {
+            const int v = static_cast<int>(m.pend[child]) - __popc(grp);
+            m.pend[child] = static_cast<uint8_t>(v);
+            ready = v == 0;
+          }
         }
-      } else if (lane >= kQKO && lane < od) {
-        child = __ldg(g.edst + m.outb[s] + lane);
+      } else if (fresh && child >= 0) {
         ready = atomicSub(jb.pending + child, 1) == 1;
       }
       const unsigned b = __ballot_sync(kFull, ready);
@@ -417,8 +449,10 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
         if (k < m.deg[s3]) {
           const uint2 ip = __ldg(pr.in_pack + m.inb[s3] + k);
           const int i = static_cast<int>(ip.x);
-          m.piq[s3 * kQKI + k] = i << 5 | jb.device_of[i];
-          m.pf[s3 * kQKI + k] = jb.finish[i];
+          // the node just committed: from registers (its stores may still be
+          // on their way to L2)
+          m.piq[s3 * kQKI + k] = i << 5 | (i == j ? p : jb.device_of[i]);
+          m.pf[s3 * kQKI + k] = i == j ? fin : jb.finish[i];
           m.pc[s3 * kQKI + k] = static_cast<int64_t>(ip.y & 0xffffu);
         }
         if (k < m.odeg[s3]) m.sco[s3 * kQKO + k] = __ldg(g.edst + m.outb[s3] + k);
@@ -465,7 +499,11 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
   }
 }
 
-size_t seq_small_smem_bytes_host(int n) { return seq_small_smem_bytes(n); }
+// launch bytes for a job: the slot tables, plus its pending counts when they fit
+size_t seq_small_smem_bytes_host(int n, int V, int maxin) {
+  const size_t b = seq_small_smem_bytes_pend(n, V);
+  return maxin < 256 && V <= kQPendV && b <= kQSmemMax ? b : seq_small_smem_bytes(n);
+}
 
 // One CTA per job (`order` lists the K2q jobs).
 void launch_seq_small(const DJob *jobs, const int32_t *order, int nj, const DGraph *graphs, const DPrep *preps,
