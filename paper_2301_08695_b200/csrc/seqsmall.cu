@@ -147,12 +147,30 @@ __device__ __forceinline__ QPar seq_parent(const QSm &m, const DJob &jb, const D
 }
 
 // schedulable_time(j, q) of ready slot s on the live tails (placers.cpp:43-79).
+// Branch-free per parent (lanes of a warp hold pairs whose parents take
+// different cases: local, cached, a new transfer), so the warp issues each
+// parent's step once instead of once per case.
 __device__ __forceinline__ int64_t seq_key(const QSm &m, const DJob &jb, const DGraph &g, const DPrep &pr,
                                            const int64_t *__restrict__ cache, int n, int s, int q) {
   int64_t key = m.F[q];
   int64_t T = m.tail[q];
   const int deg = m.deg[s];
-  for (int k = 0; k < deg; ++k) {
+  const int kk = deg < kQKI ? deg : kQKI;
+  const int base = s * kQKI;
+  for (int k = 0; k < kk; ++k) {
+    const int iq = m.piq[base + k];
+    const int64_t f = m.pf[base + k], c = m.pc[base + k];
+    const int qi = iq & 31;
+    const bool local = qi == q;
+    // (a local parent reads its own row: a harmless valid address)
+    const int64_t ca = cache[(iq >> 5) * n + q];
+    const bool cached = !local && ca >= 0;
+    const int64_t tn = max64(max64(f, T), m.tail[qi]) + c;
+    const int64_t term = local ? f : (cached ? max64(f, ca) : tn);
+    T = (local || cached) ? T : tn;
+    key = max64(key, term);
+  }
+  for (int k = kQKI; k < deg; ++k) {  // parents past the slot record: from the graph
     const QPar a = seq_parent(m, jb, g, pr, s, k);
     const int qi = a.iq & 31, i = a.iq >> 5;
     if (qi == q) {
