@@ -150,8 +150,16 @@ __device__ __forceinline__ QPar seq_parent(const QSm &m, const DJob &jb, const D
 // Branch-free per parent (lanes of a warp hold pairs whose parents take
 // different cases: local, cached, a new transfer), so the warp issues each
 // parent's step once instead of once per case.
+// The fold's new transfers (uncached remote parents, in order) are its commit
+// recipe: nt of them, the first two as (parent << 5 | device, arrival).
+struct QRecipe {
+  int nt, a0, a1;
+  int64_t t0, t1;
+};
+
 __device__ __forceinline__ int64_t seq_key(const QSm &m, const DJob &jb, const DGraph &g, const DPrep &pr,
-                                           const int64_t *__restrict__ cache, int n, int s, int q) {
+                                           const int64_t *__restrict__ cache, int n, int s, int q, QRecipe &rc) {
+  rc.nt = 0;
   int64_t key = m.F[q];
   int64_t T = m.tail[q];
   const int deg = m.deg[s];
@@ -167,8 +175,19 @@ __device__ __forceinline__ int64_t seq_key(const QSm &m, const DJob &jb, const D
     const bool cached = !local && ca >= 0;
     const int64_t tn = max64(max64(f, T), m.tail[qi]) + c;
     const int64_t term = local ? f : (cached ? max64(f, ca) : tn);
-    T = (local || cached) ? T : tn;
+    const bool xfer = !local && !cached;
+    T = xfer ? tn : T;
     key = max64(key, term);
+    if (xfer) {
+      if (rc.nt == 0) {
+        rc.a0 = iq;
+        rc.t0 = tn;
+      } else if (rc.nt == 1) {
+        rc.a1 = iq;
+        rc.t1 = tn;
+      }
+      ++rc.nt;
+    }
   }
   for (int k = kQKI; k < deg; ++k) {  // parents past the slot record: from the graph
     const QPar a = seq_parent(m, jb, g, pr, s, k);
@@ -182,6 +201,7 @@ __device__ __forceinline__ int64_t seq_key(const QSm &m, const DJob &jb, const D
       } else {
         T = max64(max64(a.f, T), m.tail[qi]) + a.c;
         key = max64(key, T);
+        rc.nt += 3;  // (past the slot record: the commit replays the full fold)
       }
     }
   }
@@ -284,6 +304,8 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
     int64_t bt = kInf;
     unsigned bi = 0xffffffffu;
     int bs = -1;
+    QRecipe best;
+    best.nt = 0;
     for (int x = lane, a = a0, q = q0; x < np; x += 32, a += da, q += dq) {
       if (q >= n) {
         q -= n;
@@ -291,12 +313,14 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
       }
       const int s = m.act[a];
       if (!((m.mask[s] >> q) & 1u)) continue;
-      const int64_t key = seq_key(m, jb, g, pr, cache, n, s, q);
+      QRecipe rc;
+      const int64_t key = seq_key(m, jb, g, pr, cache, n, s, q, rc);
       const unsigned id = static_cast<unsigned>(m.node[s]) << 5 | static_cast<unsigned>(q);
       if (key < bt || (key == bt && id < bi)) {
         bt = key;
         bi = id;
         bs = s;
+        best = rc;
       }
     }
     const int64_t mykey = bt;
@@ -308,7 +332,9 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
       break;
     }
     const unsigned owner = __ballot_sync(kFull, mykey == bt && myid == bi);
-    const int s = __shfl_sync(kFull, bs, __ffs(owner) - 1);
+    const int olane = __ffs(owner) - 1;
+    const int s = __shfl_sync(kFull, bs, olane);
+    const int nt = __shfl_sync(kFull, best.nt, olane);
     const int j = static_cast<int>(bi >> 5), p = static_cast<int>(bi & 31u);
     const int64_t t = bt;
     const int64_t needj = m.need[s];
@@ -378,7 +404,19 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
       ready = atomicSub(jb.pending + child, 1) == 1;
     }
     if (lane < n) cache[static_cast<int64_t>(j) * n + lane] = -1;  // j's arrival row
-    if (lane == 0) {
+    if (nt <= 2) {
+      // commit_schedulable_time from the winner's recipe: its fold ran on
+      // this very state, so the commit is the recipe's stores
+      if (lane == olane && nt > 0) {
+        m.tail[best.a0 & 31] = best.t0;
+        cache[(best.a0 >> 5) * n + p] = best.t0;
+        if (nt > 1) {
+          m.tail[best.a1 & 31] = best.t1;
+          cache[(best.a1 >> 5) * n + p] = best.t1;
+        }
+        m.tail[p] = nt > 1 ? best.t1 : best.t0;
+      }
+    } else if (lane == 0) {
       int64_t Tp = m.tail[p];
       for (int k = 0; k < deg; ++k) {
         const QPar a = seq_parent(m, jb, g, pr, s, k);
@@ -392,6 +430,8 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
         *slot = term;
       }
       m.tail[p] = Tp;
+    }
+    if (lane == 0) {
       m.F[p] = fin;
       m.res[p] += needj;
       jb.device_of[j] = p;
@@ -421,16 +461,12 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
         if (y < od) child = y < kQKO ? m.sco[s * kQKO + y] : __ldg(g.edst + m.outb[s] + y);
       }
       if (pend_s) {
-        // one warp owns the counts: lanes holding the same child (a repeated
-        // edge) fold into one decrement by the group's first lane
-        const unsigned has = __ballot_sync(kFull, child >= 0);
+        // one warp owns the counts, and a node's children are distinct (meta
+        // edges are unique, checked when the graph is made)
         if (child >= 0) {
-          const unsigned grp = __match_any_sync(has, child);
-          if (lane == __ffs(grp) - 1) {
-            const int v = static_cast<int>(m.pend[child]) - __popc(grp);
-            m.pend[child] = static_cast<uint8_t>(v);
-            ready = v == 0;
-          }
+          const int v = static_cast<int>(m.pend[child]) - 1;
+          m.pend[child] = static_cast<uint8_t>(v);
+          ready = v == 0;
         }
       } else if (fresh && child >= 0) {
         ready = atomicSub(jb.pending + child, 1) == 1;
