@@ -106,28 +106,22 @@ __device__ __forceinline__ int64_t key_of(const Ctx &c, int j, int q, int32_t &g
     }
     return t;
   }
+  // sequential comm: the fold on a copy of the tails (placers.cpp:83-91)
+  // without the copy — after the first new transfer the copy's tail of q is
+  // the running term T and every device it touched holds a value <= T, so a
+  // transfer from d starts at max(finish, T, tail[d]) on the LIVE tails
+  (void)gen;
   int64_t t = c.F[q];
-  ++gen;
+  int64_t T = c.tail[q];
   for (int x = b; x < e; ++x) {
-    int d = c.pdev[x];
-    int64_t f = c.pfin[x];
-    int64_t term;
-    if (d == q) {
-      term = f;
-    } else {
-      int64_t cached = c.cache[static_cast<int64_t>(c.in_src[x]) * n + q];
-      if (cached >= 0) {
-        term = max64(f, cached);
-      } else {
-        int64_t td = c.scg[d] == gen ? c.scv[d] : c.tail[d];
-        int64_t tq = c.scg[q] == gen ? c.scv[q] : c.tail[q];
-        term = max64(f, max64(td, tq)) + c.in_c[x];
-        c.scv[d] = term;
-        c.scg[d] = gen;
-        c.scv[q] = term;
-        c.scg[q] = gen;
-      }
-    }
+    const int d = c.pdev[x];
+    const int64_t f = c.pfin[x];
+    const bool local = d == q;
+    const int64_t cached = local ? -1 : c.cache[static_cast<int64_t>(c.in_src[x]) * n + q];
+    const bool xfer = !local && cached < 0;
+    const int64_t tn = max64(max64(f, T), c.tail[local ? q : d]) + c.in_c[x];
+    const int64_t term = local ? f : (xfer ? tn : max64(f, cached));
+    T = xfer ? tn : T;
     t = max64(t, term);
   }
   return t;

@@ -41,8 +41,8 @@ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? 
 
 // schedulable_time_impl (placers.cpp:43-79) as an estimate. Parallel mode
 // returns the data-ready time (t0 = 0 gives the max over parent terms);
-// sequential mode folds the queue tails in ascending in-edge order through
-// this lane's scratch copy (generation-tagged, so no copy is made).
+// sequential mode folds the queue tails in ascending in-edge order (the
+// reference folds a copy of them; the running term stands in for the copy).
 __device__ __forceinline__ int64_t est_time(const Ctx &c, int j, int p, int64_t t0, int32_t &gen) {
   int64_t t = t0;
   const int b = c.in_off[j], e = c.in_off[j + 1];
@@ -62,28 +62,22 @@ __device__ __forceinline__ int64_t est_time(const Ctx &c, int j, int p, int64_t 
       t = max64(t, term);
     }
   } else {
-    ++gen;
+    // no copy of the tails: after the first new transfer the copy's tail of
+    // p is the running term T and every device touched since holds a value
+    // <= T, so a transfer from q starts at max(finish, T, tail[q]) on the
+    // LIVE tails
+    (void)gen;
+    int64_t T = c.tail[p];
     for (int x = b; x < e; ++x) {
-      int i = c.in_src[x];
-      int q = c.device_of[i];
-      int64_t fin = c.finish[i];
-      int64_t term;
-      if (q == p) {
-        term = fin;
-      } else {
-        int64_t cached = c.cache[static_cast<int64_t>(i) * n + p];
-        if (cached >= 0) {
-          term = max64(fin, cached);
-        } else {
-          int64_t tq = c.scg[q] == gen ? c.scv[q] : c.tail[q];
-          int64_t tp = c.scg[p] == gen ? c.scv[p] : c.tail[p];
-          term = max64(fin, max64(tq, tp)) + c.in_c[x];
-          c.scv[q] = term;
-          c.scg[q] = gen;
-          c.scv[p] = term;
-          c.scg[p] = gen;
-        }
-      }
+      const int i = c.in_src[x];
+      const int q = c.device_of[i];
+      const int64_t fin = c.finish[i];
+      const bool local = q == p;
+      const int64_t cached = local ? -1 : c.cache[static_cast<int64_t>(i) * n + p];
+      const bool xfer = !local && cached < 0;
+      const int64_t tn = max64(max64(fin, T), c.tail[q]) + c.in_c[x];
+      const int64_t term = local ? fin : (xfer ? tn : max64(fin, cached));
+      T = xfer ? tn : T;
       t = max64(t, term);
     }
   }
