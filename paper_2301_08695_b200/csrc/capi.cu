@@ -730,8 +730,6 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
     // out-edges: the list placers never touch the cache (DJob::nocache)
     d.nocache = J.algo != BX_ALGO_MTOPO && J.cm.mode == BX_COMM_PARALLEL && g_nu[J.graph] == 0;
     if (!d.nocache) P->fills.push_back({d.cache, 0xffffffffu, 8 * size_t(V * n)});
-    if (J.cm.mode != BX_COMM_PARALLEL)  // generation tags of the sequential folds' scratch tails
-      P->fills.push_back({d.sc_gen, 0, 4 * size_t(256 * n)});
     if (d.skip) {  // the status record carries the host verdict (message kept host-side)
       P->fills.push_back({d.err, static_cast<uint32_t>(st), 4});
       P->fills.push_back({reinterpret_cast<char *>(d.err) + 4, static_cast<uint32_t>(E_HOST), 4});
