@@ -24,20 +24,27 @@
 //      transfer from q is max(finish_i, T, tail[q]) with the LIVE tail[q].
 //      Then two REDUX for the 64-bit key, one for (node << 5 | device); the
 //      owner lane names the winner's slot;
-//   2. discard (placers.cpp:203-219) or commit: lane 0 replays the fold on the
-//      live tails and records the arrivals (commit_schedulable_time,
-//      :95-101; a cache row is initialised when its producer commits),
-//      dev_free / reserved / outputs;
+//   2. discard (placers.cpp:203-219) or commit: the winner's key fold ran on
+//      exactly the state the commit sees, so it doubles as the commit recipe
+//      (its new transfers: parent, device, arrival) and the winner's lane
+//      stores the tails and cache arrivals (commit_schedulable_time,
+//      :95-101; a cache row is initialised when its producer commits; more
+//      than two transfers: lane 0 replays the fold), dev_free / reserved /
+//      outputs;
 //   3. readiness of the children (:256-268): the slot's first 8 children
-//      were cached when it became ready, so the pending-count atomics issue
-//      straight from shared memory; the new slots' records load in one level
-//      of independent reads past the node's offsets.
+//      were cached when it became ready; pending counts are bytes in shared
+//      memory when they fit (one warp owns them; meta edges are unique), else
+//      the job's HBM array with atomics issued before the commit; the new
+//      slots' records load in one level of independent reads past the node's
+//      offsets.
+// The per-parent step is branch-free: lanes hold pairs whose parents take
+// different cases, and a branchy fold made the warp issue every case's path.
 // Measured and rejected (the reference's layered-chain 100k x 4, sequential
 // comm): several commits per round while a commit moves no queue tail (1.33
-// commits per round there: the extra selection state costs more than it
-// saves, 265 -> 316 ms), cache arrivals mirrored into the slot records
-// (shared-memory keys, but one more load level for every new slot and a
-// propagation pass per transfer).
+// commits per round there), cache arrivals mirrored into the slot records, a
+// shared-memory table of recent producers' cache rows, the children's node
+// fields recorded with their parent's slot, L1 prefetches of them each step
+// (K2q).
 //
 // Times stay int64 (no range checks). Eligibility (checked on the device):
 // acyclic, non-negative byte counts and compute times, comm times in

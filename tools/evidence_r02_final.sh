@@ -10,7 +10,7 @@ timeout 900 python bench.py > $O/fin_bench.log 2>&1; echo "bench rc=$?"
 grep '^{' $O/fin_bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['ms_per_step'], d['roofline']['kernel_ms'], d['parity_vs_reference'])"
 timeout 900 python tools/latency_table.py C1_inception_mtopo_metf C1_inception_nocoplace C2_gnmt_metf_coplace C3_transformer_msct_tight > $O/fin_latency.jsonl 2>&1; echo "latency rc=$?"
 timeout 900 python tools/latency_table.py refchain1M_x64 >> $O/fin_latency.jsonl 2>&1; echo "refchain1M rc=$?"; tail -1 $O/fin_latency.jsonl | cut -c1-300
-timeout 900 python tools/latency_table.py seq_refchain100k_x4 seq_refchain100k_x8 seq_layered100k_x4 >> $O/fin_latency.jsonl 2>&1; echo "seq rc=$?"; tail -3 $O/fin_latency.jsonl | cut -c1-300
+timeout 900 python tools/latency_table.py seq_refchain100k_x4 seq_refchain100k_x8 seq_layered100k_x4 seq_wide100k_x16 >> $O/fin_latency.jsonl 2>&1; echo "seq rc=$?"; tail -4 $O/fin_latency.jsonl | cut -c1-300
 timeout 600 python tools/k2s_profile.py seq_refchain100k_x4 refchain100k_x4 > $O/fin_phases.jsonl 2>&1; echo "phases rc=$?"
 timeout 900 python tools/lp_bench.py > $O/fin_lp.jsonl 2>&1; echo "lp rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/fin_launches.csv \
