@@ -34,6 +34,7 @@ void launch_prep_small(const DGraph &g, const DPrep &pr, cudaStream_t s);
 void launch_small_frontier(const DJob *jobs, const int32_t *order, const int *cnt, const DGraph *graphs,
                            const DPrep *preps, const size_t *smem, bool prof, cudaStream_t s);
 size_t small_smem_bytes_host(int V, int n, int nucap, int nccap);
+size_t small_pend_bytes_host(int V, int n, int nucap, int nccap, int maxin);
 size_t seq_small_smem_bytes_host(int n, int V, int maxin);
 void launch_seq_small(const DJob *jobs, const int32_t *order, int nj, const DGraph *graphs, const DPrep *preps,
                       size_t smem, bool prof, cudaStream_t s);
@@ -755,7 +756,9 @@ static int plan_create(int32_t ngraphs, const bx_graph *graphs, int32_t njobs, c
       if (!glob || smg <= 200 * 1024) {
         d.sdone = at<int32_t>(pool, o.sdone);
         P->fills.push_back({d.sdone, 0, 4});
-        P->sf_smem[glob] = std::max(P->sf_smem[glob], glob ? smg : sm);
+        // (node state in HBM: + the pending counts as bytes when they fit)
+        P->sf_smem[glob] = std::max(P->sf_smem[glob],
+                                    glob ? smg + small_pend_bytes_host(G.V, J.n, d.nucap, nccap, d.maxin) : sm);
         P->sf_global[i] = glob;
         P->prep_small[job_prep[i]] = 1;
       }

@@ -142,6 +142,16 @@ __host__ __device__ inline size_t small_smem_bytes(int V, int n, int nucap, int 
   return b + 64;
 }
 
+// Node state in HBM: the pending counts still fit shared memory as bytes
+// (one word holds four) when every in-degree is below 256 and the slot tables
+// plus V bytes stay within kSPendMax; the extra bytes past the slot tables, or 0.
+constexpr size_t kSPendMax = 200 * 1024;
+__host__ __device__ inline size_t small_pend_bytes(int V, int n, int nucap, int nccap, int maxin) {
+  const size_t base = (small_smem_bytes(0, n, nucap, nccap) + 15) & ~size_t(15);
+  const size_t extra = base - small_smem_bytes(0, n, nucap, nccap) + ((static_cast<size_t>(V) + 3) & ~size_t(3));
+  return maxin < 256 && small_smem_bytes(0, n, nucap, nccap) + extra <= kSPendMax ? extra : 0;
+}
+
 __device__ __forceinline__ SSm small_layout(unsigned char *base, int V, int n, int nucap, int nccap) {
   SSm m;
   int64_t *p64 = reinterpret_cast<int64_t *>(base);
@@ -510,6 +520,10 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
     return;
   const int32_t cmax = static_cast<int32_t>(cmax64);
   SSm m = small_layout(smem, kGlobal ? 0 : V, n, jb.nucap, nccap);
+  // kGlobal: pending counts as bytes in shared memory when they fit
+  uint32_t *pend8 = nullptr;
+  if (kGlobal && small_pend_bytes(V, n, jb.nucap, nccap, jb.maxin) > 0)
+    pend8 = reinterpret_cast<uint32_t *>(smem + ((small_smem_bytes(0, n, jb.nucap, nccap) + 15) & ~size_t(15)));
   if (kGlobal) {
     m.info = reinterpret_cast<uint64_t *>(jb.finish);    // [V] int64
     m.pending = reinterpret_cast<uint16_t *>(jb.pending);  // [V] int32 words hold 2V halves
@@ -543,7 +557,10 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
       const int4 nd = __ldg(G.node + j);
       const int indeg = nd.z & 0xffff;
       m.info[j] = 0xffffffffull;
-      m.pending[j] = static_cast<uint16_t>(indeg);
+      if (kGlobal && pend8)
+        reinterpret_cast<uint8_t *>(pend8)[j] = static_cast<uint8_t>(indeg);
+      else
+        m.pending[j] = static_cast<uint16_t>(indeg);
       m.rpos[j] = -1;
       src = indeg == 0;
     }
@@ -738,9 +755,14 @@ __global__ void __launch_bounds__(32 * kSWarm, 1)
         child = slot_child(m, G, ito >> 16, ito & 0xffff);
         // 16-bit counters decremented through their 32-bit word (a counter
         // is >= 1 when decremented, so no borrow crosses halves)
-        unsigned *word = reinterpret_cast<unsigned *>(m.pending) + (child >> 1);
-        const int sh = 16 * (child & 1);
-        ready = ((atomicSub(word, 1u << sh) >> sh) & 0xffffu) == 1;
+        if (kGlobal && pend8) {  // bytes in shared memory, four to a word (same no-borrow argument)
+          const int sh = 8 * (child & 3);
+          ready = ((atomicSub(pend8 + (child >> 2), 1u << sh) >> sh) & 0xffu) == 1;
+        } else {
+          unsigned *word = reinterpret_cast<unsigned *>(m.pending) + (child >> 1);
+          const int sh = 16 * (child & 1);
+          ready = ((atomicSub(word, 1u << sh) >> sh) & 0xffffu) == 1;
+        }
         if (ready) asm volatile("prefetch.global.L1 [%0];" ::"l"(G.node + child));
       }
       if (hin) {
@@ -918,6 +940,9 @@ void launch_prep_small(const DGraph &g, const DPrep &pr, cudaStream_t s) {
 }
 
 size_t small_smem_bytes_host(int V, int n, int nucap, int nccap) { return small_smem_bytes(V, n, nucap, nccap); }
+size_t small_pend_bytes_host(int V, int n, int nucap, int nccap, int maxin) {
+  return small_pend_bytes(V, n, nucap, nccap, maxin);
+}
 
 // One CTA per job; `order` lists the K2s jobs, m-ETF first.
 template <bool kSct, bool kProf, bool kGlobal>
