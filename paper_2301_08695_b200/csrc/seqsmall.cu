@@ -488,13 +488,13 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
       if (ready) {
         const int r = __popc(b & ((1u << lane) - 1u));
         const int s2 = m.freel[nfree - 1 - r];
-        const int ib = g.in_off[child], ob = g.out_off[child];
-        const int ie = g.in_off[child + 1], oe = g.out_off[child + 1];
+        const int ib = __ldg(g.in_off + child), ob = __ldg(g.out_off + child);
+        const int ie = __ldg(g.in_off + child + 1), oe = __ldg(g.out_off + child + 1);
         m.act[R + r] = s2;
         m.apos[s2] = R + r;
         m.node[s2] = child;
-        m.k[s2] = g.k[child];
-        m.need[s2] = g.need[child];
+        m.k[s2] = __ldg(g.k + child);
+        m.need[s2] = __ldg(g.need + child);
         m.inb[s2] = ib;
         m.deg[s2] = ie - ib;
         m.outb[s2] = ob;
