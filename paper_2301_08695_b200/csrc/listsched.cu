@@ -74,13 +74,13 @@ constexpr int kDirty = 1, kComplete = 2;
 // from the per-slot parent arrays. Parallel mode: data-ready time (t0 = 0).
 // Sequential: the full fold through this lane's generation-tagged scratch.
 __device__ __forceinline__ int64_t key_of(const Ctx &c, int j, int q, int32_t &gen) {
-  const int b = c.in_off[j], e = c.in_off[j + 1];
+  const int b = __ldg(c.in_off + (j)), e = __ldg(c.in_off + (j + 1));
   const int n = c.n;
   if (c.mode == 1 && c.nocache) {
     int64_t t = 0;
     for (int x = b; x < e; ++x) {
       const int64_t f = c.pfin[x];
-      t = max64(t, c.pdev[x] == q ? f : f + c.in_c[x]);
+      t = max64(t, c.pdev[x] == q ? f : f + __ldg(c.in_c + (x)));
     }
     return t;
   }
@@ -90,8 +90,8 @@ __device__ __forceinline__ int64_t key_of(const Ctx &c, int j, int q, int32_t &g
     for (; x + 1 < e; x += 2) {  // two parents per round: loads issue together
       int d0 = c.pdev[x], d1 = c.pdev[x + 1];
       int64_t f0 = c.pfin[x], f1 = c.pfin[x + 1];
-      int i0 = c.in_src[x], i1 = c.in_src[x + 1];
-      int64_t c0 = c.in_c[x], c1 = c.in_c[x + 1];
+      int i0 = __ldg(c.in_src + (x)), i1 = __ldg(c.in_src + (x + 1));
+      int64_t c0 = __ldg(c.in_c + (x)), c1 = __ldg(c.in_c + (x + 1));
       int64_t a0 = d0 == q ? -1 : c.cache[static_cast<int64_t>(i0) * n + q];
       int64_t a1 = d1 == q ? -1 : c.cache[static_cast<int64_t>(i1) * n + q];
       int64_t t0 = d0 == q ? f0 : (a0 >= 0 ? max64(f0, a0) : f0 + c0);
@@ -101,8 +101,8 @@ __device__ __forceinline__ int64_t key_of(const Ctx &c, int j, int q, int32_t &g
     if (x < e) {
       int d0 = c.pdev[x];
       int64_t f0 = c.pfin[x];
-      int64_t a0 = d0 == q ? -1 : c.cache[static_cast<int64_t>(c.in_src[x]) * n + q];
-      t = max64(t, d0 == q ? f0 : (a0 >= 0 ? max64(f0, a0) : f0 + c.in_c[x]));
+      int64_t a0 = d0 == q ? -1 : c.cache[static_cast<int64_t>(__ldg(c.in_src + (x))) * n + q];
+      t = max64(t, d0 == q ? f0 : (a0 >= 0 ? max64(f0, a0) : f0 + __ldg(c.in_c + (x))));
     }
     return t;
   }
@@ -117,9 +117,9 @@ __device__ __forceinline__ int64_t key_of(const Ctx &c, int j, int q, int32_t &g
     const int d = c.pdev[x];
     const int64_t f = c.pfin[x];
     const bool local = d == q;
-    const int64_t cached = local ? -1 : c.cache[static_cast<int64_t>(c.in_src[x]) * n + q];
+    const int64_t cached = local ? -1 : c.cache[static_cast<int64_t>(__ldg(c.in_src + (x))) * n + q];
     const bool xfer = !local && cached < 0;
-    const int64_t tn = max64(max64(f, T), c.tail[local ? q : d]) + c.in_c[x];
+    const int64_t tn = max64(max64(f, T), c.tail[local ? q : d]) + __ldg(c.in_c + (x));
     const int64_t term = local ? f : (xfer ? tn : max64(f, cached));
     T = xfer ? tn : T;
     t = max64(t, term);
@@ -129,7 +129,7 @@ __device__ __forceinline__ int64_t key_of(const Ctx &c, int j, int q, int32_t &g
 
 __device__ __forceinline__ int64_t urgency_e(const Ctx &c, int j) {
   int64_t u = 0;
-  for (int x = c.in_off[j]; x < c.in_off[j + 1]; ++x) u = max64(u, c.pfin[x] + c.in_c[x]);
+  for (int x = __ldg(c.in_off + (j)); x < __ldg(c.in_off + (j + 1)); ++x) u = max64(u, c.pfin[x] + __ldg(c.in_c + (x)));
   return u;
 }
 
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
       c.F[d] = 0;
       c.tail[d] = 0;
       c.res[d] = 0;
-      c.capS[d] = c.cap[d];
+      c.capS[d] = __ldg(c.cap + (d));
       c.awu[d] = 0;
       c.awf[d] = -1;
       c.excl[d] = 0;
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
       int j = base + lane;
       bool src = false;
       if (j < V) {
-        int indeg = g.in_off[j + 1] - g.in_off[j];
+        int indeg = __ldg(g.in_off + (j + 1)) - __ldg(g.in_off + (j));
         c.pending[j] = indeg;
         c.device_of[j] = -1;  // (finish times reach the children through pfin: no per-node copy)
         src = indeg == 0;
@@ -841,8 +841,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
     // the winner's metadata and the last ready slot (swap-removed on a
     // commit; nothing before the swap writes it in a commit step), all
     // independent loads issued together
-    const int64_t needj = c.need[j], kj = c.k[j];
-    const int ib = c.in_off[j], ie = c.in_off[j + 1], ob = c.out_off[j], oe = c.out_off[j + 1];
+    const int64_t needj = __ldg(c.need + (j)), kj = __ldg(c.k + (j));
+    const int ib = __ldg(c.in_off + (j)), ie = __ldg(c.in_off + (j + 1)), ob = __ldg(c.out_off + (j)), oe = __ldg(c.out_off + (j + 1));
     const int last = R - 1;
     int mv = 0;
     int64_t mv_urg = 0, mv_kc = 0;
@@ -876,8 +876,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
       // placers.cpp:126,208): first unplaced node in ascending-need order
       int64_t minrem = 0;
       if (lane == 0) {
-        while (c.device_of[g.need_order[minptr]] >= 0) ++minptr;
-        minrem = c.need[g.need_order[minptr]];
+        while (c.device_of[__ldg(g.need_order + (minptr))] >= 0) ++minptr;
+        minrem = __ldg(c.need + (__ldg(g.need_order + (minptr))));
       }
       minrem = __shfl_sync(kFull, minrem, 0);
       if (c.res[p] + minrem > c.capS[p]) {
@@ -925,11 +925,11 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
         bool fresh = false;
         int i = 0;
         if (x < ie) {
-          i = c.in_src[x];
+          i = __ldg(c.in_src + (x));
           if (c.pdev[x] != p) {
             int64_t *slot = c.cache + static_cast<int64_t>(i) * n + p;
             if (*slot < 0) {
-              *slot = c.pfin[x] + c.in_c[x];
+              *slot = c.pfin[x] + __ldg(c.in_c + (x));
               // a producer whose out-edges all carry the same bytes caches
               // finish + the same c its other consumers already use: their
               // keys cannot change, so no re-key (parallel mode only)
@@ -947,10 +947,10 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
       for (int x = ib; x < ie; ++x) {
         int d = c.pdev[x];
         if (d == p) continue;
-        int i = c.in_src[x];
+        int i = __ldg(c.in_src + (x));
         int64_t *slot = c.cache + static_cast<int64_t>(i) * n + p;
         if (*slot >= 0) continue;
-        int64_t term = max64(c.pfin[x], max64(c.tail[d], c.tail[p])) + c.in_c[x];
+        int64_t term = max64(c.pfin[x], max64(c.tail[d], c.tail[p])) + __ldg(c.in_c + (x));
         c.tail[d] = term;
         c.tail[p] = term;
         *slot = term;
@@ -1006,7 +1006,7 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
             c.awf[q] = -1;
             T.flg[q] |= kDirty;
           }
-        int h = c.fav[j];
+        int h = __ldg(c.fav + (j));
         if (h >= 0 && c.device_of[h] < 0) {
           c.awf[p] = h;
           c.awu[p] = fin + c.cmax;
@@ -1025,8 +1025,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
       bool fresh = false;
       int child = -1;
       if (y < oe) {
-        child = c.out_dst[y];
-        int x = c.inpos[y];
+        child = __ldg(c.out_dst + (y));
+        int x = __ldg(c.inpos + (y));
         c.pdev[x] = p;
         c.pfin[x] = fin;
         fresh = --c.pending[child] == 0;
@@ -1052,8 +1052,8 @@ __global__ void __launch_bounds__(kW > 1 ? 32 * kW : 32 * BX_PPC, kW > 1 ? 1 : B
     // ---- cached parents change their other consumers' keys on p (:271-279)
     for (int a = 0; a < ncount; ++a) {
       int i = c.nc[a];
-      for (int y = c.out_off[i] + lane; y < c.out_off[i + 1]; y += 32) {
-        const int cc = c.out_dst[y];
+      for (int y = __ldg(c.out_off + (i)) + lane; y < __ldg(c.out_off + (i + 1)); y += 32) {
+        const int cc = __ldg(c.out_dst + (y));
         // the three node loads issue together (no short-circuit chain);
         // rpos is only trusted once the node is known ready and unplaced
         const int pend = c.pending[cc], dv = c.device_of[cc], s = c.rpos[cc];
@@ -1159,13 +1159,13 @@ struct RCommit {
 };
 
 __device__ __forceinline__ void rent_meta(REnt &e, const Ctx &c, const DGraph &g) {
-  e.need = c.need[e.j];
-  e.k = g.k[e.j];
-  e.fav = c.fav ? c.fav[e.j] : -1;
-  e.inb = g.in_off[e.j];
-  e.ine = g.in_off[e.j + 1];
-  e.outb = g.out_off[e.j];
-  e.oute = g.out_off[e.j + 1];
+  e.need = __ldg(c.need + (e.j));
+  e.k = __ldg(g.k + (e.j));
+  e.fav = c.fav ? __ldg(c.fav + (e.j)) : -1;
+  e.inb = __ldg(g.in_off + (e.j));
+  e.ine = __ldg(g.in_off + (e.j + 1));
+  e.outb = __ldg(g.out_off + (e.j));
+  e.oute = __ldg(g.out_off + (e.j + 1));
 }
 
 // Per-column sorted lists in shared memory, structure of arrays, entry k of
@@ -1511,7 +1511,7 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
   for (int d = tid; d < n; d += NT) {
     c.F[d] = 0;
     c.res[d] = 0;
-    c.capS[d] = c.cap[d];
+    c.capS[d] = __ldg(c.cap + (d));
     c.awu[d] = 0;
     c.awf[d] = -1;
     c.excl[d] = 0;
@@ -1520,7 +1520,7 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
   }
   __syncthreads();
   for (int j = tid; j < V; j += NT) {
-    int indeg = g.in_off[j + 1] - g.in_off[j];
+    int indeg = __ldg(g.in_off + (j + 1)) - __ldg(g.in_off + (j));
     c.pending[j] = indeg;
     c.device_of[j] = -1;
     c.rpos[j] = -1;  // read speculatively beside pending / device_of (the cached-consumer re-keys)
@@ -1797,8 +1797,8 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
           if (__any_sync(kFull, emptied)) thr = min64(thr, c.F[q]);  // its keys are >= F[q]
           int64_t minrem = 0;
           if (lane == 0) {
-            while (c.device_of[g.need_order[minptr]] >= 0) ++minptr;
-            minrem = c.need[g.need_order[minptr]];
+            while (c.device_of[__ldg(g.need_order + (minptr))] >= 0) ++minptr;
+            minrem = __ldg(c.need + (__ldg(g.need_order + (minptr))));
           }
           minrem = __shfl_sync(kFull, minrem, 0);
           if (c.res[q] + minrem > c.capS[q]) {
@@ -1969,10 +1969,10 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
         const RCommit &cm = CM[i];
         const int x = cm.inb + (w - inoff[i]);
         if (!c.nocache && c.pdev[x] != cm.q) {
-          const int par = c.in_src[x];
+          const int par = __ldg(c.in_src + (x));
           int64_t *slot = c.cache + static_cast<int64_t>(par) * n + cm.q;
           if (*slot < 0) {  // commit_schedulable_time, parallel mode
-            *slot = c.pfin[x] + c.in_c[x];
+            *slot = c.pfin[x] + __ldg(c.in_c + (x));
             if (pr.nu[par] >= 0) {  // uniform producers change no consumer key (see the warp kernel)
               int a = atomicAdd(&S->nnc, 1);
               c.nc[a] = par;
@@ -1987,8 +1987,8 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
         while (outoff[i + 1] <= w) ++i;
         const RCommit &cm = CM[i];
         const int y = cm.outb + (w - outoff[i]);
-        const int child = c.out_dst[y];
-        const int x = c.inpos[y];
+        const int child = __ldg(c.out_dst + (y));
+        const int x = __ldg(c.inpos + (y));
         c.pdev[x] = cm.q;
         c.pfin[x] = cm.fin;
         __threadfence_block();
@@ -2023,8 +2023,8 @@ __global__ void __launch_bounds__(RWARPS * 32, BX_ROUNDS_MINB)
       for (int a = warp; a < nnc; a += RWARPS) {
         const int par = c.nc[a];
         const int q = CM[jb.ncw[a]].q;
-        for (int y = g.out_off[par] + lane; y < g.out_off[par + 1]; y += 32) {
-          const int cc = c.out_dst[y];
+        for (int y = __ldg(g.out_off + (par)) + lane; y < __ldg(g.out_off + (par + 1)); y += 32) {
+          const int cc = __ldg(c.out_dst + (y));
           const int pend = c.pending[cc], dv = c.device_of[cc], s = c.rpos[cc];  // issued together
           if (pend != 0 || dv >= 0) continue;
           if (s >= R0) continue;  // new rows were keyed after the cache update

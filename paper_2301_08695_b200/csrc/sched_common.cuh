@@ -45,11 +45,11 @@ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? 
 // reference folds a copy of them; the running term stands in for the copy).
 __device__ __forceinline__ int64_t est_time(const Ctx &c, int j, int p, int64_t t0, int32_t &gen) {
   int64_t t = t0;
-  const int b = c.in_off[j], e = c.in_off[j + 1];
+  const int b = __ldg(c.in_off + (j)), e = __ldg(c.in_off + (j + 1));
   const int n = c.n;
   if (c.mode == 1) {
     for (int x = b; x < e; ++x) {
-      int i = c.in_src[x];
+      int i = __ldg(c.in_src + (x));
       int q = c.device_of[i];
       int64_t fin = c.finish[i];
       int64_t term;
@@ -57,7 +57,7 @@ __device__ __forceinline__ int64_t est_time(const Ctx &c, int j, int p, int64_t 
         term = fin;
       } else {
         int64_t cached = c.cache[static_cast<int64_t>(i) * n + p];
-        term = cached >= 0 ? max64(fin, cached) : fin + c.in_c[x];
+        term = cached >= 0 ? max64(fin, cached) : fin + __ldg(c.in_c + (x));
       }
       t = max64(t, term);
     }
@@ -69,13 +69,13 @@ __device__ __forceinline__ int64_t est_time(const Ctx &c, int j, int p, int64_t 
     (void)gen;
     int64_t T = c.tail[p];
     for (int x = b; x < e; ++x) {
-      const int i = c.in_src[x];
+      const int i = __ldg(c.in_src + (x));
       const int q = c.device_of[i];
       const int64_t fin = c.finish[i];
       const bool local = q == p;
       const int64_t cached = local ? -1 : c.cache[static_cast<int64_t>(i) * n + p];
       const bool xfer = !local && cached < 0;
-      const int64_t tn = max64(max64(fin, T), c.tail[q]) + c.in_c[x];
+      const int64_t tn = max64(max64(fin, T), c.tail[q]) + __ldg(c.in_c + (x));
       const int64_t term = local ? fin : (xfer ? tn : max64(fin, cached));
       T = xfer ? tn : T;
       t = max64(t, term);
@@ -97,8 +97,8 @@ static __device__ int64_t commit_fold(const Ctx &c, int j, int p, int *count) {
   int cnt = 0;
   const int n = c.n;
   int64_t t = c.F[p];
-  for (int x = c.in_off[j]; x < c.in_off[j + 1]; ++x) {
-    int i = c.in_src[x];
+  for (int x = __ldg(c.in_off + (j)); x < __ldg(c.in_off + (j + 1)); ++x) {
+    int i = __ldg(c.in_src + (x));
     int q = c.device_of[i];
     int64_t fin = c.finish[i];
     if (q == p) {
@@ -112,9 +112,9 @@ static __device__ int64_t commit_fold(const Ctx &c, int j, int p, int *count) {
     }
     int64_t term;
     if (c.mode == 1) {
-      term = fin + c.in_c[x];
+      term = fin + __ldg(c.in_c + (x));
     } else {
-      term = max64(fin, max64(c.tail[q], c.tail[p])) + c.in_c[x];
+      term = max64(fin, max64(c.tail[q], c.tail[p])) + __ldg(c.in_c + (x));
       c.tail[q] = term;
       c.tail[p] = term;
     }
@@ -253,7 +253,7 @@ __device__ __forceinline__ int ready_append(const Ctx &c, int R, bool flag, int 
 // transfer time, ignoring caches and queues.
 __device__ __forceinline__ int64_t urgency(const Ctx &c, int j) {
   int64_t u = 0;
-  for (int x = c.in_off[j]; x < c.in_off[j + 1]; ++x) u = max64(u, c.finish[c.in_src[x]] + c.in_c[x]);
+  for (int x = __ldg(c.in_off + (j)); x < __ldg(c.in_off + (j + 1)); ++x) u = max64(u, c.finish[__ldg(c.in_src + (x))] + __ldg(c.in_c + (x)));
   return u;
 }
 
