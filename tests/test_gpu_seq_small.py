@@ -170,3 +170,20 @@ def test_seq_small_midrun_overflow_hands_off(bx):
         assert oe is None and st == 0
         _same(p, o)
         assert kern != "seq-small", kern
+
+
+def test_seq_small_wide_times(bx):
+    """Compute times whose sum passes 2^31 us: K2q keeps int64 times (no
+    range hand-off, unlike K2s), results stay exact."""
+    for seed in range(2):
+        m = W.as_meta_dict(W.branchy(6, seed))
+        m["k"] = m["k"] * 20_000_000
+        gg = bx.MetaGraph.from_dict(m)
+        need = m["perm"] + m["out"] + m["temp"]
+        for n in (2, 4):
+            caps = [int((need.sum() / n + need.max()) * 1.1)] * n
+            o, oe = _oracle(m, caps, (5.0, 0.001, 0))
+            st, msg, p, kern = _plan_one(bx, gg, "m-etf", caps, bx.CommModel(5.0, 0.001, 0))
+            assert oe is None and st == 0
+            _same(p, o)
+            assert kern == "seq-small", kern
